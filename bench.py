@@ -1,0 +1,574 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the B200 index-array path.
+
+Headline workload (BASELINE.json configs[1], the metric's single-GPU config):
+  c2 = filter (x >= 0) + mkFlags (flag array from a segment shape) + sgmSum
+  (segmented inclusive sum) over N = 2^28 int32 per GPU, m = 2^20 segments.
+A "step" is one pass of the pipeline over one batch (the whole N).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1|c3|c4|c5] [--quick]
+
+Prints ONE JSON line on rank 0.  `value` is whole-job Gelem/s with inputs
+resident in HBM (device-timed with CUDA events, max over ranks); `e2e` is
+the same metric through the public C-ABI call with pinned host buffers and
+the H2D/D2H copies inside the timed region; `roofline` is the dominant
+kernel's algorithmic bytes / its event-timed duration against the measured
+HBM copy peak; `cpu_baseline` is the oracle port (oracle/, OpenMP, all host
+threads) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gelem/s and HBM GB/s (% of roofline), checked vs elided speedup, at 1/2/4/8 B200"
+FALLBACK_HBM = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- dist
+def dist_init():
+    import torch
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, ws, local
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ----------------------------------------------------------------- workloads
+class C2:
+    """filter + mkFlags + sgmSum (corpus/c2_filter_sgmsum.ixl)."""
+
+    name = "c2"
+
+    def __init__(self, quick, rank, ws):
+        from paper_2506_23058_b200 import gen
+        from paper_2506_23058_b200.pred import Pred
+
+        self.N = (1 << 22) if quick else (1 << 28)
+        self.m = (1 << 14) if quick else (1 << 20)
+        self.p = Pred.ge(0)
+        self.rank, self.ws = rank, ws
+        # each rank owns one contiguous shard of the global xs
+        self.xs_h = gen.uniform(0, self.N, -128, 127, np.int32, offset=rank * self.N)
+        self.k = int(np.count_nonzero(self.xs_h >= 0))
+        self.shape_h = gen.segment_shape(1 + rank, self.m, self.k)
+        self.workload = (f"c2 = filter (x >= 0) + mkFlags + sgmSum: N=2^{self.N.bit_length() - 1} int32 uniform "
+                         f"[-128,127] per GPU, m=2^{self.m.bit_length() - 1} segments (i64 shape, sum = k, >=1% empty), "
+                         "zs int32")
+
+    def setup_device(self):
+        import torch
+
+        from paper_2506_23058_b200 import ops
+
+        dev = torch.device("cuda")
+        self.xs = torch.from_numpy(self.xs_h).to(dev)
+        self.shape = torch.from_numpy(self.shape_h).to(dev)
+        self.ys = torch.empty(self.N, dtype=torch.int32, device=dev)
+        self.zs = torch.empty(self.N, dtype=torch.int32, device=dev)
+        self.dk = torch.empty(1, dtype=torch.int64, device=dev)
+        self.st = ops.Status(dev)
+
+    def step(self, variant):
+        from paper_2506_23058_b200 import ops
+
+        ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
+
+    def check(self, want):
+        k = int(self.dk.item())
+        s = self.st.read()
+        ok = (s.ok and not s.narrow and k == self.k)
+        if want is not None:
+            ok = ok and np.array_equal(self.ys[:k].cpu().numpy(), want[0]) and np.array_equal(
+                self.zs[:k].cpu().numpy(), want[1])
+        return ok
+
+    def units(self):
+        return self.N
+
+    def algo_bytes_step(self):
+        return 4 * self.N + 8 * self.m + 8 * self.k
+
+    def kernel(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        # the fused filter+sgmSum kernel: xs read once, ys and zs written once
+        return L.K_FILTER_FUSED, 4 * self.N + 8 * self.k, "k_filter<int32,int32,seg> (fused filter + sgmSum)"
+
+    def e2e_step(self, bufs):
+        """pinned host -> device, pipeline, k -> host, ys/zs -> host."""
+        from paper_2506_23058_b200 import ops
+
+        xs_p, shape_p, ys_p, zs_p, variant = bufs
+        self.xs.copy_(xs_p, non_blocking=True)
+        self.shape.copy_(shape_p, non_blocking=True)
+        ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
+        k = int(self.dk.item())
+        ys_p[:k].copy_(self.ys[:k], non_blocking=True)
+        zs_p[:k].copy_(self.zs[:k], non_blocking=True)
+        return 4 * self.N + 8 * self.m, 8 + 8 * k
+
+    def e2e_bufs(self, variant):
+        import torch
+
+        return (torch.from_numpy(self.xs_h).pin_memory(), torch.from_numpy(self.shape_h).pin_memory(),
+                torch.empty(self.N, dtype=torch.int32).pin_memory(),
+                torch.empty(self.N, dtype=torch.int32).pin_memory(), variant)
+
+    def cpu_run(self, xs, shape, threads=0):
+        from oracle import ixoracle as O
+
+        return O.par_c2_i32(self.p, xs, shape, threads)
+
+    def cpu_sample(self, budget_s):
+        """the full per-GPU workload when it fits the budget, else a prefix."""
+        return self.xs_h, self.shape_h, self.N
+
+
+class C1:
+    """partition2 (corpus partition2.ixl), 2^20 int32 (BASELINE configs[0]);
+    with --config c5 the same program at 2^32 (configs[4])."""
+
+    name = "c1"
+
+    def __init__(self, quick, rank, ws, big=False):
+        from paper_2506_23058_b200 import gen
+        from paper_2506_23058_b200.pred import Pred
+
+        self.name = "c5" if big else "c1"
+        self.N = ((1 << 24) if quick else (1 << 32) // ws) if big else (1 << 20)
+        self.p = Pred.lt(0)
+        self.xs_h = None if big else gen.uniform(0, self.N, -(1 << 31), (1 << 31) - 1, np.int32, offset=rank * self.N)
+        self.big, self.rank = big, rank
+        self.workload = (f"partition2 (x < 0), N=2^{self.N.bit_length() - 1} int32 uniform over int32"
+                         + (" per GPU (2^32 total)" if big else ""))
+
+    def setup_device(self):
+        import torch
+
+        from paper_2506_23058_b200 import ops
+
+        dev = torch.device("cuda")
+        if self.big:
+            self.xs = ops.gen_uniform(self.N, -(1 << 31), (1 << 31) - 1, 0, torch.int32, offset=self.rank * self.N)
+        else:
+            self.xs = torch.from_numpy(self.xs_h).to(dev)
+        self.ys = torch.empty(self.N, dtype=torch.int32, device=dev)
+        self.dnt = torch.empty(1, dtype=torch.int64, device=dev)
+        self.st = ops.Status(dev)
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if not self.big else None
+
+    def step(self, variant):
+        from paper_2506_23058_b200 import ops
+
+        if self.flush is not None:
+            self.flush.zero_()  # 256 MB write: evicts the 126 MB L2 between steps
+        ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
+
+    def check(self, want):
+        s = self.st.read()
+        ok = s.ok
+        if want is not None:
+            ok = ok and int(self.dnt.item()) == want[0] and np.array_equal(self.ys.cpu().numpy(), want[1])
+        return ok
+
+    def units(self):
+        return self.N
+
+    def algo_bytes_step(self):
+        return 8 * self.N + 8
+
+    def kernel(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        return L.K_PLACE, 8 * self.N, "k_place<int32,2> (stable placement pass)"
+
+    def e2e_bufs(self, variant):
+        import torch
+
+        xs_h = self.xs_h if self.xs_h is not None else self.xs.cpu().numpy()
+        return (torch.from_numpy(xs_h).pin_memory(), torch.empty(self.N, dtype=torch.int32).pin_memory(), variant)
+
+    def e2e_step(self, bufs):
+        from paper_2506_23058_b200 import ops
+
+        xs_p, ys_p, variant = bufs
+        self.xs.copy_(xs_p, non_blocking=True)
+        ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
+        ys_p.copy_(self.ys, non_blocking=True)
+        int(self.dnt.item())
+        return 4 * self.N, 4 * self.N + 8
+
+    def cpu_run(self, xs, threads=0):
+        from oracle import ixoracle as O
+
+        return O.par_partition2_i32(self.p, xs, threads)
+
+    def cpu_sample(self, budget_s):
+        if self.xs_h is None:
+            from paper_2506_23058_b200 import gen
+
+            n = min(self.N, 1 << 28)
+            return gen.uniform(0, n, -(1 << 31), (1 << 31) - 1, np.int32), n
+        return self.xs_h, self.N
+
+
+# ----------------------------------------------------------------- timing
+def time_steps(wl, variant, steps, warmup, ws, kernel_id=None):
+    import torch
+
+    from paper_2506_23058_b200 import _lib as L
+    from paper_2506_23058_b200 import ops
+
+    lib = L.load(require_device=True)
+    for _ in range(warmup):
+        wl.step(variant)
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    launches0 = ops.launch_count()
+    if kernel_id:
+        lib.ixg_timer_start(kernel_id)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        wl.step(variant)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    launches = ops.launch_count() - launches0
+    kms = None
+    if kernel_id:
+        import ctypes
+
+        tot, cnt = ctypes.c_double(0), ctypes.c_int64(0)
+        L.check(lib.ixg_timer_stop(ctypes.byref(tot), ctypes.byref(cnt)), "timer")
+        kms = tot.value / max(cnt.value, 1)
+    barrier(ws)
+    return max_over_ranks(ms, ws), launches, kms
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2506_23058_b200 import _lib as L
+
+    rank, ws, local = dist_init()
+    wl = make_workload(args, rank, ws)
+    wl.setup_device()
+    hbm, peak_kind = _peaks()
+    selected = L.VARIANT_ELIDED  # the verifier's selection for every site of c2 / partition2
+    # parity of the measured configuration against the CPU port
+    want = None
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(wl, args)
+        want = cpu.pop("_result", None)
+    wl.step(selected)
+    torch.cuda.synchronize()
+    parity = wl.check(want)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    # soak so the clock sampler sees the loaded state
+    t_end = time.time() + (0.3 if args.quick else 1.5)
+    while time.time() < t_end:
+        wl.step(selected)
+    torch.cuda.synchronize()
+    kid, kbytes, kname = wl.kernel()
+    ms, launches, kms = time_steps(wl, selected, args.steps, args.warmup, ws, kid)
+    clocks = sampler.stop()
+    ms_chk, _, _ = time_steps(wl, L.VARIANT_CHECKED, max(3, args.steps // 4), 2, ws)
+    parity_chk = wl.check(want)
+
+    # e2e: pinned host buffers, copies inside the timed region
+    bufs = wl.e2e_bufs(selected)
+    for _ in range(2):
+        wl.e2e_step(bufs)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(e2e_steps):
+        h2d, d2h = wl.e2e_step(bufs)
+    t1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(t0.elapsed_time(t1) / e2e_steps, ws)
+    units_total = wl.units() * ws
+    value = units_total / (ms * 1e-3) / 1e9
+    achieved = (kbytes / (kms * 1e-3) / 1e9) if kms else None
+    traffic = _ncu_traffic(wl.name)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "Gelem/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int32",
+        "data": "synthetic",
+        "config": {
+            "workload": wl.workload,
+            "variant": "verifier-selected (ELIDED: Sc1 scatters fused, mkFlags Ss2)",
+            "parallelism": f"shards{ws}" if ws > 1 else "single",
+            "l2": "inputs larger than the 126 MB L2, no flush" if wl.name in ("c2", "c5") else "256 MB L2 flush write between steps",
+            "parity_vs_cpu_port": bool(parity) if want is not None else "checked in tests",
+            "parity_checked_variant": bool(parity_chk) if want is not None else "checked in tests",
+        },
+        "hbm_gbs_step": round(wl.algo_bytes_step() / (ms * 1e-3) / 1e9, 1),
+        "checked": {
+            "ms_per_step": round(ms_chk, 4),
+            "value": round(units_total / (ms_chk * 1e-3) / 1e9, 3),
+            "elided_speedup": round(ms_chk / ms, 3),
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": kname,
+            "achieved": round(achieved, 1) if achieved else None,
+            "peak": hbm,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": round(achieved / hbm, 4) if achieved else None,
+            "traffic": traffic,
+            "algo_bytes_per_launch": kbytes,
+            "kernel_ms": round(kms, 5) if kms else None,
+        },
+        "e2e": {
+            "value": round(units_total / (e2e_ms * 1e-3) / 1e9, 4),
+            "unit": "Gelem/s",
+            "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(e2e_ms, 3),
+        },
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(name):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_<name>_full.json), else null."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_{name}_full.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(wl, args):
+    """The oracle port (OpenMP, all host threads) on the same workload."""
+    from oracle import ixoracle as O
+
+    threads = O.threads()
+    inputs = wl.cpu_sample(20.0)
+    n = inputs[-1]
+    res = wl.cpu_run(*inputs[:-1], threads)
+    times = []
+    t_budget = time.time() + (3.0 if args.quick else 10.0)
+    while True:
+        t0 = time.perf_counter()
+        wl.cpu_run(*inputs[:-1], threads)
+        times.append(time.perf_counter() - t0)
+        if time.time() > t_budget or len(times) >= 20:
+            break
+    best = statistics.median(times)
+    out = {
+        "value": round(n / best / 1e9, 4),
+        "unit": "Gelem/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{len(times)} runs of the full {wl.name} workload (n={n}) by oracle/ixoracle_par.c, median",
+        "ms_per_run": round(best * 1e3, 2),
+    }
+    if n == wl.units():
+        out["_result"] = (res[0], res[1]) if wl.name == "c2" else (res[0], res[1])
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path on the host cores.  The
+    reference is Python and cannot travel to the GPU box, so this is its
+    restatement oracle/ (C, OpenMP, every host thread) on the same config."""
+    rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import ixoracle as O
+
+    wl = make_workload(args, 0, 1)
+    threads = O.threads()
+    inputs = wl.cpu_sample(20.0)
+    n = inputs[-1]
+    for _ in range(args.warmup):
+        wl.cpu_run(*inputs[:-1], threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        wl.cpu_run(*inputs[:-1], threads)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    value = n / (ms * 1e-3) / 1e9
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "Gelem/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": wl.workload, "per_step": f"one full pass over n={n}"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gelem/s", "cores": threads, "kind": "port",
+                         "sample": f"n={n} per step, oracle/ixoracle_par.c (OpenMP)"},
+        "e2e": {"value": round(value, 4), "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def make_workload(args, rank, ws):
+    if args.config == "c2":
+        return C2(args.quick, rank, ws)
+    if args.config == "c1":
+        return C1(args.quick, rank, ws)
+    if args.config == "c5":
+        return C1(args.quick, rank, ws, big=True)
+    raise SystemExit(f"unknown config {args.config}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c5"])
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

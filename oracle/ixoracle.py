@@ -1,0 +1,268 @@
+"""TEST INFRASTRUCTURE ONLY -- numpy/ctypes front-end of oracle/libixoracle.so.
+
+The C library restates the reference interpreter (``oracle.py:90-333`` of
+``/root/reference/pkg/src/ixverify``) and the corpus programs.  Only tests,
+``__graft_entry__.smoke()`` and bench.py's CPU-baseline legs may import this
+module; the product package never does.  Every function takes numpy arrays
+(int64 unless stated) and returns numpy arrays, raising :class:`OracleFail`
+with the reference's status code where the reference interpreter would raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libixoracle.so")
+
+OK, OOB, CONFLICT, LENGTH, BADARG, NOMEM, OVERFLOW = range(7)
+HIST_MIN, HIST_MAX, HIST_ADD = 0, 1, 2
+
+
+class OracleFail(Exception):
+    def __init__(self, code, site=None, elem=None):
+        super().__init__(f"oracle status {code} (site={site}, elem={elem})")
+        self.code, self.site, self.elem = code, site, elem
+
+
+class _Pred(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32), ("thr", ctypes.c_int64), ("seed", ctypes.c_uint64)]
+
+
+class _Status(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("site", ctypes.c_int32), ("elem", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        _lib = ctypes.CDLL(LIB_PATH)
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else ctypes.c_void_p(0)
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def cpred(p) -> _Pred:
+    """Any object with kind/thr/seed (paper_2506_23058_b200.Pred)."""
+    return _Pred(int(p.kind), 0, int(p.thr), int(p.seed) & ((1 << 64) - 1))
+
+
+def _ok(rc, st=None):
+    if rc != OK:
+        if st is not None and st.code:
+            raise OracleFail(rc, st.site, st.elem)
+        raise OracleFail(rc)
+
+
+# ---------------------------------------------------------------- builtins
+def scan_add(xs, ne=0):
+    xs = _i64(xs)
+    out = np.empty_like(xs)
+    _ok(lib().ixo_scan_add(ctypes.c_int64(ne), _p(xs), ctypes.c_int64(len(xs)), _p(out)))
+    return out
+
+
+def sgmsum(flags, xs):
+    flags, xs = _i64(flags), _i64(xs)
+    out = np.empty_like(xs)
+    _ok(lib().ixo_sgmsum(_p(flags), _p(xs), ctypes.c_int64(len(xs)), _p(out)))
+    return out
+
+
+def scatter(dst, is_, vs):
+    dst, is_, vs = _i64(dst), _i64(is_), _i64(vs)
+    out = np.empty_like(dst)
+    _ok(lib().ixo_scatter(_p(dst), ctypes.c_int64(len(dst)), _p(is_), ctypes.c_int64(len(is_)), _p(vs),
+                          ctypes.c_int64(len(vs)), _p(out)))
+    return out
+
+
+def hist(op, ne, dlen, is_, vs):
+    is_, vs = _i64(is_), _i64(vs)
+    out = np.empty(max(dlen, 0), dtype=np.int64)
+    _ok(lib().ixo_hist(op, ctypes.c_int64(ne), ctypes.c_int64(dlen), _p(is_), ctypes.c_int64(len(is_)), _p(vs),
+                       ctypes.c_int64(len(vs)), _p(out)))
+    return out
+
+
+def gather(arr, idx):
+    arr, idx = _i64(arr), _i64(idx)
+    out = np.empty_like(idx)
+    bad = ctypes.c_int64(-1)
+    rc = lib().ixo_gather(_p(arr), ctypes.c_int64(len(arr)), _p(idx), ctypes.c_int64(len(idx)), _p(out),
+                          ctypes.byref(bad))
+    if rc:
+        raise OracleFail(rc, 0, bad.value)
+    return out
+
+
+# ---------------------------------------------------------------- corpus
+def sum_(xs):
+    xs = _i64(xs)
+    out = ctypes.c_int64(0)
+    _ok(lib().ixo_sum(_p(xs), ctypes.c_int64(len(xs)), ctypes.byref(out)))
+    return out.value
+
+
+def partition2(p, xs):
+    xs = _i64(xs)
+    ys = np.empty_like(xs)
+    nt = ctypes.c_int64(0)
+    cp = cpred(p)
+    _ok(lib().ixo_partition2(ctypes.byref(cp), _p(xs), ctypes.c_int64(len(xs)), ctypes.byref(nt), _p(ys)))
+    return nt.value, ys
+
+
+def partition3(p, q, xs):
+    xs = _i64(xs)
+    ys = np.empty_like(xs)
+    m1, m2 = ctypes.c_int64(0), ctypes.c_int64(0)
+    cp, cq = cpred(p), cpred(q)
+    _ok(lib().ixo_partition3(ctypes.byref(cp), ctypes.byref(cq), _p(xs), ctypes.c_int64(len(xs)), ctypes.byref(m1),
+                             ctypes.byref(m2), _p(ys)))
+    return m1.value, m2.value, ys
+
+
+def filter_(p, xs):
+    xs = _i64(xs)
+    ys = np.empty_like(xs)
+    cnt = ctypes.c_int64(0)
+    cp = cpred(p)
+    _ok(lib().ixo_filter(ctypes.byref(cp), _p(xs), ctypes.c_int64(len(xs)), _p(ys), ctypes.byref(cnt)))
+    return ys[: cnt.value].copy()
+
+
+def filter_by(cs, xs):
+    cs, xs = _i64(cs), _i64(xs)
+    ys = np.empty_like(xs)
+    cnt = ctypes.c_int64(0)
+    _ok(lib().ixo_filter_by(_p(cs), _p(xs), ctypes.c_int64(len(xs)), _p(ys), ctypes.byref(cnt)))
+    return ys[: cnt.value].copy()
+
+
+def mksgmdescr(shape, xs):
+    shape, xs = _i64(shape), _i64(xs)
+    cap = int(max(0, shape.sum())) if len(shape) else 0
+    cap = max(cap, 1)
+    for _ in range(2):
+        res = np.empty(cap, dtype=np.int64)
+        ln = ctypes.c_int64(0)
+        rc = lib().ixo_mksgmdescr(_p(shape), _p(xs), ctypes.c_int64(len(shape)), _p(res), ctypes.c_int64(cap),
+                                  ctypes.byref(ln))
+        if rc == BADARG and ln.value > cap:
+            cap = ln.value
+            continue
+        _ok(rc)
+        return res[: ln.value].copy()
+    raise OracleFail(BADARG)
+
+
+def mkii(shape):
+    shape = _i64(shape)
+    cap = max(1, int(max(0, shape.sum())) if len(shape) else 0)
+    out = np.empty(cap, dtype=np.int64)
+    ln = ctypes.c_int64(0)
+    _ok(lib().ixo_mkii(_p(shape), ctypes.c_int64(len(shape)), _p(out), ctypes.c_int64(cap), ctypes.byref(ln)))
+    return out[: ln.value].copy()
+
+
+def mkflags(k, shape):
+    shape = _i64(shape)
+    out = np.empty(max(k, 1), dtype=np.int64)
+    _ok(lib().ixo_mkflags(ctypes.c_int64(k), _p(shape), ctypes.c_int64(len(shape)), _p(out)))
+    return out[: max(k, 0)].copy()
+
+
+def c2(p, xs, shape):
+    xs, shape = _i64(xs), _i64(shape)
+    ys = np.empty(max(len(xs), 1), dtype=np.int64)
+    zs = np.empty(max(len(xs), 1), dtype=np.int64)
+    k = ctypes.c_int64(0)
+    cp = cpred(p)
+    _ok(lib().ixo_c2(ctypes.byref(cp), _p(xs), ctypes.c_int64(len(xs)), _p(shape), ctypes.c_int64(len(shape)), _p(ys),
+                     _p(zs), ctypes.byref(k)))
+    return ys[: k.value].copy(), zs[: k.value].copy()
+
+
+def get_smallest_pairs(n_verts, n_es, es, is_):
+    es, is_ = _i64(es), _i64(is_)
+    n = len(es)
+    xs = np.empty(max(n, 1), dtype=np.int64)
+    ys = np.empty(max(n, 1), dtype=np.int64)
+    cnt = ctypes.c_int64(0)
+    st = _Status()
+    rc = lib().ixo_get_smallest_pairs(ctypes.c_int64(n_verts), ctypes.c_int64(n_es), _p(es), _p(is_),
+                                      ctypes.c_int64(n), _p(xs), _p(ys), ctypes.byref(cnt), ctypes.byref(st))
+    _ok(rc, st)
+    return xs[: cnt.value].copy(), ys[: cnt.value].copy()
+
+
+def kmeans_ker(row, pointers, cluster, values, indices):
+    pointers, indices = _i64(pointers), _i64(indices)
+    cluster = np.ascontiguousarray(np.asarray(cluster, dtype=np.float64))
+    values = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+    out = ctypes.c_double(0.0)
+    st = _Status()
+    rc = lib().ixo_kmeans_ker(ctypes.c_int64(row), _p(pointers), ctypes.c_int64(len(pointers)), _p(cluster),
+                              ctypes.c_int64(len(cluster)), _p(values), _p(indices), ctypes.c_int64(len(indices)),
+                              ctypes.byref(out), ctypes.byref(st))
+    _ok(rc, st)
+    return out.value
+
+
+def csrg(x, values, indices):
+    x, values, indices = _i64(x), _i64(values), _i64(indices)
+    out = np.empty_like(values)
+    bad = ctypes.c_int64(-1)
+    rc = lib().ixo_csrg(_p(x), ctypes.c_int64(len(x)), _p(values), _p(indices), ctypes.c_int64(len(values)), _p(out),
+                        ctypes.byref(bad))
+    if rc:
+        raise OracleFail(rc, 0, bad.value)
+    return out
+
+
+# ---------------------------------------------------------------- CPU baseline (OpenMP)
+def threads() -> int:
+    return int(lib().ixo_par_threads())
+
+
+def par_c2_i32(p, xs, shape, nthreads=0):
+    xs = np.ascontiguousarray(xs, dtype=np.int32)
+    shape = _i64(shape)
+    ys = np.empty(max(len(xs), 1), dtype=np.int32)
+    zs = np.empty(max(len(xs), 1), dtype=np.int32)
+    k = ctypes.c_int64(0)
+    cp = cpred(p)
+    _ok(lib().ixo_par_c2_i32(ctypes.byref(cp), _p(xs), ctypes.c_int64(len(xs)), _p(shape), ctypes.c_int64(len(shape)),
+                             _p(ys), _p(zs), ctypes.byref(k), int(nthreads)))
+    return ys[: k.value], zs[: k.value]
+
+
+def par_partition2_i32(p, xs, nthreads=0):
+    xs = np.ascontiguousarray(xs, dtype=np.int32)
+    ys = np.empty(max(len(xs), 1), dtype=np.int32)
+    nt = ctypes.c_int64(0)
+    cp = cpred(p)
+    _ok(lib().ixo_par_partition2_i32(ctypes.byref(cp), _p(xs), ctypes.c_int64(len(xs)), ctypes.byref(nt), _p(ys),
+                                     int(nthreads)))
+    return nt.value, ys[: len(xs)]

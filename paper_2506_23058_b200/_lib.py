@@ -1,0 +1,111 @@
+"""ctypes binding of libixgpu.so (the C ABI declared in include/ixgpu.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``).  There is no fallback: if the
+library or a B200 device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libixgpu.so")
+
+# status / return codes (include/ixgpu.h)
+OK, OOB, CONFLICT, LENGTH, BADARG, NOMEM, OVERFLOW, NODEVICE = 0, 1, 2, 3, 4, 5, 6, 7
+CUDA_ERR = 100
+I32, I64, U8, F64 = 0, 1, 2, 3
+V_BOUNDS, V_CONFLICT, V_INIT = 1, 2, 4
+VARIANT_CHECKED = 0x77777777
+VARIANT_ELIDED = 0
+F_DUP, F_NARROW = 1, 2
+HIST_MIN, HIST_MAX, HIST_ADD = 0, 1, 2
+OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR = range(1, 9)
+
+
+class ixg_pred(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32), ("thr", ctypes.c_int64), ("seed", ctypes.c_uint64)]
+
+
+class ixg_status(ctypes.Structure):
+    _fields_ = [("first", ctypes.c_uint64), ("codes", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_U32 = ctypes.c_uint32
+_U64 = ctypes.c_uint64
+_SZ = ctypes.c_size_t
+_PP = ctypes.POINTER(ixg_pred)
+
+# name -> (restype, argtypes); every symbol include/ixgpu.h declares
+SIGNATURES = {
+    "ixg_version": (_I, []),
+    "ixg_device_check": (_I, []),
+    "ixg_ws_bytes": (_SZ, [_I, _I64, _I64]),
+    "ixg_ws_init": (_I, [_P, _SZ, _P]),
+    "ixg_status_init": (_I, [_P, _P]),
+    "ixg_launch_count": (ctypes.c_ulonglong, []),
+    "ixg_scan_add": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _SZ, _P]),
+    "ixg_segscan_add": (_I, [_I, _P, _I, _P, _I64, _I, _I64, _P, _P, _P, _SZ, _P]),
+    "ixg_scatter": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _U32, _I, _I, _P, _P, _SZ, _P]),
+    "ixg_gather": (_I, [_I, _P, _I64, _P, _I64, _P, _U32, _I, _I, _P, _P]),
+    "ixg_hist": (_I, [_I, _I64, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "ixg_fill": (_I, [_I, _P, _I64, _I64, _P]),
+    "ixg_iota": (_I, [_P, _I64, _P]),
+    "ixg_filter": (_I, [_I, _P, _I64, _PP, _P, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_filter_by": (_I, [_I, _P, _P, _I64, _P, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_partition2": (_I, [_I, _P, _I64, _PP, _P, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_partition3": (_I, [_I, _P, _I64, _PP, _PP, _P, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_c2": (_I, [_I, _P, _I64, _PP, _P, _I64, _P, _I, _P, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_mksgmdescr": (_I, [_P, _P, _I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_csr_gather": (_I, [_I, _P, _I64, _P, _P, _I64, _P, _U32, _P, _P]),
+    "ixg_kmeans_ker": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _U32, _P, _P]),
+    "ixg_eq_gather": (_I, [_P, _I64, _P, _P, _I64, _P, _U32, _I, _P, _P]),
+    "ixg_gen_uniform": (_I, [_I, _P, _I64, _I64, _I64, _U64, _I64, _P]),
+    "ixg_timer_start": (_I, [_I]),
+    "ixg_timer_stop": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
+}
+K_FILTER_FUSED, K_PLACE, K_CLASS_COUNT, K_SCAN, K_SCATTER, K_CSR_GATHER = 1, 2, 3, 4, 5, 6
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeUnavailable(RuntimeError):
+    """libixgpu.so is missing or no sm_100 device is visible (no fallback)."""
+
+
+def load(require_device: bool = False):
+    """Load libixgpu.so (raises NativeUnavailable when absent)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailable(
+                    f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    if require_device:
+        rc = _lib.ixg_device_check()
+        if rc != OK:
+            raise NativeUnavailable("libixgpu.so needs an sm_100 (B200) CUDA device; none is current")
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == OK:
+        return
+    if rc >= CUDA_ERR:
+        raise RuntimeError(f"{what}: CUDA error {rc - CUDA_ERR}")
+    names = {BADARG: "bad argument", NOMEM: "out of memory", NODEVICE: "no sm_100 device"}
+    raise RuntimeError(f"{what}: {names.get(rc, rc)}")

@@ -1,0 +1,639 @@
+// abi.cu -- the extern "C" entry points of libixgpu.so (include/ixgpu.h).
+//
+// Each function validates its arguments, lays out its workspace with a bump
+// allocator (the same code path sizes it for ixg_ws_bytes), picks the fused
+// ELIDED kernel or the materialising CHECKED sequence from the site bits,
+// and enqueues everything on the caller's stream.  No host synchronisation.
+#include <atomic>
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "k_compact.cuh"
+#include "k_generic.cuh"
+
+using namespace ixg;
+
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};
+
+// ---- kernel timer (ixg_timer_start/stop): event pairs around one family
+struct Timer {
+  int target = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  size_t used = 0;
+} g_timer;
+
+struct TimedLaunch {
+  cudaEvent_t stop = nullptr;
+  cudaStream_t s;
+  TimedLaunch(int kid, cudaStream_t s_) : s(s_) {
+    if (g_timer.target != kid) return;
+    if (g_timer.used == g_timer.pool.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      g_timer.pool.emplace_back(a, b);
+    }
+    auto& pr = g_timer.pool[g_timer.used++];
+    cudaEventRecord(pr.first, s);
+    stop = pr.second;
+  }
+  ~TimedLaunch() {
+    if (stop) cudaEventRecord(stop, s);
+  }
+};
+
+constexpr size_t kHdrBlock = 8 * 256;  // fixed-offset look-back headers (8 channels)
+
+struct WS {
+  char* base;
+  size_t off;
+  bool dry;
+  explicit WS(void* p) : base((char*)p), off(kHdrBlock), dry(p == nullptr) {}
+  void* take(size_t bytes, size_t align = 256) {
+    off = (off + align - 1) / align * align;
+    void* p = dry ? nullptr : base + off;
+    off += bytes ? bytes : 1;
+    return p;
+  }
+  LBHeader* hdr(int i) const { return dry ? nullptr : (LBHeader*)(base + i * 256); }
+  LBChan chan(int i, long long tiles) {
+    LBChan c;
+    const size_t t = (size_t)(tiles > 0 ? tiles : 1);
+    c.hdr = hdr(i);
+    c.flags = (uint32_t*)take(t * 4);
+    c.agg = (longlong2*)take(t * sizeof(longlong2));
+    c.incl = (longlong2*)take(t * sizeof(longlong2));
+    return c;
+  }
+};
+
+inline long long tiles_of(long long n, int tile) { return (n + tile - 1) / tile; }
+inline size_t bitmap_bytes(long long nbits) { return (size_t)((nbits + 31) / 32 + 2 + 128) * 4; }
+inline int grid_for(long long work, int per_block = kGThreads) {
+  long long g = (work + per_block - 1) / per_block;
+  long long cap = (long long)num_sms() * 8;
+  if (g > cap) g = cap;
+  return (int)(g > 0 ? g : 1);
+}
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+#define LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
+#define CHECK_LAUNCH()                          \
+  do {                                          \
+    cudaError_t e__ = cudaGetLastError();       \
+    if (e__ != cudaSuccess) return cuda_rc(e__); \
+  } while (0)
+
+template <typename K>
+void allow_smem(K kernel, int bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// ------------------------------------------------------------------ pieces
+template <class M, class Src, class Epi>
+int launch_scan(long long n, Src src, Epi epi, LBChan ch, cudaStream_t s) {
+  if (n <= 0) return IXG_OK;
+  TimedLaunch tl(IXG_K_SCAN, s);
+  k_scan<M, Src, Epi><<<(unsigned)tiles_of(n, kGTile), kGThreads, 0, s>>>(n, src, epi, ch);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+template <typename E>
+int launch_fill(E* out, long long n, const long long* d_n, E v, cudaStream_t s) {
+  k_fill<E><<<grid_for(d_n ? (long long)num_sms() * 8 * kGThreads : n), kGThreads, 0, s>>>(out, n, d_n, v);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+// checked/elided scatter of m pairs into out[0..ndst) (ndst from d_ndst when given)
+template <typename E>
+int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long ndst_cap, const long long* is,
+                   const E* vs, long long m, uint32_t bits, int stmt, int site, ixg_status* st, WS& ws,
+                   int hdr_idx, cudaStream_t s) {
+  const bool check = (bits & IXG_V_CONFLICT) != 0;
+  uint32_t* claim = nullptr;
+  if (check) claim = (uint32_t*)ws.take(bitmap_bytes(ndst_cap));
+  if (ws.dry || m <= 0) return IXG_OK;
+  LBHeader* hdr = ws.hdr(hdr_idx);
+  if (check) {
+    cudaMemsetAsync(claim, 0, bitmap_bytes(ndst_cap), s);
+    LAUNCHED();
+  }
+  {
+    TimedLaunch tl(IXG_K_SCATTER, s);
+    k_scatter<E><<<grid_for(m), kGThreads, 0, s>>>(out, ndst, d_ndst, is, vs, m, check ? 1 : 0, claim, hdr);
+  }
+  LAUNCHED();
+  CHECK_LAUNCH();
+  if (check) {
+    k_scatter_verify<E><<<grid_for(m), kGThreads, 0, s>>>(out, ndst, d_ndst, is, vs, m, hdr, st, stmt, site);
+    LAUNCHED();
+    CHECK_LAUNCH();
+  }
+  return IXG_OK;
+}
+
+// --------------------------------------------------------------- filter
+template <typename T, typename Z, bool kByCs, bool kSeg>
+int launch_filter_fused(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, Z* zs,
+                        const uint32_t* segbits, long long out_base, LBChan c0, LBChan c1, long long* d_count,
+                        longlong2* d_seg_total, ixg_status* st, cudaStream_t s) {
+  auto kern = k_filter<T, Z, kByCs, kSeg>;
+  const int smem = kTile * (int)sizeof(T) + (kSeg ? kTile * (int)sizeof(Z) : 0);
+  static bool attr = false;
+  if (!attr) {
+    allow_smem(kern, smem);
+    attr = true;
+  }
+  TimedLaunch tl(IXG_K_FILTER_FUSED, s);
+  kern<<<(unsigned)tiles_of(n, kTile), kThreads, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, c0, c1,
+                                                            d_count, d_seg_total, st);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+// filter / filter_by on element type T.  Sites: 0 = offs[n-1], 1 = scatter.
+template <typename T>
+int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T* ys, long long* d_count,
+              uint32_t variant, ixg_status* st, WS& ws, cudaStream_t s) {
+  const uint32_t sb = IXG_SITE_BITS(variant, 1);
+  const bool fused = (sb & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;  // Sc1 proved
+  ixg_pred pp = p ? *p : ixg_pred{IXG_PRED_TRUE, 0, 0, 0};
+  if (fused) {
+    LBChan c0 = ws.chan(0, tiles_of(n, kTile));
+    if (ws.dry) return IXG_OK;
+    if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
+    if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
+    if (cs) return launch_filter_fused<T, T, true, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, c0,
+                                                           d_count, nullptr, st, s);
+    return launch_filter_fused<T, T, false, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, c0, d_count,
+                                                    nullptr, st, s);
+  }
+  // CHECKED: offs/inds materialised (filter.ixl:10-12), then the scatter
+  // into `replicate count 0` with the dynamic checks (filter.ixl:13-14).
+  LBChan c0 = ws.chan(0, tiles_of(n, kGTile));
+  long long* inds = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
+  if (ws.dry) return launch_scatter<T>(ys, 0, d_count, n, inds, xs, n, sb, 1, 1, st, ws, 1, s);
+  if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
+  int rc = launch_scan<SumOp>(n, SrcPred{sizeof(T) == 4 ? IXG_I32 : IXG_I64, xs, cs, pp},
+                              EpiFilterInds{n, inds, d_count}, c0, s);
+  if (rc) return rc;
+  if (sb & IXG_V_INIT) {
+    if ((rc = launch_fill<T>(ys, 0, d_count, T(0), s))) return rc;
+  }
+  return launch_scatter<T>(ys, 0, d_count, n, inds, xs, n, sb, 1, 1, st, ws, 1, s);
+}
+
+// ------------------------------------------------------------ partition2/3
+template <typename T, int kClasses>
+int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q, T* ys, long long* d_tot,
+                 uint32_t variant, ixg_status* st, WS& ws, cudaStream_t s) {
+  const int scatter_site = kClasses == 2 ? 1 : 2;
+  const uint32_t sb = IXG_SITE_BITS(variant, scatter_site);
+  const bool fused = (sb & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;
+  const ixg_pred pp = *p;
+  const ixg_pred qq = q ? *q : ixg_pred{IXG_PRED_FALSE, 0, 0, 0};
+  const int cgrid = grid_for(n / (16 / (int)sizeof(T)) + 1);
+  long long* partials = (long long*)ws.take((size_t)cgrid * 2 * 8);
+  if (fused) {
+    LBChan c0 = ws.chan(0, tiles_of(n, kTile));
+    if (ws.dry) return IXG_OK;
+    if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
+    if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
+    {
+      TimedLaunch tl(IXG_K_CLASS_COUNT, s);
+      k_class_count<T, kClasses><<<cgrid, kThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
+    }
+    LAUNCHED();
+    CHECK_LAUNCH();
+    auto kern = k_place<T, kClasses>;
+    const int smem = kTile * (int)sizeof(T);
+    static bool attr = false;
+    if (!attr) {
+      allow_smem(kern, smem);
+      attr = true;
+    }
+    {
+      TimedLaunch tl(IXG_K_PLACE, s);
+      kern<<<(unsigned)tiles_of(n, kTile), kThreads, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0);
+    }
+    LAUNCHED();
+    CHECK_LAUNCH();
+    return IXG_OK;
+  }
+  // CHECKED: indices materialised exactly as partition2.ixl:9-16 /
+  // partition3.ixl:12-24, then the checked scatter into `replicate n 0`.
+  LBChan c0 = ws.chan(0, tiles_of(n, kGTile));
+  long long* inds = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
+  if (ws.dry) return launch_scatter<T>(ys, n, nullptr, n, inds, xs, n, sb, scatter_site, scatter_site, st, ws, 1, s);
+  if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
+  k_class_count<T, kClasses><<<cgrid, kThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  const int dt = sizeof(T) == 4 ? IXG_I32 : IXG_I64;
+  int rc;
+  if constexpr (kClasses == 2) {
+    rc = launch_scan<SumOp>(n, SrcPred{dt, xs, nullptr, pp}, EpiPart2Inds{d_tot, inds}, c0, s);
+  } else {
+    rc = launch_scan<Sum2Op>(n, SrcClass3{dt, xs, pp, qq}, EpiPart3Inds{d_tot, inds}, c0, s);
+  }
+  if (rc) return rc;
+  if (sb & IXG_V_INIT) {
+    if ((rc = launch_fill<T>(ys, n, nullptr, T(0), s))) return rc;
+  }
+  return launch_scatter<T>(ys, n, nullptr, n, inds, xs, n, sb, scatter_site, scatter_site, st, ws, 1, s);
+}
+
+// --------------------------------------------------------------------- c2
+// Sites: 0 = filter offs[n-1], 1 = filter scatter, 2 = mkFlags shape[i-1],
+// 3 = mkFlags scatter.
+template <typename T, typename Z>
+int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, long long m, T* ys, Z* zs,
+          long long* d_k, uint32_t variant, ixg_status* st, WS& ws, cudaStream_t s) {
+  const uint32_t sb1 = IXG_SITE_BITS(variant, 1);
+  const uint32_t sb3 = IXG_SITE_BITS(variant, 3);
+  const bool fused = (sb1 & (IXG_V_CONFLICT | IXG_V_INIT)) == 0 && (sb3 & IXG_V_CONFLICT) == 0;
+  const ixg_pred pp = *p;
+  if (fused) {
+    // mkFlags as a bitmap over the output positions: `replicate k 0` is the
+    // memset (k <= n), the Ss2-proved scatter of ones is an atomicOr per
+    // segment start (no conflict check), starts >= k are never read.
+    uint32_t* bits = (uint32_t*)ws.take(bitmap_bytes(n));
+    LBChan cs = ws.chan(2, tiles_of(m, kGTile));
+    LBChan c0 = ws.chan(0, tiles_of(n, kTile));
+    LBChan c1 = ws.chan(1, tiles_of(n, kTile));
+    if (ws.dry) return IXG_OK;
+    if (n <= 0) return cuda_rc(cudaMemsetAsync(d_k, 0, sizeof(long long), s));
+    if (!aligned16(xs) || !aligned16(ys) || !aligned16(zs)) return IXG_BADARG;
+    cudaMemsetAsync(bits, 0, bitmap_bytes(n), s);
+    LAUNCHED();
+    int rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
+    if (rc) return rc;
+    return launch_filter_fused<T, Z, false, true>(xs, nullptr, n, pp, ys, zs, bits, 0, c0, c1, d_k, nullptr, st, s);
+  }
+  // CHECKED: filter (checked), mkFlags with materialised ind/flags arrays
+  // and the checked scatter of `replicate m 1`, sgmSum as a 2-ary scan.
+  int rc = do_filter<T>(xs, nullptr, n, p, ys, d_k, variant, st, ws, s);
+  if (rc) return rc;
+  LBChan cs = ws.chan(2, tiles_of(m, kGTile));
+  LBChan cz = ws.chan(3, tiles_of(n, kGTile));
+  long long* ind = (long long*)ws.take((size_t)(m > 0 ? m : 1) * 8);
+  long long* ones = (long long*)ws.take((size_t)(m > 0 ? m : 1) * 8);
+  long long* flags = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
+  if (ws.dry) return launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s);
+  if (n <= 0) return IXG_OK;
+  if ((rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr}, cs, s)))
+    return rc;
+  if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
+  if ((rc = launch_fill<long long>(flags, 0, d_k, 0LL, s))) return rc;
+  if ((rc = launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s))) return rc;
+  // sgmSum over k elements: k is on the device, so scan all n positions of
+  // the capacity; positions >= k are never read back (ys beyond k unused).
+  return launch_scan<SegOp>(n, SrcSeg{IXG_I64, sizeof(T) == 4 ? IXG_I32 : IXG_I64, flags, ys},
+                            EpiSegOut{sizeof(Z) == 4 ? IXG_I32 : IXG_I64, zs, nullptr, st}, cz, s);
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+int ixg_version(void) { return 1; }
+
+int ixg_device_check(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return IXG_NODEVICE;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? IXG_OK : IXG_NODEVICE;
+}
+
+unsigned long long ixg_launch_count(void) { return g_launches.load(); }
+
+int ixg_timer_start(int kernel_id) {
+  g_timer.target = kernel_id;
+  g_timer.used = 0;
+  return IXG_OK;
+}
+
+int ixg_timer_stop(double* total_ms, int64_t* launches) {
+  double tot = 0.0;
+  for (size_t i = 0; i < g_timer.used; ++i) {
+    auto& pr = g_timer.pool[i];
+    cudaError_t e = cudaEventSynchronize(pr.second);
+    if (e != cudaSuccess) return cuda_rc(e);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (int64_t)g_timer.used;
+  g_timer.target = 0;
+  g_timer.used = 0;
+  return IXG_OK;
+}
+
+int ixg_ws_init(void* ws, size_t ws_bytes, void* stream) {
+  if (!ws) return IXG_BADARG;
+  LAUNCHED();
+  return cuda_rc(cudaMemsetAsync(ws, 0, ws_bytes, S(stream)));
+}
+
+int ixg_status_init(ixg_status* st, void* stream) {
+  if (!st) return IXG_BADARG;
+  ixg_status h;
+  h.first = ~0ULL;
+  h.codes = 0;
+  h.flags = 0;
+  LAUNCHED();
+  return cuda_rc(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, S(stream)));
+}
+
+size_t ixg_ws_bytes(int op, int64_t n, int64_t m) {
+  WS ws(nullptr);
+  ixg_pred p{IXG_PRED_TRUE, 0, 0, 0};
+  switch (op) {
+    case IXG_OP_SCAN: ws.chan(0, tiles_of(n, kGTile)); break;
+    case IXG_OP_SEGSCAN: ws.chan(0, tiles_of(n, kGTile)); break;
+    case IXG_OP_SCATTER: ws.take(bitmap_bytes(m)); break;  // n = pairs, m = ndst
+    case IXG_OP_FILTER:
+      do_filter<int64_t>(nullptr, nullptr, n, &p, nullptr, nullptr, IXG_VARIANT_CHECKED, nullptr, ws, 0);
+      {
+        WS w2(nullptr);
+        do_filter<int64_t>(nullptr, nullptr, n, &p, nullptr, nullptr, 0, nullptr, w2, 0);
+        if (w2.off > ws.off) ws.off = w2.off;
+      }
+      break;
+    case IXG_OP_PARTITION2:
+    case IXG_OP_PARTITION3: {
+      do_partition<int64_t, 3>(nullptr, n, &p, &p, nullptr, nullptr, IXG_VARIANT_CHECKED, nullptr, ws, 0);
+      WS w2(nullptr);
+      do_partition<int64_t, 3>(nullptr, n, &p, &p, nullptr, nullptr, 0, nullptr, w2, 0);
+      if (w2.off > ws.off) ws.off = w2.off;
+      break;
+    }
+    case IXG_OP_C2: {
+      do_c2<int64_t, int64_t>(nullptr, n, &p, nullptr, m, nullptr, nullptr, nullptr, IXG_VARIANT_CHECKED, nullptr,
+                              ws, 0);
+      WS w2(nullptr);
+      do_c2<int64_t, int64_t>(nullptr, n, &p, nullptr, m, nullptr, nullptr, nullptr, 0, nullptr, w2, 0);
+      if (w2.off > ws.off) ws.off = w2.off;
+      break;
+    }
+    case IXG_OP_MKSGMDESCR:
+      ws.chan(0, tiles_of(m, kGTile));
+      ws.take((size_t)(m > 0 ? m : 1) * 8);
+      ws.take(bitmap_bytes(n));  // n = destination capacity
+      break;
+    default: return 0;
+  }
+  return ws.off + 256;
+}
+
+int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, int64_t* out, void* ws,
+                 size_t ws_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!xs || !out))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, n, 0)) return IXG_BADARG;
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(n, kGTile));
+  return launch_scan<SumOp>(n, SrcArr{dt, xs}, EpiScanOut{ne, exclusive, (long long*)out}, c, S(stream));
+}
+
+int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64_t n, int f0, int64_t v0,
+                    int64_t* out_v, uint8_t* out_f, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!flags || !xs || !out_v))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_SEGSCAN, n, 0)) return IXG_BADARG;
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(n, kGTile));
+  (void)f0;
+  (void)v0;
+  if (f0 != 0 || v0 != 0) return IXG_BADARG;  // only the (false, 0) neutral of sgmSum is supported
+  return launch_scan<SegOp>(n, SrcSeg{dt_f, dt_x, flags, xs}, EpiSegOut{IXG_I64, out_v, out_f, nullptr}, c,
+                            S(stream));
+}
+
+int ixg_scatter(int dt, void* out, int64_t ndst, const int64_t* is, int64_t nis, const void* vs, int64_t nvs,
+                uint32_t site_bits, int stmt, int site, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  const long long m = nis < nvs ? nis : nvs;  // zip truncation, oracle.py:299
+  if (ndst < 0 || m < 0 || (m > 0 && (!is || !vs)) || (ndst > 0 && !out)) return IXG_BADARG;
+  if ((site_bits & IXG_V_CONFLICT) && ws_bytes < ixg_ws_bytes(IXG_OP_SCATTER, m, ndst)) return IXG_BADARG;
+  WS w(ws);
+  if (dt == IXG_I32)
+    return launch_scatter<int32_t>((int32_t*)out, ndst, nullptr, ndst, (const long long*)is, (const int32_t*)vs, m,
+                                   site_bits, stmt, site, st, w, 1, S(stream));
+  return launch_scatter<long long>((long long*)out, ndst, nullptr, ndst, (const long long*)is,
+                                   (const long long*)vs, m, site_bits, stmt, site, st, w, 1, S(stream));
+}
+
+int ixg_gather(int dt, const void* arr, int64_t len, const int64_t* idx, int64_t n, void* out,
+               uint32_t site_bits, int stmt, int site, ixg_status* st, void* stream) {
+  if (n < 0 || (n > 0 && (!idx || !out))) return IXG_BADARG;
+  if (n == 0) return IXG_OK;
+  const int check = (site_bits & IXG_V_BOUNDS) ? 1 : 0;
+  cudaStream_t s = S(stream);
+  if (dt == IXG_I32)
+    k_gather<int32_t><<<grid_for(n), kGThreads, 0, s>>>((const int32_t*)arr, len, (const long long*)idx, n,
+                                                         (int32_t*)out, check, st, stmt, site);
+  else if (dt == IXG_F64)
+    k_gather<double><<<grid_for(n), kGThreads, 0, s>>>((const double*)arr, len, (const long long*)idx, n,
+                                                        (double*)out, check, st, stmt, site);
+  else
+    k_gather<long long><<<grid_for(n), kGThreads, 0, s>>>((const long long*)arr, len, (const long long*)idx, n,
+                                                           (long long*)out, check, st, stmt, site);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_hist(int op, int64_t ne, int64_t dlen, const int64_t* is, int64_t nis, const int64_t* vs, int64_t nvs,
+             int64_t* out, void* stream) {
+  const long long m = nis < nvs ? nis : nvs;
+  if (dlen < 0) dlen = 0;  // [ne] * negative == []
+  if (op < 0 || op > 2 || m < 0 || (dlen > 0 && !out)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  int rc;
+  if (dlen > 0 && (rc = launch_fill<long long>((long long*)out, dlen, nullptr, (long long)ne, s))) return rc;
+  if (m == 0 || dlen == 0) return IXG_OK;
+  k_hist<<<grid_for(m), kGThreads, 0, s>>>(op, dlen, (const long long*)is, (const long long*)vs, m,
+                                            (long long*)out);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_fill(int dt, void* out, int64_t n, int64_t v, void* stream) {
+  if (n <= 0) return IXG_OK;
+  if (!out) return IXG_BADARG;
+  if (dt == IXG_I32) return launch_fill<int32_t>((int32_t*)out, n, nullptr, (int32_t)v, S(stream));
+  if (dt == IXG_U8) {
+    LAUNCHED();
+    return cuda_rc(cudaMemsetAsync(out, (int)(uint8_t)v, (size_t)n, S(stream)));
+  }
+  return launch_fill<long long>((long long*)out, n, nullptr, (long long)v, S(stream));
+}
+
+int ixg_iota(int64_t* out, int64_t n, void* stream) {
+  if (n <= 0) return IXG_OK;
+  k_iota<<<grid_for(n), kGThreads, 0, S(stream)>>>((long long*)out, n);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_filter(int dt, const void* xs, int64_t n, const ixg_pred* p, void* ys, int64_t* d_count, uint32_t variant,
+               ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !p || !d_count || (n > 0 && (!xs || !ys))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_FILTER, n, 0)) return IXG_BADARG;
+  WS w(ws);
+  if (dt == IXG_I32)
+    return do_filter<int32_t>((const int32_t*)xs, nullptr, n, p, (int32_t*)ys, (long long*)d_count, variant, st, w,
+                              S(stream));
+  return do_filter<int64_t>((const int64_t*)xs, nullptr, n, p, (int64_t*)ys, (long long*)d_count, variant, st, w,
+                            S(stream));
+}
+
+int ixg_filter_by(int dt, const uint8_t* cs, const void* xs, int64_t n, void* ys, int64_t* d_count,
+                  uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !d_count || (n > 0 && (!cs || !xs || !ys))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_FILTER, n, 0)) return IXG_BADARG;
+  WS w(ws);
+  if (dt == IXG_I32)
+    return do_filter<int32_t>((const int32_t*)xs, cs, n, nullptr, (int32_t*)ys, (long long*)d_count, variant, st,
+                              w, S(stream));
+  return do_filter<int64_t>((const int64_t*)xs, cs, n, nullptr, (int64_t*)ys, (long long*)d_count, variant, st, w,
+                            S(stream));
+}
+
+int ixg_partition2(int dt, const void* xs, int64_t n, const ixg_pred* p, void* ys, int64_t* d_num_true,
+                   uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !p || !d_num_true || (n > 0 && (!xs || !ys))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_PARTITION2, n, 0)) return IXG_BADARG;
+  WS w(ws);
+  if (dt == IXG_I32)
+    return do_partition<int32_t, 2>((const int32_t*)xs, n, p, nullptr, (int32_t*)ys, (long long*)d_num_true,
+                                    variant, st, w, S(stream));
+  return do_partition<int64_t, 2>((const int64_t*)xs, n, p, nullptr, (int64_t*)ys, (long long*)d_num_true, variant,
+                                  st, w, S(stream));
+}
+
+int ixg_partition3(int dt, const void* xs, int64_t n, const ixg_pred* p, const ixg_pred* q, void* ys, int64_t* d_m,
+                   uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !p || !q || !d_m || (n > 0 && (!xs || !ys))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_PARTITION3, n, 0)) return IXG_BADARG;
+  WS w(ws);
+  if (dt == IXG_I32)
+    return do_partition<int32_t, 3>((const int32_t*)xs, n, p, q, (int32_t*)ys, (long long*)d_m, variant, st, w,
+                                    S(stream));
+  return do_partition<int64_t, 3>((const int64_t*)xs, n, p, q, (int64_t*)ys, (long long*)d_m, variant, st, w,
+                                  S(stream));
+}
+
+int ixg_c2(int dt, const void* xs, int64_t n, const ixg_pred* p, const int64_t* shape, int64_t m, void* ys, int dt_z,
+           void* zs, int64_t* d_k, uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || m < 0 || !p || !d_k || (n > 0 && (!xs || !ys || !zs)) || (m > 0 && !shape)) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_C2, n, m)) return IXG_BADARG;
+  WS w(ws);
+  cudaStream_t s = S(stream);
+  const long long* sh = (const long long*)shape;
+  long long* dk = (long long*)d_k;
+  if (dt == IXG_I32 && dt_z == IXG_I32)
+    return do_c2<int32_t, int32_t>((const int32_t*)xs, n, p, sh, m, (int32_t*)ys, (int32_t*)zs, dk, variant, st, w, s);
+  if (dt == IXG_I32)
+    return do_c2<int32_t, int64_t>((const int32_t*)xs, n, p, sh, m, (int32_t*)ys, (int64_t*)zs, dk, variant, st, w, s);
+  if (dt_z == IXG_I32) return IXG_BADARG;
+  return do_c2<int64_t, int64_t>((const int64_t*)xs, n, p, sh, m, (int64_t*)ys, (int64_t*)zs, dk, variant, st, w, s);
+}
+
+int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t* res, int64_t cap, int64_t* d_len,
+                   uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (m < 0 || cap < 0 || !d_len || (m > 0 && (!shape || !xs)) || (cap > 0 && !res)) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_MKSGMDESCR, cap, m)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(m, kGTile));
+  long long* ind = (long long*)w.take((size_t)(m > 0 ? m : 1) * 8);
+  if (m == 0) return cuda_rc(cudaMemsetAsync(d_len, 0, 8, s));
+  // scn / ind / len (mksgmdescr.ixl:6-9); len = scn[m-1] + shape[m-1] = sum shape
+  int rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape},
+                              EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, (long long*)d_len}, c, s);
+  if (rc || cap == 0) return rc;
+  // the scatter is never proved for mkSgmDescr: the host
+  // passes cap >= len (read back from d_len), res[0..len) = 0, checked scatter.
+  const uint32_t sb = IXG_SITE_BITS(variant, 3) | IXG_V_INIT;
+  if ((rc = launch_fill<long long>((long long*)res, 0, (const long long*)d_len, 0LL, s))) return rc;
+  return launch_scatter<long long>((long long*)res, 0, (const long long*)d_len, cap, ind, (const long long*)xs, m, sb,
+                                   3, 3, st, w, 1, s);
+}
+
+int ixg_csr_gather(int dt, const void* x, int64_t num_cols, const void* values, const int64_t* indices, int64_t nnz,
+                   void* out, uint32_t variant, ixg_status* st, void* stream) {
+  if (nnz < 0 || (nnz > 0 && (!values || !indices || !out))) return IXG_BADARG;
+  if (nnz == 0) return IXG_OK;
+  if (!aligned16(values) || !aligned16(indices) || !aligned16(out)) return IXG_BADARG;
+  const int check = (IXG_SITE_BITS(variant, 0) & IXG_V_BOUNDS) ? 1 : 0;
+  cudaStream_t s = S(stream);
+  const long long work = nnz / 4 + 1;
+  TimedLaunch tl(IXG_K_CSR_GATHER, s);
+  if (dt == IXG_I32)
+    k_csr_gather<int32_t><<<grid_for(work), kGThreads, 0, s>>>((const int32_t*)x, num_cols, (const int32_t*)values,
+                                                                (const long long*)indices, nnz, (int32_t*)out, check,
+                                                                st);
+  else
+    k_csr_gather<long long><<<grid_for(work), kGThreads, 0, s>>>((const long long*)x, num_cols,
+                                                                  (const long long*)values, (const long long*)indices,
+                                                                  nnz, (long long*)out, check, st);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_kmeans_ker(const int64_t* rows, int64_t nrows, const int64_t* pointers, int64_t np1, const double* cluster,
+                   int64_t num_cols, const double* values, const int64_t* indices, int64_t nnz, double* out,
+                   uint32_t variant, ixg_status* st, void* stream) {
+  if (nrows < 0 || (nrows > 0 && (!rows || !out))) return IXG_BADARG;
+  if (nrows == 0) return IXG_OK;
+  k_kmeans<<<(unsigned)((nrows + 127) / 128), 128, 0, S(stream)>>>(
+      (const long long*)rows, nrows, (const long long*)pointers, np1, cluster, num_cols, values,
+      (const long long*)indices, nnz, out, variant, st);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_eq_gather(const int64_t* H, int64_t hlen, const int64_t* es, const int64_t* is, int64_t n, uint8_t* cs,
+                  uint32_t variant, int stmt, ixg_status* st, void* stream) {
+  if (n < 0 || (n > 0 && (!es || !is || !cs))) return IXG_BADARG;
+  if (n == 0) return IXG_OK;
+  const int check = (IXG_SITE_BITS(variant, 0) & IXG_V_BOUNDS) ? 1 : 0;
+  k_eq_gather<<<grid_for(n), kGThreads, 0, S(stream)>>>((const long long*)H, hlen, (const long long*)es,
+                                                         (const long long*)is, n, cs, check, st, stmt);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_gen_uniform(int dt, void* out, int64_t n, int64_t lo, int64_t hi, uint64_t seed, int64_t offset,
+                    void* stream) {
+  if (n <= 0) return IXG_OK;
+  if (!out || hi < lo) return IXG_BADARG;
+  const unsigned long long span = (unsigned long long)hi - (unsigned long long)lo + 1ULL;  // 0 = full 2^64
+  const uint64_t smix = seed_mix_host(seed);
+  cudaStream_t s = S(stream);
+  if (dt == IXG_I32)
+    k_gen_uniform<int32_t><<<grid_for(n), kGThreads, 0, s>>>((int32_t*)out, n, lo, span, smix, offset);
+  else
+    k_gen_uniform<long long><<<grid_for(n), kGThreads, 0, s>>>((long long*)out, n, lo, span, smix, offset);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// common.cuh -- shared device helpers for the sm_100a index-array kernels.
+//
+// Everything on this path is HBM-bound integer work, so the
+// helpers here are about moving bytes: 128-bit streaming loads/stores with
+// cache hints, warp-ballot ranking, and the decoupled look-back tile state
+// used by every single-pass scan (lookback.cuh).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ixgpu.h"
+
+#define IXG_DEV __device__ __forceinline__
+
+namespace ixg {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------- memory ops
+// Streaming (read-once) 128-bit load: bypass L1 allocation, evict-first in L2.
+IXG_DEV int4 ld_stream_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+IXG_DEV void st_stream_v4(void* p, int4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+IXG_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+IXG_DEV void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+IXG_DEV long long ld_relaxed_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+IXG_DEV void st_relaxed_s64(long long* p, long long v) {
+  asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+IXG_DEV uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+IXG_DEV int lane_id() { return threadIdx.x & 31; }
+IXG_DEV int warp_id() { return threadIdx.x >> 5; }
+
+// ----------------------------------------------- generator + predicate semantics
+// Bit-identical to oracle/ixoracle.c (ixo_mix64 / ixo_rand / ixo_pred_eval)
+// and to paper_2506_23058_b200/pred.py.
+IXG_DEV uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+IXG_DEV uint64_t rand_at(uint64_t seed_mixed, uint64_t i) {
+  return mix64(i * 0x9E3779B97F4A7C15ULL + seed_mixed);
+}
+__host__ __device__ inline uint64_t seed_mix_host(uint64_t seed) {
+  uint64_t z = seed ^ 0x5851F42D4C957F2DULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// The predicate is passed by value; kind is warp-uniform so the switch does
+// not diverge.  `p x` of the reference (oracle.py:327-329).
+IXG_DEV bool pred_eval(const ixg_pred& p, long long x) {
+  switch (p.kind) {
+    case IXG_PRED_LT: return x < p.thr;
+    case IXG_PRED_GT: return x > p.thr;
+    case IXG_PRED_LE: return x <= p.thr;
+    case IXG_PRED_GE: return x >= p.thr;
+    case IXG_PRED_EQ: return x == p.thr;
+    case IXG_PRED_NE: return x != p.thr;
+    case IXG_PRED_HASH: return (mix64((uint64_t)x ^ p.seed) >> 63) != 0;
+    case IXG_PRED_TRUE: return true;
+    default: return false;
+  }
+}
+
+// ------------------------------------------------------------ status word
+// First failure in the reference's sequential order: key =
+// [stmt:8][elem:48][site:8]; the smallest key wins (atomicMin).  The host
+// (errors.py) maps it back to OutOfBounds / NonIdempotentScatter.
+IXG_DEV unsigned long long status_key(int stmt, long long elem, int site) {
+  return ((unsigned long long)(stmt & 0xff) << 56) |
+         (((unsigned long long)elem & 0xffffffffffffULL) << 8) | (unsigned long long)(site & 0xff);
+}
+IXG_DEV void status_fail(ixg_status* st, int code, int stmt, long long elem, int site) {
+  if (!st) return;
+  atomicMin(&st->first, status_key(stmt, elem, site));
+  atomicOr(&st->codes, 1u << code);
+}
+
+// --------------------------------------------------------- vector helpers
+template <typename T>
+struct Vec;
+template <>
+struct Vec<int32_t> {
+  static constexpr int N = 4;
+  IXG_DEV static void unpack(int4 v, int32_t (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+  IXG_DEV static int4 pack(const int32_t (&o)[4]) { return make_int4(o[0], o[1], o[2], o[3]); }
+};
+template <>
+struct Vec<int64_t> {
+  static constexpr int N = 2;
+  IXG_DEV static void unpack(int4 v, int64_t (&o)[2]) {
+    o[0] = (int64_t)(((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x);
+    o[1] = (int64_t)(((uint64_t)(uint32_t)v.w << 32) | (uint32_t)v.z);
+  }
+  IXG_DEV static int4 pack(const int64_t (&o)[2]) {
+    return make_int4((int)(uint32_t)o[0], (int)(uint32_t)((uint64_t)o[0] >> 32), (int)(uint32_t)o[1],
+                     (int)(uint32_t)((uint64_t)o[1] >> 32));
+  }
+};
+
+template <>
+struct Vec<long long> {
+  static constexpr int N = 2;
+  IXG_DEV static void unpack(int4 v, long long (&o)[2]) {
+    o[0] = (long long)(((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x);
+    o[1] = (long long)(((uint64_t)(uint32_t)v.w << 32) | (uint32_t)v.z);
+  }
+  IXG_DEV static int4 pack(const long long (&o)[2]) {
+    return make_int4((int)(uint32_t)o[0], (int)(uint32_t)((uint64_t)o[0] >> 32), (int)(uint32_t)o[1],
+                     (int)(uint32_t)((uint64_t)o[1] >> 32));
+  }
+};
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? IXG_OK : IXG_CUDA_ERR + (int)e; }
+
+}  // namespace ixg

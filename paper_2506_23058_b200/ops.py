@@ -1,0 +1,364 @@
+"""Tensor-level API over libixgpu.so.
+
+Every function takes CUDA tensors (torch is used only for device memory and
+streams) and calls exactly one C-ABI entry point on the current stream.
+Data-dependent scalars come back as device tensors; nothing here
+synchronises the host unless the caller reads a result.  There is no CPU
+path: without libixgpu.so and an sm_100 device, the first call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib as L
+from .pred import Pred
+
+_DT = {torch.int32: L.I32, torch.int64: L.I64, torch.uint8: L.U8, torch.bool: L.U8, torch.float64: L.F64}
+
+
+def _lib():
+    return L.load(require_device=True)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else ctypes.c_void_p(0)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}") from None
+
+
+def _c_pred(p: Pred) -> L.ixg_pred:
+    if not isinstance(p, Pred):
+        raise TypeError(
+            "predicate arguments must be paper_2506_23058_b200.Pred descriptors "
+            f"(got {type(p).__name__}); opaque Python callables cannot run on the device"
+        )
+    return L.ixg_pred(p.kind, 0, p.thr, p.seed & ((1 << 64) - 1))
+
+
+def _contig(t: torch.Tensor) -> torch.Tensor:
+    t = t.contiguous()
+    if t.numel() and t.data_ptr() % 16:
+        t = t.clone()
+    return t
+
+
+# ------------------------------------------------------------------ workspace
+class Workspace:
+    """Per-(device, op) scratch, zeroed whenever its layout (op, n, m) changes.
+
+    The kernels leave their look-back state ready for the next launch
+    (epoch-tagged flags), so steady-state calls do no memset."""
+
+    def __init__(self):
+        self._bufs: dict = {}
+
+    def get(self, op: int, n: int, m: int, device) -> torch.Tensor:
+        need = int(_lib().ixg_ws_bytes(op, n, m))
+        key = (device.index if isinstance(device, torch.device) else device, op)
+        ent = self._bufs.get(key)
+        if ent is None or ent[1].numel() < need:
+            buf = torch.zeros(max(need, 4096), dtype=torch.uint8, device=device)
+            self._bufs[key] = ((n, m), buf)
+            return buf
+        if ent[0] != (n, m):
+            ent[1].zero_()
+            self._bufs[key] = ((n, m), ent[1])
+        return ent[1]
+
+
+WS = Workspace()
+
+
+def _ws(op: int, n: int, m: int, device):
+    buf = WS.get(op, n, m, device)
+    return ctypes.c_void_p(buf.data_ptr()), ctypes.c_size_t(buf.numel())
+
+
+# ------------------------------------------------------------------ status
+@dataclass
+class StatusView:
+    first: int
+    codes: int
+    flags: int
+
+    @property
+    def ok(self) -> bool:
+        return self.codes == 0
+
+    @property
+    def stmt(self) -> int:
+        return (self.first >> 56) & 0xFF
+
+    @property
+    def elem(self) -> int:
+        return (self.first >> 8) & 0xFFFFFFFFFFFF
+
+    @property
+    def site(self) -> int:
+        return self.first & 0xFF
+
+    @property
+    def narrow(self) -> bool:
+        return bool(self.flags & L.F_NARROW)
+
+
+class Status:
+    """Device-resident ixg_status (first failure in sequential order)."""
+
+    def __init__(self, device=None):
+        self.t = torch.empty(2, dtype=torch.int64, device=device or torch.device("cuda"))
+        self.reset()
+
+    def reset(self):
+        L.check(_lib().ixg_status_init(_ptr(self.t), _stream()), "ixg_status_init")
+
+    @property
+    def ptr(self):
+        return _ptr(self.t)
+
+    def read(self) -> StatusView:
+        h = self.t.cpu().numpy().view("uint64")
+        return StatusView(int(h[0]), int(h[1]) & 0xFFFFFFFF, int(h[1]) >> 32)
+
+
+# ------------------------------------------------------------------ builtins
+def scan_add(xs: torch.Tensor, ne: int = 0, exclusive: bool = False, out=None) -> torch.Tensor:
+    """scan (+) ne xs (oracle.py:281-293): int64 inclusive (or exclusive) sums."""
+    xs = _contig(xs)
+    n = xs.numel()
+    out = torch.empty(n, dtype=torch.int64, device=xs.device) if out is None else out
+    ws, wsb = _ws(L.OP_SCAN, n, 0, xs.device)
+    L.check(_lib().ixg_scan_add(_dt(xs), _ptr(xs), n, ne, int(exclusive), _ptr(out), ws, wsb, _stream()), "scan_add")
+    return out
+
+
+def segscan_add(flags: torch.Tensor, xs: torch.Tensor, want_flags: bool = False):
+    """sgmSum's 2-ary scan; returns values (and flags)."""
+    flags, xs = _contig(flags), _contig(xs)
+    n = flags.numel()
+    out_v = torch.empty(n, dtype=torch.int64, device=xs.device)
+    out_f = torch.empty(n, dtype=torch.uint8, device=xs.device) if want_flags else None
+    ws, wsb = _ws(L.OP_SEGSCAN, n, 0, xs.device)
+    L.check(
+        _lib().ixg_segscan_add(_dt(flags), _ptr(flags), _dt(xs), _ptr(xs), n, 0, 0, _ptr(out_v), _ptr(out_f), ws, wsb,
+                               _stream()),
+        "segscan_add",
+    )
+    return (out_v, out_f) if want_flags else out_v
+
+
+def scatter(out: torch.Tensor, is_: torch.Tensor, vs: torch.Tensor, site_bits: int, status: Status,
+            stmt: int = 0, site: int = 0) -> torch.Tensor:
+    """scatter into `out` in place (oracle.py:294-305); `out` already holds dst
+    unless the site's V_INIT bit is clear."""
+    is_, vs = _contig(is_), _contig(vs)
+    m = min(is_.numel(), vs.numel())
+    ws, wsb = _ws(L.OP_SCATTER, m, out.numel(), out.device)
+    L.check(
+        _lib().ixg_scatter(_dt(out), _ptr(out), out.numel(), _ptr(is_), is_.numel(), _ptr(vs), vs.numel(),
+                           site_bits, stmt, site, status.ptr, ws, wsb, _stream()),
+        "scatter",
+    )
+    return out
+
+
+def gather(arr: torch.Tensor, idx: torch.Tensor, site_bits: int, status: Status, stmt: int = 0, site: int = 0):
+    """out[i] = arr[idx[i]] with (V_BOUNDS) or without the bounds check."""
+    arr, idx = _contig(arr), _contig(idx)
+    out = torch.empty(idx.numel(), dtype=arr.dtype, device=idx.device)
+    if arr.numel() == 0 and idx.numel() and not (site_bits & L.V_BOUNDS):
+        raise ValueError("elided gather from an empty array")
+    L.check(
+        _lib().ixg_gather(_dt(arr), _ptr(arr), arr.numel(), _ptr(idx), idx.numel(), _ptr(out), site_bits, stmt, site,
+                          status.ptr, _stream()),
+        "gather",
+    )
+    return out
+
+
+def hist(op: int, ne: int, dlen: int, is_: torch.Tensor, vs: torch.Tensor) -> torch.Tensor:
+    """hist op ne dlen is vs (oracle.py:306-316)."""
+    is_, vs = _contig(is_), _contig(vs)
+    out = torch.empty(max(dlen, 0), dtype=torch.int64, device=is_.device)
+    L.check(
+        _lib().ixg_hist(op, ne, dlen, _ptr(is_), is_.numel(), _ptr(vs), vs.numel(), _ptr(out), _stream()), "hist"
+    )
+    return out
+
+
+def fill(n: int, v: int, dtype=torch.int64, device=None) -> torch.Tensor:
+    out = torch.empty(max(n, 0), dtype=dtype, device=device or torch.device("cuda"))
+    L.check(_lib().ixg_fill(_dt(out), _ptr(out), out.numel(), int(v), _stream()), "fill")
+    return out
+
+
+def iota(n: int, device=None) -> torch.Tensor:
+    out = torch.empty(max(n, 0), dtype=torch.int64, device=device or torch.device("cuda"))
+    L.check(_lib().ixg_iota(_ptr(out), out.numel(), _stream()), "iota")
+    return out
+
+
+# ------------------------------------------------------------------ pipelines
+def filter(xs: torch.Tensor, p: Pred, variant: int, status: Status, ys=None, d_count=None):
+    """filter p xs (corpus filter.ixl); returns (ys capacity buffer, device count)."""
+    xs = _contig(xs)
+    n = xs.numel()
+    ys = torch.empty(n, dtype=xs.dtype, device=xs.device) if ys is None else ys
+    d_count = torch.empty(1, dtype=torch.int64, device=xs.device) if d_count is None else d_count
+    ws, wsb = _ws(L.OP_FILTER, n, 0, xs.device)
+    cp = _c_pred(p)
+    L.check(
+        _lib().ixg_filter(_dt(xs), _ptr(xs), n, ctypes.byref(cp), _ptr(ys), _ptr(d_count), variant, status.ptr, ws, wsb,
+                          _stream()),
+        "filter",
+    )
+    return ys, d_count
+
+
+def filter_by(cs: torch.Tensor, xs: torch.Tensor, variant: int, status: Status):
+    """filter_by cs xs (maxmatching.ixl:1-9)."""
+    cs, xs = _contig(cs.to(torch.uint8)), _contig(xs)
+    n = xs.numel()
+    ys = torch.empty(n, dtype=xs.dtype, device=xs.device)
+    d_count = torch.empty(1, dtype=torch.int64, device=xs.device)
+    ws, wsb = _ws(L.OP_FILTER, n, 0, xs.device)
+    L.check(
+        _lib().ixg_filter_by(_dt(xs), _ptr(cs), _ptr(xs), n, _ptr(ys), _ptr(d_count), variant, status.ptr, ws, wsb,
+                             _stream()),
+        "filter_by",
+    )
+    return ys, d_count
+
+
+def partition2(xs: torch.Tensor, p: Pred, variant: int, status: Status, ys=None, d_nt=None):
+    """partition2 p xs (corpus partition2.ixl); returns (ys, device num_true)."""
+    xs = _contig(xs)
+    n = xs.numel()
+    ys = torch.empty(n, dtype=xs.dtype, device=xs.device) if ys is None else ys
+    d_nt = torch.empty(1, dtype=torch.int64, device=xs.device) if d_nt is None else d_nt
+    ws, wsb = _ws(L.OP_PARTITION2, n, 0, xs.device)
+    cp = _c_pred(p)
+    L.check(
+        _lib().ixg_partition2(_dt(xs), _ptr(xs), n, ctypes.byref(cp), _ptr(ys), _ptr(d_nt), variant, status.ptr, ws,
+                              wsb, _stream()),
+        "partition2",
+    )
+    return ys, d_nt
+
+
+def partition3(xs: torch.Tensor, p: Pred, q: Pred, variant: int, status: Status):
+    """partition3 p q xs (corpus partition3.ixl); returns (ys, device (m1, m2))."""
+    xs = _contig(xs)
+    n = xs.numel()
+    ys = torch.empty(n, dtype=xs.dtype, device=xs.device)
+    d_m = torch.empty(2, dtype=torch.int64, device=xs.device)
+    ws, wsb = _ws(L.OP_PARTITION3, n, 0, xs.device)
+    cp, cq = _c_pred(p), _c_pred(q)
+    L.check(
+        _lib().ixg_partition3(_dt(xs), _ptr(xs), n, ctypes.byref(cp), ctypes.byref(cq), _ptr(ys), _ptr(d_m), variant,
+                              status.ptr, ws, wsb, _stream()),
+        "partition3",
+    )
+    return ys, d_m
+
+
+def c2(xs: torch.Tensor, p: Pred, shape: torch.Tensor, variant: int, status: Status, z_dtype=None, ys=None, zs=None,
+       d_k=None):
+    """c2 p xs shape = filter + mkFlags + sgmSum (corpus/c2_filter_sgmsum.ixl)."""
+    xs, shape = _contig(xs), _contig(shape.to(torch.int64))
+    n, m = xs.numel(), shape.numel()
+    z_dtype = z_dtype or xs.dtype
+    ys = torch.empty(n, dtype=xs.dtype, device=xs.device) if ys is None else ys
+    zs = torch.empty(n, dtype=z_dtype, device=xs.device) if zs is None else zs
+    d_k = torch.empty(1, dtype=torch.int64, device=xs.device) if d_k is None else d_k
+    ws, wsb = _ws(L.OP_C2, n, m, xs.device)
+    cp = _c_pred(p)
+    L.check(
+        _lib().ixg_c2(_dt(xs), _ptr(xs), n, ctypes.byref(cp), _ptr(shape), m, _ptr(ys), _dt(zs), _ptr(zs), _ptr(d_k),
+                      variant, status.ptr, ws, wsb, _stream()),
+        "c2",
+    )
+    return ys, zs, d_k
+
+
+def mksgmdescr(shape: torch.Tensor, xs: torch.Tensor, variant: int, status: Status):
+    """mkSgmDescr shape xs (corpus mksgmdescr.ixl).  Two calls: the first
+    computes len = sum shape on the device, the second scatters into
+    `replicate len 0` (the result length is data-dependent)."""
+    shape, xs = _contig(shape), _contig(xs)
+    m = shape.numel()
+    d_len = torch.empty(1, dtype=torch.int64, device=xs.device)
+    ws, wsb = _ws(L.OP_MKSGMDESCR, 0, m, xs.device)
+    lib = _lib()
+    L.check(lib.ixg_mksgmdescr(_ptr(shape), _ptr(xs), m, _ptr(None), 0, _ptr(d_len), variant, status.ptr, ws, wsb,
+                               _stream()), "mksgmdescr")
+    cap = int(d_len.item())
+    res = torch.empty(max(cap, 0), dtype=torch.int64, device=xs.device)
+    if cap > 0:
+        ws, wsb = _ws(L.OP_MKSGMDESCR, cap, m, xs.device)
+        L.check(lib.ixg_mksgmdescr(_ptr(shape), _ptr(xs), m, _ptr(res), cap, _ptr(d_len), variant, status.ptr, ws,
+                                   wsb, _stream()), "mksgmdescr")
+    return res
+
+
+def csr_gather(x: torch.Tensor, values: torch.Tensor, indices: torch.Tensor, variant: int, status: Status, out=None):
+    """map2 (\\v c -> v * x[c]) values indices (corpus/c4_csr_gather.ixl)."""
+    x, values, indices = _contig(x), _contig(values), _contig(indices)
+    out = torch.empty(values.numel(), dtype=values.dtype, device=values.device) if out is None else out
+    L.check(
+        _lib().ixg_csr_gather(_dt(values), _ptr(x), x.numel(), _ptr(values), _ptr(indices), values.numel(), _ptr(out),
+                              variant, status.ptr, _stream()),
+        "csr_gather",
+    )
+    return out
+
+
+def kmeans_ker(rows: torch.Tensor, pointers, cluster, values, indices, variant: int, status: Status):
+    """kmeans_ker for each row in `rows` (corpus kmeans_ker.ixl)."""
+    rows, pointers, indices = _contig(rows), _contig(pointers), _contig(indices)
+    cluster, values = _contig(cluster.to(torch.float64)), _contig(values.to(torch.float64))
+    out = torch.empty(rows.numel(), dtype=torch.float64, device=rows.device)
+    L.check(
+        _lib().ixg_kmeans_ker(_ptr(rows), rows.numel(), _ptr(pointers), pointers.numel(), _ptr(cluster),
+                              cluster.numel(), _ptr(values), _ptr(indices), indices.numel(), _ptr(out), variant,
+                              status.ptr, _stream()),
+        "kmeans_ker",
+    )
+    return out
+
+
+def eq_gather(H: torch.Tensor, es: torch.Tensor, is_: torch.Tensor, variant: int, status: Status, stmt: int = 0):
+    """cs[i] = H[es[i]] == is[i] (maxmatching.ixl:18)."""
+    H, es, is_ = _contig(H), _contig(es), _contig(is_)
+    cs = torch.empty(es.numel(), dtype=torch.uint8, device=es.device)
+    L.check(
+        _lib().ixg_eq_gather(_ptr(H), H.numel(), _ptr(es), _ptr(is_), es.numel(), _ptr(cs), variant, stmt, status.ptr,
+                             _stream()),
+        "eq_gather",
+    )
+    return cs
+
+
+def gen_uniform(n: int, lo: int, hi: int, seed: int, dtype=torch.int32, offset: int = 0, device=None, out=None):
+    """Device-side counter-based input, identical to gen.uniform()."""
+    out = torch.empty(n, dtype=dtype, device=device or torch.device("cuda")) if out is None else out
+    L.check(_lib().ixg_gen_uniform(_dt(out), _ptr(out), n, lo, hi, seed, offset, _stream()), "gen_uniform")
+    return out
+
+
+def launch_count() -> int:
+    return int(_lib().ixg_launch_count())

@@ -1,0 +1,206 @@
+"""Selector: the reference verifier's proved obligations -> kernel variant
+bits per source site.
+
+The verifier (``ixverify.infer.Analyzer``, /root/reference/pkg/src/ixverify/
+infer.py:172-226) records an ``Obligation(kind, pos, text, proved)``
+(infer.py:132-137) for every indexing site (two ``bounds`` obligations,
+``_bounds_check`` infer.py:612-632) and every scatter (one
+``scatter-safety`` obligation via Ss1/Ss2/Ss3, infer.py:1091-1100,
+1129-1143).  ``analyze_program`` stops at the first failure, so the
+selector runs ``Analyzer.analyze_fun`` per definition itself and keeps the
+partial obligation list of a failing definition.
+
+Per site:
+  * bounds site  -> ELIDED iff every obligation recorded at its pos is proved;
+  * scatter site -> the idempotence check is ELIDED iff scatter-safety is
+    proved; destination init + OOB test are ELIDED only when the result is
+    the Sc1 bijection ``for i < n . true => x[is^-1[i]]`` (detected with
+    ``props._inv_pattern`` on the bound result, props.py:561-578,
+    infer.py:1101-1122) -- Sc1 is not itself an Obligation.
+  * unrecorded sites (after a failure, or in callers of a failed callee) are
+    CHECKED.
+
+The verifier only exists where the reference is installed; the verdicts for
+the bundled corpus are frozen in ``data/selection.json`` (keyed by
+``ir.fingerprint``) so the GPU box can select without it.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+from dataclasses import asdict, dataclass, field
+from typing import Optional
+
+from . import _lib as L
+from . import ir
+
+DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
+REFERENCE_SRC = os.environ.get("IXVERIFY_SRC", "/root/reference/pkg/src")
+
+
+@dataclass
+class SiteVerdict:
+    kind: str  # "bounds" | "scatter-safety"
+    pos: tuple
+    text: str
+    recorded: bool = False
+    proved: bool = False
+    rule: str = ""
+    sc1: bool = False
+
+    @property
+    def bits(self) -> int:
+        if self.kind == "bounds":
+            return 0 if (self.recorded and self.proved) else L.V_BOUNDS
+        b = 0
+        if not (self.recorded and self.proved):
+            b |= L.V_CONFLICT
+        if not self.sc1:
+            b |= L.V_INIT
+        return b
+
+
+@dataclass
+class FunSelection:
+    name: str
+    fingerprint: str
+    status: str
+    sites: list = field(default_factory=list)
+
+    def bits(self, ordinal: int) -> int:
+        return self.sites[ordinal].bits
+
+    def by_pos(self, pos) -> Optional[SiteVerdict]:
+        for s in self.sites:
+            if tuple(s.pos) == tuple(pos):
+                return s
+        return None
+
+    def to_json(self):
+        d = asdict(self)
+        for s in d["sites"]:
+            s["pos"] = list(s["pos"])
+        return d
+
+    @classmethod
+    def from_json(cls, d):
+        sites = [SiteVerdict(**{**s, "pos": tuple(s["pos"])}) for s in d["sites"]]
+        return cls(d["name"], d["fingerprint"], d["status"], sites)
+
+
+@dataclass
+class Selection:
+    funcs: dict
+
+    def __getitem__(self, name) -> FunSelection:
+        return self.funcs[name]
+
+    def to_json(self):
+        return {k: v.to_json() for k, v in self.funcs.items()}
+
+
+def _import_reference():
+    if REFERENCE_SRC not in sys.path and os.path.isdir(REFERENCE_SRC):
+        sys.path.insert(0, REFERENCE_SRC)
+    import ixverify.infer as infer  # noqa: F401
+    import ixverify.props as props  # noqa: F401
+
+    return sys.modules["ixverify.infer"], sys.modules["ixverify.props"]
+
+
+def reference_available() -> bool:
+    try:
+        _import_reference()
+        return True
+    except Exception:
+        return False
+
+
+def _scatter_result_names(fundef):
+    """pos of each scatter App -> the let-bound name of its result."""
+    out = {}
+
+    def walk(e):
+        if ir.kind(e) == "Let" and len(e.names) == 1:
+            r = e.rhs
+            if ir.kind(r) == "App" and ir.kind(r.fun) == "VarE" and r.fun.name == "scatter":
+                out[tuple(r.pos)] = e.names[0]
+        for c in ir.children(e):
+            walk(c)
+
+    walk(fundef.body)
+    return out
+
+
+def select(program, max_rewrites: int = 1000) -> Selection:
+    """Run the reference verifier per definition and derive site verdicts.
+    `program` must be the reference's normalized Program."""
+    infer, props = _import_reference()
+    a = infer.Analyzer(program, max_rewrites=max_rewrites)
+    funcs = {}
+    for f in program.defs:
+        status = "verified"
+        try:
+            a.infos[f.name] = a.analyze_fun(f)
+        except infer.InferError as exc:  # keep the partial obligation list
+            status = f"failed: {type(exc).__name__}: {exc}"
+        obls = list(getattr(a, "obligations", []))
+        info = a.infos.get(f.name)
+        names = _scatter_result_names(f)
+        sites = []
+        for kind, pos, node in ir.sites(f):
+            rec = [o for o in obls if tuple(o.pos) == pos and o.kind == kind]
+            v = SiteVerdict(kind, pos, ir.expr_str(node), recorded=bool(rec), proved=bool(rec) and all(o.proved for o in rec))
+            if kind == "scatter-safety" and rec:
+                v.rule = rec[0].text.replace("scatter via ", "").replace("scatter", "").strip()
+                nm = names.get(pos)
+                if v.proved and info is not None and nm in info.gamma:
+                    try:
+                        v.sc1 = props._inv_pattern(info.gamma[nm]) is not None
+                    except Exception:
+                        v.sc1 = False
+            sites.append(v)
+        funcs[f.name] = FunSelection(f.name, ir.fingerprint(f), status, sites)
+    return Selection(funcs)
+
+
+# ----------------------------------------------------------------- frozen
+_FROZEN = None
+
+
+def frozen() -> dict:
+    """fingerprint -> FunSelection for the bundled corpus (data/selection.json)."""
+    global _FROZEN
+    if _FROZEN is None:
+        path = os.path.join(DATA, "selection.json")
+        _FROZEN = {}
+        if os.path.exists(path):
+            with open(path) as fh:
+                for d in json.load(fh).values():
+                    fs = FunSelection.from_json(d)
+                    _FROZEN[fs.fingerprint] = fs
+    return _FROZEN
+
+
+def checked_selection(fundef) -> FunSelection:
+    """Every site CHECKED: the reference interpreter's own behaviour."""
+    sites = [SiteVerdict(k, pos, ir.expr_str(n)) for k, pos, n in ir.sites(fundef)]
+    return FunSelection(fundef.name, ir.fingerprint(fundef), "checked (no verdict)", sites)
+
+
+def selection_for(program, fundef, live: bool = True) -> FunSelection:
+    """Verdicts for one function: live verifier when importable, else the
+    frozen corpus table by fingerprint, else all CHECKED."""
+    fp = ir.fingerprint(fundef)
+    fz = frozen().get(fp)
+    if fz is not None:
+        # positions may differ from the frozen source: re-key by ordinal
+        cur = ir.sites(fundef)
+        if len(cur) == len(fz.sites):
+            sites = [SiteVerdict(**{**asdict(s), "pos": pos}) for s, (_, pos, _) in zip(fz.sites, cur)]
+            return FunSelection(fundef.name, fp, fz.status, sites)
+    if live and reference_available() and type(program).__module__.startswith("ixverify"):
+        return select(program)[fundef.name]
+    return checked_selection(fundef)

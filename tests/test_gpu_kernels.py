@@ -1,0 +1,339 @@
+"""GPU parity: every libixgpu.so entry point against the CPU oracle
+(oracle/ixoracle.c, itself pinned to the Python reference by
+tests/test_oracle_golden.py) on the same seeded inputs.  Integer work, so
+the bar is bit-exact."""
+
+import numpy as np
+import pytest
+
+from oracle import ixoracle as O
+from paper_2506_23058_b200 import _lib as L
+from paper_2506_23058_b200 import gen
+from paper_2506_23058_b200.pred import Pred
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [0, 1, 5, 4095, 4096, 4097, 12_345, 300_001]
+VARIANTS = [L.VARIANT_ELIDED, L.VARIANT_CHECKED]
+PREDS = [Pred.lt(0), Pred.ge(3), Pred.hash(0xABCDEF), Pred(7)]  # 7 = TRUE
+
+
+def _t(a, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_partition2(cuda, n, dtype, variant):
+    from paper_2506_23058_b200 import ops
+
+    xs = gen.uniform(n + 1, n, -50, 50, dtype)
+    for p in PREDS:
+        nt, ys = O.partition2(p, xs)
+        st = ops.Status(cuda)
+        gys, dnt = ops.partition2(_t(xs, cuda), p, variant, st)
+        assert int(dnt.item()) == nt
+        assert np.array_equal(_np(gys).astype(np.int64), ys)
+        assert st.read().ok
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_partition3(cuda, n, dtype, variant):
+    from paper_2506_23058_b200 import ops
+
+    xs = gen.uniform(n + 2, n, -50, 50, dtype)
+    p, q = Pred.lt(-10), Pred.hash(99)
+    m1, m2, ys = O.partition3(p, q, xs)
+    st = ops.Status(cuda)
+    gys, dm = ops.partition3(_t(xs, cuda), p, q, variant, st)
+    assert _np(dm).tolist() == [m1, m2]
+    assert np.array_equal(_np(gys).astype(np.int64), ys)
+    assert st.read().ok
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_filter(cuda, n, dtype, variant):
+    from paper_2506_23058_b200 import ops
+
+    xs = gen.uniform(n + 3, n, -1000, 1000, dtype)
+    for p in PREDS:
+        want = O.filter_(p, xs)
+        st = ops.Status(cuda)
+        gys, dk = ops.filter(_t(xs, cuda), p, variant, st)
+        k = int(dk.item())
+        assert k == len(want)
+        assert np.array_equal(_np(gys)[:k].astype(np.int64), want)
+        assert st.read().ok
+    cs = (gen.uniform(n + 4, n, 0, 3, np.int64) == 0).astype(np.uint8)
+    want = O.filter_by(cs, xs)
+    st = ops.Status(cuda)
+    gys, dk = ops.filter_by(_t(cs, cuda), _t(xs, cuda), variant, st)
+    k = int(dk.item())
+    assert np.array_equal(_np(gys)[:k].astype(np.int64), want)
+
+
+@pytest.mark.parametrize("n", SIZES + [1 << 21])
+@pytest.mark.parametrize("zdt", ["i32", "i64"])
+@pytest.mark.parametrize("variant", VARIANTS + [0x2000])  # 0x2000: only mkFlags' conflict check on
+def test_c2(cuda, n, zdt, variant):
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    xs = gen.uniform(n + 5, n, -128, 127, np.int32)
+    p = Pred.ge(0)
+    k = int((xs >= 0).sum())
+    for m in (0, 1, 7, 1000):
+        shape = gen.segment_shape(m + n, m, k) if m else np.zeros(0, np.int64)
+        want_ys, want_zs = O.c2(p, xs, shape)
+        st = ops.Status(cuda)
+        zt = torch.int32 if zdt == "i32" else torch.int64
+        ys, zs, dk = ops.c2(_t(xs, cuda), p, _t(shape, cuda), variant, st, z_dtype=zt)
+        kk = int(dk.item())
+        assert kk == len(want_ys)
+        assert np.array_equal(_np(ys)[:kk].astype(np.int64), want_ys)
+        assert np.array_equal(_np(zs)[:kk].astype(np.int64), want_zs)
+        assert st.read().ok
+
+
+def test_c2_sum_below_k(cuda):
+    """shape sums to less / more than k: flags past k are dropped (OOB)."""
+    from paper_2506_23058_b200 import ops
+
+    n = 20_000
+    xs = gen.uniform(11, n, -128, 127, np.int32)
+    p = Pred.ge(0)
+    k = int((xs >= 0).sum())
+    for tot in (k // 2, 3 * k):
+        shape = gen.segment_shape(12, 100, tot)
+        want_ys, want_zs = O.c2(p, xs, shape)
+        for variant in VARIANTS:
+            st = ops.Status(cuda)
+            ys, zs, dk = ops.c2(_t(xs, cuda), p, _t(shape, cuda), variant, st)
+            kk = int(dk.item())
+            assert np.array_equal(_np(zs)[:kk].astype(np.int64), want_zs)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_scan_add(cuda, n):
+    from paper_2506_23058_b200 import ops
+
+    for dtype in (np.int32, np.int64, np.uint8):
+        xs = gen.uniform(n, n, 0, 200, np.int64).astype(dtype)
+        for ne in (0, 5, -7):
+            want = O.scan_add(xs, ne)
+            got = _np(ops.scan_add(_t(xs, cuda), ne))
+            assert np.array_equal(got, want)
+            got = _np(ops.scan_add(_t(xs, cuda), ne, exclusive=True))
+            assert np.array_equal(got, want - xs.astype(np.int64))
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_segscan(cuda, n):
+    from paper_2506_23058_b200 import ops
+
+    flags = (gen.uniform(n + 9, n, 0, 9, np.int64) == 0).astype(np.uint8)
+    xs = gen.uniform(n + 10, n, -100, 100, np.int64)
+    want = O.sgmsum(flags, xs)
+    assert np.array_equal(_np(ops.segscan_add(_t(flags, cuda), _t(xs, cuda))), want)
+
+
+@pytest.mark.parametrize("n", [0, 1, 1000, 1 << 20])
+def test_scatter_perm(cuda, n):
+    """Injective scatter (a partition2 permutation): all variants agree."""
+    from paper_2506_23058_b200 import ops
+
+    xs = gen.uniform(21, n, -(1 << 31), (1 << 31) - 1, np.int64)
+    is_ = np.argsort(np.argsort(xs, kind="stable"), kind="stable").astype(np.int64)
+    vs = gen.uniform(22, n, -1000, 1000, np.int64)
+    dst = np.zeros(n, np.int64)
+    want = O.scatter(dst, is_, vs)
+    for bits in (0, L.V_INIT, L.V_CONFLICT | L.V_INIT):
+        st = ops.Status(cuda)
+        out = _t(dst, cuda).clone()
+        ops.scatter(out, _t(is_, cuda), _t(vs, cuda), bits, st)
+        assert np.array_equal(_np(out), want)
+        assert st.read().ok
+
+
+def test_scatter_semantics(cuda):
+    """Appendix A of SURVEY.md: zip truncation, OOB ignore, equal dups, conflicts."""
+    from paper_2506_23058_b200 import ops
+
+    cases = [
+        ([0, 0, 0], [0, 1, 2], [7, 8], [7, 8, 0]),
+        ([0, 0, 0], [-1, 3, 2, 100], [5, 6, 9, 1], [0, 0, 9]),
+        ([0, 0, 0], [1, 1], [5, 5], [0, 5, 0]),
+        ([0, 0], [5, 5], [1, 2], [0, 0]),  # conflicting but out of bounds
+    ]
+    for dst, is_, vs, want in cases:
+        st = ops.Status(cuda)
+        out = _t(np.array(dst, np.int64), cuda)
+        ops.scatter(out, _t(np.array(is_, np.int64), cuda), _t(np.array(vs, np.int64), cuda),
+                    L.V_CONFLICT | L.V_INIT, st, stmt=0, site=3)
+        assert _np(out).tolist() == want
+        assert st.read().ok
+    st = ops.Status(cuda)
+    out = _t(np.zeros(4, np.int64), cuda)
+    ops.scatter(out, _t(np.array([0, 2, 0], np.int64), cuda), _t(np.array([1, 2, 3], np.int64), cuda),
+                L.V_CONFLICT | L.V_INIT, st, stmt=0, site=3)
+    s = st.read()
+    assert not s.ok and s.codes & (1 << L.CONFLICT) and s.site == 3
+    # large random scatter with one injected conflict
+    n = 1 << 20
+    is_ = np.random.default_rng(0).permutation(n).astype(np.int64)
+    vs = np.arange(n, dtype=np.int64)
+    is_[n // 2] = is_[n // 3]
+    st = ops.Status(cuda)
+    out = _t(np.zeros(n, np.int64), cuda)
+    ops.scatter(out, _t(is_, cuda), _t(vs, cuda), L.V_CONFLICT | L.V_INIT, st)
+    assert not st.read().ok
+    # same duplicate, equal values: no conflict, same result as the oracle
+    vs2 = vs.copy()
+    vs2[n // 2] = vs2[n // 3]
+    st = ops.Status(cuda)
+    out = _t(np.zeros(n, np.int64), cuda)
+    ops.scatter(out, _t(is_, cuda), _t(vs2, cuda), L.V_CONFLICT | L.V_INIT, st)
+    assert st.read().ok
+    assert np.array_equal(_np(out), O.scatter(np.zeros(n, np.int64), is_, vs2))
+
+
+def test_gather_checked(cuda):
+    from paper_2506_23058_b200 import ops
+
+    arr = np.arange(10, dtype=np.int64) * 3
+    idx = np.array([0, 9, 4, 10, 2, -1], np.int64)
+    st = ops.Status(cuda)
+    ops.gather(_t(arr, cuda), _t(idx, cuda), L.V_BOUNDS, st, stmt=2, site=4)
+    s = st.read()
+    assert not s.ok and s.elem == 3 and s.site == 4 and s.stmt == 2
+    idx = np.array([0, 9, 4, 2], np.int64)
+    for bits in (0, L.V_BOUNDS):
+        st = ops.Status(cuda)
+        got = ops.gather(_t(arr, cuda), _t(idx, cuda), bits, st)
+        assert _np(got).tolist() == O.gather(arr, idx).tolist()
+        assert st.read().ok
+
+
+def test_hist(cuda):
+    from paper_2506_23058_b200 import ops
+
+    assert _np(ops.hist(L.HIST_MIN, 99, 3, _t(np.array([0, 0, 2, 5, -1]), cuda),
+                        _t(np.array([4, 2, 7, 1, 1]), cuda))).tolist() == [2, 99, 7]
+    n = 100_000
+    is_ = gen.uniform(1, n, -5, 1000, np.int64)
+    vs = gen.uniform(2, n, -(1 << 40), 1 << 40, np.int64)
+    for op in (L.HIST_MIN, L.HIST_MAX, L.HIST_ADD):
+        want = O.hist(op, 7, 990, is_, vs)
+        assert np.array_equal(_np(ops.hist(op, 7, 990, _t(is_, cuda), _t(vs, cuda))), want)
+    assert ops.hist(L.HIST_MIN, 1, -3, _t(is_, cuda), _t(vs, cuda)).numel() == 0
+
+
+@pytest.mark.parametrize("nnz", [0, 1, 7, 4096, 1_000_003])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_csr_gather(cuda, nnz, dtype):
+    from paper_2506_23058_b200 import ops
+
+    ncols = 5000
+    x = gen.uniform(31, ncols, -(1 << 15), (1 << 15) - 1, dtype)
+    vals = gen.uniform(32, nnz, -(1 << 15), (1 << 15) - 1, dtype)
+    idx = gen.uniform(33, nnz, 0, ncols - 1, np.int64)
+    want = O.csrg(x, vals, idx)
+    for variant in VARIANTS:
+        st = ops.Status(cuda)
+        got = ops.csr_gather(_t(x, cuda), _t(vals, cuda), _t(idx, cuda), variant, st)
+        assert np.array_equal(_np(got).astype(np.int64), want)
+        assert st.read().ok
+    if nnz > 10:
+        bad = idx.copy()
+        bad[nnz // 2] = ncols
+        bad[nnz - 2] = -4
+        st = ops.Status(cuda)
+        ops.csr_gather(_t(x, cuda), _t(vals, cuda), _t(bad, cuda), L.VARIANT_CHECKED, st)
+        s = st.read()
+        assert not s.ok and s.elem == nnz // 2
+
+
+def test_kmeans(cuda):
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    rng = np.random.default_rng(5)
+    nrows, ncols = 300, 50
+    lens = rng.integers(0, 40, nrows)
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(ptr[-1])
+    vals = np.round(rng.uniform(-4, 9, nnz), 2)
+    cols = rng.integers(0, ncols, nnz).astype(np.int64)
+    cl = np.round(rng.uniform(-4, 9, ncols), 2)
+    rows = np.arange(nrows, dtype=np.int64)
+    st = ops.Status(cuda)
+    got = _np(ops.kmeans_ker(_t(rows, cuda), _t(ptr, cuda), torch.from_numpy(cl).to(cuda),
+                             torch.from_numpy(vals).to(cuda), _t(cols, cuda), L.VARIANT_CHECKED, st))
+    want = np.array([O.kmeans_ker(int(r), ptr, cl, vals, cols) for r in rows])
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))  # bit-exact f64
+    st = ops.Status(cuda)
+    ops.kmeans_ker(_t(np.array([nrows], np.int64), cuda), _t(ptr, cuda), torch.from_numpy(cl).to(cuda),
+                   torch.from_numpy(vals).to(cuda), _t(cols, cuda), L.VARIANT_CHECKED, st)
+    s = st.read()
+    assert not s.ok and s.site == 1  # pointers[row+1] fails first
+
+
+def test_mksgmdescr(cuda):
+    from paper_2506_23058_b200 import ops
+
+    for shape, xs in [([0, 2, 1, 0, 3], [1, 2, 3, 4, 5]), ([], []), ([0, 0], [4, 5])]:
+        st = ops.Status(cuda)
+        got = ops.mksgmdescr(_t(np.array(shape, np.int64), cuda), _t(np.array(xs, np.int64), cuda),
+                             L.VARIANT_CHECKED, st)
+        assert _np(got).tolist() == O.mksgmdescr(shape, xs).tolist()
+    m = 10_000
+    shape = gen.uniform(3, m, 0, 9, np.int64)
+    xs = gen.uniform(4, m, -9, 9, np.int64)
+    st = ops.Status(cuda)
+    got = ops.mksgmdescr(_t(shape, cuda), _t(xs, cuda), L.VARIANT_CHECKED, st)
+    assert np.array_equal(_np(got), O.mksgmdescr(shape, xs))
+    # negative shapes violate the precondition; the checked scatter must flag conflicts
+    shape = np.array([3, -3, 4, 1], np.int64)
+    xs = np.array([1, 2, 3, 4], np.int64)
+    with pytest.raises(O.OracleFail):
+        O.mksgmdescr(shape, xs)
+    st = ops.Status(cuda)
+    ops.mksgmdescr(_t(shape, cuda), _t(xs, cuda), L.VARIANT_CHECKED, st)
+    assert st.read().codes & (1 << L.CONFLICT)
+
+
+def test_gen_uniform(cuda):
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    for dtype, tdt, lo, hi in [(np.int32, torch.int32, -(1 << 31), (1 << 31) - 1), (np.int64, torch.int64, -5, 17),
+                               (np.int32, torch.int32, -128, 127)]:
+        got = _np(ops.gen_uniform(100_003, lo, hi, 42, dtype=tdt, offset=77, device=cuda))
+        assert np.array_equal(got, gen.uniform(42, 100_003, lo, hi, dtype, offset=77))
+
+
+def test_workspace_reuse(cuda):
+    """Self-resetting look-back state: many launches, changing sizes."""
+    from paper_2506_23058_b200 import ops
+
+    for rep in range(40):
+        n = [5000, 123_456, 4096, 1][rep % 4]
+        xs = gen.uniform(rep, n, -9, 9, np.int32)
+        st = ops.Status(cuda)
+        gys, dnt = ops.partition2(_t(xs, cuda), Pred.lt(0), L.VARIANT_ELIDED, st)
+        nt, ys = O.partition2(Pred.lt(0), xs)
+        assert int(dnt.item()) == nt and np.array_equal(_np(gys).astype(np.int64), ys)
