@@ -119,6 +119,7 @@ typedef struct ixg_status {
 #define IXG_OP_PARTITION3 6
 #define IXG_OP_C2 7
 #define IXG_OP_MKSGMDESCR 8
+#define IXG_OP_MKFLAGS 9
 
 /* ---- library / device --------------------------------------------------- */
 int ixg_version(void);
@@ -228,6 +229,52 @@ int ixg_kmeans_ker(const int64_t* rows, int64_t nrows, const int64_t* pointers, 
  * site 0 = H[i]. */
 int ixg_eq_gather(const int64_t* H, int64_t hlen, const int64_t* es, const int64_t* is, int64_t n,
                   uint8_t* cs, uint32_t variant, int stmt, ixg_status* st, void* stream);
+
+/* mkFlags (corpus/c2_filter_sgmsum.ixl; sites 0 = shape[i-1], 1 = scatter):
+ * flags[0..k) = 0, then 1 at the exclusive scan of shape for non-empty
+ * segments (scatter of `replicate m 1`). */
+int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint32_t variant, ixg_status* st,
+                void* ws, size_t ws_bytes, void* stream);
+
+/* ---- map with a compiled lambda (oracle.py:274-280) ----------------------
+ * The host compiles the lambda body (paper_2506_23058_b200/vm.py) into a
+ * short register program; the kernel interprets it per element, all
+ * elements in parallel.  Registers are int64 (bools are 0/1).  Indexing
+ * (IXG_VM_IDX) is bounds-checked when its site bit is set, failing at
+ * (stmt, element, site) in `st` exactly like the reference's IndexE. */
+#define IXG_VM_MAX_INSN 96
+#define IXG_VM_MAX_IN 8
+#define IXG_VM_MAX_OUT 4
+#define IXG_VM_MAX_PRED 4
+#define IXG_VM_REGS 24
+enum {
+  IXG_VM_HALT = 0,
+  IXG_VM_IN,     /* r[dst] = in[a][i]                                  */
+  IXG_VM_CONST,  /* r[dst] = imm                                       */
+  IXG_VM_ADD, IXG_VM_SUB, IXG_VM_MUL,
+  IXG_VM_EQ, IXG_VM_NE, IXG_VM_LT, IXG_VM_LE, IXG_VM_GT, IXG_VM_GE,
+  IXG_VM_NOT,    /* r[dst] = !r[a]                                     */
+  IXG_VM_MOV,    /* r[dst] = r[a]                                      */
+  IXG_VM_JZ,     /* if r[a] == 0: pc = c                               */
+  IXG_VM_JMP,    /* pc = c                                             */
+  IXG_VM_IDX,    /* r[dst] = in[b][r[a]]; site c; imm != 0: check       */
+  IXG_VM_PRED,   /* r[dst] = pred[b](r[a])                             */
+  IXG_VM_OUT,    /* out[b][i] = r[a]                                   */
+  IXG_VM_LEN,    /* r[dst] = len(in[b])                                */
+  IXG_VM_IDX_F64 /* reserved                                           */
+};
+typedef struct ixg_vm_insn {
+  int32_t op, dst, a, b, c, pad;
+  int64_t imm;
+} ixg_vm_insn;
+typedef struct ixg_array {
+  const void* ptr;
+  int64_t len;
+  int32_t dt;
+  int32_t pad;
+} ixg_array;
+int ixg_map(const ixg_vm_insn* prog, int ninsn, const ixg_array* ins, int nins, const ixg_array* outs, int nouts,
+            const ixg_pred* preds, int npreds, int64_t n, int stmt, ixg_status* st, void* stream);
 
 /* ---- measurement: CUDA events recorded on the launching stream around
  * every launch of one kernel family (bench.py's roofline numerator). ------ */

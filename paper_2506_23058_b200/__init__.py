@@ -9,4 +9,18 @@ CHECKED or ELIDED kernel variant from the reference verifier's obligations.
 
 from .pred import Pred  # noqa: F401
 
-__all__ = ["Pred"]
+
+def __getattr__(name):
+    # lazy: importing the package must not require torch or a GPU
+    if name in ("eval_program", "Interp"):
+        from . import executor
+
+        return getattr(executor, name)
+    if name == "select":
+        from .select import select
+
+        return select
+    raise AttributeError(name)
+
+
+__all__ = ["Pred", "eval_program", "Interp", "select"]

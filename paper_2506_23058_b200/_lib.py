@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libixgpu.so")
+LIB_PATH = os.environ.get("IXGPU_LIB") or os.path.join(_HERE, "libixgpu.so")  # IXGPU_LIB: dev A/B builds
 
 # status / return codes (include/ixgpu.h)
 OK, OOB, CONFLICT, LENGTH, BADARG, NOMEM, OVERFLOW, NODEVICE = 0, 1, 2, 3, 4, 5, 6, 7
@@ -23,11 +23,25 @@ VARIANT_CHECKED = 0x77777777
 VARIANT_ELIDED = 0
 F_DUP, F_NARROW = 1, 2
 HIST_MIN, HIST_MAX, HIST_ADD = 0, 1, 2
-OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR = range(1, 9)
+OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR, OP_MKFLAGS = range(1, 10)
 
 
 class ixg_pred(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32), ("thr", ctypes.c_int64), ("seed", ctypes.c_uint64)]
+
+
+class ixg_vm_insn(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("dst", ctypes.c_int32), ("a", ctypes.c_int32), ("b", ctypes.c_int32),
+                ("c", ctypes.c_int32), ("pad", ctypes.c_int32), ("imm", ctypes.c_int64)]
+
+
+class ixg_array(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("len", ctypes.c_int64), ("dt", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+VM_MAX_INSN, VM_MAX_IN, VM_MAX_OUT, VM_MAX_PRED, VM_REGS = 96, 8, 4, 4, 24
+(VM_HALT, VM_IN, VM_CONST, VM_ADD, VM_SUB, VM_MUL, VM_EQ, VM_NE, VM_LT, VM_LE, VM_GT, VM_GE, VM_NOT, VM_MOV, VM_JZ,
+ VM_JMP, VM_IDX, VM_PRED, VM_OUT, VM_LEN) = range(20)
 
 
 class ixg_status(ctypes.Structure):
@@ -67,6 +81,8 @@ SIGNATURES = {
     "ixg_kmeans_ker": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _U32, _P, _P]),
     "ixg_eq_gather": (_I, [_P, _I64, _P, _P, _I64, _P, _U32, _I, _P, _P]),
     "ixg_gen_uniform": (_I, [_I, _P, _I64, _I64, _I64, _U64, _I64, _P]),
+    "ixg_mkflags": (_I, [_I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_map": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _I64, _I, _P, _P]),
     "ixg_timer_start": (_I, [_I]),
     "ixg_timer_stop": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
 }

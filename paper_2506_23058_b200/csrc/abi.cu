@@ -11,6 +11,7 @@
 
 #include "k_compact.cuh"
 #include "k_generic.cuh"
+#include "k_vm.cuh"
 
 using namespace ixg;
 
@@ -63,9 +64,7 @@ struct WS {
     LBChan c;
     const size_t t = (size_t)(tiles > 0 ? tiles : 1);
     c.hdr = hdr(i);
-    c.flags = (uint32_t*)take(t * 4);
-    c.agg = (longlong2*)take(t * sizeof(longlong2));
-    c.incl = (longlong2*)take(t * sizeof(longlong2));
+    c.slot = (ulonglong2*)take(t * sizeof(ulonglong2));
     return c;
   }
 };
@@ -388,6 +387,12 @@ size_t ixg_ws_bytes(int op, int64_t n, int64_t m) {
       if (w2.off > ws.off) ws.off = w2.off;
       break;
     }
+    case IXG_OP_MKFLAGS:
+      ws.chan(0, tiles_of(m, kGTile));
+      ws.take((size_t)(m > 0 ? m : 1) * 8);
+      ws.take((size_t)(m > 0 ? m : 1) * 8);
+      ws.take(bitmap_bytes(n));  // n = k
+      break;
     case IXG_OP_MKSGMDESCR:
       ws.chan(0, tiles_of(m, kGTile));
       ws.take((size_t)(m > 0 ? m : 1) * 8);
@@ -631,6 +636,60 @@ int ixg_gen_uniform(int dt, void* out, int64_t n, int64_t lo, int64_t hi, uint64
     k_gen_uniform<int32_t><<<grid_for(n), kGThreads, 0, s>>>((int32_t*)out, n, lo, span, smix, offset);
   else
     k_gen_uniform<long long><<<grid_for(n), kGThreads, 0, s>>>((long long*)out, n, lo, span, smix, offset);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint32_t variant, ixg_status* st,
+                void* ws, size_t ws_bytes, void* stream) {
+  if (m < 0 || (m > 0 && !shape) || (k > 0 && !flags)) return IXG_BADARG;
+  if (k < 0) k = 0;  // replicate k 0 with k < 0 is []
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_MKFLAGS, k, m)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(m, kGTile));
+  long long* ind = (long long*)w.take((size_t)(m > 0 ? m : 1) * 8);
+  long long* ones = (long long*)w.take((size_t)(m > 0 ? m : 1) * 8);
+  int rc;
+  if (k > 0 && (rc = launch_fill<long long>((long long*)flags, k, nullptr, 0LL, s))) return rc;
+  if (m == 0) return IXG_OK;
+  if ((rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape},
+                               EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr}, c, s)))
+    return rc;
+  if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
+  return launch_scatter<long long>((long long*)flags, k, nullptr, k, ind, ones, m,
+                                   IXG_SITE_BITS(variant, 1) | IXG_V_INIT, 1, 1, st, w, 1, s);
+}
+
+int ixg_map(const ixg_vm_insn* prog, int ninsn, const ixg_array* ins, int nins, const ixg_array* outs, int nouts,
+            const ixg_pred* preds, int npreds, int64_t n, int stmt, ixg_status* st, void* stream) {
+  if (ninsn < 0 || ninsn > IXG_VM_MAX_INSN || nins < 0 || nins > IXG_VM_MAX_IN || nouts < 0 ||
+      nouts > IXG_VM_MAX_OUT || npreds < 0 || npreds > IXG_VM_MAX_PRED || n < 0)
+    return IXG_BADARG;
+  if (n == 0) return IXG_OK;
+  VmProgram P;
+  memset(&P, 0, sizeof(P));
+  for (int i = 0; i < ninsn; ++i) {
+    const ixg_vm_insn& I = prog[i];
+    if (I.dst < 0 || I.dst >= IXG_VM_REGS || I.a < 0 || I.a >= IXG_VM_REGS) return IXG_BADARG;
+    if ((I.op == IXG_VM_JZ || I.op == IXG_VM_JMP) && (I.c < 0 || I.c > ninsn)) return IXG_BADARG;
+    if ((I.op == IXG_VM_ADD || I.op == IXG_VM_SUB || I.op == IXG_VM_MUL || (I.op >= IXG_VM_EQ && I.op <= IXG_VM_GE)) &&
+        (I.b < 0 || I.b >= IXG_VM_REGS))
+      return IXG_BADARG;
+    if ((I.op == IXG_VM_IN && I.a >= nins) || ((I.op == IXG_VM_IDX || I.op == IXG_VM_LEN) && (I.b < 0 || I.b >= nins)) ||
+        (I.op == IXG_VM_OUT && (I.b < 0 || I.b >= nouts)) || (I.op == IXG_VM_PRED && (I.b < 0 || I.b >= npreds)))
+      return IXG_BADARG;
+    P.insn[i] = I;
+  }
+  for (int i = 0; i < nins; ++i) P.in[i] = ins[i];
+  for (int i = 0; i < nouts; ++i) P.out[i] = outs[i];
+  for (int i = 0; i < npreds; ++i) P.pred[i] = preds[i];
+  P.ninsn = ninsn;
+  P.nin = nins;
+  P.nout = nouts;
+  P.npred = npreds;
+  k_map_vm<<<grid_for(n), 256, 0, S(stream)>>>(P, n, stmt, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;

@@ -55,7 +55,10 @@ class Node:
 
 
 def _mk(name, fields):
-    cls = dataclass(type(name, (), {"__annotations__": {f: Any for f in fields}}))
+    ns = {"__annotations__": {f: Any for f in fields}}
+    if fields[-1] == "pos":
+        ns["pos"] = (0, 0)
+    cls = dataclass(type(name, (), ns))
     return cls
 
 

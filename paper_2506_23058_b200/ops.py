@@ -315,6 +315,38 @@ def mksgmdescr(shape: torch.Tensor, xs: torch.Tensor, variant: int, status: Stat
     return res
 
 
+def mkflags(k: int, shape: torch.Tensor, variant: int, status: Status) -> torch.Tensor:
+    """mkFlags k shape (corpus/c2_filter_sgmsum.ixl): int64 flag array of length k."""
+    shape = _contig(shape.to(torch.int64))
+    m = shape.numel()
+    k = max(int(k), 0)
+    out = torch.empty(k, dtype=torch.int64, device=shape.device)
+    ws, wsb = _ws(L.OP_MKFLAGS, k, m, shape.device)
+    L.check(_lib().ixg_mkflags(k, _ptr(shape), m, _ptr(out), variant, status.ptr, ws, wsb, _stream()), "mkflags")
+    return out
+
+
+def _arr(t: torch.Tensor) -> L.ixg_array:
+    return L.ixg_array(t.data_ptr() if t.numel() else 0, t.numel(), _dt(t), 0)
+
+
+def map_vm(compiled, n: int, status: Status, stmt: int = 0, out_dtype=torch.int64, device=None) -> torch.Tensor:
+    """map f xs... with a lambda compiled by vm.compile_map (oracle.py:274-280)."""
+    out = torch.empty(n, dtype=out_dtype, device=device or torch.device("cuda"))
+    ins = [_contig(t) for t in compiled.inputs]
+    prog = (L.ixg_vm_insn * max(len(compiled.insns), 1))(*[L.ixg_vm_insn(op, d, a, b, c, 0, imm)
+                                                          for op, d, a, b, c, imm in compiled.insns])
+    arr_in = (L.ixg_array * max(len(ins), 1))(*[_arr(t) for t in ins])
+    arr_out = (L.ixg_array * 1)(_arr(out))
+    preds = (L.ixg_pred * max(len(compiled.preds), 1))(*[_c_pred(p) for p in compiled.preds])
+    L.check(
+        _lib().ixg_map(prog, len(compiled.insns), arr_in, len(ins), arr_out, 1, preds, len(compiled.preds), n, stmt,
+                       status.ptr, _stream()),
+        "map",
+    )
+    return out
+
+
 def csr_gather(x: torch.Tensor, values: torch.Tensor, indices: torch.Tensor, variant: int, status: Status, out=None):
     """map2 (\\v c -> v * x[c]) values indices (corpus/c4_csr_gather.ixl)."""
     x, values, indices = _contig(x), _contig(values), _contig(indices)

@@ -1,0 +1,234 @@
+"""Generate the golden fixtures from the Python reference itself.
+
+Run in the build container (the reference is importable there, never on the
+GPU box):
+
+    python tests/golden/make_golden.py
+
+Writes
+  tests/golden/cases.json                  -- (program, fun, args) -> result or
+                                              exception, computed by
+                                              ixverify.oracle.eval_program
+  paper_2506_23058_b200/data/programs.json -- normalized ASTs (ir.to_json) of
+                                              every corpus program
+  paper_2506_23058_b200/data/selection.json -- the verifier's per-site verdicts
+                                              (select.select) keyed by
+                                              function fingerprint
+
+Inputs: the reference's own generator ``gen_args`` (oracle.py:602-620; sizes
+0-12, precondition-satisfying) with its predicate callables replaced by
+``Pred`` descriptors drawn from the same RNG (``x < thr``, ``x > thr`` or a
+hash table, mirroring oracle.py:686-696), plus larger counter-generated
+inputs, the SPEC/paper demo values and hand-made unsafe inputs that exercise
+the CHECKED error paths.
+"""
+
+from __future__ import annotations
+
+import glob
+import json
+import os
+import random
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, ROOT)
+sys.path.insert(0, REF)
+
+import numpy as np  # noqa: E402
+from ixverify.normalize import check_well_formed, normalize  # noqa: E402
+from ixverify.oracle import Interp, OracleError, eval_program, gen_args  # noqa: E402
+from ixverify.parser import parse_program  # noqa: E402
+
+from paper_2506_23058_b200 import gen, ir  # noqa: E402
+from paper_2506_23058_b200 import select as sel  # noqa: E402
+from paper_2506_23058_b200.pred import GT, HASH, LT, Pred  # noqa: E402
+
+BUDGET = 10**9
+
+
+def corpus_files():
+    ref = sorted(glob.glob("/root/reference/pkg/corpus/*.ixl"))
+    own = sorted(glob.glob(os.path.join(ROOT, "corpus", "*.ixl")))
+    return [("ref", p) for p in ref] + [("own", p) for p in own]
+
+
+def key_of(origin, path):
+    return f"{origin}:{os.path.basename(path)}"
+
+
+def enc(v):
+    if isinstance(v, Pred):
+        return v.to_json()
+    if isinstance(v, bool):
+        return v
+    if isinstance(v, int):
+        return v
+    if isinstance(v, float):
+        return {"f": v.hex()}
+    if isinstance(v, tuple):
+        return {"tuple": [enc(x) for x in v]}
+    if isinstance(v, list):
+        return [enc(x) for x in v]
+    raise TypeError(type(v))
+
+
+def run(program, fun, args):
+    try:
+        return {"result": enc(eval_program(program, fun, args, BUDGET))}
+    except OracleError as e:
+        d = {"error": type(e).__name__}
+        if hasattr(e, "site"):
+            d["site"] = e.site
+        if getattr(e, "pos", None) is not None:
+            d["pos"] = list(e.pos)
+        return d
+
+
+def swap_preds(args, rng):
+    out = []
+    for a in args:
+        if callable(a):
+            mode = rng.randrange(3)
+            thr = rng.randint(-2, 9)
+            out.append(Pred(LT, thr) if mode == 0 else Pred(GT, thr) if mode == 1 else Pred(HASH, 0, rng.getrandbits(64)))
+        else:
+            out.append(a)
+    return out
+
+
+def big_cases(fun):
+    """Larger counter-generated inputs for the pipeline functions."""
+    out = []
+    for lg, seed in ((10, 1), (12, 2)):
+        n = 1 << lg
+        xs = gen.uniform(seed, n, -500, 500, np.int64).tolist()
+        if fun in ("filter", "partition2"):
+            out.append([Pred(LT, 7), xs])
+            out.append([Pred(HASH, 0, 0xDEADBEEF + seed), xs])
+        elif fun == "partition3":
+            out.append([Pred(LT, -100), Pred(HASH, 0, 77), xs])
+        elif fun == "filter_by":
+            cs = [bool(c) for c in (gen.uniform(seed + 5, n, 0, 2, np.int64) == 0)]
+            out.append([cs, xs])
+        elif fun == "sum":
+            out.append([xs])
+        elif fun == "c2":
+            k = sum(1 for x in xs if x >= 0)
+            shape = gen.segment_shape(seed, 37, k).tolist()
+            out.append([Pred.ge(0), xs, shape])
+        elif fun in ("mkSgmDescr",):
+            m = n // 16
+            shape = gen.uniform(seed + 1, m, 0, 9, np.int64).tolist()
+            out.append([shape, gen.uniform(seed + 2, m, -9, 9, np.int64).tolist()])
+        elif fun == "mkII":
+            out.append([gen.uniform(seed + 1, n // 16, 0, 9, np.int64).tolist()])
+        elif fun == "sgmSum":
+            flags = [bool(c) for c in (gen.uniform(seed + 3, n, 0, 7, np.int64) == 0)]
+            out.append([flags, xs])
+        elif fun == "mkFlags":
+            m = 64
+            shape = gen.segment_shape(seed, m, n // 2).tolist()
+            out.append([n // 2, shape])
+        elif fun in ("sc_bij", "sc_inj", "sc_any"):
+            perm = np.argsort(np.argsort(np.array(xs), kind="stable"), kind="stable").tolist()
+            out.append([[0] * n, perm, gen.uniform(seed + 4, n, -99, 99, np.int64).tolist()])
+        elif fun in ("csrg", "csrg_any"):
+            ncols = 97
+            out.append([gen.uniform(seed + 6, ncols, -300, 300, np.int64).tolist(),
+                        gen.uniform(seed + 7, n, -300, 300, np.int64).tolist(),
+                        gen.uniform(seed + 8, n, 0, ncols - 1, np.int64).tolist()])
+        elif fun == "get_smallest_pairs":
+            nv = 50
+            es = gen.uniform(seed + 9, 200, 0, nv - 1, np.int64).tolist()
+            is_ = np.random.default_rng(seed).permutation(1000)[:200].tolist()
+            out.append([nv, 10**6, es, is_])
+    return out
+
+
+def kmeans_cases(rng_seed):
+    rng = np.random.default_rng(rng_seed)
+    out = []
+    for nrows in (1, 4, 9):
+        lens = rng.integers(0, 7, nrows)
+        ptr = [0] + np.cumsum(lens).tolist()
+        nnz = ptr[-1]
+        ncols = int(rng.integers(1, 6))
+        vals = [round(float(v), 2) for v in rng.uniform(-4, 9, nnz)]
+        cols = rng.integers(0, ncols, nnz).tolist()
+        cl = [round(float(v), 2) for v in rng.uniform(-4, 9, ncols)]
+        for row in range(nrows):
+            out.append([row, ptr, cl, vals, cols])
+    return out
+
+
+def error_cases(fun):
+    """Inputs that violate the annotations, so the CHECKED paths fire."""
+    if fun == "sc_any":
+        return [[[0, 0, 0, 0], [0, 2, 0], [1, 2, 3]],      # conflicting duplicate
+                [[0, 0, 0], [1, 1, 7, -1], [5, 5, 9, 9]],  # equal duplicate + OOB
+                [[0, 0, 0], [0, 1, 2], [7, 8]]]            # zip truncation
+    if fun == "csrg_any":
+        return [[[1, 2, 3], [4, 5, 6, 7], [0, 2, 3, 1]], [[1, 2, 3], [4, 5], [-1, 0]]]
+    if fun == "kmeans_ker":
+        return [[2, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],         # pointers[row+1] OOB
+                [0, [0, 3], [1.0], [0.5, 1.0, 2.0], [0, 0, 0]],          # values[...] OOB at j=2
+                [0, [0, 2], [1.0, 2.0], [0.5, 1.0], [1, 5]]]             # cluster[column] OOB
+    if fun == "mkSgmDescr":
+        return [[[3, -3, 4, 1], [1, 2, 3, 4]]]                           # negative shape -> conflict
+    if fun == "get_smallest_pairs":
+        return [[3, 99, [0, 5, 1], [4, 2, 7]]]                           # H[i] OOB
+    return []
+
+
+DEMOS = {
+    ("ref:partition2.ixl", "partition2"): [[Pred(LT, 5), [5, 4, 2, 8, 7, 3]]],
+    ("ref:mksgmdescr.ixl", "mkSgmDescr"): [[[0, 2, 1, 0, 3], [1, 2, 3, 4, 5]]],
+    ("own:mkii.ixl", "mkII"): [[[0, 2, 1, 0, 3]]],
+}
+
+
+def main():
+    programs, selection, cases = {}, {}, []
+    for origin, path in corpus_files():
+        key = key_of(origin, path)
+        src = open(path).read()
+        prog = normalize(parse_program(src, os.path.basename(path)))
+        check_well_formed(prog)
+        programs[key] = {"source": src, "program": ir.to_json(prog)}
+        s = sel.select(prog)
+        for name, fs in s.funcs.items():
+            selection[f"{key}:{name}"] = fs.to_json()
+        interp = Interp(prog, BUDGET)
+        for f in prog.defs:
+            rng = random.Random(hash((key, f.name)) & 0xFFFF if False else sum(map(ord, key + f.name)))
+            draws = []
+            if f.name != "kmeans_ker":
+                for _ in range(40):
+                    a = gen_args(f, rng, interp)
+                    if a is not None:
+                        draws.append(("gen_args", swap_preds(a, rng)))
+            else:
+                draws += [("kmeans", a) for a in kmeans_cases(sum(map(ord, key)))]
+            draws += [("big", a) for a in big_cases(f.name)]
+            draws += [("error", a) for a in error_cases(f.name)]
+            draws += [("demo", a) for a in DEMOS.get((key, f.name), [])]
+            for origin_kind, a in draws:
+                rec = {"program": key, "fun": f.name, "kind": origin_kind, "args": enc(a)}
+                rec.update(run(prog, f.name, a))
+                cases.append(rec)
+    data = os.path.join(ROOT, "paper_2506_23058_b200", "data")
+    os.makedirs(data, exist_ok=True)
+    with open(os.path.join(data, "programs.json"), "w") as fh:
+        json.dump(programs, fh)
+    with open(os.path.join(data, "selection.json"), "w") as fh:
+        json.dump(selection, fh, indent=1)
+    with open(os.path.join(ROOT, "tests", "golden", "cases.json"), "w") as fh:
+        json.dump(cases, fh)
+    errs = sum(1 for c in cases if "error" in c)
+    print(f"{len(programs)} programs, {len(selection)} function verdicts, {len(cases)} cases ({errs} raising)")
+
+
+if __name__ == "__main__":
+    main()

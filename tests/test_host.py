@@ -1,0 +1,153 @@
+"""CPU tests of the host side: program snapshots, fingerprints, the selector
+against the live reference verifier, the lambda compiler, the C-ABI exports."""
+
+import ctypes
+import json
+import os
+import re
+
+import pytest
+
+from paper_2506_23058_b200 import _lib as L
+from paper_2506_23058_b200 import ir, vm
+from paper_2506_23058_b200 import select as sel
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROGRAMS = json.load(open(os.path.join(ROOT, "paper_2506_23058_b200", "data", "programs.json")))
+SELECTION = json.load(open(os.path.join(ROOT, "paper_2506_23058_b200", "data", "selection.json")))
+
+
+def test_abi_exports_every_declared_symbol():
+    """libixgpu.so loads (no GPU needed) and exports every function include/ixgpu.h declares."""
+    hdr = open(os.path.join(ROOT, "include", "ixgpu.h")).read()
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(ixg_\w+)\(", hdr, re.M))
+    assert len(declared) >= 25
+    lib = L.load(require_device=False)
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in L.SIGNATURES, name
+    assert lib.ixg_version() == 1
+    assert lib.ixg_ws_bytes(L.OP_C2, 1 << 20, 1 << 10) > (1 << 20) // 8
+
+
+def test_oracle_not_imported_by_product():
+    for dirpath, _, files in os.walk(os.path.join(ROOT, "paper_2506_23058_b200")):
+        for fn in files:
+            if fn.endswith(".py"):
+                src = open(os.path.join(dirpath, fn)).read()
+                assert not re.search(r"^\s*(from\s+oracle\b|import\s+oracle\b)", src, re.M), fn
+                assert not re.search(r"^\s*(from|import)\s+\S*ixoracle", src, re.M), fn
+                assert "libixoracle" not in src, fn
+
+
+def test_snapshot_round_trip_and_fingerprints():
+    for key, d in PROGRAMS.items():
+        prog = ir.from_json(d["program"])
+        assert ir.to_json(prog) == d["program"]
+        for f in prog.defs:
+            assert SELECTION[f"{key}:{f.name}"]["fingerprint"] == ir.fingerprint(f)
+
+
+def test_frozen_selection_golden():
+    """SURVEY.md Appendix B, as frozen in data/selection.json."""
+    def bits(key):
+        return [(s["kind"], tuple(s["pos"]), sel.SiteVerdict(**{**s, "pos": tuple(s["pos"])}).bits)
+                for s in SELECTION[key]["sites"]]
+    assert bits("ref:partition2.ixl:partition2") == [("bounds", (12, 40), 0), ("scatter-safety", (18, 12), 0)]
+    assert bits("ref:filter.ixl:filter") == [("bounds", (11, 33), 0), ("scatter-safety", (14, 12), 0)]
+    assert bits("ref:partition3.ixl:partition3")[-1] == ("scatter-safety", (26, 12), 0)
+    assert bits("ref:maxmatching.ixl:get_smallest_pairs") == [("bounds", (18, 27), 0)]
+    assert all(b == 0 for _, _, b in bits("ref:kmeans_ker.ixl:kmeans_ker"))
+    # mkSgmDescr: bounds proved, the scatter never reached -> fully CHECKED
+    mk = bits("ref:mksgmdescr.ixl:mkSgmDescr")
+    assert [b for _, _, b in mk[:3]] == [0, 0, 0] and mk[3][2] == L.V_CONFLICT | L.V_INIT
+    # mkFlags: Ss2 proved (no conflict check) but no conversion rule: init kept
+    assert bits("own:c2_filter_sgmsum.ixl:mkFlags")[-1][2] == L.V_INIT
+    assert bits("own:c3_scatter.ixl:sc_bij") == [("scatter-safety", (6, 12), 0)]
+    assert bits("own:c3_scatter.ixl:sc_inj")[0][2] == L.V_INIT
+    assert bits("own:c3_scatter.ixl:sc_any")[0][2] == L.V_CONFLICT | L.V_INIT
+    assert bits("own:c4_csr_gather.ixl:csrg")[0][2] == 0
+    assert bits("own:c4_csr_gather.ixl:csrg_any")[0][2] == L.V_BOUNDS
+
+
+@pytest.mark.reference
+def test_live_selector_matches_frozen(reference):
+    from ixverify.normalize import normalize
+    from ixverify.parser import parse_program
+
+    for key, d in PROGRAMS.items():
+        prog = normalize(parse_program(d["source"], key.split(":")[1]))
+        s = sel.select(prog)
+        for name, fs in s.funcs.items():
+            assert fs.to_json() == SELECTION[f"{key}:{name}"], (key, name)
+
+
+@pytest.mark.reference
+def test_snapshot_matches_reference_parse(reference):
+    """A program parsed by the reference fingerprints like its snapshot (the
+    fingerprint ignores the fresh %aN names normalization invents)."""
+    from ixverify.normalize import normalize
+    from ixverify.parser import parse_program
+
+    for key, d in PROGRAMS.items():
+        a = normalize(parse_program(d["source"]))
+        b = ir.from_json(d["program"])
+        for fa, fb in zip(a.defs, b.defs):
+            assert ir.fingerprint(fa) == ir.fingerprint(fb)
+            assert [(k, p) for k, p, _ in ir.sites(fa)] == [(k, p) for k, p, _ in ir.sites(fb)]
+
+
+def test_expr_str_matches_reference_sites():
+    prog = ir.from_json(PROGRAMS["ref:kmeans_ker.ixl"]["program"])
+    f = ir.find_def(prog, "kmeans_ker")
+    assert [ir.expr_str(n) for _, _, n in ir.sites(f)] == [
+        "pointers[row]", "pointers[row + 1]", "values[index_start + j]", "indices[index_start + j]",
+        "cluster[column]"]
+
+
+def test_vm_compiles_corpus_lambdas():
+    """Every map lambda of the corpus compiles to the register program."""
+    n = 0
+    for key, d in PROGRAMS.items():
+        prog = ir.from_json(d["program"])
+        for f in prog.defs:
+            def walk(e):
+                nonlocal n
+                if ir.kind(e) == "App" and ir.kind(e.fun) == "VarE" and e.fun.name == "map" and ir.kind(e.args[0]) == "Lambda":
+                    lam = e.args[0]
+                    env = {}
+                    for p in f.params:
+                        env[p.name] = ("pred", object()) if ir.kind(p.type) == "TFun" else ("array", object())
+                    env.update({s: ("scalar", 3) for s in f.sizes})
+                    for nm in ("num_true", "m1", "m2", "count", "len"):
+                        env.setdefault(nm, ("scalar", 1))
+                    for nm in ("H", "shape", "x"):
+                        env.setdefault(nm, ("array", object()))
+                    arrs = [object() for _ in lam.params]
+                    c = vm.compile_map(lam, arrs, env)
+                    assert c.insns[-1][0] == L.VM_OUT and len(c.insns) <= L.VM_MAX_INSN
+                    n += 1
+                for c in ir.children(e):
+                    walk(c)
+            walk(f.body)
+    assert n >= 20
+
+
+def test_vm_short_circuit_and_if_guard_indexing():
+    # \i -> if i == 0 then 0 else shape[i-1]: the IndexE sits behind a jump
+    lam = ir.Lambda(("i",), ir.If(ir.BinOp("==", ir.VarE("i"), ir.Const(0)), ir.Const(0),
+                                   ir.IndexE(ir.VarE("shape"), ir.BinOp("-", ir.VarE("i"), ir.Const(1)), (6, 51))),
+                    (0, 0))
+    c = vm.compile_map(lam, [object()], {"shape": ("array", object())})
+    ops = [i[0] for i in c.insns]
+    jz = ops.index(L.VM_JZ)
+    assert ops.index(L.VM_IDX) > jz
+    assert c.sites[0].pos == (6, 51)
+
+
+def test_errors_mirror():
+    from paper_2506_23058_b200 import errors
+
+    e = errors.OutOfBounds("xs[i]", (3, 4))
+    assert str(e) == "out of bounds: xs[i]" and e.site == "xs[i]" and e.pos == (3, 4)
+    assert isinstance(errors.NonIdempotentScatter((1, 2)), errors.OracleError)

@@ -1,0 +1,161 @@
+"""Pin the C oracle (oracle/ixoracle.c) to the Python reference.
+
+tests/golden/cases.json holds (program, function, arguments) -> result or
+exception as computed by the reference interpreter itself
+(ixverify.oracle.eval_program, run by tests/golden/make_golden.py).  Every
+case is replayed through the C restatement and must match exactly -- values,
+exception class, and for OutOfBounds the failing site.  CPU only.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ixoracle as O
+from paper_2506_23058_b200 import gen
+from paper_2506_23058_b200.pred import Pred, mix64
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CASES = json.load(open(os.path.join(HERE, "golden", "cases.json")))
+
+KMEANS_SITES = ["pointers[row]", "pointers[row + 1]", "values[index_start + j]", "indices[index_start + j]",
+                "cluster[column]"]
+
+
+def dec(v):
+    if isinstance(v, dict):
+        if "pred" in v:
+            return Pred.from_json(v)
+        if "f" in v:
+            return float.fromhex(v["f"])
+        if "tuple" in v:
+            return tuple(dec(x) for x in v["tuple"])
+    if isinstance(v, list):
+        return [dec(x) for x in v]
+    return v
+
+
+def ints(a):
+    return [int(x) for x in a]
+
+
+def run_oracle(fun, a):
+    """Dispatch one corpus function to its C restatement; returns the value in
+    the reference's own shape (list / int / tuple / float)."""
+    if fun == "sum":
+        return O.sum_(a[0])
+    if fun == "filter":
+        return ints(O.filter_(a[0], a[1]))
+    if fun == "filter_by":
+        return ints(O.filter_by([int(c) for c in a[0]], a[1]))
+    if fun == "partition2":
+        nt, ys = O.partition2(a[0], a[1])
+        return (nt, ints(ys))
+    if fun == "partition3":
+        m1, m2, ys = O.partition3(a[0], a[1], a[2])
+        return (m1, m2, ints(ys))
+    if fun == "get_smallest_pairs":
+        xs, ys = O.get_smallest_pairs(a[0], a[1], a[2], a[3])
+        return (ints(xs), ints(ys))
+    if fun == "mkSgmDescr":
+        return ints(O.mksgmdescr(a[0], a[1]))
+    if fun == "mkII":
+        return ints(O.mkii(a[0]))
+    if fun == "sgmSum":
+        return ints(O.sgmsum([int(c) for c in a[0]], a[1]))
+    if fun == "mkFlags":
+        return ints(O.mkflags(a[0], a[1]))
+    if fun == "c2":
+        ys, zs = O.c2(a[0], a[1], a[2])
+        return (ints(ys), ints(zs))
+    if fun in ("sc_bij", "sc_inj", "sc_any"):
+        return ints(O.scatter(a[0], a[1], a[2]))
+    if fun in ("csrg", "csrg_any"):
+        return ints(O.csrg(a[0], a[1], a[2]))
+    if fun == "kmeans_ker":
+        return O.kmeans_ker(a[0], a[1], a[2], a[3], a[4])
+    raise KeyError(fun)
+
+
+def test_golden_file_covers_corpus():
+    funs = {c["fun"] for c in CASES}
+    assert {"partition2", "partition3", "filter", "filter_by", "get_smallest_pairs", "mkSgmDescr", "kmeans_ker",
+            "c2", "mkFlags", "sgmSum", "mkII", "sc_any", "csrg_any"} <= funs
+    assert any("error" in c for c in CASES)
+    assert len(CASES) > 500
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)))
+def test_oracle_matches_reference(idx):
+    case = CASES[idx]
+    a = dec(case["args"])
+    if "error" in case:
+        with pytest.raises(O.OracleFail) as ei:
+            run_oracle(case["fun"], a)
+        want = {"OutOfBounds": O.OOB, "NonIdempotentScatter": O.CONFLICT}[case["error"]]
+        assert ei.value.code == want
+        if case["fun"] == "kmeans_ker":
+            assert KMEANS_SITES[ei.value.site] == case["site"]
+        return
+    got = run_oracle(case["fun"], a)
+    want = dec(case["result"])
+    if isinstance(want, float) or case["fun"] == "kmeans_ker":
+        assert float(got).hex() == float(want).hex()
+    else:
+        assert got == want
+
+
+def test_demo_values():
+    """SPEC.md:509-511 / PAPER.md:380-417 demo values."""
+    nt, ys = O.partition2(Pred.lt(5), [5, 4, 2, 8, 7, 3])
+    assert (nt, ys.tolist()) == (3, [4, 2, 3, 5, 8, 7])
+    assert O.mksgmdescr([0, 2, 1, 0, 3], [1, 2, 3, 4, 5]).tolist() == [2, 0, 3, 5, 0, 0]
+    assert O.mkii([0, 2, 1, 0, 3]).tolist() == [1, 1, 2, 4, 4, 4]
+    assert O.scan_add([1, 2, 3], 5).tolist() == [6, 8, 11]
+    assert O.hist(O.HIST_MIN, 99, 3, [0, 0, 2, 5, -1], [4, 2, 7, 1, 1]).tolist() == [2, 99, 7]
+
+
+def test_pred_and_generator_mirrors():
+    """Python Pred/gen are bit-identical to the C restatement."""
+    lib = O.lib()
+    import ctypes
+
+    lib.ixo_mix64.restype = ctypes.c_uint64
+    lib.ixo_mix64.argtypes = [ctypes.c_uint64]
+    lib.ixo_rand.restype = ctypes.c_uint64
+    lib.ixo_rand.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+    lib.ixo_pred_eval.restype = ctypes.c_int
+    for z in (0, 1, 2**63, 2**64 - 1, 12345678901234567):
+        assert lib.ixo_mix64(z) == mix64(z)
+    r = gen.rand_u64(99, 1000, offset=17)
+    assert all(int(r[i]) == lib.ixo_rand(99, 17 + i) for i in range(0, 1000, 37))
+    for p in (Pred.lt(3), Pred.gt(-2), Pred.le(0), Pred.ge(7), Pred(4, 5), Pred(5, 5), Pred.hash(0xFEED), Pred(7),
+              Pred(8)):
+        cp = O.cpred(p)
+        for x in range(-20, 20):
+            assert bool(lib.ixo_pred_eval(ctypes.byref(cp), ctypes.c_int64(x))) == p(x)
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 1000, 100_003])
+def test_parallel_port_matches_sequential(n):
+    xs = gen.uniform(n, n, -128, 127, np.int32)
+    p = Pred.ge(0)
+    k = int((xs >= 0).sum())
+    shape = gen.segment_shape(3, 50, k) if n else np.zeros(0, np.int64)
+    ys, zs = O.c2(p, xs, shape)
+    pys, pzs = O.par_c2_i32(p, xs, shape, 4)
+    assert np.array_equal(pys, ys) and np.array_equal(pzs, zs)
+    xs2 = gen.uniform(n + 1, n, -(1 << 31), (1 << 31) - 1, np.int32)
+    nt, ys2 = O.partition2(Pred.lt(0), xs2)
+    pnt, pys2 = O.par_partition2_i32(Pred.lt(0), xs2, 3)
+    assert pnt == nt and np.array_equal(pys2, ys2)
+
+
+def test_segment_shape_generator():
+    for m, k in ((1, 0), (1, 10), (1000, 12345), (97 * 3, 5)):
+        s = gen.segment_shape(1, m, k)
+        assert len(s) == m and s.sum() == k and (s >= 0).all()
+    s = gen.segment_shape(2, 10_000, 1_000_000)
+    assert (s == 0).mean() >= 0.01
