@@ -5,12 +5,13 @@
 // ELIDED kernel or the materialising CHECKED sequence from the site bits,
 // and enqueues everything on the caller's stream.  No host synchronisation.
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
 
-#include "k_compact.cuh"
 #include "k_generic.cuh"
+#include "k_stream.cuh"
 #include "k_vm.cuh"
 
 using namespace ixg;
@@ -64,7 +65,7 @@ struct WS {
     LBChan c;
     const size_t t = (size_t)(tiles > 0 ? tiles : 1);
     c.hdr = hdr(i);
-    c.slot = (ulonglong2*)take(t * sizeof(ulonglong2));
+    c.slot = (ulonglong2*)take(t * sizeof(ulonglong2) * kSlotStride);
     return c;
   }
 };
@@ -93,11 +94,21 @@ void allow_smem(K kernel, int bytes) {
 }
 
 // ------------------------------------------------------------------ pieces
+// per-launch nonce for look-back slots (lookback.cuh): 24 bits, never 0
+std::atomic<uint32_t> g_nonce{0};
+inline uint32_t next_nonce() {
+  uint32_t v;
+  do {
+    v = (g_nonce.fetch_add(1, std::memory_order_relaxed) + 1) & kNonceMask;
+  } while (v == 0);
+  return v;
+}
+
 template <class M, class Src, class Epi>
 int launch_scan(long long n, Src src, Epi epi, LBChan ch, cudaStream_t s) {
   if (n <= 0) return IXG_OK;
   TimedLaunch tl(IXG_K_SCAN, s);
-  k_scan<M, Src, Epi><<<(unsigned)tiles_of(n, kGTile), kGThreads, 0, s>>>(n, src, epi, ch);
+  k_scan<M, Src, Epi><<<(unsigned)tiles_of(n, kGTile), kGThreads, 0, s>>>(n, src, epi, ch, next_nonce());
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -140,20 +151,39 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
 }
 
 // --------------------------------------------------------------- filter
+// Persistent streaming compaction (k_stream.cuh).  All CTAs must be
+// co-resident (they wait on each other's look-back slots): the grid is the
+// occupancy-derived resident capacity, never more.
 template <typename T, typename Z, bool kByCs, bool kSeg>
-int launch_filter_fused(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, Z* zs,
-                        const uint32_t* segbits, long long out_base, LBChan c0, LBChan c1, long long* d_count,
-                        longlong2* d_seg_total, ixg_status* st, cudaStream_t s) {
-  auto kern = k_filter<T, Z, kByCs, kSeg>;
-  const int smem = kTile * (int)sizeof(T) + (kSeg ? kTile * (int)sizeof(Z) : 0);
+int launch_filter_p(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, Z* zs,
+                    const uint32_t* segbits, long long out_base, LBChan ch, long long* d_count, SegTileMeta* meta,
+                    ixg_status* st, cudaStream_t s) {
+  const int smem = (kSTile + 32 / (int)sizeof(T)) * (int)sizeof(T) +
+                   (kSeg ? (kSTile + 32 / (int)sizeof(Z)) * (int)sizeof(Z) : 0);
+  const long long tiles = tiles_of(n, kSTile);
+  TimedLaunch tl(IXG_K_FILTER_FUSED, s);
+  auto kern = k_filter_s<T, Z, kByCs, kSeg>;
   static bool attr = false;
   if (!attr) {
     allow_smem(kern, smem);
     attr = true;
   }
-  TimedLaunch tl(IXG_K_FILTER_FUSED, s);
-  kern<<<(unsigned)tiles_of(n, kTile), kThreads, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, c0, c1,
-                                                            d_count, d_seg_total, st);
+  kern<<<(unsigned)tiles, kSThreads, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, ch, next_nonce(), d_count,
+                                                meta, st);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+// tiles' carries for the segmented sum (k_stream.cuh fix-up), then the fix-up
+template <typename Z>
+int launch_seg_fixup(SegTileMeta* meta, long long n, const uint32_t* segbits, long long out_base, Z* zs,
+                     long long carry_v, int carry_f, ixg_status* st, cudaStream_t s) {
+  const long long tiles = tiles_of(n, kSTile);
+  k_seg_tile_scan<<<1, 1024, 0, s>>>(meta, tiles, carry_v, carry_f);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  k_seg_fixup<Z><<<grid_for(tiles * 256), 256, 0, s>>>(meta, tiles, segbits, out_base, zs, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -167,14 +197,14 @@ int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T*
   const bool fused = (sb & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;  // Sc1 proved
   ixg_pred pp = p ? *p : ixg_pred{IXG_PRED_TRUE, 0, 0, 0};
   if (fused) {
-    LBChan c0 = ws.chan(0, tiles_of(n, kTile));
+    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
-    if (cs) return launch_filter_fused<T, T, true, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, c0,
-                                                           d_count, nullptr, st, s);
-    return launch_filter_fused<T, T, false, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, c0, d_count,
-                                                    nullptr, st, s);
+    if (cs) return launch_filter_p<T, T, true, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, d_count,
+                                                       nullptr, st, s);
+    return launch_filter_p<T, T, false, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, d_count, nullptr,
+                                                st, s);
   }
   // CHECKED: offs/inds materialised (filter.ixl:10-12), then the scatter
   // into `replicate count 0` with the dynamic checks (filter.ixl:13-14).
@@ -203,18 +233,18 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
   const int cgrid = grid_for(n / (16 / (int)sizeof(T)) + 1);
   long long* partials = (long long*)ws.take((size_t)cgrid * 2 * 8);
   if (fused) {
-    LBChan c0 = ws.chan(0, tiles_of(n, kTile));
+    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
     {
       TimedLaunch tl(IXG_K_CLASS_COUNT, s);
-      k_class_count<T, kClasses><<<cgrid, kThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
+      k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
     }
     LAUNCHED();
     CHECK_LAUNCH();
-    auto kern = k_place<T, kClasses>;
-    const int smem = kTile * (int)sizeof(T);
+    auto kern = k_place_s<T, kClasses>;
+    const int smem = kClasses * (kSTile + 32 / (int)sizeof(T)) * (int)sizeof(T);
     static bool attr = false;
     if (!attr) {
       allow_smem(kern, smem);
@@ -222,7 +252,7 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
     }
     {
       TimedLaunch tl(IXG_K_PLACE, s);
-      kern<<<(unsigned)tiles_of(n, kTile), kThreads, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0);
+      kern<<<(unsigned)tiles_of(n, kSTile), kSThreads, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0, next_nonce());
     }
     LAUNCHED();
     CHECK_LAUNCH();
@@ -234,7 +264,7 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
   long long* inds = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<T>(ys, n, nullptr, n, inds, xs, n, sb, scatter_site, scatter_site, st, ws, 1, s);
   if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
-  k_class_count<T, kClasses><<<cgrid, kThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
+  k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
   LAUNCHED();
   CHECK_LAUNCH();
   const int dt = sizeof(T) == 4 ? IXG_I32 : IXG_I64;
@@ -267,16 +297,18 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     // segment start (no conflict check), starts >= k are never read.
     uint32_t* bits = (uint32_t*)ws.take(bitmap_bytes(n));
     LBChan cs = ws.chan(2, tiles_of(m, kGTile));
-    LBChan c0 = ws.chan(0, tiles_of(n, kTile));
-    LBChan c1 = ws.chan(1, tiles_of(n, kTile));
+    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
+    SegTileMeta* meta = (SegTileMeta*)ws.take((size_t)tiles_of(n, kSTile) * sizeof(SegTileMeta) + 64);
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_k, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys) || !aligned16(zs)) return IXG_BADARG;
     cudaMemsetAsync(bits, 0, bitmap_bytes(n), s);
     LAUNCHED();
-    int rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
+    int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
     if (rc) return rc;
-    return launch_filter_fused<T, Z, false, true>(xs, nullptr, n, pp, ys, zs, bits, 0, c0, c1, d_k, nullptr, st, s);
+    if ((rc = launch_filter_p<T, Z, false, true>(xs, nullptr, n, pp, ys, zs, bits, 0, c0, d_k, meta, st, s)))
+      return rc;
+    return launch_seg_fixup<Z>(meta, n, bits, 0, zs, 0, 0, st, s);
   }
   // CHECKED: filter (checked), mkFlags with materialised ind/flags arrays
   // and the checked scatter of `replicate m 1`, sgmSum as a 2-ary scan.
@@ -289,7 +321,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
   long long* flags = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s);
   if (n <= 0) return IXG_OK;
-  if ((rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr}, cs, s)))
+  if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr}, cs, s)))
     return rc;
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
   if ((rc = launch_fill<long long>(flags, 0, d_k, 0LL, s))) return rc;
@@ -409,7 +441,10 @@ int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, i
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, n, 0)) return IXG_BADARG;
   WS w(ws);
   LBChan c = w.chan(0, tiles_of(n, kGTile));
-  return launch_scan<SumOp>(n, SrcArr{dt, xs}, EpiScanOut{ne, exclusive, (long long*)out}, c, S(stream));
+  const EpiScanOut epi{ne, exclusive, (long long*)out};
+  if (dt == IXG_I32) return launch_scan<SumOp>(n, SrcArrT<int32_t>{(const int32_t*)xs}, epi, c, S(stream));
+  if (dt == IXG_U8) return launch_scan<SumOp>(n, SrcArrT<uint8_t>{(const uint8_t*)xs}, epi, c, S(stream));
+  return launch_scan<SumOp>(n, SrcArrT<long long>{(const long long*)xs}, epi, c, S(stream));
 }
 
 int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64_t n, int f0, int64_t v0,
@@ -567,7 +602,7 @@ int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t* 
   long long* ind = (long long*)w.take((size_t)(m > 0 ? m : 1) * 8);
   if (m == 0) return cuda_rc(cudaMemsetAsync(d_len, 0, 8, s));
   // scn / ind / len (mksgmdescr.ixl:6-9); len = scn[m-1] + shape[m-1] = sum shape
-  int rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape},
+  int rc = launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
                               EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, (long long*)d_len}, c, s);
   if (rc || cap == 0) return rc;
   // the scatter is never proved for mkSgmDescr: the host
@@ -654,7 +689,7 @@ int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint
   int rc;
   if (k > 0 && (rc = launch_fill<long long>((long long*)flags, k, nullptr, 0LL, s))) return rc;
   if (m == 0) return IXG_OK;
-  if ((rc = launch_scan<SumOp>(m, SrcArr{IXG_I64, shape},
+  if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
                                EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr}, c, s)))
     return rc;
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;

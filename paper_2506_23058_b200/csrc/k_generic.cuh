@@ -32,10 +32,34 @@ IXG_DEV void store_dt(int dt, void* p, long long i, long long v) {
   else reinterpret_cast<int64_t*>(p)[i] = v;
 }
 
-struct SrcArr {  // scan (+) over an integer array
+struct SrcArr {  // scan (+) over an integer array (any element width)
   int dt;
   const void* xs;
   IXG_DEV SumOp::T operator()(long long i) const { return SumOp::T{load_dt(dt, xs, i)}; }
+};
+template <typename E>
+struct SrcArrT {  // scan (+) over E[], 16 elements per thread through 256-bit loads
+  const E* xs;
+  IXG_DEV SumOp::T operator()(long long i) const { return SumOp::T{(long long)xs[i]}; }
+  IXG_DEV void load16(long long i0, long long n, SumOp::T (&v)[kGItems]) const {
+    if (sizeof(E) >= 2 && i0 + kGItems <= n && (((uintptr_t)(xs + i0)) & 31) == 0) {
+      constexpr int PER = 32 / (int)sizeof(E);
+#pragma unroll
+      for (int k = 0; k < kGItems / PER; ++k) {
+        uint32_t r[8];
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "l"(xs + i0 + k * PER));
+        const E* e = reinterpret_cast<const E*>(r);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) v[k * PER + q] = SumOp::T{(long long)e[q]};
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kGItems; ++j) v[j] = SumOp::T{(i0 + j < n) ? (long long)xs[i0 + j] : 0};
+    }
+  }
 };
 struct SrcPred {  // map (\x -> if p x then 1 else 0) xs, fused into the scan
   int dt;
@@ -135,29 +159,32 @@ struct EpiSegStarts {  // mkSgmDescr / mkFlags: ind[i] = if shape[i] <= 0 then -
 };
 
 // Single-pass blocked scan with a source functor and an epilogue functor.
+// tile = blockIdx.x (see lookback.cuh / k_stream.cuh for the protocol); a
+// source may provide load16() with 256-bit loads of its 16 elements.
+template <class Src, class T>
+IXG_DEV auto src_load16(const Src& src, long long i0, long long n, T (&v)[kGItems], int)
+    -> decltype(src.load16(i0, n, v), void()) {
+  src.load16(i0, n, v);
+}
+template <class Src, class T>
+IXG_DEV void src_load16(const Src& src, long long i0, long long n, T (&v)[kGItems], long) {
+#pragma unroll
+  for (int j = 0; j < kGItems; ++j) v[j] = (i0 + j < n) ? src(i0 + j) : T{};
+}
+
 template <class M, class Src, class Epi>
-__global__ void __launch_bounds__(kGThreads) k_scan(long long n, Src src, Epi epi, LBChan ch) {
+__global__ void __launch_bounds__(kGThreads) k_scan(long long n, Src src, Epi epi, LBChan ch, uint32_t nonce) {
   using T = typename M::T;
-  __shared__ long long s_tile;
-  __shared__ uint32_t s_ep;
   __shared__ T s_w[kGThreads / 32];
   __shared__ T s_carry;
-  if (threadIdx.x == 0) {
-    long long t;
-    uint32_t ep;
-    lb_ticket(ch, &t, &ep);
-    s_tile = t;
-    s_ep = ep;
-  }
-  __syncthreads();
-  const long long tile = s_tile;
-  const uint32_t ep = s_ep;
+  const long long tile = blockIdx.x;
   const long long i0 = tile * kGTile + (long long)threadIdx.x * kGItems;
   T v[kGItems];
+  src_load16(src, i0, n, v, 0);
   T a = M::identity();
 #pragma unroll
   for (int j = 0; j < kGItems; ++j) {
-    v[j] = (i0 + j < n) ? src(i0 + j) : M::identity();
+    if (i0 + j >= n) v[j] = M::identity();
     a = M::op(a, v[j]);
   }
   T inc = warp_inclusive<M>(a);
@@ -171,13 +198,13 @@ __global__ void __launch_bounds__(kGThreads) k_scan(long long n, Src src, Epi ep
     if (w < warp_id()) wpre = M::op(wpre, s_w[w]);
     tagg = M::op(tagg, s_w[w]);
   }
-  if (threadIdx.x == 0) lb_publish<M>(ch, ep, tile, tagg, tile == 0);
+  if (threadIdx.x == 0) lb_publish<M>(ch, nonce, tile, tagg, tile == 0);
   if (warp_id() == 0) {
     T c = M::identity();
-    if (tile > 0) c = lb_lookback<M>(ch, ep, tile);
+    if (tile > 0) c = lb_lookback<M>(ch, nonce, tile);
     if (lane_id() == 0) {
       s_carry = c;
-      if (tile > 0) lb_publish<M>(ch, ep, tile, M::op(c, tagg), true);
+      if (tile > 0) lb_publish<M>(ch, nonce, tile, M::op(c, tagg), true);
     }
   }
   __syncthreads();
@@ -189,7 +216,6 @@ __global__ void __launch_bounds__(kGThreads) k_scan(long long n, Src src, Epi ep
       epi(i0 + j, run, v[j]);
     }
   }
-  if (threadIdx.x == 0) lb_retire(ch, ep);
 }
 
 // ---------------------------------------------------------------- scatter

@@ -1,0 +1,519 @@
+// k_stream.cuh -- single-pass stream compaction for sm_100a: filter /
+// filter_by (+ the flag-array segmented sum of BASELINE C2) and the stable
+// 2-/3-way partition placement.
+//
+// Why these can be fused at all: the verifier proved the final scatter of
+// each program safe AND bijective onto its destination (Sc1, SURVEY.md App. B:
+// filter (14,12), partition2 (18,12), partition3 (26,12)), so the destination
+// needs no initialisation, no OOB test and no duplicate check, and every
+// element's destination is determined by the running count alone.  The
+// scatter collapses into a stable compaction inside the scan tile: xs is read
+// once, ys (and zs) written once.
+//
+// Shape of the kernel (chosen by measurement):
+//   * one CTA per 4096-element tile, tile = blockIdx.x (CTAs are dispatched in
+//     index order, so a CTA only waits on tiles already resident or done --
+//     the same forward-progress argument CUB's single-pass scan relies on);
+//     no ticket or retire atomics on the critical path, and the look-back
+//     slots are tagged with a per-launch nonce passed by the host, so the
+//     workspace never needs a reset;
+//     (a persistent, ticket-driven variant with register prefetch measured
+//     2-3x SLOWER: all CTAs reach their look-back in lock-step and the walk
+//     spans the whole previous wave)
+//   * blocked layout: 16 consecutive elements per thread via two 256-bit
+//     loads (LDG.E.256); a thread's selected elements are consecutive in the
+//     output, so ranks are one popc + a warp/CTA prefix of per-thread counts
+//     and the segmented sum of C2 is a serial fold per thread plus one warp
+//     scan -- no shared-memory transpose, ~6x fewer instructions per element
+//     than a ballot-per-element ranking;
+//   * the compacted run is staged in shared memory at its global 32-byte
+//     phase and written with aligned 256-bit stores (scalar only at the two
+//     run ends);
+//   * C2 needs only the count look-back: the segmented sum is computed with a
+//     tile-local carry and each tile's aggregate is written out; a small
+//     fix-up pass (k_seg_tile_scan + k_seg_fixup) adds the carry of the
+//     preceding tiles to the tile's output prefix before its first segment
+//     start (segments average 128 elements at C2: a few % of zs).
+#pragma once
+#include <type_traits>
+
+#include "lookback.cuh"
+
+namespace ixg {
+
+constexpr int kSThreads = 256;
+constexpr int kSItems = 16;
+constexpr int kSTile = kSThreads * kSItems;  // 4096
+constexpr int kSWarps = kSThreads / 32;
+
+IXG_DEV void ld256(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+IXG_DEV void st256(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+// 16 consecutive elements of type T per thread
+template <typename T>
+struct Blk16 {
+  T x[kSItems];
+  IXG_DEV void load(const T* __restrict__ xs, long long i0, long long n) {
+    if (i0 + kSItems <= n) {
+      constexpr int NV = kSItems * (int)sizeof(T) / 32;  // 256-bit loads
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        uint32_t r[8];
+        ld256(xs + i0 + v * (32 / (int)sizeof(T)), r);
+#pragma unroll
+        for (int e = 0; e < 32 / (int)sizeof(T); ++e) {
+          if constexpr (sizeof(T) == 4) x[v * 8 + e] = (T)r[e];
+          else x[v * 4 + e] = (T)(((unsigned long long)r[2 * e + 1] << 32) | r[2 * e]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j) x[j] = (i0 + j < n) ? xs[i0 + j] : T(0);
+    }
+  }
+};
+
+IXG_DEV uint32_t valid_mask(long long i0, long long n) {
+  const long long valid = n - i0;
+  return valid <= 0 ? 0u : (valid >= kSItems ? 0xffffu : ((1u << valid) - 1u));
+}
+
+// selection mask of 16 elements; the predicate kind is hoisted (uniform)
+template <typename T>
+IXG_DEV uint32_t select_mask(const ixg_pred& p, const T (&x)[kSItems]) {
+  uint32_t m = 0;
+  const long long t = p.thr;
+#define IXG_SEL(expr)                                    \
+  _Pragma("unroll") for (int j = 0; j < kSItems; ++j) {  \
+    const long long v = (long long)x[j];                 \
+    m |= (uint32_t)(expr) << j;                          \
+  }
+  switch (p.kind) {
+    case IXG_PRED_LT: IXG_SEL(v < t) break;
+    case IXG_PRED_GT: IXG_SEL(v > t) break;
+    case IXG_PRED_LE: IXG_SEL(v <= t) break;
+    case IXG_PRED_GE: IXG_SEL(v >= t) break;
+    case IXG_PRED_EQ: IXG_SEL(v == t) break;
+    case IXG_PRED_NE: IXG_SEL(v != t) break;
+    case IXG_PRED_HASH: IXG_SEL((mix64((uint64_t)v ^ p.seed) >> 63) != 0) break;
+    case IXG_PRED_TRUE: m = 0xffffu; break;
+    default: m = 0; break;
+  }
+#undef IXG_SEL
+  return m;
+}
+
+// CTA-wide exclusive prefix of per-thread counts; returns the thread's
+// exclusive prefix, *total = the CTA total.  Contains one __syncthreads.
+IXG_DEV int cta_exclusive(int c, int* s_w, int* total) {
+  const int lane = lane_id(), w = warp_id();
+  int inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < kSWarps; ++k) {
+    const int v = s_w[k];
+    pre += (k < w) ? v : 0;
+    tot += v;
+  }
+  *total = tot;
+  return pre + inc - c;
+}
+
+// store the run staged at stage[shift .. shift+cnt) (shift = base % VS, i.e.
+// stage index = (g - base) + shift for global position g) to out[base ..]
+template <typename E>
+IXG_DEV void store_aligned(E* __restrict__ out, long long base, int cnt, const E* stage) {
+  constexpr int VS = 32 / (int)sizeof(E);
+  if (cnt <= 0) return;
+  const long long c0 = base / VS, c1 = (base + cnt - 1) / VS;
+  const int shift = (int)(base - c0 * VS);
+  for (long long c = c0 + threadIdx.x; c <= c1; c += kSThreads) {
+    const int q0 = (int)(c - c0) * VS;
+    const long long g0 = c * VS;
+    if (g0 >= base && g0 + VS <= base + cnt) {
+      uint32_t r[8];
+      const uint4 a = *reinterpret_cast<const uint4*>(stage + q0);
+      const uint4 b = *reinterpret_cast<const uint4*>(stage + q0 + VS / 2);
+      r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+      r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+      st256(out + g0, r);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VS; ++e) {
+        const int q = q0 + e;
+        if (q >= shift && q < shift + cnt) out[g0 + e] = stage[q];
+      }
+    }
+  }
+}
+
+// Per-tile output of the segmented fused kernel, for the fix-up pass.
+struct SegTileMeta {
+  long long v;     // tile aggregate value; after k_seg_tile_scan: the carry INTO the tile
+  long long f;     // tile has a flag
+  long long base;  // first output position of the tile
+  long long cnt;   // outputs of the tile
+};
+
+// ---------------------------------------------------------------------------
+// filter / filter_by [+ sgmSum over the output with flags from a bitmap]
+template <typename T, typename Z, bool kByCs, bool kSeg>
+__global__ void __launch_bounds__(kSThreads, 4) k_filter_s(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
+                                                            long long n, ixg_pred p, T* __restrict__ ys,
+                                                            Z* __restrict__ zs, const uint32_t* __restrict__ segbits,
+                                                            long long out_base, LBChan ch, uint32_t nonce,
+                                                            long long* d_count, SegTileMeta* __restrict__ meta,
+                                                            ixg_status* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int VS = 32 / (int)sizeof(T);
+  constexpr int VZ = 32 / (int)sizeof(Z);
+  T* stage = reinterpret_cast<T*>(smem_raw);
+  Z* stage_z = reinterpret_cast<Z*>(smem_raw + (kSTile + VS) * sizeof(T));
+  __shared__ int s_w[kSWarps];
+  __shared__ long long s_excl;
+  __shared__ SegOp::T s_seg[kSWarps];
+
+  const long long tile = blockIdx.x;
+  const long long i0 = tile * kSTile + threadIdx.x * kSItems;
+  Blk16<T> cur;
+  cur.load(xs, i0, n);
+  uint32_t mask;
+  if (kByCs) {
+    mask = 0;
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) mask |= (uint32_t)((i0 + j < n) && cs[i0 + j] != 0) << j;
+  } else {
+    mask = select_mask<T>(p, cur.x) & valid_mask(i0, n);
+  }
+  const int c = __popc(mask);
+  int cnt;
+  const int rank = cta_exclusive(c, s_w, &cnt);
+  if (threadIdx.x == 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
+  if (warp_id() == 0) {
+    long long ex = 0;
+    if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
+    if (lane_id() == 0) {
+      s_excl = ex;
+      if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
+      if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
+    }
+  }
+  __syncthreads();
+  const long long base = s_excl;
+  const int shift = (int)(base % VS);
+  if (!kSeg) {
+    int k = 0;
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j)
+      if ((mask >> j) & 1u) stage[shift + rank + k++] = cur.x[j];
+  } else {
+    // flags of the thread's output positions [pos0, pos0 + c)
+    const long long pos0 = out_base + base + rank;
+    uint64_t bits = 0;
+    if (c) {
+      const long long wd = pos0 >> 5;
+      bits = (((uint64_t)__ldg(&segbits[wd + 1]) << 32) | (uint64_t)__ldg(&segbits[wd])) >> (pos0 & 31);
+    }
+    SegOp::T a = SegOp::identity();
+    {
+      int k = 0;
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j)
+        if ((mask >> j) & 1u) {
+          a = SegOp::op(a, SegOp::T{(long long)cur.x[j], (int)((bits >> k) & 1)});
+          ++k;
+        }
+    }
+    SegOp::T inc = warp_inclusive<SegOp>(a);
+    SegOp::T lex = SegOp::shfl_up(inc, 1);
+    if (lane_id() == 0) lex = SegOp::identity();
+    if (lane_id() == 31) s_seg[warp_id()] = inc;
+    __syncthreads();
+    SegOp::T run = SegOp::identity(), tagg = SegOp::identity();
+#pragma unroll
+    for (int w = 0; w < kSWarps; ++w) {
+      if (w < warp_id()) run = SegOp::op(run, s_seg[w]);
+      tagg = SegOp::op(tagg, s_seg[w]);
+    }
+    run = SegOp::op(run, lex);
+    const int shz = (int)(base % VZ);
+    bool narrow = false;
+    int k = 0;
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j)
+      if ((mask >> j) & 1u) {
+        run = SegOp::op(run, SegOp::T{(long long)cur.x[j], (int)((bits >> k) & 1)});
+        if (sizeof(Z) == 4 && run.v != (long long)(int)run.v) narrow = true;
+        stage[shift + rank + k] = cur.x[j];
+        stage_z[shz + rank + k] = (Z)run.v;
+        ++k;
+      }
+    if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+    if (threadIdx.x == 0) meta[tile] = SegTileMeta{tagg.v, (long long)tagg.f, base, (long long)cnt};
+  }
+  __syncthreads();
+  store_aligned<T>(ys, base, cnt, stage);
+  if (kSeg) store_aligned<Z>(zs, base, cnt, stage_z);
+}
+
+// ---------------------------------------------------------------------------
+// partition2 / partition3: class counts (pass 1), stable placement (pass 2).
+// kClasses = 2: class 0 = p x, class 1 = !p x.
+// kClasses = 3: class 0 = p x, class 1 = !p x && q x, class 2 = rest.
+template <typename T, int kClasses>
+IXG_DEV int classify(const ixg_pred& p, const ixg_pred& q, T x) {
+  if (pred_eval(p, (long long)x)) return 0;
+  if (kClasses == 3 && pred_eval(q, (long long)x)) return 1;
+  return kClasses - 1;
+}
+
+// Pass 1: per-CTA class counts, the last CTA adds them up into d_tot
+// (self-resetting through hdr->done).
+template <typename T, int kClasses>
+__global__ void __launch_bounds__(kSThreads) k_class_count(const T* __restrict__ xs, long long n, ixg_pred p,
+                                                           ixg_pred q, long long* partials, LBHeader* hdr,
+                                                           long long* d_tot) {
+  constexpr int V = 16 / (int)sizeof(T);
+  long long c0 = 0, c1 = 0;
+  const long long nv = n / V;
+  const long long stride = (long long)gridDim.x * kSThreads;
+  for (long long i = (long long)blockIdx.x * kSThreads + threadIdx.x; i < nv; i += stride) {
+    T x[V];
+    Vec<T>::unpack(ld_stream_v4(xs + i * V), x);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int c = classify<T, kClasses>(p, q, x[e]);
+      c0 += (c == 0);
+      if (kClasses == 3) c1 += (c == 1);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (long long i = nv * V + threadIdx.x; i < n; i += kSThreads) {
+      const int c = classify<T, kClasses>(p, q, xs[i]);
+      c0 += (c == 0);
+      if (kClasses == 3) c1 += (c == 1);
+    }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    c0 += __shfl_xor_sync(0xffffffffu, c0, d);
+    c1 += __shfl_xor_sync(0xffffffffu, c1, d);
+  }
+  __shared__ long long s0[kSWarps], s1[kSWarps];
+  __shared__ bool s_last;
+  if (lane_id() == 0) {
+    s0[warp_id()] = c0;
+    s1[warp_id()] = c1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long a = 0, b = 0;
+    for (int w = 0; w < kSWarps; ++w) {
+      a += s0[w];
+      b += s1[w];
+    }
+    __stcg(&partials[2 * blockIdx.x], a);
+    __stcg(&partials[2 * blockIdx.x + 1], b);
+    __threadfence();
+    s_last = atomicAdd(&hdr->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    long long a = 0, b = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kSThreads) {
+      a += __ldcg(&partials[2 * i]);
+      b += __ldcg(&partials[2 * i + 1]);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, d);
+      b += __shfl_xor_sync(0xffffffffu, b, d);
+    }
+    if (lane_id() == 0) {
+      s0[warp_id()] = a;
+      s1[warp_id()] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long ta = 0, tb = 0;
+      for (int w = 0; w < kSWarps; ++w) {
+        ta += s0[w];
+        tb += s1[w];
+      }
+      d_tot[0] = ta;
+      if (kClasses == 3) d_tot[1] = tb;
+      hdr->done = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// partition2 / partition3 placement (pass 2; the class totals come from
+// k_class_count).  Class c of a tile is one contiguous run of the output at
+//   (totals of the classes before c) + (class-c elements in earlier tiles),
+// and a thread's class-c elements are consecutive inside it.  The look-back
+// carries the class-0 (and class-1) prefix; the last class's prefix is the
+// tile start minus the others.
+template <typename T, int kClasses>
+__global__ void __launch_bounds__(kSThreads, 3) k_place_s(const T* __restrict__ xs, long long n, ixg_pred p,
+                                                           ixg_pred q, T* __restrict__ ys,
+                                                           const long long* __restrict__ d_tot, LBChan ch,
+                                                           uint32_t nonce) {
+  using M = typename std::conditional<kClasses == 2, SumOp, Sum2Op>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int VS = 32 / (int)sizeof(T);
+  constexpr int SLOT = kSTile + VS;
+  T* stage0 = reinterpret_cast<T*>(smem_raw);
+  T* stage_last = stage0 + SLOT;
+  T* stage1 = stage_last + SLOT;  // partition3 only
+  __shared__ int s_w[kSWarps];
+  __shared__ int s_w1[kSWarps];
+  __shared__ long long s_ex[2];
+
+  const long long tile = blockIdx.x;
+  const long long tile_base = tile * kSTile;
+  const long long i0 = tile_base + threadIdx.x * kSItems;
+  Blk16<T> cur;
+  cur.load(xs, i0, n);
+  const int tile_len = (int)min((long long)kSTile, n - tile_base);
+  const int before = min((int)threadIdx.x * kSItems, tile_len);  // elements of earlier threads
+  const uint32_t vm = valid_mask(i0, n);
+  const uint32_t m0 = select_mask<T>(p, cur.x) & vm;
+  uint32_t m1 = 0;
+  if (kClasses == 3) m1 = select_mask<T>(q, cur.x) & vm & ~m0;
+  const uint32_t m2 = vm & ~m0 & ~m1;
+  const int c0 = __popc(m0), c1 = __popc(m1);
+  int cnt0, cnt1 = 0;
+  const int r0 = cta_exclusive(c0, s_w, &cnt0);
+  int r1 = 0;
+  if (kClasses == 3) r1 = cta_exclusive(c1, s_w1, &cnt1);
+  const int r2 = before - r0 - r1;
+  typename M::T agg;
+  if constexpr (kClasses == 2) agg = typename M::T{cnt0};
+  else agg = typename M::T{cnt0, cnt1};
+  if (threadIdx.x == 0) lb_publish<M>(ch, nonce, tile, agg, tile == 0);
+  if (warp_id() == 0) {
+    typename M::T ex = M::identity();
+    if (tile > 0) ex = lb_lookback<M>(ch, nonce, tile);
+    if (lane_id() == 0) {
+      if constexpr (kClasses == 2) {
+        s_ex[0] = ex.v;
+        s_ex[1] = 0;
+      } else {
+        s_ex[0] = ex.a;
+        s_ex[1] = ex.b;
+      }
+      if (tile > 0) lb_publish<M>(ch, nonce, tile, M::op(ex, agg), true);
+    }
+  }
+  __syncthreads();
+  const long long t0 = d_tot[0];
+  const long long t1 = kClasses == 3 ? d_tot[1] : 0;
+  const long long e0 = s_ex[0], e1 = s_ex[1];
+  const long long e2 = tile_base - e0 - e1;
+  const long long b0 = e0, b1 = t0 + e1, b2 = t0 + t1 + e2;
+  const int sh0 = (int)(b0 % VS), sh1 = (int)(b1 % VS), sh2 = (int)(b2 % VS);
+  int k0 = 0, k1 = 0, k2 = 0;
+#pragma unroll
+  for (int j = 0; j < kSItems; ++j) {
+    if ((m0 >> j) & 1u) stage0[sh0 + r0 + k0++] = cur.x[j];
+    else if (kClasses == 3 && ((m1 >> j) & 1u)) stage1[sh1 + r1 + k1++] = cur.x[j];
+    else if ((m2 >> j) & 1u) stage_last[sh2 + r2 + k2++] = cur.x[j];
+  }
+  __syncthreads();
+  const int cnt2 = tile_len - cnt0 - cnt1;
+  store_aligned<T>(ys, b0, cnt0, stage0);
+  if (kClasses == 3) store_aligned<T>(ys, b1, cnt1, stage1);
+  store_aligned<T>(ys, b2, cnt2, stage_last);
+}
+
+// ---------------------------------------------------------------------------
+// C2 fix-up: carry of the preceding tiles (and of preceding shards, `carry0`)
+// added to each tile's outputs before its first segment start.
+// Pass 1 (one CTA): exclusive segmented scan over the tile aggregates.
+__global__ void __launch_bounds__(1024) k_seg_tile_scan(SegTileMeta* __restrict__ meta, long long ntiles,
+                                                        long long carry_v, int carry_f) {
+  __shared__ SegOp::T s_w[32];
+  __shared__ SegOp::T s_carry;
+  if (threadIdx.x == 0) s_carry = SegOp::T{carry_v, carry_f};
+  __syncthreads();
+  for (long long b = 0; b < ntiles; b += blockDim.x) {
+    const long long t = b + threadIdx.x;
+    SegOp::T x = SegOp::identity();
+    if (t < ntiles) x = SegOp::T{meta[t].v, (int)meta[t].f};
+    SegOp::T inc = warp_inclusive<SegOp>(x);
+    if (lane_id() == 31) s_w[warp_id()] = inc;
+    __syncthreads();
+    SegOp::T pre = s_carry;
+    for (int w = 0; w < warp_id(); ++w) pre = SegOp::op(pre, s_w[w]);
+    SegOp::T lex = SegOp::shfl_up(inc, 1);
+    if (lane_id() == 0) lex = SegOp::identity();
+    const SegOp::T ex = SegOp::op(pre, lex);
+    __syncthreads();
+    if (t < ntiles) meta[t].v = ex.v;  // carry INTO tile t (value since the last flag)
+    if (threadIdx.x == blockDim.x - 1) s_carry = SegOp::op(ex, x);
+    __syncthreads();
+  }
+}
+
+// Pass 2: zs[q] += carry(tile) for q in [base, first flag of the tile).
+template <typename Z>
+__global__ void __launch_bounds__(256) k_seg_fixup(const SegTileMeta* __restrict__ meta, long long ntiles,
+                                                   const uint32_t* __restrict__ segbits, long long out_base,
+                                                   Z* __restrict__ zs, ixg_status* st) {
+  __shared__ long long s_stop;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long c = meta[t].v;
+    const long long base = meta[t].base, cnt = meta[t].cnt;
+    if (c == 0 || cnt == 0) continue;  // uniform per CTA
+    if (warp_id() == 0) {  // first set flag bit in [base, base + cnt)
+      long long stop = base + cnt;
+      for (long long q = base; q < base + cnt; q += 32 * 32) {
+        const long long ql = q + lane_id() * 32;
+        uint32_t w = 0;
+        if (ql < base + cnt) {
+          const long long g = out_base + ql;
+          const long long wd = g >> 5;
+          w = (uint32_t)((((uint64_t)segbits[wd + 1] << 32) | segbits[wd]) >> (g & 31));
+          const long long lim = base + cnt - ql;
+          if (lim < 32) w &= (1u << lim) - 1u;
+        }
+        const uint32_t any = __ballot_sync(0xffffffffu, w != 0);
+        if (any) {
+          const int l = __ffs(any) - 1;
+          const uint32_t wl = __shfl_sync(0xffffffffu, w, l);
+          stop = q + l * 32 + (__ffs(wl) - 1);
+          break;
+        }
+      }
+      if (lane_id() == 0) s_stop = stop;
+    }
+    __syncthreads();
+    const long long stop = s_stop;
+    bool narrow = false;
+    for (long long q = base + threadIdx.x; q < stop; q += blockDim.x) {
+      const long long v = (long long)zs[q] + c;
+      if (sizeof(Z) == 4 && v != (long long)(int)v) narrow = true;
+      zs[q] = (Z)v;
+    }
+    if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+    __syncthreads();
+  }
+}
+
+}  // namespace ixg

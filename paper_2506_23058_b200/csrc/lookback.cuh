@@ -2,46 +2,58 @@
 //
 // Every scan on the hot path (scan (+) of oracle.py:281-293, the segmented
 // scan of PAPER.md:399-402, the count/offset scans inside filter/partition)
-// is ONE pass over HBM: a CTA takes a tile ticket, reduces its tile, publishes
-// the aggregate, and warp 0 walks back over its predecessors' published
-// aggregates/prefixes 32 tiles at a time until it meets an inclusive prefix.
+// is ONE pass over HBM: tile t (= blockIdx.x) reduces its elements, publishes
+// the aggregate, and its warp 0 walks back over the predecessors' published
+// aggregates / inclusive prefixes, 32 x kPerLane tiles per L2 round trip,
+// until it meets an inclusive prefix.
 //
 // Tile state = one 16-byte slot per tile, written with one 16-byte store and
-// polled with one 16-byte L2 load (one round trip per 32-tile window):
+// polled with one 16-byte L2 load:
 //   w0 = payload (int64 sum / segmented value / two packed 32-bit counts)
-//   w1 = [epoch:24][status:2][flag:1][pad:5][check:32]
+//   w1 = [nonce:24][status:2][flag:1][pad:5][check:32]
 // status 1 = aggregate, 2 = inclusive prefix.  A slot is first written with
 // its aggregate and later overwritten with its inclusive prefix; `check`
-// (a function of w0 and the epoch) lets a reader reject a torn read of the
-// two 8-byte halves and retry.
+// (a function of w0 and the nonce) lets a reader reject a torn read of the
+// two 8-byte halves and retry.  The nonce is a per-launch value from the
+// host, so slots left by earlier launches are never mistaken for current
+// ones and the workspace is never reset.
 //
-// Forward progress on sm_100a: tiles are handed out by an atomic ticket
-// (not blockIdx), so a CTA only ever waits on tiles owned by CTAs that are
-// already resident.
-//
-// The workspace is self-resetting: slots carry a 24-bit launch epoch, and
-// the last CTA of a launch bumps the epoch and zeroes the ticket, so a
-// zero-initialised workspace can be reused by any number of stream-ordered
-// launches without a memset.
+// Slots of consecutive tiles are kSlotStride x 16 B apart: every warp that
+// is looking back polls the slots of the most recent tiles, and packed slots
+// put all of that traffic on a handful of L2 lines (one LTS slice).
+// Measured at 2^28 (tools/_ab2.sh): stride 8 + a 32-tile window is the best
+// of {stride 1, 8, 16} x {32, 64, 128, 512}-tile windows -- wider windows
+// cost more in polling traffic than they save in walk length.
 #pragma once
 #include "common.cuh"
 
 namespace ixg {
 
-struct LBHeader {
+struct LBHeader {  // scratch words of the non-scan kernels (scatter dup flag, count partials)
   unsigned int ticket;
   unsigned int done;
   unsigned int epoch;
-  unsigned int dup;  // scatter: "a destination was claimed twice" (self-reset by verify)
+  unsigned int dup;
 };
 
 struct LBChan {
   LBHeader* hdr;
-  ulonglong2* slot;  // [tiles]
+  ulonglong2* slot;  // [tiles * kSlotStride]
 };
 
 constexpr uint32_t kStAgg = 1, kStIncl = 2;
-constexpr uint32_t kEpochMask = 0xffffffu;
+constexpr uint32_t kNonceMask = 0xffffffu;
+
+#ifndef IXG_SLOT_STRIDE
+#define IXG_SLOT_STRIDE 8
+#endif
+#ifndef IXG_LB_PER_LANE
+#define IXG_LB_PER_LANE 1
+#endif
+constexpr int kSlotStride = IXG_SLOT_STRIDE;
+constexpr int kPerLane = IXG_LB_PER_LANE;
+
+IXG_DEV ulonglong2* slot_at(const LBChan& ch, long long tile) { return ch.slot + tile * kSlotStride; }
 
 // ------------------------------------------------------------ monoids
 // payload(): value -> (w0, flag bit);  from(): (w0, flag) -> value
@@ -98,70 +110,36 @@ struct SegOp {
 };
 
 // ------------------------------------------------------------ slot codec
-IXG_DEV uint32_t slot_check(unsigned long long w0, uint32_t epoch) {
-  return (uint32_t)w0 ^ (uint32_t)(w0 >> 32) ^ (epoch * 0x9E3779B1u) ^ 0x5bd1e995u;
+IXG_DEV uint32_t slot_check(unsigned long long w0, uint32_t nonce) {
+  return (uint32_t)w0 ^ (uint32_t)(w0 >> 32) ^ (nonce * 0x9E3779B1u) ^ 0x5bd1e995u;
 }
-IXG_DEV void slot_store(ulonglong2* p, unsigned long long w0, uint32_t epoch, uint32_t status, uint32_t flag) {
-  const unsigned long long w1 = ((unsigned long long)((epoch << 8) | (status << 6) | (flag << 5)) << 32) |
-                                (unsigned long long)slot_check(w0, epoch);
+IXG_DEV void slot_store(ulonglong2* p, unsigned long long w0, uint32_t nonce, uint32_t status, uint32_t flag) {
+  const unsigned long long w1 = ((unsigned long long)((nonce << 8) | (status << 6) | (flag << 5)) << 32) |
+                                (unsigned long long)slot_check(w0, nonce);
   asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
 }
 // returns status (0 = not ready / stale / torn)
-IXG_DEV uint32_t slot_load(const ulonglong2* p, uint32_t epoch, unsigned long long* w0, uint32_t* flag) {
+IXG_DEV uint32_t slot_load(const ulonglong2* p, uint32_t nonce, unsigned long long* w0, uint32_t* flag) {
   unsigned long long a, b;
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
   const uint32_t hi = (uint32_t)(b >> 32);
-  if ((hi >> 8) != epoch || (uint32_t)b != slot_check(a, epoch)) return 0;
+  if ((hi >> 8) != nonce || (uint32_t)b != slot_check(a, nonce)) return 0;
   *w0 = a;
   *flag = (hi >> 5) & 1u;
   return (hi >> 6) & 3u;
 }
 
-// ------------------------------------------------------------ tile protocol
-// Called by thread 0: take a ticket and read the launch epoch.
-IXG_DEV void lb_ticket(const LBChan& ch, long long* tile, uint32_t* epoch) {
-  volatile LBHeader* h = ch.hdr;
-  *epoch = h->epoch & kEpochMask;
-  *tile = (long long)atomicAdd(&ch.hdr->ticket, 1u);
-}
-IXG_DEV uint32_t lb_epoch(const LBChan& ch) { return ((volatile LBHeader*)ch.hdr)->epoch & kEpochMask; }
-
-// Called by thread 0 at the very end of the CTA: the last CTA resets the header.
-IXG_DEV void lb_retire(const LBChan& ch, uint32_t epoch) {
-  __threadfence();
-  unsigned int prev = atomicAdd(&ch.hdr->done, 1u);
-  if (prev == gridDim.x - 1) {
-    volatile LBHeader* h = ch.hdr;
-    h->ticket = 0;
-    h->done = 0;
-    h->epoch = (epoch + 1) & kEpochMask;
-    __threadfence();
-  }
-}
-
 template <class M>
-IXG_DEV void lb_publish(const LBChan& ch, uint32_t epoch, long long tile, typename M::T v, bool inclusive) {
+IXG_DEV void lb_publish(const LBChan& ch, uint32_t nonce, long long tile, typename M::T v, bool inclusive) {
   uint32_t f;
   const unsigned long long w = M::payload(v, &f);
-  slot_store(&ch.slot[tile], w, epoch, inclusive ? kStIncl : kStAgg, f);
+  slot_store(slot_at(ch, tile), w, nonce, inclusive ? kStIncl : kStAgg, f);
 }
 
 // Warp-collective (all 32 lanes of one warp): exclusive prefix of `tile`
 // (tile > 0) from its predecessors.
-//
-// Window = 32 lanes x kPerLane tiles = 256 predecessors per L2 round trip.
-// The window must cover every tile whose look-back is still in flight
-// (aggregate published, inclusive prefix not yet): that lag is one round
-// trip r (~0.5-1 us under load) / tile interval delta (~4 ns for a 4096
-// x int32 tile at 6.5 TB/s) ~ 150-250 tiles.  A 32-tile window cannot
-// cover it and the walk degenerates into many serial round trips.
-#ifndef IXG_LB_PER_LANE
-#define IXG_LB_PER_LANE 8
-#endif
-constexpr int kPerLane = IXG_LB_PER_LANE;
-
 template <class M>
-IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t epoch, long long tile) {
+IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long tile) {
   using T = typename M::T;
   const int lane = lane_id();
   T excl = M::identity();
@@ -176,7 +154,7 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t epoch, long long ti
       st[j] = kStIncl;  // virtual inclusive identity before tile 0
       w[j] = 0;
       f[j] = 0;
-      if (idx >= 0) st[j] = slot_load(&ch.slot[idx], epoch, &w[j], &f[j]);
+      if (idx >= 0) st[j] = slot_load(slot_at(ch, idx), nonce, &w[j], &f[j]);
     }
     // re-poll only the slots that were not ready
     int spins = 0;
@@ -189,7 +167,7 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t epoch, long long ti
 #pragma unroll
       for (int j = 0; j < kPerLane; ++j) {
         const long long idx = pred - (lane * kPerLane + j);
-        if (st[j] == 0) st[j] = slot_load(&ch.slot[idx], epoch, &w[j], &f[j]);
+        if (st[j] == 0) st[j] = slot_load(slot_at(ch, idx), nonce, &w[j], &f[j]);
       }
     }
     // this lane's newest inclusive slot (kPerLane = none)

@@ -380,6 +380,7 @@ class Interp:
         if name in self.funs:
             sub = Interp.__new__(Interp)
             sub.__dict__.update(self.__dict__)
+            sub.as_tensors = True  # arrays stay on the device between calls
             vals = [ev(a) for a in e.args]
             return sub.call(name, vals)
         fn = ev(e.fun) if ir.kind(e.fun) != "Lambda" else e.fun
