@@ -285,6 +285,9 @@ int ixg_map(const ixg_vm_insn* prog, int ninsn, const ixg_array* ins, int nins, 
 #define IXG_K_SCATTER 5      /* k_scatter                                  */
 #define IXG_K_CSR_GATHER 6   /* k_csr_gather                               */
 int ixg_timer_start(int kernel_id);
+/* development builds (-DIXG_TRACE) only: per-CTA %globaltimer trace of the
+ * compaction kernels; IXG_BADARG otherwise */
+int ixg_trace_read(unsigned long long* host, size_t count);
 /* synchronises the recorded events; total device time (ms) and launch count */
 int ixg_timer_stop(double* total_ms, int64_t* launches);
 

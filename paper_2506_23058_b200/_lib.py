@@ -84,6 +84,7 @@ SIGNATURES = {
     "ixg_mkflags": (_I, [_I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
     "ixg_map": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _I64, _I, _P, _P]),
     "ixg_timer_start": (_I, [_I]),
+    "ixg_trace_read": (_I, [_P, _SZ]),
     "ixg_timer_stop": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
 }
 K_FILTER_FUSED, K_PLACE, K_CLASS_COUNT, K_SCAN, K_SCATTER, K_CSR_GATHER = 1, 2, 3, 4, 5, 6

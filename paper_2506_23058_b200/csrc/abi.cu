@@ -168,7 +168,7 @@ int launch_filter_p(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
     allow_smem(kern, smem);
     attr = true;
   }
-  kern<<<(unsigned)tiles, kSThreads, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, ch, next_nonce(), d_count,
+  kern<<<(unsigned)tiles, kNT, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, ch, next_nonce(), d_count,
                                                 meta, st);
   LAUNCHED();
   CHECK_LAUNCH();
@@ -252,7 +252,7 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
     }
     {
       TimedLaunch tl(IXG_K_PLACE, s);
-      kern<<<(unsigned)tiles_of(n, kSTile), kSThreads, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0, next_nonce());
+      kern<<<(unsigned)tiles_of(n, kSTile), kNT, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0, next_nonce());
     }
     LAUNCHED();
     CHECK_LAUNCH();
@@ -348,6 +348,18 @@ int ixg_device_check(void) {
 }
 
 unsigned long long ixg_launch_count(void) { return g_launches.load(); }
+
+int ixg_trace_read(unsigned long long* host, size_t count) {
+#ifdef IXG_TRACE
+  const size_t cap = sizeof(g_trace) / sizeof(g_trace[0]);
+  if (count > cap) count = cap;
+  return cuda_rc(cudaMemcpyFromSymbol(host, g_trace, count * sizeof(unsigned long long)));
+#else
+  (void)host;
+  (void)count;
+  return IXG_BADARG;
+#endif
+}
 
 int ixg_timer_start(int kernel_id) {
   g_timer.target = kernel_id;

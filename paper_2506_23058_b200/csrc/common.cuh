@@ -138,6 +138,26 @@ struct Vec<long long> {
   }
 };
 
+// ---------------------------------------------------------------- tracing
+// Build with -DIXG_TRACE to record %globaltimer at fixed points of the
+// compaction kernels (thread 0 of the first 2^17 CTAs); read with
+// ixg_trace_read().  Compiled out otherwise.
+#ifdef IXG_TRACE
+__device__ unsigned long long g_trace[(1 << 17) * 8];
+#define IXG_TR(slot)                                                        \
+  do {                                                                      \
+    if (threadIdx.x == 0 && blockIdx.x < (1u << 17)) {                      \
+      unsigned long long t__;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));               \
+      g_trace[blockIdx.x * 8 + (slot)] = t__;                               \
+    }                                                                       \
+  } while (0)
+#else
+#define IXG_TR(slot) \
+  do {               \
+  } while (0)
+#endif
+
 inline int num_sms() {
   static int sms = 0;
   if (!sms) {

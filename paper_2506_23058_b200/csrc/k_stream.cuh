@@ -10,30 +10,28 @@
 // scatter collapses into a stable compaction inside the scan tile: xs is read
 // once, ys (and zs) written once.
 //
-// Shape of the kernel (chosen by measurement):
-//   * one CTA per 4096-element tile, tile = blockIdx.x (CTAs are dispatched in
-//     index order, so a CTA only waits on tiles already resident or done --
-//     the same forward-progress argument CUB's single-pass scan relies on);
-//     no ticket or retire atomics on the critical path, and the look-back
-//     slots are tagged with a per-launch nonce passed by the host, so the
-//     workspace never needs a reset;
-//     (a persistent, ticket-driven variant with register prefetch measured
-//     2-3x SLOWER: all CTAs reach their look-back in lock-step and the walk
-//     spans the whole previous wave)
-//   * blocked layout: 16 consecutive elements per thread via two 256-bit
-//     loads (LDG.E.256); a thread's selected elements are consecutive in the
+// Shape of the kernels (chosen by measurement):
+//   * one CTA per tile of NT x 16 elements, tile = blockIdx.x (CTAs are
+//     dispatched in index order, so a CTA only waits on tiles already
+//     resident or done -- the forward-progress argument CUB's single-pass
+//     scan relies on); no ticket/retire atomics, and the look-back slots are
+//     tagged with a per-launch nonce from the host so the workspace never
+//     needs a reset.  A persistent ticket-driven variant with register
+//     prefetch measured 2-3x slower (all CTAs reach their look-back in
+//     lock-step).  The look-back resolves ~32 tiles per L2 round trip, so
+//     throughput scales with the tile size: NT = 512 (8192 elements).
+//   * blocked layout: 16 consecutive elements per thread via 256-bit loads
+//     (LDG.E.256); a thread's selected elements are consecutive in the
 //     output, so ranks are one popc + a warp/CTA prefix of per-thread counts
-//     and the segmented sum of C2 is a serial fold per thread plus one warp
-//     scan -- no shared-memory transpose, ~6x fewer instructions per element
-//     than a ballot-per-element ranking;
+//     and the segmented sum of C2 is a per-thread fold plus one warp scan.
 //   * the compacted run is staged in shared memory at its global 32-byte
 //     phase and written with aligned 256-bit stores (scalar only at the two
-//     run ends);
+//     run ends).
 //   * C2 needs only the count look-back: the segmented sum is computed with a
-//     tile-local carry and each tile's aggregate is written out; a small
-//     fix-up pass (k_seg_tile_scan + k_seg_fixup) adds the carry of the
-//     preceding tiles to the tile's output prefix before its first segment
-//     start (segments average 128 elements at C2: a few % of zs).
+//     tile-local carry and each tile's aggregate is written out; a fix-up
+//     pass (k_seg_tile_scan + k_seg_fixup) adds the carry of the preceding
+//     tiles to the tile's output prefix before its first segment start
+//     (segments average 128 elements at C2: a few % of zs).
 #pragma once
 #include <type_traits>
 
@@ -41,10 +39,14 @@
 
 namespace ixg {
 
-constexpr int kSThreads = 256;
+constexpr int kSThreads = 256;  // non-tiled helper kernels
 constexpr int kSItems = 16;
-constexpr int kSTile = kSThreads * kSItems;  // 4096
 constexpr int kSWarps = kSThreads / 32;
+#ifndef IXG_STREAM_THREADS
+#define IXG_STREAM_THREADS 512
+#endif
+constexpr int kNT = IXG_STREAM_THREADS;  // threads of the compaction kernels
+constexpr int kSTile = kNT * kSItems;    // elements per tile
 
 IXG_DEV void ld256(const void* p, uint32_t (&r)[8]) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -113,6 +115,7 @@ IXG_DEV uint32_t select_mask(const ixg_pred& p, const T (&x)[kSItems]) {
 
 // CTA-wide exclusive prefix of per-thread counts; returns the thread's
 // exclusive prefix, *total = the CTA total.  Contains one __syncthreads.
+template <int NT>
 IXG_DEV int cta_exclusive(int c, int* s_w, int* total) {
   const int lane = lane_id(), w = warp_id();
   int inc = c;
@@ -125,7 +128,7 @@ IXG_DEV int cta_exclusive(int c, int* s_w, int* total) {
   __syncthreads();
   int pre = 0, tot = 0;
 #pragma unroll
-  for (int k = 0; k < kSWarps; ++k) {
+  for (int k = 0; k < NT / 32; ++k) {
     const int v = s_w[k];
     pre += (k < w) ? v : 0;
     tot += v;
@@ -136,13 +139,13 @@ IXG_DEV int cta_exclusive(int c, int* s_w, int* total) {
 
 // store the run staged at stage[shift .. shift+cnt) (shift = base % VS, i.e.
 // stage index = (g - base) + shift for global position g) to out[base ..]
-template <typename E>
+template <typename E, int NT>
 IXG_DEV void store_aligned(E* __restrict__ out, long long base, int cnt, const E* stage) {
   constexpr int VS = 32 / (int)sizeof(E);
   if (cnt <= 0) return;
   const long long c0 = base / VS, c1 = (base + cnt - 1) / VS;
   const int shift = (int)(base - c0 * VS);
-  for (long long c = c0 + threadIdx.x; c <= c1; c += kSThreads) {
+  for (long long c = c0 + threadIdx.x; c <= c1; c += NT) {
     const int q0 = (int)(c - c0) * VS;
     const long long g0 = c * VS;
     if (g0 >= base && g0 + VS <= base + cnt) {
@@ -173,24 +176,26 @@ struct SegTileMeta {
 // ---------------------------------------------------------------------------
 // filter / filter_by [+ sgmSum over the output with flags from a bitmap]
 template <typename T, typename Z, bool kByCs, bool kSeg>
-__global__ void __launch_bounds__(kSThreads, 4) k_filter_s(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
-                                                            long long n, ixg_pred p, T* __restrict__ ys,
-                                                            Z* __restrict__ zs, const uint32_t* __restrict__ segbits,
-                                                            long long out_base, LBChan ch, uint32_t nonce,
-                                                            long long* d_count, SegTileMeta* __restrict__ meta,
-                                                            ixg_status* st) {
+__global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
+                                                      long long n, ixg_pred p, T* __restrict__ ys,
+                                                      Z* __restrict__ zs, const uint32_t* __restrict__ segbits,
+                                                      long long out_base, LBChan ch, uint32_t nonce,
+                                                      long long* d_count, SegTileMeta* __restrict__ meta,
+                                                      ixg_status* st) {
+  constexpr int NT = kNT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int VS = 32 / (int)sizeof(T);
   constexpr int VZ = 32 / (int)sizeof(Z);
   T* stage = reinterpret_cast<T*>(smem_raw);
   Z* stage_z = reinterpret_cast<Z*>(smem_raw + (kSTile + VS) * sizeof(T));
-  __shared__ int s_w[kSWarps];
+  __shared__ int s_w[NT / 32];
   __shared__ long long s_excl;
-  __shared__ SegOp::T s_seg[kSWarps];
+  __shared__ SegOp::T s_seg[NT / 32];
 
   const long long tile = blockIdx.x;
   const long long i0 = tile * kSTile + threadIdx.x * kSItems;
   Blk16<T> cur;
+  IXG_TR(0);
   cur.load(xs, i0, n);
   uint32_t mask;
   if (kByCs) {
@@ -201,8 +206,10 @@ __global__ void __launch_bounds__(kSThreads, 4) k_filter_s(const T* __restrict__
     mask = select_mask<T>(p, cur.x) & valid_mask(i0, n);
   }
   const int c = __popc(mask);
+  IXG_TR(1);
   int cnt;
-  const int rank = cta_exclusive(c, s_w, &cnt);
+  const int rank = cta_exclusive<NT>(c, s_w, &cnt);
+  IXG_TR(2);
   if (threadIdx.x == 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
   if (warp_id() == 0) {
     long long ex = 0;
@@ -213,62 +220,123 @@ __global__ void __launch_bounds__(kSThreads, 4) k_filter_s(const T* __restrict__
       if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
     }
   }
+  IXG_TR(3);
   __syncthreads();
+  IXG_TR(4);
   const long long base = s_excl;
   const int shift = (int)(base % VS);
-  if (!kSeg) {
-    int k = 0;
+  int idx = shift + rank;
 #pragma unroll
-    for (int j = 0; j < kSItems; ++j)
-      if ((mask >> j) & 1u) stage[shift + rank + k++] = cur.x[j];
-  } else {
-    // flags of the thread's output positions [pos0, pos0 + c)
+  for (int j = 0; j < kSItems; ++j) {
+    if ((mask >> j) & 1u) stage[idx] = cur.x[j];
+    idx += (mask >> j) & 1u;
+  }
+  if (kSeg) {
+    // Flags of the thread's c output positions [pos0, pos0 + c) are bits of
+    // the mkFlags bitmap (L2-resident).  Their load depends on `base`, so it
+    // is issued first and the ys run is written while it is in flight.
     const long long pos0 = out_base + base + rank;
-    uint64_t bits = 0;
+    const long long wd = pos0 >> 5;
+    uint32_t bw0 = 0, bw1 = 0;
     if (c) {
-      const long long wd = pos0 >> 5;
-      bits = (((uint64_t)__ldg(&segbits[wd + 1]) << 32) | (uint64_t)__ldg(&segbits[wd])) >> (pos0 & 31);
+      bw0 = __ldg(&segbits[wd]);
+      bw1 = __ldg(&segbits[wd + 1]);
     }
-    SegOp::T a = SegOp::identity();
-    {
-      int k = 0;
+    __syncthreads();
+    IXG_TR(5);
+    store_aligned<T, NT>(ys, base, cnt, stage);
+    uint32_t fb = (uint32_t)((((uint64_t)bw1 << 32) | (uint64_t)bw0) >> (pos0 & 31));
+    fb &= (c >= 32) ? 0xffffffffu : ((1u << c) - 1u);
+    // segments average ~128 outputs, so a thread rarely holds a segment
+    // start: expand the (sparse) flag bits to input slots
+    uint32_t fm = 0;
+    while (fb) {
+      const int b = __ffs(fb) - 1;
+      fb &= fb - 1;
+      fm |= 1u << __fns(mask, 0, b + 1);
+    }
+    // thread aggregate: (has flag, sum of the selected values from its last flag on)
+    const uint32_t tail = fm ? (mask & ~((1u << (31 - __clz(fm))) - 1u)) : mask;
+    long long s64;
+    if constexpr (sizeof(T) == 4) {
+      int s32 = 0, ovf = 0;
 #pragma unroll
-      for (int j = 0; j < kSItems; ++j)
-        if ((mask >> j) & 1u) {
-          a = SegOp::op(a, SegOp::T{(long long)cur.x[j], (int)((bits >> k) & 1)});
-          ++k;
-        }
+      for (int j = 0; j < kSItems; ++j) {
+        const int xv = ((tail >> j) & 1u) ? (int)cur.x[j] : 0;
+        const int r = s32 + xv;
+        ovf |= (s32 ^ r) & (xv ^ r);
+        s32 = r;
+      }
+      if (ovf < 0) {  // rare: redo in 64 bits
+        s64 = 0;
+#pragma unroll
+        for (int j = 0; j < kSItems; ++j) s64 += ((tail >> j) & 1u) ? (long long)cur.x[j] : 0LL;
+      } else {
+        s64 = s32;
+      }
+    } else {
+      s64 = 0;
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j) s64 += ((tail >> j) & 1u) ? (long long)cur.x[j] : 0LL;
     }
+    const SegOp::T a{s64, fm != 0};
     SegOp::T inc = warp_inclusive<SegOp>(a);
     SegOp::T lex = SegOp::shfl_up(inc, 1);
     if (lane_id() == 0) lex = SegOp::identity();
     if (lane_id() == 31) s_seg[warp_id()] = inc;
     __syncthreads();
-    SegOp::T run = SegOp::identity(), tagg = SegOp::identity();
+    SegOp::T pre = SegOp::identity(), tagg = SegOp::identity();
 #pragma unroll
-    for (int w = 0; w < kSWarps; ++w) {
-      if (w < warp_id()) run = SegOp::op(run, s_seg[w]);
+    for (int w = 0; w < NT / 32; ++w) {
+      if (w < warp_id()) pre = SegOp::op(pre, s_seg[w]);
       tagg = SegOp::op(tagg, s_seg[w]);
     }
-    run = SegOp::op(run, lex);
-    const int shz = (int)(base % VZ);
+    const long long start = SegOp::op(pre, lex).v;
+    const int iz0 = (int)(base % VZ) + rank;
     bool narrow = false;
-    int k = 0;
+    if constexpr (sizeof(T) == 4 && sizeof(Z) == 4) {
+      // every run value is a zs value, so 32-bit arithmetic with an
+      // overflow check is exact whenever zs fits its int32 storage
+      int run = (int)start, ovf = 0, iz = iz0;
+      narrow = start != (long long)run;
 #pragma unroll
-    for (int j = 0; j < kSItems; ++j)
-      if ((mask >> j) & 1u) {
-        run = SegOp::op(run, SegOp::T{(long long)cur.x[j], (int)((bits >> k) & 1)});
-        if (sizeof(Z) == 4 && run.v != (long long)(int)run.v) narrow = true;
-        stage[shift + rank + k] = cur.x[j];
-        stage_z[shz + rank + k] = (Z)run.v;
-        ++k;
+      for (int j = 0; j < kSItems; ++j) {
+        const uint32_t sel = (mask >> j) & 1u;
+        const int b = ((fm >> j) & 1u) ? 0 : run;
+        const int r = b + (int)cur.x[j];
+        if (sel) {
+          ovf |= (b ^ r) & ((int)cur.x[j] ^ r);
+          run = r;
+          stage_z[iz] = (Z)r;
+        }
+        iz += sel;
       }
+      narrow |= ovf < 0;
+    } else {
+      long long run = start, hi = 0;
+      int iz = iz0;
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j) {
+        const uint32_t sel = (mask >> j) & 1u;
+        const long long nv = (((fm >> j) & 1u) ? 0LL : run) + (long long)cur.x[j];
+        run = sel ? nv : run;
+        if (sel) stage_z[iz] = (Z)run;
+        iz += sel;
+        if (sizeof(Z) == 4) hi |= (run >> 31) ^ (run >> 63);  // nonzero iff run leaves int32
+      }
+      narrow = hi != 0;
+    }
     if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
     if (threadIdx.x == 0) meta[tile] = SegTileMeta{tagg.v, (long long)tagg.f, base, (long long)cnt};
+    __syncthreads();
+    store_aligned<Z, NT>(zs, base, cnt, stage_z);
+    IXG_TR(6);
+  } else {
+    __syncthreads();
+    IXG_TR(5);
+    store_aligned<T, NT>(ys, base, cnt, stage);
+    IXG_TR(6);
   }
-  __syncthreads();
-  store_aligned<T>(ys, base, cnt, stage);
-  if (kSeg) store_aligned<Z>(zs, base, cnt, stage_z);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,13 +356,14 @@ template <typename T, int kClasses>
 __global__ void __launch_bounds__(kSThreads) k_class_count(const T* __restrict__ xs, long long n, ixg_pred p,
                                                            ixg_pred q, long long* partials, LBHeader* hdr,
                                                            long long* d_tot) {
-  constexpr int V = 16 / (int)sizeof(T);
+  constexpr int V = 32 / (int)sizeof(T);
   long long c0 = 0, c1 = 0;
   const long long nv = n / V;
   const long long stride = (long long)gridDim.x * kSThreads;
   for (long long i = (long long)blockIdx.x * kSThreads + threadIdx.x; i < nv; i += stride) {
-    T x[V];
-    Vec<T>::unpack(ld_stream_v4(xs + i * V), x);
+    uint32_t r[8];
+    ld256(xs + i * V, r);
+    const T* x = reinterpret_cast<const T*>(r);
 #pragma unroll
     for (int e = 0; e < V; ++e) {
       const int c = classify<T, kClasses>(p, q, x[e]);
@@ -362,18 +431,16 @@ __global__ void __launch_bounds__(kSThreads) k_class_count(const T* __restrict__
   }
 }
 
-// ---------------------------------------------------------------------------
-// partition2 / partition3 placement (pass 2; the class totals come from
-// k_class_count).  Class c of a tile is one contiguous run of the output at
-//   (totals of the classes before c) + (class-c elements in earlier tiles),
-// and a thread's class-c elements are consecutive inside it.  The look-back
-// carries the class-0 (and class-1) prefix; the last class's prefix is the
-// tile start minus the others.
+// Pass 2: placement.  Class c of a tile is one contiguous run of the output
+// at (totals of the classes before c) + (class-c elements in earlier
+// tiles), and a thread's class-c elements are consecutive inside it.  The
+// look-back carries the class-0 (and class-1) prefix; the last class's
+// prefix is the tile start minus the others.
 template <typename T, int kClasses>
-__global__ void __launch_bounds__(kSThreads, 3) k_place_s(const T* __restrict__ xs, long long n, ixg_pred p,
-                                                           ixg_pred q, T* __restrict__ ys,
-                                                           const long long* __restrict__ d_tot, LBChan ch,
-                                                           uint32_t nonce) {
+__global__ void __launch_bounds__(kNT, 2) k_place_s(const T* __restrict__ xs, long long n, ixg_pred p, ixg_pred q,
+                                                     T* __restrict__ ys, const long long* __restrict__ d_tot,
+                                                     LBChan ch, uint32_t nonce) {
+  constexpr int NT = kNT;
   using M = typename std::conditional<kClasses == 2, SumOp, Sum2Op>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int VS = 32 / (int)sizeof(T);
@@ -381,8 +448,8 @@ __global__ void __launch_bounds__(kSThreads, 3) k_place_s(const T* __restrict__ 
   T* stage0 = reinterpret_cast<T*>(smem_raw);
   T* stage_last = stage0 + SLOT;
   T* stage1 = stage_last + SLOT;  // partition3 only
-  __shared__ int s_w[kSWarps];
-  __shared__ int s_w1[kSWarps];
+  __shared__ int s_w[NT / 32];
+  __shared__ int s_w1[NT / 32];
   __shared__ long long s_ex[2];
 
   const long long tile = blockIdx.x;
@@ -397,11 +464,10 @@ __global__ void __launch_bounds__(kSThreads, 3) k_place_s(const T* __restrict__ 
   uint32_t m1 = 0;
   if (kClasses == 3) m1 = select_mask<T>(q, cur.x) & vm & ~m0;
   const uint32_t m2 = vm & ~m0 & ~m1;
-  const int c0 = __popc(m0), c1 = __popc(m1);
   int cnt0, cnt1 = 0;
-  const int r0 = cta_exclusive(c0, s_w, &cnt0);
+  const int r0 = cta_exclusive<NT>(__popc(m0), s_w, &cnt0);
   int r1 = 0;
-  if (kClasses == 3) r1 = cta_exclusive(c1, s_w1, &cnt1);
+  if (kClasses == 3) r1 = cta_exclusive<NT>(__popc(m1), s_w1, &cnt1);
   const int r2 = before - r0 - r1;
   typename M::T agg;
   if constexpr (kClasses == 2) agg = typename M::T{cnt0};
@@ -427,19 +493,22 @@ __global__ void __launch_bounds__(kSThreads, 3) k_place_s(const T* __restrict__ 
   const long long e0 = s_ex[0], e1 = s_ex[1];
   const long long e2 = tile_base - e0 - e1;
   const long long b0 = e0, b1 = t0 + e1, b2 = t0 + t1 + e2;
-  const int sh0 = (int)(b0 % VS), sh1 = (int)(b1 % VS), sh2 = (int)(b2 % VS);
-  int k0 = 0, k1 = 0, k2 = 0;
+  int k0 = (int)(b0 % VS) + r0, k1 = (int)(b1 % VS) + r1, k2 = (int)(b2 % VS) + r2;
 #pragma unroll
   for (int j = 0; j < kSItems; ++j) {
-    if ((m0 >> j) & 1u) stage0[sh0 + r0 + k0++] = cur.x[j];
-    else if (kClasses == 3 && ((m1 >> j) & 1u)) stage1[sh1 + r1 + k1++] = cur.x[j];
-    else if ((m2 >> j) & 1u) stage_last[sh2 + r2 + k2++] = cur.x[j];
+    const uint32_t s0 = (m0 >> j) & 1u, s1 = (m1 >> j) & 1u, s2 = (m2 >> j) & 1u;
+    if (s0) stage0[k0] = cur.x[j];
+    if (kClasses == 3 && s1) stage1[k1] = cur.x[j];
+    if (s2) stage_last[k2] = cur.x[j];
+    k0 += s0;
+    k1 += s1;
+    k2 += s2;
   }
   __syncthreads();
   const int cnt2 = tile_len - cnt0 - cnt1;
-  store_aligned<T>(ys, b0, cnt0, stage0);
-  if (kClasses == 3) store_aligned<T>(ys, b1, cnt1, stage1);
-  store_aligned<T>(ys, b2, cnt2, stage_last);
+  store_aligned<T, NT>(ys, b0, cnt0, stage0);
+  if (kClasses == 3) store_aligned<T, NT>(ys, b1, cnt1, stage1);
+  store_aligned<T, NT>(ys, b2, cnt2, stage_last);
 }
 
 // ---------------------------------------------------------------------------

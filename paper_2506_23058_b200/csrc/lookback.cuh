@@ -144,7 +144,28 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long ti
   const int lane = lane_id();
   T excl = M::identity();
   long long pred = tile - 1;
+#ifdef IXG_TRACE
+  unsigned int tr_rounds = 0, tr_spins = 0;
+#endif
+  // wait (one lane, one slot) until the newest predecessor has published;
+  // the older ones almost always have by then, so the window read below is
+  // one round trip instead of 32 lanes polling in a loop
+  if (lane == 0) {
+    unsigned long long w;
+    uint32_t f;
+    int spins = 0;
+    while (slot_load(slot_at(ch, pred), nonce, &w, &f) == 0) {
+      if (++spins > 8) __nanosleep(64);
+#ifdef IXG_TRACE
+      ++tr_spins;
+#endif
+    }
+  }
+  __syncwarp();
   while (true) {
+#ifdef IXG_TRACE
+    ++tr_rounds;
+#endif
     // lane l holds tiles pred - (l*kPerLane + j), j = 0 (newest) .. kPerLane-1
     unsigned long long w[kPerLane];
     uint32_t f[kPerLane], st[kPerLane];
@@ -195,6 +216,9 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long ti
     if (incl_mask) break;
     pred -= 32 * kPerLane;
   }
+#ifdef IXG_TRACE
+  if (lane == 0 && blockIdx.x < (1u << 17)) g_trace[blockIdx.x * 8 + 7] = ((unsigned long long)tr_rounds << 32) | tr_spins;
+#endif
   return excl;
 }
 

@@ -1,0 +1,65 @@
+"""Per-CTA timeline of the compaction kernel (development tool).
+
+Needs a library built with -DIXG_TRACE (IXGPU_LIB=...):
+    python tools/trace_filter.py <filter|c2|partition2> [log2n]
+Prints per-phase durations (ns) over CTAs and the number of CTAs in flight.
+"""
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_23058_b200 import _lib as L  # noqa: E402
+from paper_2506_23058_b200 import gen, ops  # noqa: E402
+from paper_2506_23058_b200.pred import Pred  # noqa: E402
+
+
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "filter"
+    n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 28)
+    dev = torch.device("cuda")
+    st = ops.Status(dev)
+    xs = ops.gen_uniform(n, -128, 127, 0, torch.int32, device=dev)
+    ys = torch.empty(n, dtype=torch.int32, device=dev)
+    zs = torch.empty(n, dtype=torch.int32, device=dev)
+    dk = torch.empty(1, dtype=torch.int64, device=dev)
+    k = int((xs >= 0).sum().item())
+    shape = torch.from_numpy(gen.segment_shape(1, max(1, n >> 8), k)).to(dev)
+    for _ in range(3):
+        if what == "c2":
+            ops.c2(xs, Pred.ge(0), shape, 0, st, ys=ys, zs=zs, d_k=dk)
+        else:
+            ops.filter(xs, Pred.ge(0), 0, st, ys=ys, d_count=dk)
+    torch.cuda.synchronize()
+    lib = L.load()
+    cnt = (1 << 17) * 8
+    buf = (ctypes.c_ulonglong * cnt)()
+    L.check(lib.ixg_trace_read(buf, cnt), "trace")
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8).astype(np.int64)
+    tiles = int(dk.numel() and (n + 8191) // 8192)
+    tiles = min(tiles, a.shape[0])
+    a = a[:tiles]
+    t0 = a[:, 0].min()
+    a[:, :7] -= t0
+    names = ["load", "cta_scan", "lookback", "bar", "stage", "store"]
+    print(f"tiles {tiles}, kernel span {a[:, 6].max() / 1e3:.1f} us")
+    for i, nm in enumerate(names):
+        d = a[:, i + 1] - a[:, i]
+        print(f"  {nm:9s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
+    life = a[:, 6] - a[:, 0]
+    print(f"  life      median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
+    # CTAs in flight at the middle of the kernel
+    mid = a[:, 6].max() / 2
+    print("  in flight at mid:", int(((a[:, 0] <= mid) & (a[:, 6] >= mid)).sum()))
+    starts = np.sort(a[:, 0])
+    print(f"  start interval (median over tiles) {np.median(np.diff(starts)):.1f} ns")
+    rounds, spins = a[:, 7] >> 32, a[:, 7] & 0xFFFFFFFF
+    print(f"  look-back rounds mean {rounds.mean():.2f} max {rounds.max()}, first-slot spins mean {spins.mean():.1f} p90 {np.percentile(spins, 90):.0f}")
+
+
+if __name__ == "__main__":
+    main()
