@@ -284,6 +284,7 @@ int ixg_map(const ixg_vm_insn* prog, int ninsn, const ixg_array* ins, int nins, 
 #define IXG_K_SCAN 4         /* k_scan (every generic single-pass scan)    */
 #define IXG_K_SCATTER 5      /* k_scatter                                  */
 #define IXG_K_CSR_GATHER 6   /* k_csr_gather                               */
+#define IXG_K_SEGSUM 7       /* k_segsum_b (C2 sgmSum pass)                */
 int ixg_timer_start(int kernel_id);
 /* development builds (-DIXG_TRACE) only: per-CTA %globaltimer trace of the
  * compaction kernels; IXG_BADARG otherwise */

@@ -87,7 +87,7 @@ SIGNATURES = {
     "ixg_trace_read": (_I, [_P, _SZ]),
     "ixg_timer_stop": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
 }
-K_FILTER_FUSED, K_PLACE, K_CLASS_COUNT, K_SCAN, K_SCATTER, K_CSR_GATHER = 1, 2, 3, 4, 5, 6
+K_FILTER_FUSED, K_PLACE, K_CLASS_COUNT, K_SCAN, K_SCATTER, K_CSR_GATHER, K_SEGSUM = 1, 2, 3, 4, 5, 6, 7
 
 _lib = None
 _lock = threading.Lock()

@@ -12,6 +12,7 @@
 
 #include "k_generic.cuh"
 #include "k_stream.cuh"
+#include "k_big.cuh"
 #include "k_vm.cuh"
 
 using namespace ixg;
@@ -168,8 +169,55 @@ int launch_filter_p(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
     allow_smem(kern, smem);
     attr = true;
   }
-  kern<<<(unsigned)tiles, kNT, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, ch, next_nonce(), d_count,
+  kern<<<(unsigned)tiles, kNT + 32, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, ch, next_nonce(), d_count,
                                                 meta, st);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+// Big-tile kernels (k_big.cuh) are the default; IXG_BIG=0 selects the
+// register-tiled kernels of k_stream.cuh (kept for A/B measurements).
+inline bool big_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_BIG");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
+template <typename T, bool kByCs>
+int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, LBChan ch,
+                    long long* d_count, cudaStream_t s) {
+  auto kern = k_filter_b<T, kByCs>;
+  static bool attr = false;
+  if (!attr) {
+    allow_smem(kern, Big<T>::SMEM);
+    attr = true;
+  }
+  TimedLaunch tl(IXG_K_FILTER_FUSED, s);
+  kern<<<(unsigned)tiles_of(n, Big<T>::TILE), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(),
+                                                                           d_count);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+// zs = sgmSum over the first *d_n elements of vs (capacity n)
+template <typename T, typename Z>
+int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32_t* bits, long long flag_base, Z* zs,
+                    LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s) {
+  auto kern = k_segsum_b<T, Z>;
+  static bool attr = false;
+  if (!attr) {
+    allow_smem(kern, Big<T>::SMEM);
+    attr = true;
+  }
+  TimedLaunch tl(IXG_K_SEGSUM, s);
+  kern<<<(unsigned)tiles_of(n, Big<T>::TILE), kBT + 32, Big<T>::SMEM, s>>>(vs, n, d_n, bits, flag_base, zs, ch,
+                                                                           next_nonce(), carry_v, carry_f, d_total,
+                                                                           st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -197,10 +245,14 @@ int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T*
   const bool fused = (sb & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;  // Sc1 proved
   ixg_pred pp = p ? *p : ixg_pred{IXG_PRED_TRUE, 0, 0, 0};
   if (fused) {
-    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
+    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));  // >= tiles of either kernel
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
+    if (big_mode()) {
+      if (cs) return launch_filter_b<T, true>(xs, cs, n, pp, ys, c0, d_count, s);
+      return launch_filter_b<T, false>(xs, cs, n, pp, ys, c0, d_count, s);
+    }
     if (cs) return launch_filter_p<T, T, true, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, d_count,
                                                        nullptr, st, s);
     return launch_filter_p<T, T, false, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, d_count, nullptr,
@@ -252,7 +304,7 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
     }
     {
       TimedLaunch tl(IXG_K_PLACE, s);
-      kern<<<(unsigned)tiles_of(n, kSTile), kNT, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0, next_nonce());
+      kern<<<(unsigned)tiles_of(n, kSTile), kNT + 32, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0, next_nonce());
     }
     LAUNCHED();
     CHECK_LAUNCH();
@@ -298,6 +350,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     uint32_t* bits = (uint32_t*)ws.take(bitmap_bytes(n));
     LBChan cs = ws.chan(2, tiles_of(m, kGTile));
     LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
+    LBChan c1 = ws.chan(1, tiles_of(n, kSTile));
     SegTileMeta* meta = (SegTileMeta*)ws.take((size_t)tiles_of(n, kSTile) * sizeof(SegTileMeta) + 64);
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_k, 0, sizeof(long long), s));
@@ -306,6 +359,12 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     LAUNCHED();
     int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
     if (rc) return rc;
+    if (big_mode()) {
+      // ys = filter p xs (one pass), then zs = sgmSum flags ys over the k
+      // outputs (one pass; the flag of output j is bit j of the bitmap)
+      if ((rc = launch_filter_b<T, false>(xs, nullptr, n, pp, ys, c0, d_k, s))) return rc;
+      return launch_segsum_b<T, Z>(ys, n, d_k, bits, 0, zs, c1, 0, 0, nullptr, st, s);
+    }
     if ((rc = launch_filter_p<T, Z, false, true>(xs, nullptr, n, pp, ys, zs, bits, 0, c0, d_k, meta, st, s)))
       return rc;
     return launch_seg_fixup<Z>(meta, n, bits, 0, zs, 0, 0, st, s);

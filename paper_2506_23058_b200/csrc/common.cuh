@@ -52,6 +52,10 @@ IXG_DEV uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+// named barrier over the first `nthreads` threads (id 0 is __syncthreads)
+IXG_DEV void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 IXG_DEV int lane_id() { return threadIdx.x & 31; }
 IXG_DEV int warp_id() { return threadIdx.x >> 5; }
 
@@ -152,9 +156,20 @@ __device__ unsigned long long g_trace[(1 << 17) * 8];
       g_trace[blockIdx.x * 8 + (slot)] = t__;                               \
     }                                                                       \
   } while (0)
+#define IXG_TR_LANE0(slot)                                                  \
+  do {                                                                      \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < (1u << 17)) {               \
+      unsigned long long t__;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));               \
+      g_trace[blockIdx.x * 8 + (slot)] = t__;                               \
+    }                                                                       \
+  } while (0)
 #else
 #define IXG_TR(slot) \
   do {               \
+  } while (0)
+#define IXG_TR_LANE0(slot) \
+  do {                     \
   } while (0)
 #endif
 

@@ -1,0 +1,338 @@
+// k_big.cuh -- big-tile streaming kernels: the tile is staged in shared
+// memory with asynchronous 16-byte copies (cp.async, LDGSTS), so a CTA keeps
+// 64-96 KB of HBM reads in flight without spending registers on them.
+//
+// Why: a %globaltimer trace of the register-tiled kernels
+// showed every CTA spending ~5 us alive for 32 KB of input, most of it behind
+// the look-back (each L2 round trip ~1 us under full HBM load).  Throughput
+// per SM = bytes-in-flight / CTA life, so the lever is bytes per CTA: three
+// 8192-element chunks per tile (96 KB of int32) with ONE look-back per tile,
+// resolved by a dedicated warp while the copies land.
+//
+//   k_filter_b   filter / filter_by: count pass over the staged chunks, one
+//                CTA-wide scan of the packed per-chunk counts, stable
+//                compaction IN PLACE in shared memory (an element's output
+//                slot never lies after its input slot), aligned 256-bit
+//                stores of the run.
+//   k_segsum_b   sgmSum over an array (C2's zs = sgmSum flags ys): flags are
+//                bits of the mkFlags bitmap at the element's own position, so
+//                they are fetched together with the data; the segmented
+//                aggregate of the tile takes the look-back; every thread
+//                writes its 16 results with two 256-bit stores.
+//
+// Shared-memory layout of a thread's 16 elements: one 16*sizeof(T)-byte
+// block per chunk, its 16-byte pieces XOR-swizzled by the thread index so
+// that the LDS.128 reads of a quarter-warp hit 8 distinct bank groups.
+#pragma once
+#include "k_stream.cuh"
+
+namespace ixg {
+
+constexpr int kBW = 16;                 // worker warps
+constexpr int kBT = kBW * 32;           // worker threads
+constexpr int kBChunk = kBT * kSItems;  // 8192 elements per chunk
+
+template <typename T>
+struct Big {
+  static constexpr int P = (int)sizeof(T);           // 16-byte pieces per thread block (16 elements)
+  static constexpr int EP = 16 / (int)sizeof(T);     // elements per piece
+  static constexpr int CH = sizeof(T) == 4 ? 3 : 1;  // chunks per tile (96 KB / 64 KB)
+  static constexpr int PAD = 32 / (int)sizeof(T);    // >= the 32-byte store phase
+  static constexpr int TILE = CH * kBChunk;
+  static constexpr int SMEM = (PAD + TILE) * (int)sizeof(T);
+  IXG_DEV static int swz(int t, int j) { return j ^ ((t * P / 8) & (P - 1)); }
+  // element offset (within the buffer) of piece j of thread t in chunk c
+  IXG_DEV static int piece(int c, int t, int j) { return PAD + c * kBChunk + kSItems * t + swz(t, j) * EP; }
+};
+
+IXG_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+IXG_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+IXG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+IXG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// issue the copies of thread t's blocks for all chunks of the tile
+template <typename T>
+IXG_DEV void big_issue(T* buf, const T* __restrict__ xs, long long n, long long tile_base, int t) {
+  using B = Big<T>;
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+#pragma unroll
+    for (int j = 0; j < B::P; ++j) {
+      const long long ge = tile_base + (long long)c * kBChunk + (long long)kSItems * t + j * B::EP;
+      long long valid = (n - ge) * (long long)sizeof(T);
+      valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+      cp_async16(buf + B::piece(c, t, j), valid ? (const void*)(xs + ge) : (const void*)xs, (int)valid);
+    }
+  }
+  cp_async_commit();
+}
+
+template <typename T>
+IXG_DEV void big_read(const T* buf, int c, int t, T (&x)[kSItems]) {
+  using B = Big<T>;
+#pragma unroll
+  for (int j = 0; j < B::P; ++j) {
+    const uint4 v = *reinterpret_cast<const uint4*>(buf + B::piece(c, t, j));
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int q = 0; q < B::EP; ++q) x[j * B::EP + q] = e[q];
+  }
+}
+
+// CTA-wide exclusive scan of up to 3 per-thread counts (< 2^21 each) packed
+// into one 64-bit value; one named barrier over the kBT workers.
+IXG_DEV unsigned long long cta_exclusive3(unsigned long long v, unsigned long long* s_w, unsigned long long* total) {
+  const int lane = lane_id(), w = warp_id();
+  unsigned long long inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_w[w] = inc;
+  bar_sync(1, kBT);
+  unsigned long long pre = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < kBW; ++k) {
+    const unsigned long long x = s_w[k];
+    pre += (k < w) ? x : 0ull;
+    tot += x;
+  }
+  *total = tot;
+  return pre + inc - v;
+}
+IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) & 0x1fffffull); }
+
+// ---------------------------------------------------------------------------
+template <typename T, bool kByCs>
+__global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
+                                                          long long n, ixg_pred p, T* __restrict__ ys, LBChan ch,
+                                                          uint32_t nonce, long long* d_count) {
+  using B = Big<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* buf = reinterpret_cast<T*>(smem_raw);
+  __shared__ unsigned long long s_w[kBW];
+  __shared__ int s_cnt;
+  __shared__ long long s_excl;
+
+  const long long tile = blockIdx.x;
+  const long long tile_base = tile * B::TILE;
+  const int t = threadIdx.x;
+  if (warp_id() == kBW) {  // look-back warp
+    long long ex = 0;
+    if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
+    if (lane_id() == 0) s_excl = ex;
+    IXG_TR_LANE0(3);
+    bar_sync(2, kBT + 32);
+    if (lane_id() == 0) {
+      const int cnt = s_cnt;
+      if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
+      if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
+    }
+    return;
+  }
+  IXG_TR(0);
+  big_issue<T>(buf, xs, n, tile_base, t);
+  // selection masks of the thread's blocks (filter_by: read cs meanwhile)
+  uint32_t m[B::CH];
+  unsigned long long packed = 0;
+  if (kByCs) {
+#pragma unroll
+    for (int c = 0; c < B::CH; ++c) {
+      const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
+      uint32_t mm = 0;
+      if (g + kSItems <= n) {
+        const uint4 v = *reinterpret_cast<const uint4*>(cs + g);
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < kSItems; ++j) mm |= (uint32_t)(((w4[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0) << j;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kSItems; ++j) mm |= (uint32_t)((g + j < n) && cs[g + j] != 0) << j;
+      }
+      m[c] = mm;
+      packed |= (unsigned long long)__popc(mm) << (21 * c);
+    }
+    cp_async_wait_all();
+  } else {
+    cp_async_wait_all();
+#pragma unroll
+    for (int c = 0; c < B::CH; ++c) {
+      T x[kSItems];
+      big_read<T>(buf, c, t, x);
+      const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
+      m[c] = select_mask<T>(p, x) & valid_mask(g, n);
+      packed |= (unsigned long long)__popc(m[c]) << (21 * c);
+    }
+  }
+  unsigned long long tot;
+  IXG_TR(1);
+  const unsigned long long ex3 = cta_exclusive3(packed, s_w, &tot);
+  IXG_TR(2);
+  int cnt = 0, before[B::CH];
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    before[c] = cnt + field21(ex3, c);
+    cnt += field21(tot, c);
+  }
+  if (t == 0) {
+    s_cnt = cnt;
+    lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
+  }
+  bar_sync(2, kBT + 32);
+  IXG_TR(4);
+  const long long base = s_excl;
+  const int shift = (int)(base % B::PAD);
+  // in-place stable compaction, chunk by chunk: output slot shift + r of
+  // an element never exceeds its input slot PAD + i, and chunk c's outputs
+  // end before chunk c+1's inputs begin
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    T x[kSItems];
+    big_read<T>(buf, c, t, x);
+    bar_sync(1, kBT);
+    int idx = shift + before[c];
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) {
+      if ((m[c] >> j) & 1u) buf[idx] = x[j];
+      idx += (m[c] >> j) & 1u;
+    }
+  }
+  bar_sync(1, kBT);
+  // store buf[shift .. shift + cnt) to ys[base ..] (same convention as store_aligned)
+  IXG_TR(5);
+  store_aligned<T, kBT>(ys, base, cnt, buf);
+  IXG_TR(6);
+}
+
+// ---------------------------------------------------------------------------
+// zs = sgmSum flags vs over n elements; flag of element i = bit (flag_base + i)
+// of `bits` (mkFlags' bitmap over output positions).  Z: zs storage.
+template <typename T, typename Z>
+__global__ void __launch_bounds__(kBT + 32, 2) k_segsum_b(const T* __restrict__ vs, long long n,
+                                                          const long long* __restrict__ d_n,
+                                                          const uint32_t* __restrict__ bits, long long flag_base,
+                                                          Z* __restrict__ zs, LBChan ch, uint32_t nonce,
+                                                          long long carry_v, int carry_f, longlong2* d_total,
+                                                          ixg_status* st) {
+  using B = Big<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* buf = reinterpret_cast<T*>(smem_raw);
+  __shared__ SegOp::T s_w[B::CH][kBW];
+  __shared__ SegOp::T s_agg;
+  __shared__ SegOp::T s_carry;
+
+  if (d_n) n = *d_n;  // length known only on the device (C2: k = filter's count)
+  const long long ntiles = (n + B::TILE - 1) / B::TILE;
+  const long long tile = blockIdx.x;
+  if (tile >= ntiles) return;  // capacity grid: tiles past the data do nothing
+  const long long tile_base = tile * B::TILE;
+  const int t = threadIdx.x;
+  if (warp_id() == kBW) {  // look-back warp
+    SegOp::T ex = SegOp::T{carry_v, carry_f};  // carry into the first tile (earlier shards)
+    if (tile > 0) ex = lb_lookback<SegOp>(ch, nonce, tile);
+    if (lane_id() == 0) s_carry = ex;
+    bar_sync(2, kBT + 32);
+    if (lane_id() == 0) {
+      const SegOp::T incl = SegOp::op(ex, s_agg);
+      if (tile > 0) lb_publish<SegOp>(ch, nonce, tile, incl, true);
+      if (tile == ntiles - 1 && d_total) *d_total = make_longlong2(incl.v, incl.f);
+    }
+    return;
+  }
+  big_issue<T>(buf, vs, n, tile_base, t);
+  // the thread's 16 flag bits per chunk (positions are known up front)
+  uint32_t fl[B::CH];
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
+    const long long pos = flag_base + g;
+    const long long wd = pos >> 5;
+    uint32_t f = 0;
+    if (g < n) f = (uint32_t)((((uint64_t)__ldg(&bits[wd + 1]) << 32) | (uint64_t)__ldg(&bits[wd])) >> (pos & 31));
+    fl[c] = f & valid_mask(g, n);
+  }
+  cp_async_wait_all();
+  SegOp::T a[B::CH];
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    T x[kSItems];
+    big_read<T>(buf, c, t, x);
+    const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
+    const uint32_t vm = valid_mask(g, n);
+    const uint32_t tail = fl[c] ? (vm & ~((1u << (31 - __clz(fl[c]))) - 1u)) : vm;
+    long long s = 0;
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) s += ((tail >> j) & 1u) ? (long long)x[j] : 0LL;
+    a[c] = SegOp::T{s, fl[c] != 0};
+    SegOp::T inc = warp_inclusive<SegOp>(a[c]);
+    if (lane_id() == 31) s_w[c][warp_id()] = inc;
+    SegOp::T lex = SegOp::shfl_up(inc, 1);
+    if (lane_id() == 0) lex = SegOp::identity();
+    a[c] = lex;  // the lane's exclusive prefix within its warp and chunk
+  }
+  bar_sync(1, kBT);
+  // tile aggregate (chunk-major order) and each (chunk, warp) prefix
+  SegOp::T tagg = SegOp::identity();
+  SegOp::T chunk_pre[B::CH];
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    chunk_pre[c] = tagg;
+    SegOp::T wp = SegOp::identity();
+#pragma unroll
+    for (int w = 0; w < kBW; ++w) {
+      if (w < warp_id()) wp = SegOp::op(wp, s_w[c][w]);
+      tagg = SegOp::op(tagg, s_w[c][w]);
+    }
+    chunk_pre[c] = SegOp::op(SegOp::op(chunk_pre[c], wp), a[c]);
+  }
+  if (t == 0) {
+    s_agg = tagg;
+    if (tile == 0) lb_publish<SegOp>(ch, nonce, tile, SegOp::op(SegOp::T{carry_v, carry_f}, tagg), true);
+    else lb_publish<SegOp>(ch, nonce, tile, tagg, false);
+  }
+  bar_sync(2, kBT + 32);
+  const SegOp::T carry = s_carry;
+  bool narrow = false;
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    T x[kSItems];
+    big_read<T>(buf, c, t, x);
+    const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
+    long long run = SegOp::op(carry, chunk_pre[c]).v;
+    Z z[kSItems];
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) {
+      run = (((fl[c] >> j) & 1u) ? 0LL : run) + (long long)x[j];
+      if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
+      z[j] = (Z)run;
+    }
+    if (g + kSItems <= n) {
+      constexpr int ZV = 32 / (int)sizeof(Z);  // elements per 256-bit store
+#pragma unroll
+      for (int v = 0; v < kSItems / ZV; ++v) {
+        uint32_t r[8];
+#pragma unroll
+        for (int e = 0; e < ZV; ++e) {
+          if constexpr (sizeof(Z) == 4) {
+            r[e] = (uint32_t)z[v * ZV + e];
+          } else {
+            r[2 * e] = (uint32_t)(unsigned long long)z[v * ZV + e];
+            r[2 * e + 1] = (uint32_t)((unsigned long long)z[v * ZV + e] >> 32);
+          }
+        }
+        st256(zs + g + v * ZV, r);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j)
+        if (g + j < n) zs[g + j] = z[j];
+    }
+  }
+  if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+}
+
+}  // namespace ixg

@@ -114,7 +114,7 @@ IXG_DEV uint32_t select_mask(const ixg_pred& p, const T (&x)[kSItems]) {
 }
 
 // CTA-wide exclusive prefix of per-thread counts; returns the thread's
-// exclusive prefix, *total = the CTA total.  Contains one __syncthreads.
+// exclusive prefix, *total = the CTA total.  Contains one named barrier (id 1) over the NT worker threads.
 template <int NT>
 IXG_DEV int cta_exclusive(int c, int* s_w, int* total) {
   const int lane = lane_id(), w = warp_id();
@@ -125,7 +125,7 @@ IXG_DEV int cta_exclusive(int c, int* s_w, int* total) {
     if (lane >= d) inc += o;
   }
   if (lane == 31) s_w[w] = inc;
-  __syncthreads();
+  bar_sync(1, NT);
   int pre = 0, tot = 0;
 #pragma unroll
   for (int k = 0; k < NT / 32; ++k) {
@@ -176,12 +176,12 @@ struct SegTileMeta {
 // ---------------------------------------------------------------------------
 // filter / filter_by [+ sgmSum over the output with flags from a bitmap]
 template <typename T, typename Z, bool kByCs, bool kSeg>
-__global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
-                                                      long long n, ixg_pred p, T* __restrict__ ys,
-                                                      Z* __restrict__ zs, const uint32_t* __restrict__ segbits,
-                                                      long long out_base, LBChan ch, uint32_t nonce,
-                                                      long long* d_count, SegTileMeta* __restrict__ meta,
-                                                      ixg_status* st) {
+__global__ void __launch_bounds__(kNT + 32, 2) k_filter_s(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
+                                                           long long n, ixg_pred p, T* __restrict__ ys,
+                                                           Z* __restrict__ zs, const uint32_t* __restrict__ segbits,
+                                                           long long out_base, LBChan ch, uint32_t nonce,
+                                                           long long* d_count, SegTileMeta* __restrict__ meta,
+                                                           ixg_status* st) {
   constexpr int NT = kNT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int VS = 32 / (int)sizeof(T);
@@ -189,10 +189,26 @@ __global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, c
   T* stage = reinterpret_cast<T*>(smem_raw);
   Z* stage_z = reinterpret_cast<Z*>(smem_raw + (kSTile + VS) * sizeof(T));
   __shared__ int s_w[NT / 32];
+  __shared__ int s_cnt;
   __shared__ long long s_excl;
   __shared__ SegOp::T s_seg[NT / 32];
 
   const long long tile = blockIdx.x;
+  if (warp_id() == NT / 32) {
+    // look-back warp: resolves the tile's exclusive prefix while the worker
+    // warps' loads are in flight (it needs only the predecessors' slots)
+    long long ex = 0;
+    if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
+    if (lane_id() == 0) s_excl = ex;
+    IXG_TR_LANE0(3);
+    bar_sync(2, NT + 32);  // the workers have published the aggregate
+    if (lane_id() == 0) {
+      const int cnt = s_cnt;
+      if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
+      if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
+    }
+    return;
+  }
   const long long i0 = tile * kSTile + threadIdx.x * kSItems;
   Blk16<T> cur;
   IXG_TR(0);
@@ -210,18 +226,11 @@ __global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, c
   int cnt;
   const int rank = cta_exclusive<NT>(c, s_w, &cnt);
   IXG_TR(2);
-  if (threadIdx.x == 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
-  if (warp_id() == 0) {
-    long long ex = 0;
-    if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
-    if (lane_id() == 0) {
-      s_excl = ex;
-      if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
-      if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
-    }
+  if (threadIdx.x == 0) {
+    s_cnt = cnt;
+    lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
   }
-  IXG_TR(3);
-  __syncthreads();
+  bar_sync(2, NT + 32);
   IXG_TR(4);
   const long long base = s_excl;
   const int shift = (int)(base % VS);
@@ -242,7 +251,7 @@ __global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, c
       bw0 = __ldg(&segbits[wd]);
       bw1 = __ldg(&segbits[wd + 1]);
     }
-    __syncthreads();
+    bar_sync(1, NT);
     IXG_TR(5);
     store_aligned<T, NT>(ys, base, cnt, stage);
     uint32_t fb = (uint32_t)((((uint64_t)bw1 << 32) | (uint64_t)bw0) >> (pos0 & 31));
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, c
     SegOp::T lex = SegOp::shfl_up(inc, 1);
     if (lane_id() == 0) lex = SegOp::identity();
     if (lane_id() == 31) s_seg[warp_id()] = inc;
-    __syncthreads();
+    bar_sync(1, NT);
     SegOp::T pre = SegOp::identity(), tagg = SegOp::identity();
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) {
@@ -328,11 +337,11 @@ __global__ void __launch_bounds__(kNT, 2) k_filter_s(const T* __restrict__ xs, c
     }
     if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
     if (threadIdx.x == 0) meta[tile] = SegTileMeta{tagg.v, (long long)tagg.f, base, (long long)cnt};
-    __syncthreads();
+    bar_sync(1, NT);
     store_aligned<Z, NT>(zs, base, cnt, stage_z);
     IXG_TR(6);
   } else {
-    __syncthreads();
+    bar_sync(1, NT);
     IXG_TR(5);
     store_aligned<T, NT>(ys, base, cnt, stage);
     IXG_TR(6);
@@ -437,9 +446,10 @@ __global__ void __launch_bounds__(kSThreads) k_class_count(const T* __restrict__
 // look-back carries the class-0 (and class-1) prefix; the last class's
 // prefix is the tile start minus the others.
 template <typename T, int kClasses>
-__global__ void __launch_bounds__(kNT, 2) k_place_s(const T* __restrict__ xs, long long n, ixg_pred p, ixg_pred q,
-                                                     T* __restrict__ ys, const long long* __restrict__ d_tot,
-                                                     LBChan ch, uint32_t nonce) {
+__global__ void __launch_bounds__(kNT + 32, 2) k_place_s(const T* __restrict__ xs, long long n, ixg_pred p,
+                                                          ixg_pred q, T* __restrict__ ys,
+                                                          const long long* __restrict__ d_tot, LBChan ch,
+                                                          uint32_t nonce) {
   constexpr int NT = kNT;
   using M = typename std::conditional<kClasses == 2, SumOp, Sum2Op>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -451,8 +461,25 @@ __global__ void __launch_bounds__(kNT, 2) k_place_s(const T* __restrict__ xs, lo
   __shared__ int s_w[NT / 32];
   __shared__ int s_w1[NT / 32];
   __shared__ long long s_ex[2];
+  __shared__ typename std::conditional<kClasses == 2, SumOp, Sum2Op>::type::T s_agg;
 
   const long long tile = blockIdx.x;
+  if (warp_id() == NT / 32) {  // look-back warp (see k_filter_s)
+    typename M::T ex = M::identity();
+    if (tile > 0) ex = lb_lookback<M>(ch, nonce, tile);
+    if (lane_id() == 0) {
+      if constexpr (kClasses == 2) {
+        s_ex[0] = ex.v;
+        s_ex[1] = 0;
+      } else {
+        s_ex[0] = ex.a;
+        s_ex[1] = ex.b;
+      }
+    }
+    bar_sync(2, NT + 32);
+    if (lane_id() == 0 && tile > 0) lb_publish<M>(ch, nonce, tile, M::op(ex, s_agg), true);
+    return;
+  }
   const long long tile_base = tile * kSTile;
   const long long i0 = tile_base + threadIdx.x * kSItems;
   Blk16<T> cur;
@@ -472,22 +499,11 @@ __global__ void __launch_bounds__(kNT, 2) k_place_s(const T* __restrict__ xs, lo
   typename M::T agg;
   if constexpr (kClasses == 2) agg = typename M::T{cnt0};
   else agg = typename M::T{cnt0, cnt1};
-  if (threadIdx.x == 0) lb_publish<M>(ch, nonce, tile, agg, tile == 0);
-  if (warp_id() == 0) {
-    typename M::T ex = M::identity();
-    if (tile > 0) ex = lb_lookback<M>(ch, nonce, tile);
-    if (lane_id() == 0) {
-      if constexpr (kClasses == 2) {
-        s_ex[0] = ex.v;
-        s_ex[1] = 0;
-      } else {
-        s_ex[0] = ex.a;
-        s_ex[1] = ex.b;
-      }
-      if (tile > 0) lb_publish<M>(ch, nonce, tile, M::op(ex, agg), true);
-    }
+  if (threadIdx.x == 0) {
+    s_agg = agg;
+    lb_publish<M>(ch, nonce, tile, agg, tile == 0);
   }
-  __syncthreads();
+  bar_sync(2, NT + 32);
   const long long t0 = d_tot[0];
   const long long t1 = kClasses == 3 ? d_tot[1] : 0;
   const long long e0 = s_ex[0], e1 = s_ex[1];
@@ -504,7 +520,7 @@ __global__ void __launch_bounds__(kNT, 2) k_place_s(const T* __restrict__ xs, lo
     k1 += s1;
     k2 += s2;
   }
-  __syncthreads();
+  bar_sync(1, NT);
   const int cnt2 = tile_len - cnt0 - cnt1;
   store_aligned<T, NT>(ys, b0, cnt0, stage0);
   if (kClasses == 3) store_aligned<T, NT>(ys, b1, cnt1, stage1);

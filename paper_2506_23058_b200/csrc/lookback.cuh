@@ -147,21 +147,6 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long ti
 #ifdef IXG_TRACE
   unsigned int tr_rounds = 0, tr_spins = 0;
 #endif
-  // wait (one lane, one slot) until the newest predecessor has published;
-  // the older ones almost always have by then, so the window read below is
-  // one round trip instead of 32 lanes polling in a loop
-  if (lane == 0) {
-    unsigned long long w;
-    uint32_t f;
-    int spins = 0;
-    while (slot_load(slot_at(ch, pred), nonce, &w, &f) == 0) {
-      if (++spins > 8) __nanosleep(64);
-#ifdef IXG_TRACE
-      ++tr_spins;
-#endif
-    }
-  }
-  __syncwarp();
   while (true) {
 #ifdef IXG_TRACE
     ++tr_rounds;
@@ -184,6 +169,9 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long ti
 #pragma unroll
       for (int j = 0; j < kPerLane; ++j) ready &= st[j] != 0;
       if (ready) break;
+#ifdef IXG_TRACE
+      ++tr_spins;
+#endif
       if (++spins > 32) __nanosleep(16);
 #pragma unroll
       for (int j = 0; j < kPerLane; ++j) {

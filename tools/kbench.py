@@ -85,6 +85,10 @@ def main():
     out["place_kernel"]["algoGBps"] = 8 * n / out["place_kernel"]["ms"] / 1e6
     out["count_kernel"]["GBps"] = 4 * n / out["count_kernel"]["ms"] / 1e6
 
+    # library reference points (CUB via torch): stream compaction and scan
+    mask = xs >= 0
+    out["torch_masked_select"] = {"ms": timeit(lambda: torch.masked_select(xs, mask), reps=5)}
+    out["torch_cumsum_i32"] = {"ms": timeit(lambda: torch.cumsum(xs, 0, dtype=torch.int64), reps=5)}
     x64 = xs.to(torch.int64)
     so = torch.empty(n, dtype=torch.int64, device=dev)
     ms = timeit(lambda: ops.scan_add(x64, 0, out=so))

@@ -40,12 +40,12 @@ def main():
     buf = (ctypes.c_ulonglong * cnt)()
     L.check(lib.ixg_trace_read(buf, cnt), "trace")
     a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8).astype(np.int64)
-    tiles = int(dk.numel() and (n + 8191) // 8192)
-    tiles = min(tiles, a.shape[0])
+    tile = int(os.environ.get("IXG_TILE", "8192"))
+    tiles = min((n + tile - 1) // tile, a.shape[0])
     a = a[:tiles]
     t0 = a[:, 0].min()
     a[:, :7] -= t0
-    names = ["load", "cta_scan", "lookback", "bar", "stage", "store"]
+    names = ["load", "cta_scan", "lb_done", "bar2", "stage", "store"]
     print(f"tiles {tiles}, kernel span {a[:, 6].max() / 1e3:.1f} us")
     for i, nm in enumerate(names):
         d = a[:, i + 1] - a[:, i]
