@@ -153,10 +153,21 @@ class C2:
         # each rank owns one contiguous shard of the global xs
         self.xs_h = gen.uniform(0, self.N, -128, 127, np.int32, offset=rank * self.N)
         self.k = int(np.count_nonzero(self.xs_h >= 0))
-        self.shape_h = gen.segment_shape(1 + rank, self.m, self.k)
+        if ws > 1:
+            # weak scaling: the global problem is ws shards of N; the segment
+            # shape covers ALL shards' outputs (m per GPU, sum = global k)
+            from paper_2506_23058_b200 import dist as D
+
+            ks = [r[0] for r in D.all_gather_ints([self.k])]
+            self.k_total = sum(ks)
+            self.shape_h = gen.segment_shape(1, self.m * ws, self.k_total)
+        else:
+            self.k_total = self.k
+            self.shape_h = gen.segment_shape(1 + rank, self.m, self.k)
         self.workload = (f"c2 = filter (x >= 0) + mkFlags + sgmSum: N=2^{self.N.bit_length() - 1} int32 uniform "
-                         f"[-128,127] per GPU, m=2^{self.m.bit_length() - 1} segments (i64 shape, sum = k, >=1% empty), "
-                         "zs int32")
+                         f"[-128,127] per GPU, m=2^{self.m.bit_length() - 1} segments per GPU (i64 shape, sum = k, "
+                         ">=1% empty), zs int32" + (f"; {ws} contiguous shards, all-gathers of counts and "
+                                                     "segmented aggregates" if ws > 1 else ""))
 
     def setup_device(self):
         import torch
@@ -170,10 +181,20 @@ class C2:
         self.zs = torch.empty(self.N, dtype=torch.int32, device=dev)
         self.dk = torch.empty(1, dtype=torch.int64, device=dev)
         self.st = ops.Status(dev)
+        if self.ws > 1:
+            from paper_2506_23058_b200 import dist as D
+
+            self.local = D.GpuC2Local(self.xs, self.p, self.shape)
+            self.local.ys, self.local.zs, self.local.dk, self.local.st = self.ys, self.zs, self.dk, self.st
 
     def step(self, variant):
         from paper_2506_23058_b200 import ops
 
+        if self.ws > 1:
+            from paper_2506_23058_b200 import dist as D
+
+            D.c2_sharded(self.local)
+            return
         ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
 
     def check(self, want):
@@ -194,8 +215,14 @@ class C2:
     def kernel(self):
         from paper_2506_23058_b200 import _lib as L
 
-        # the fused filter+sgmSum kernel: xs read once, ys and zs written once
-        return L.K_FILTER_FUSED, 4 * self.N + 8 * self.k, "k_filter<int32,int32,seg> (fused filter + sgmSum)"
+        # the dominant kernel of the step: the single-pass filter (xs read
+        # once, ys written once); the sgmSum pass is reported alongside
+        return L.K_FILTER_FUSED, 4 * self.N + 4 * self.k, "k_filter_b<int32> (single-pass filter, 96 KB cp.async tiles)"
+
+    def kernels_extra(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        return [(L.K_SEGSUM, 8 * self.k, "k_segsum_b<int32,int32> (sgmSum over ys, flags from the mkFlags bitmap)")]
 
     def e2e_step(self, bufs):
         """pinned host -> device, pipeline, k -> host, ys/zs -> host."""
@@ -204,8 +231,14 @@ class C2:
         xs_p, shape_p, ys_p, zs_p, variant = bufs
         self.xs.copy_(xs_p, non_blocking=True)
         self.shape.copy_(shape_p, non_blocking=True)
-        ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
-        k = int(self.dk.item())
+        if self.ws > 1:
+            from paper_2506_23058_b200 import dist as D
+
+            D.c2_sharded(self.local)
+            k = self.local.k
+        else:
+            ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
+            k = int(self.dk.item())
         ys_p[:k].copy_(self.ys[:k], non_blocking=True)
         zs_p[:k].copy_(self.zs[:k], non_blocking=True)
         return 4 * self.N + 8 * self.m, 8 + 8 * k
@@ -315,6 +348,183 @@ class C1:
         return self.xs_h, self.N
 
 
+class C3:
+    """scatter dst is vs, n = m = 2^29 (BASELINE configs[2]): `is` = the
+    partition2 destination index of random xs (two monotone streams, a true
+    permutation); ELIDED = Sc1 (sc_bij: no init, no checks), CHECKED =
+    sc_any (dst init + OOB test + idempotence check)."""
+
+    name = "c3"
+    cpu_threads = 1
+    cpu_desc = "oracle/ixoracle.c ixo_scatter (sequential restatement of oracle.py:294-305, 2^24 prefix)"
+
+    def __init__(self, quick, rank, ws):
+        self.N = (1 << 22) if quick else (1 << 29)
+        self.workload = (f"scatter dst is vs: n = m = 2^{self.N.bit_length() - 1}, is = partition2 indices of random "
+                         "xs (i64 permutation, two monotone streams), vs int32, dst int32 zeros")
+        self.rank = rank
+
+    def setup_device(self):
+        import torch
+
+        from paper_2506_23058_b200 import ops
+
+        dev = torch.device("cuda")
+        xs = ops.gen_uniform(self.N, -(1 << 31), (1 << 31) - 1, 11, torch.int32, offset=self.rank * self.N)
+        c = xs < 0
+        t = torch.cumsum(c, 0, dtype=torch.int64)
+        nt = t[-1]
+        i1 = torch.arange(1, self.N + 1, device=dev, dtype=torch.int64)
+        self.is_ = torch.where(c, t - 1, nt + (i1 - t) - 1)
+        del xs, c, t, i1
+        self.vs = ops.gen_uniform(self.N, -(1 << 31), (1 << 31) - 1, 12, torch.int32, offset=self.rank * self.N)
+        self.dst = torch.zeros(self.N, dtype=torch.int32, device=dev)
+        self.out = torch.empty_like(self.dst)
+        self.st = ops.Status(dev)
+
+    def step(self, variant):
+        from paper_2506_23058_b200 import _lib as L
+        from paper_2506_23058_b200 import ops
+
+        if variant == L.VARIANT_ELIDED:
+            ops.scatter(self.out, self.is_, self.vs, 0, self.st)
+        else:
+            self.out.copy_(self.dst)  # dst init (the reference copies dst, oracle.py:295)
+            ops.scatter(self.out, self.is_, self.vs, L.V_CONFLICT | L.V_INIT, self.st)
+
+    def check(self, want):
+        import torch
+
+        ok = self.st.read().ok
+        # a permutation scatter: out[is] == vs everywhere
+        ok = ok and bool(torch.equal(self.out[self.is_], self.vs))
+        return ok
+
+    def units(self):
+        return self.N
+
+    def algo_bytes_step(self):
+        return 16 * self.N
+
+    def kernel(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        return L.K_SCATTER, 16 * self.N, "k_scatter<int32> (is i64 + vs i32 read, dst i32 written)"
+
+    def e2e_bufs(self, variant):
+        import torch
+
+        return (self.is_.cpu().pin_memory(), self.vs.cpu().pin_memory(), torch.empty(self.N, dtype=torch.int32).pin_memory(),
+                variant)
+
+    def e2e_step(self, bufs):
+        from paper_2506_23058_b200 import ops
+
+        is_p, vs_p, out_p, variant = bufs
+        self.is_.copy_(is_p, non_blocking=True)
+        self.vs.copy_(vs_p, non_blocking=True)
+        ops.scatter(self.out, self.is_, self.vs, 0, self.st)
+        out_p.copy_(self.out, non_blocking=True)
+        return 12 * self.N, 4 * self.N
+
+    def cpu_run(self, is_, vs, threads=0):
+        from oracle import ixoracle as O
+
+        return O.scatter(np.zeros(len(is_), np.int64), is_, vs)
+
+    def cpu_sample(self, budget_s):
+        import torch
+
+        from paper_2506_23058_b200 import ops
+
+        n = min(self.N, 1 << 24)  # the sequential port on a 2^24 instance of the same construction
+        xs = ops.gen_uniform(n, -(1 << 31), (1 << 31) - 1, 11, torch.int32)
+        c = xs < 0
+        t = torch.cumsum(c, 0, dtype=torch.int64)
+        i1 = torch.arange(1, n + 1, device=xs.device, dtype=torch.int64)
+        is_ = torch.where(c, t - 1, t[-1] + (i1 - t) - 1)
+        return is_.cpu().numpy(), self.vs[:n].cpu().numpy().astype(np.int64), n
+
+
+class C4:
+    """CSR flat gather map2 (\\v c -> v * x[c]) values indices (BASELINE
+    configs[3]): nnz = 2^28, num_cols = 2^20, indices sorted within rows of
+    64; ELIDED = csrg (Range proved), CHECKED = csrg_any (bounds checks)."""
+
+    name = "c4"
+    cpu_threads = 1
+    cpu_desc = "oracle/ixoracle.c ixo_csrg (sequential restatement, 2^24-nnz prefix)"
+
+    def __init__(self, quick, rank, ws):
+        self.N = (1 << 22) if quick else (1 << 28)
+        self.ncols = 1 << 20
+        self.rank = rank
+        self.workload = (f"CSR gather v * x[c]: nnz = 2^{self.N.bit_length() - 1}, num_cols = 2^20, values/x int32 in "
+                         "[-2^15, 2^15), indices i64 sorted within rows of 64")
+
+    def setup_device(self):
+        import torch
+
+        from paper_2506_23058_b200 import ops
+
+        dev = torch.device("cuda")
+        self.x = ops.gen_uniform(self.ncols, -(1 << 15), (1 << 15) - 1, 21, torch.int32)
+        self.vals = ops.gen_uniform(self.N, -(1 << 15), (1 << 15) - 1, 22, torch.int32, offset=self.rank * self.N)
+        idx = ops.gen_uniform(self.N, 0, self.ncols - 1, 23, torch.int64, offset=self.rank * self.N)
+        self.idx = idx.view(-1, 64).sort(dim=1).values.reshape(-1).contiguous()
+        self.out = torch.empty(self.N, dtype=torch.int32, device=dev)
+        self.st = ops.Status(dev)
+
+    def step(self, variant):
+        from paper_2506_23058_b200 import ops
+
+        ops.csr_gather(self.x, self.vals, self.idx, variant, self.st, out=self.out)
+
+    def check(self, want):
+        import torch
+
+        s = self.st.read()
+        ref = (self.vals[:4096].long() * self.x[self.idx[:4096]].long()).int()
+        return s.ok and bool(torch.equal(self.out[:4096], ref))
+
+    def units(self):
+        return self.N
+
+    def algo_bytes_step(self):
+        return 16 * self.N + 4 * self.ncols
+
+    def kernel(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        return L.K_CSR_GATHER, 16 * self.N + 4 * self.ncols, "k_csr_gather<int32>"
+
+    def e2e_bufs(self, variant):
+        import torch
+
+        return (self.vals.cpu().pin_memory(), self.idx.cpu().pin_memory(), torch.empty(self.N, dtype=torch.int32).pin_memory(),
+                variant)
+
+    def e2e_step(self, bufs):
+        from paper_2506_23058_b200 import ops
+
+        v_p, i_p, o_p, variant = bufs
+        self.vals.copy_(v_p, non_blocking=True)
+        self.idx.copy_(i_p, non_blocking=True)
+        ops.csr_gather(self.x, self.vals, self.idx, variant, self.st, out=self.out)
+        o_p.copy_(self.out, non_blocking=True)
+        return 12 * self.N, 4 * self.N
+
+    def cpu_run(self, x, vals, idx, threads=0):
+        from oracle import ixoracle as O
+
+        return O.csrg(x, vals, idx)
+
+    def cpu_sample(self, budget_s):
+        n = min(self.N, 1 << 24)
+        return (self.x.cpu().numpy().astype(np.int64), self.vals[:n].cpu().numpy().astype(np.int64),
+                self.idx[:n].cpu().numpy(), n)
+
+
 # ----------------------------------------------------------------- timing
 def time_steps(wl, variant, steps, warmup, ws, kernel_id=None):
     import torch
@@ -380,8 +590,17 @@ def run_ours(args):
     kid, kbytes, kname = wl.kernel()
     ms, launches, kms = time_steps(wl, selected, args.steps, args.warmup, ws, kid)
     clocks = sampler.stop()
-    ms_chk, _, _ = time_steps(wl, L.VARIANT_CHECKED, max(3, args.steps // 4), 2, ws)
-    parity_chk = wl.check(want)
+    others = []
+    for okid, obytes, oname in (wl.kernels_extra() if hasattr(wl, "kernels_extra") else []):
+        _, _, oms = time_steps(wl, selected, max(5, args.steps // 5), 2, ws, okid)
+        if oms:
+            others.append({"kernel": oname, "kernel_ms": round(oms, 5), "algo_bytes_per_launch": obytes,
+                           "achieved": round(obytes / (oms * 1e-3) / 1e9, 1),
+                           "frac": round(obytes / (oms * 1e-3) / 1e9 / hbm, 4)})
+    ms_chk = parity_chk = None
+    if ws == 1:  # the CHECKED pipeline is single-GPU (the sharded path is the verified one)
+        ms_chk, _, _ = time_steps(wl, L.VARIANT_CHECKED, max(3, args.steps // 4), 2, ws)
+        parity_chk = wl.check(want)
 
     # e2e: pinned host buffers, copies inside the timed region
     bufs = wl.e2e_bufs(selected)
@@ -428,7 +647,7 @@ def run_ours(args):
             "ms_per_step": round(ms_chk, 4),
             "value": round(units_total / (ms_chk * 1e-3) / 1e9, 3),
             "elided_speedup": round(ms_chk / ms, 3),
-        },
+        } if ms_chk else None,
         "roofline": {
             "bound": "hbm",
             "kernel": kname,
@@ -440,6 +659,10 @@ def run_ours(args):
             "traffic": traffic,
             "algo_bytes_per_launch": kbytes,
             "kernel_ms": round(kms, 5) if kms else None,
+            "step": {"algo_bytes": wl.algo_bytes_step(), "ms": round(ms, 4),
+                     "achieved": round(wl.algo_bytes_step() / (ms * 1e-3) / 1e9, 1),
+                     "frac": round(wl.algo_bytes_step() / (ms * 1e-3) / 1e9 / hbm, 4)},
+            "other_kernels": others,
         },
         "e2e": {
             "value": round(units_total / (e2e_ms * 1e-3) / 1e9, 4),
@@ -474,7 +697,7 @@ def cpu_baseline(wl, args):
     """The oracle port (OpenMP, all host threads) on the same workload."""
     from oracle import ixoracle as O
 
-    threads = O.threads()
+    threads = getattr(wl, "cpu_threads", None) or O.threads()
     inputs = wl.cpu_sample(20.0)
     n = inputs[-1]
     res = wl.cpu_run(*inputs[:-1], threads)
@@ -492,7 +715,8 @@ def cpu_baseline(wl, args):
         "unit": "Gelem/s",
         "cores": threads,
         "kind": "port",
-        "sample": f"{len(times)} runs of the full {wl.name} workload (n={n}) by oracle/ixoracle_par.c, median",
+        "sample": (f"{len(times)} runs of the {wl.name} workload at n={n} by "
+                   f"{getattr(wl, 'cpu_desc', 'oracle/ixoracle_par.c (OpenMP)')}, median"),
         "ms_per_run": round(best * 1e3, 2),
     }
     if n == wl.units():
@@ -550,6 +774,10 @@ def make_workload(args, rank, ws):
         return C1(args.quick, rank, ws)
     if args.config == "c5":
         return C1(args.quick, rank, ws, big=True)
+    if args.config == "c3":
+        return C3(args.quick, rank, ws)
+    if args.config == "c4":
+        return C4(args.quick, rank, ws)
     raise SystemExit(f"unknown config {args.config}")
 
 
@@ -559,7 +787,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4", "c5"])
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -236,6 +236,26 @@ int ixg_eq_gather(const int64_t* H, int64_t hlen, const int64_t* es, const int64
 int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint32_t variant, ixg_status* st,
                 void* ws, size_t ws_bytes, void* stream);
 
+/* ---- C2 building blocks for sharded (multi-GPU) execution ---------------
+ * A rank filters its contiguous shard (ixg_filter), learns its global output
+ * offset K from an all-gather of counts, then:
+ *   ixg_flag_bitmap  the mkFlags array of ALL shards' outputs as a bitmap
+ *                    (bit scn[i] for non-empty segments below nbits);
+ *   ixg_segsum       zs = sgmSum over its n (or *d_n) outputs, flags = bits
+ *                    [flag_base + j], seeded with the carry (carry_v, carry_f);
+ *                    *d_total (2 x int64) = its segmented aggregate (v, f);
+ *   ixg_seg_carry    after the all-gather of aggregates: adds the carry of
+ *                    the earlier ranks to its outputs before its first flag.
+ * ixg_bitmap_words(nbits) = uint32 words to allocate for `bits`. */
+int64_t ixg_bitmap_words(int64_t nbits);
+int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, void* ws, size_t ws_bytes,
+                    void* stream);
+int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,
+               int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total, ixg_status* st, void* ws,
+               size_t ws_bytes, void* stream);
+int ixg_seg_carry(const uint32_t* bits, int64_t flag_base, int dt_z, void* zs, int64_t n, const int64_t* d_n,
+                  int64_t carry_v, void* scratch8, ixg_status* st, void* stream);
+
 /* ---- map with a compiled lambda (oracle.py:274-280) ----------------------
  * The host compiles the lambda body (paper_2506_23058_b200/vm.py) into a
  * short register program; the kernel interprets it per element, all

@@ -768,6 +768,65 @@ int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint
                                    IXG_SITE_BITS(variant, 1) | IXG_V_INIT, 1, 1, st, w, 1, s);
 }
 
+int64_t ixg_bitmap_words(int64_t nbits) { return (int64_t)(bitmap_bytes(nbits) / 4); }
+
+int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (m < 0 || nbits < 0 || (m > 0 && !shape) || !bits) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, m, 0)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(m, kGTile));
+  cudaMemsetAsync(bits, 0, bitmap_bytes(nbits), s);
+  LAUNCHED();
+  return launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
+                            EpiSegStarts{m, (const long long*)shape, nullptr, bits, nbits, nullptr}, c, s);
+}
+
+int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,
+               int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total, ixg_status* st, void* ws,
+               size_t ws_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!vs || !zs || !bits))) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_SEGSCAN, n, 0)) return IXG_BADARG;
+  if (n == 0) return IXG_OK;
+  if (!aligned16(vs) || !aligned16(zs)) return IXG_BADARG;
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(n, kGTile));
+  cudaStream_t s = S(stream);
+  const long long* dn = (const long long*)d_n;
+  longlong2* tot = (longlong2*)d_total;
+  if (dt == IXG_I32 && dt_z == IXG_I32)
+    return launch_segsum_b<int32_t, int32_t>((const int32_t*)vs, n, dn, bits, flag_base, (int32_t*)zs, c, carry_v,
+                                             carry_f, tot, st, s);
+  if (dt == IXG_I32)
+    return launch_segsum_b<int32_t, long long>((const int32_t*)vs, n, dn, bits, flag_base, (long long*)zs, c,
+                                               carry_v, carry_f, tot, st, s);
+  if (dt_z == IXG_I32) return IXG_BADARG;
+  return launch_segsum_b<long long, long long>((const long long*)vs, n, dn, bits, flag_base, (long long*)zs, c,
+                                               carry_v, carry_f, tot, st, s);
+}
+
+int ixg_seg_carry(const uint32_t* bits, int64_t flag_base, int dt_z, void* zs, int64_t n, const int64_t* d_n,
+                  int64_t carry_v, void* scratch8, ixg_status* st, void* stream) {
+  if (n < 0 || !bits || !scratch8 || (n > 0 && !zs)) return IXG_BADARG;
+  if (n == 0 || carry_v == 0) return IXG_OK;
+  cudaStream_t s = S(stream);
+  unsigned long long* first = (unsigned long long*)scratch8;
+  cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), s);
+  LAUNCHED();
+  k_first_flag<<<grid_for(n / 32 + 1), 256, 0, s>>>(bits, flag_base, n, (const long long*)d_n, first);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  if (dt_z == IXG_I32)
+    k_add_prefix<int32_t><<<grid_for(n), 256, 0, s>>>((int32_t*)zs, first, n, (const long long*)d_n, carry_v, st);
+  else
+    k_add_prefix<long long><<<grid_for(n), 256, 0, s>>>((long long*)zs, first, n, (const long long*)d_n, carry_v,
+                                                        st);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
 int ixg_map(const ixg_vm_insn* prog, int ninsn, const ixg_array* ins, int nins, const ixg_array* outs, int nouts,
             const ixg_pred* preds, int npreds, int64_t n, int stmt, ixg_status* st, void* stream) {
   if (ninsn < 0 || ninsn > IXG_VM_MAX_INSN || nins < 0 || nins > IXG_VM_MAX_IN || nouts < 0 ||

@@ -335,4 +335,41 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_segsum_b(const T* __restrict__ 
   if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
 }
 
+// ---------------------------------------------------------------------------
+// Shard carry (multi-GPU C2): the first flag at or after `flag_base` within
+// [flag_base, flag_base + n), then zs[0 .. first) += carry.
+__global__ void __launch_bounds__(256) k_first_flag(const uint32_t* __restrict__ bits, long long flag_base,
+                                                    long long n, const long long* __restrict__ d_n,
+                                                    unsigned long long* first) {
+  if (d_n) n = *d_n;
+  const long long nw = (n + 31) / 32 + 1;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nw; k += stride) {
+    const long long q0 = k * 32;  // local position of this window
+    if (q0 >= n) break;
+    const long long g = flag_base + q0;
+    uint32_t w = (uint32_t)((((uint64_t)bits[(g >> 5) + 1] << 32) | bits[g >> 5]) >> (g & 31));
+    const long long lim = n - q0;
+    if (lim < 32) w &= (1u << lim) - 1u;
+    if (w) atomicMin(first, (unsigned long long)(q0 + __ffs(w) - 1));
+  }
+}
+
+template <typename Z>
+__global__ void __launch_bounds__(256) k_add_prefix(Z* __restrict__ zs, const unsigned long long* __restrict__ first,
+                                                    long long n, const long long* __restrict__ d_n, long long c,
+                                                    ixg_status* st) {
+  if (d_n) n = *d_n;
+  long long stop = (long long)*first;
+  if (stop > n) stop = n;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool narrow = false;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < stop; q += stride) {
+    const long long v = (long long)zs[q] + c;
+    if (sizeof(Z) == 4 && v != (long long)(int)v) narrow = true;
+    zs[q] = (Z)v;
+  }
+  if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+}
+
 }  // namespace ixg

@@ -326,6 +326,39 @@ def mkflags(k: int, shape: torch.Tensor, variant: int, status: Status) -> torch.
     return out
 
 
+def flag_bitmap(shape: torch.Tensor, nbits: int) -> torch.Tensor:
+    """mkFlags over nbits output positions as a bitmap (int32 words)."""
+    shape = _contig(shape.to(torch.int64))
+    words = int(_lib().ixg_bitmap_words(nbits))
+    bits = torch.empty(words, dtype=torch.int32, device=shape.device)
+    ws, wsb = _ws(L.OP_SCAN, shape.numel(), 0, shape.device)
+    L.check(_lib().ixg_flag_bitmap(_ptr(shape), shape.numel(), _ptr(bits), nbits, ws, wsb, _stream()), "flag_bitmap")
+    return bits
+
+
+def segsum(vs: torch.Tensor, n: int, bits: torch.Tensor, flag_base: int, zs: torch.Tensor, carry_v: int,
+           carry_f: bool, d_total: torch.Tensor, status: Status):
+    """zs[0..n) = sgmSum over vs with flags bits[flag_base + j] (ixg_segsum)."""
+    ws, wsb = _ws(L.OP_SEGSCAN, vs.numel(), 0, vs.device)
+    L.check(
+        _lib().ixg_segsum(_dt(vs), _ptr(vs), n, _ptr(None), _ptr(bits), flag_base, _dt(zs), _ptr(zs), carry_v,
+                          int(carry_f), _ptr(d_total), status.ptr, ws, wsb, _stream()),
+        "segsum",
+    )
+    return zs
+
+
+def seg_carry(bits: torch.Tensor, flag_base: int, zs: torch.Tensor, n: int, carry_v: int, scratch: torch.Tensor,
+              status: Status):
+    """zs[q] += carry_v for q before the first flag of [flag_base, flag_base + n)."""
+    L.check(
+        _lib().ixg_seg_carry(_ptr(bits), flag_base, _dt(zs), _ptr(zs), n, _ptr(None), carry_v, _ptr(scratch),
+                             status.ptr, _stream()),
+        "seg_carry",
+    )
+    return zs
+
+
 def _arr(t: torch.Tensor) -> L.ixg_array:
     return L.ixg_array(t.data_ptr() if t.numel() else 0, t.numel(), _dt(t), 0)
 

@@ -1,0 +1,122 @@
+"""Multi-rank host logic of the sharded path (paper_2506_23058_b200.dist) on
+CPU: world_size 2 and 3 over gloo, each rank running a numpy stand-in for
+its GPU's local kernels, results compared with the single-process oracle.
+The same orchestration code drives the CUDA kernels on the GPU box."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import ixoracle as O
+from paper_2506_23058_b200 import dist as D
+from paper_2506_23058_b200 import gen
+from paper_2506_23058_b200.pred import Pred
+
+
+def test_arithmetic():
+    assert D.exclusive_offsets([3, 0, 5]) == [0, 3, 3]
+    assert D.seg_combine((5, False), (2, False)) == (7, False)
+    assert D.seg_combine((5, True), (2, True)) == (2, True)
+    assert D.seg_carries([(4, False), (3, True), (1, False)]) == [(0, False), (4, False), (3, True)]
+    nt, runs = D.partition2_runs([2, 1], [5, 4], 1)
+    assert nt == 3 and runs.starts == [2, 3 + 3] and runs.lengths == [1, 3]
+
+
+class NpC2Local:
+    def __init__(self, xs, pred, shape):
+        self.xs, self.pred, self.shape = xs, pred, shape
+
+    def filter(self):
+        self.ys = np.array([x for x in self.xs if self.pred(int(x))], dtype=np.int64)
+        return len(self.ys)
+
+    def flag_bitmap(self, k_total):
+        self.flags = O.mkflags(k_total, self.shape)
+
+    def segsum(self, flag_base):
+        fl = self.flags[flag_base:flag_base + len(self.ys)]
+        self.zs = O.sgmsum(fl, self.ys) if len(self.ys) else np.zeros(0, np.int64)
+        f = bool(fl.any())
+        last = int(np.nonzero(fl)[0][-1]) if f else 0
+        v = int(self.ys[last:].sum()) if len(self.ys) else 0
+        return v, f
+
+    def seg_carry(self, flag_base, carry_v):
+        fl = self.flags[flag_base:flag_base + len(self.ys)]
+        first = int(np.nonzero(fl)[0][0]) if fl.any() else len(self.ys)
+        self.zs[:first] += carry_v
+
+
+class NpPart2Local:
+    def __init__(self, xs, pred):
+        self.xs, self.pred = xs, pred
+
+    def partition2(self):
+        nt, ys = O.partition2(self.pred, self.xs)
+        self.ys = ys
+        return nt, len(self.xs)
+
+
+def _worker(rank, world, port, n, m, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = rank * n // world, (rank + 1) * n // world
+        xs = gen.uniform(5, n, -20, 20, np.int64)
+        p = Pred.ge(0)
+        k_total = int((xs >= 0).sum())
+        shape = gen.segment_shape(9, m, k_total)
+        loc = NpC2Local(xs[lo:hi], p, shape)
+        K, k, kt = D.c2_sharded(loc)
+        assert kt == k_total
+        zs_all = [None] * world
+        dist.all_gather_object(zs_all, (K, loc.ys.tolist(), loc.zs.tolist()))
+        p2 = NpPart2Local(xs[lo:hi], Pred.lt(3))
+        nt, runs = D.partition2_sharded(p2)
+        parts = [None] * world
+        dist.all_gather_object(parts, (runs.starts, runs.lengths, p2.ys.tolist()))
+        if rank == 0:
+            ys_g = np.zeros(k_total, np.int64)
+            zs_g = np.zeros(k_total, np.int64)
+            for K_r, ys_r, zs_r in zs_all:
+                ys_g[K_r:K_r + len(ys_r)] = ys_r
+                zs_g[K_r:K_r + len(zs_r)] = zs_r
+            want_ys, want_zs = O.c2(p, xs, shape)
+            p_out = np.zeros(n, np.int64)
+            for starts, lengths, ys_r in parts:
+                off = 0
+                for s, ln in zip(starts, lengths):
+                    p_out[s:s + ln] = ys_r[off:off + ln]
+                    off += ln
+            want_nt, want_p = O.partition2(Pred.lt(3), xs)
+            q.put((np.array_equal(ys_g, want_ys), np.array_equal(zs_g, want_zs), nt == want_nt,
+                   np.array_equal(p_out, want_p)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("world,n,m", [(2, 1000, 23), (3, 2001, 40), (2, 7, 3)])
+def test_sharded_c2_and_partition2_gloo(world, n, m):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+        assert pr.exitcode == 0
+    assert q.get() == (True, True, True, True)

@@ -1,0 +1,45 @@
+"""GPU side of the sharded path: the per-rank kernels of dist.GpuC2Local
+(ixg_filter, ixg_flag_bitmap, ixg_segsum with flag offset and carry,
+ixg_seg_carry), driven for G simulated ranks one after the other on one GPU
+(no kernel waits on another rank), with the same all-gather arithmetic as
+dist.c2_sharded.  The concatenated result must equal the single-process C2."""
+
+import numpy as np
+import pytest
+
+from oracle import ixoracle as O
+from paper_2506_23058_b200 import dist as D
+from paper_2506_23058_b200 import gen
+from paper_2506_23058_b200.pred import Pred
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("G,n,m", [(2, 100_000, 300), (4, 1_000_003, 5000), (8, 3_000_000, 20_000), (3, 50, 7)])
+def test_c2_sharded_kernels(cuda, G, n, m):
+    import torch
+
+    xs = gen.uniform(G * 1000 + n, n, -128, 127, np.int32)
+    p = Pred.ge(0)
+    k_total = int((xs >= 0).sum())
+    shape = gen.segment_shape(G, m, k_total)
+    want_ys, want_zs = O.c2(p, xs, shape)
+    locs = []
+    for r in range(G):
+        lo, hi = r * n // G, (r + 1) * n // G
+        locs.append(D.GpuC2Local(torch.from_numpy(xs[lo:hi].copy()).to(cuda), p, torch.from_numpy(shape).to(cuda)))
+    ks = [loc.filter() for loc in locs]                      # all-gather #1: counts
+    K = D.exclusive_offsets(ks)
+    assert sum(ks) == k_total
+    for loc in locs:
+        loc.flag_bitmap(k_total)
+    aggs = [loc.segsum(K[r]) for r, loc in enumerate(locs)]  # all-gather #2: aggregates
+    for r, (loc, c) in enumerate(zip(locs, D.seg_carries(aggs))):
+        if c[0] != 0:
+            loc.seg_carry(K[r], c[0])
+    ys = np.concatenate([loc.ys[: loc.k].cpu().numpy() for loc in locs]).astype(np.int64)
+    zs = np.concatenate([loc.zs[: loc.k].cpu().numpy() for loc in locs]).astype(np.int64)
+    assert np.array_equal(ys, want_ys)
+    assert np.array_equal(zs, want_zs)
+    for loc in locs:
+        assert loc.st.read().ok
