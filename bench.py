@@ -638,7 +638,8 @@ def run_ours(args):
             "workload": wl.workload,
             "variant": "verifier-selected (ELIDED: Sc1 scatters fused, mkFlags Ss2)",
             "parallelism": f"shards{ws}" if ws > 1 else "single",
-            "l2": "inputs larger than the 126 MB L2, no flush" if wl.name in ("c2", "c5") else "256 MB L2 flush write between steps",
+            "l2": ("256 MB L2 flush write between steps (8 MB working set)" if wl.name == "c1"
+                   else "inputs larger than the 126 MB L2, no flush"),
             "parity_vs_cpu_port": bool(parity) if want is not None else "checked in tests",
             "parity_checked_variant": bool(parity_chk) if want is not None else "checked in tests",
         },

@@ -187,10 +187,21 @@ inline bool big_mode() {
   return mode == 1;
 }
 
-template <typename T, bool kByCs>
+// IXG_SEG_SPLIT=1: C2 as two passes (filter, then sgmSum over ys) for A/B
+inline bool seg_split_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_SEG_SPLIT");
+    mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  return mode == 1;
+}
+
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T>
 int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, LBChan ch,
-                    long long* d_count, cudaStream_t s) {
-  auto kern = k_filter_b<T, kByCs>;
+                    long long* d_count, cudaStream_t s, Z* zs = nullptr, const uint32_t* segbits = nullptr,
+                    long long out_base = 0, SegTileMeta* meta = nullptr, ixg_status* st = nullptr) {
+  auto kern = k_filter_b<T, kByCs, kSeg, Z>;
   static bool attr = false;
   if (!attr) {
     allow_smem(kern, Big<T>::SMEM);
@@ -198,7 +209,7 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
   }
   TimedLaunch tl(IXG_K_FILTER_FUSED, s);
   kern<<<(unsigned)tiles_of(n, Big<T>::TILE), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(),
-                                                                           d_count);
+                                                                           d_count, zs, segbits, out_base, meta, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -226,8 +237,8 @@ int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32
 // tiles' carries for the segmented sum (k_stream.cuh fix-up), then the fix-up
 template <typename Z>
 int launch_seg_fixup(SegTileMeta* meta, long long n, const uint32_t* segbits, long long out_base, Z* zs,
-                     long long carry_v, int carry_f, ixg_status* st, cudaStream_t s) {
-  const long long tiles = tiles_of(n, kSTile);
+                     long long carry_v, int carry_f, ixg_status* st, cudaStream_t s, int tile = kSTile) {
+  const long long tiles = tiles_of(n, tile);
   k_seg_tile_scan<<<1, 1024, 0, s>>>(meta, tiles, carry_v, carry_f);
   LAUNCHED();
   CHECK_LAUNCH();
@@ -360,8 +371,17 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
     if (rc) return rc;
     if (big_mode()) {
-      // ys = filter p xs (one pass), then zs = sgmSum flags ys over the k
-      // outputs (one pass; the flag of output j is bit j of the bitmap)
+      if constexpr (sizeof(Z) == sizeof(T)) {
+        if (!seg_split_mode()) {
+          // one pass: filter + tile-local sgmSum in shared memory, then the
+          // carry fix-up across tiles (k_seg_tile_scan + k_seg_fixup)
+          if ((rc = launch_filter_b<T, false, true, Z>(xs, nullptr, n, pp, ys, c0, d_k, s, zs, bits, 0, meta, st)))
+            return rc;
+          return launch_seg_fixup<Z>(meta, n, bits, 0, zs, 0, 0, st, s, Big<T>::TILE);
+        }
+      }
+      // two passes: ys = filter p xs, then zs = sgmSum flags ys over the k
+      // outputs (the flag of output j is bit j of the bitmap)
       if ((rc = launch_filter_b<T, false>(xs, nullptr, n, pp, ys, c0, d_k, s))) return rc;
       return launch_segsum_b<T, Z>(ys, n, d_k, bits, 0, zs, c1, 0, 0, nullptr, st, s);
     }

@@ -107,13 +107,25 @@ IXG_DEV unsigned long long cta_exclusive3(unsigned long long v, unsigned long lo
 IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) & 0x1fffffull); }
 
 // ---------------------------------------------------------------------------
-template <typename T, bool kByCs>
+// kSeg (C2, Z the width of zs == sizeof(T)): after ys is stored, the
+// compacted run still in shared memory is scanned again for zs = sgmSum
+// flags ys with flags at the output positions (bits out_base + base + q of
+// the mkFlags bitmap) and a TILE-LOCAL carry; the tile's segmented aggregate
+// goes to meta[tile] for the fix-up pass (k_seg_tile_scan + k_seg_fixup)
+// that adds the carry of earlier tiles before each tile's first segment.
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T>
 __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
                                                           long long n, ixg_pred p, T* __restrict__ ys, LBChan ch,
-                                                          uint32_t nonce, long long* d_count) {
+                                                          uint32_t nonce, long long* d_count,
+                                                          Z* __restrict__ zs = nullptr,
+                                                          const uint32_t* __restrict__ segbits = nullptr,
+                                                          long long out_base = 0, SegTileMeta* meta = nullptr,
+                                                          ixg_status* st = nullptr) {
+  static_assert(!kSeg || sizeof(Z) == sizeof(T), "zs is computed in place of ys");
   using B = Big<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
+  __shared__ SegOp::T s_seg[kBW];
   __shared__ unsigned long long s_w[kBW];
   __shared__ int s_cnt;
   __shared__ long long s_excl;
@@ -186,6 +198,24 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   IXG_TR(4);
   const long long base = s_excl;
   const int shift = (int)(base % B::PAD);
+  // kSeg: thread t later scans the output piece [q0, q1) of odd length L
+  // (L <= 49 outputs: its flags span <= 3 bitmap words); the L2 loads of
+  // those words are issued now and land during the compaction
+  int L = 0, q0 = 0, q1 = 0;
+  long long g0 = 0;
+  uint32_t bw0 = 0, bw1 = 0, bw2 = 0;
+  if constexpr (kSeg) {
+    L = ((cnt + kBT - 1) / kBT) | 1;
+    q0 = min(t * L, cnt);
+    q1 = min(q0 + L, cnt);
+    g0 = out_base + base + q0;
+    if (q1 > q0) {
+      const long long wd = g0 >> 5;
+      bw0 = __ldg(&segbits[wd]);
+      bw1 = __ldg(&segbits[wd + 1]);
+      bw2 = __ldg(&segbits[wd + 2]);
+    }
+  }
   // in-place stable compaction, chunk by chunk: output slot shift + r of
   // an element never exceeds its input slot PAD + i, and chunk c's outputs
   // end before chunk c+1's inputs begin
@@ -206,6 +236,45 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   IXG_TR(5);
   store_aligned<T, kBT>(ys, base, cnt, buf);
   IXG_TR(6);
+  if constexpr (kSeg) {
+    // thread t scans the run piece [q0, q1) of odd length L (odd stride:
+    // the scalar shared-memory reads of a warp hit 32 distinct banks)
+    const int sh = (int)(g0 & 31);
+    uint64_t fw = ((((uint64_t)bw1 << 32) | bw0) >> sh) | (sh ? ((uint64_t)bw2 << (64 - sh)) : 0ull);
+    const int len = q1 - q0;
+    const uint64_t lenmask = len >= 64 ? ~0ull : ((1ull << len) - 1ull);
+    fw &= lenmask;
+    // pass 1: the piece's segmented aggregate
+    const int last = fw ? 63 - __clzll(fw) : 0;
+    long long s = 0;
+    for (int j = last; j < len; ++j) s += (long long)buf[shift + q0 + j];
+    const SegOp::T a{s, fw != 0};
+    SegOp::T inc = warp_inclusive<SegOp>(a);
+    SegOp::T lex = SegOp::shfl_up(inc, 1);
+    if (lane_id() == 0) lex = SegOp::identity();
+    if (lane_id() == 31) s_seg[warp_id()] = inc;
+    bar_sync(1, kBT);  // also: every thread has finished storing ys from buf
+    SegOp::T pre = SegOp::identity(), tagg = SegOp::identity();
+#pragma unroll
+    for (int w = 0; w < kBW; ++w) {
+      if (w < warp_id()) pre = SegOp::op(pre, s_seg[w]);
+      tagg = SegOp::op(tagg, s_seg[w]);
+    }
+    // pass 2: zs in place of ys
+    long long run = SegOp::op(pre, lex).v;
+    bool narrow = false;
+    Z* zbuf = reinterpret_cast<Z*>(buf);
+    for (int j = 0; j < len; ++j) {
+      const long long x = (long long)buf[shift + q0 + j];
+      run = (((fw >> j) & 1ull) ? 0LL : run) + x;
+      if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
+      zbuf[shift + q0 + j] = (Z)run;
+    }
+    if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+    if (t == 0) meta[tile] = SegTileMeta{tagg.v, (long long)tagg.f, base, (long long)cnt};
+    bar_sync(1, kBT);
+    store_aligned<Z, kBT>(zs, base, cnt, zbuf);
+  }
 }
 
 // ---------------------------------------------------------------------------
