@@ -235,14 +235,14 @@ int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32
 }
 
 // tiles' carries for the segmented sum (k_stream.cuh fix-up), then the fix-up
-template <typename Z>
-int launch_seg_fixup(SegTileMeta* meta, long long n, const uint32_t* segbits, long long out_base, Z* zs,
+template <typename Z, typename T>
+int launch_seg_fixup(SegTileMeta* meta, long long n, const uint32_t* segbits, long long out_base, Z* zs, const T* ys,
                      long long carry_v, int carry_f, ixg_status* st, cudaStream_t s, int tile = kSTile) {
   const long long tiles = tiles_of(n, tile);
   k_seg_tile_scan<<<1, 1024, 0, s>>>(meta, tiles, carry_v, carry_f);
   LAUNCHED();
   CHECK_LAUNCH();
-  k_seg_fixup<Z><<<grid_for(tiles * 256), 256, 0, s>>>(meta, tiles, segbits, out_base, zs, st);
+  k_seg_fixup<Z, T><<<grid_for(tiles * 256), 256, 0, s>>>(meta, tiles, segbits, out_base, zs, ys, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -377,7 +377,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
           // carry fix-up across tiles (k_seg_tile_scan + k_seg_fixup)
           if ((rc = launch_filter_b<T, false, true, Z>(xs, nullptr, n, pp, ys, c0, d_k, s, zs, bits, 0, meta, st)))
             return rc;
-          return launch_seg_fixup<Z>(meta, n, bits, 0, zs, 0, 0, st, s, Big<T>::TILE);
+          return launch_seg_fixup<Z, T>(meta, n, bits, 0, zs, ys, 0, 0, st, s, Big<T>::TILE);
         }
       }
       // two passes: ys = filter p xs, then zs = sgmSum flags ys over the k
@@ -387,7 +387,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     }
     if ((rc = launch_filter_p<T, Z, false, true>(xs, nullptr, n, pp, ys, zs, bits, 0, c0, d_k, meta, st, s)))
       return rc;
-    return launch_seg_fixup<Z>(meta, n, bits, 0, zs, 0, 0, st, s);
+    return launch_seg_fixup<Z, T>(meta, n, bits, 0, zs, ys, 0, 0, st, s);
   }
   // CHECKED: filter (checked), mkFlags with materialised ind/flags arrays
   // and the checked scatter of `replicate m 1`, sgmSum as a 2-ary scan.

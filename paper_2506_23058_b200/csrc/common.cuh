@@ -6,7 +6,10 @@
 // used by every single-pass scan (lookback.cuh).
 #pragma once
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "../../include/ixgpu.h"
 
@@ -91,6 +94,45 @@ IXG_DEV bool pred_eval(const ixg_pred& p, long long x) {
     case IXG_PRED_TRUE: return true;
     default: return false;
   }
+}
+
+// The six comparison kinds as one interval test in the element's own width:
+// `p x` <=> ((U)(x - lo) <= span) xor inv, with [lo, lo + span] the set of
+// T values satisfying the comparison (clamped to T's range; `none` = empty).
+// One subtract + one unsigned compare per element instead of a sign-extended
+// 64-bit compare; identical truth table to pred_eval for every T value.
+template <typename T>
+struct PredRange {
+  using U = typename std::conditional<sizeof(T) == 4, uint32_t, unsigned long long>::type;
+  U lo, span;
+  uint32_t keep, flip;  // mask = (mask & keep) ^ flip over 16 bits
+  IXG_DEV bool test(T x) const { return (U)((U)x - lo) <= span; }
+};
+template <typename T>
+IXG_DEV PredRange<T> pred_range(const ixg_pred& p) {
+  using U = typename PredRange<T>::U;
+  constexpr long long TMIN = sizeof(T) == 4 ? (long long)INT32_MIN : LLONG_MIN;
+  constexpr long long TMAX = sizeof(T) == 4 ? (long long)INT32_MAX : LLONG_MAX;
+  long long lo = LLONG_MIN, hi = LLONG_MAX;
+  const long long t = p.thr;
+  bool none = false, inv = false;
+  switch (p.kind) {
+    case IXG_PRED_LT: none = (t == LLONG_MIN); hi = t - (none ? 0 : 1); break;
+    case IXG_PRED_GT: none = (t == LLONG_MAX); lo = t + (none ? 0 : 1); break;
+    case IXG_PRED_LE: hi = t; break;
+    case IXG_PRED_GE: lo = t; break;
+    case IXG_PRED_EQ: lo = hi = t; break;
+    default: lo = hi = t; inv = true; break;  // NE
+  }
+  lo = lo < TMIN ? TMIN : lo;
+  hi = hi > TMAX ? TMAX : hi;
+  none = none || lo > hi;
+  PredRange<T> r;
+  r.lo = none ? (U)0 : (U)lo;
+  r.span = none ? (U)0 : (U)((U)hi - (U)lo);
+  r.keep = none ? 0u : 0xffffu;
+  r.flip = inv ? 0xffffu : 0u;
+  return r;
 }
 
 // ------------------------------------------------------------ status word

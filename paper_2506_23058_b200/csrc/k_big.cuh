@@ -50,6 +50,9 @@ IXG_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
                : "memory");
 }
+IXG_DEV void cp_async16_full(uint32_t saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
+}
 IXG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 IXG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -57,6 +60,18 @@ IXG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "me
 template <typename T>
 IXG_DEV void big_issue(T* buf, const T* __restrict__ xs, long long n, long long tile_base, int t) {
   using B = Big<T>;
+  if (tile_base + B::TILE <= n) {  // full tile: no per-piece bounds
+    const T* src = xs + tile_base + kSItems * t;
+    const uint32_t s0 = smem_u32(buf + B::PAD + kSItems * t);
+#pragma unroll
+    for (int c = 0; c < B::CH; ++c)
+#pragma unroll
+      for (int j = 0; j < B::P; ++j)
+        cp_async16_full(s0 + (uint32_t)((c * kBChunk + B::swz(t, j) * B::EP) * (int)sizeof(T)),
+                        src + c * kBChunk + j * B::EP);
+    cp_async_commit();
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
 #pragma unroll
@@ -94,15 +109,36 @@ IXG_DEV unsigned long long cta_exclusive3(unsigned long long v, unsigned long lo
   }
   if (lane == 31) s_w[w] = inc;
   bar_sync(1, kBT);
-  unsigned long long pre = 0, tot = 0;
+  // every warp scans the kBW warp totals itself (lanes >= kBW hold 0)
+  unsigned long long x = lane < kBW ? s_w[lane] : 0ull;
 #pragma unroll
-  for (int k = 0; k < kBW; ++k) {
-    const unsigned long long x = s_w[k];
-    pre += (k < w) ? x : 0ull;
-    tot += x;
+  for (int d = 1; d < kBW; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += o;
   }
-  *total = tot;
-  return pre + inc - v;
+  const unsigned long long pre = __shfl_sync(0xffffffffu, x, (w + 31) & 31);  // lane w-1 (lane 31 = 0 for w = 0)
+  *total = __shfl_sync(0xffffffffu, x, kBW - 1);
+  return (w ? pre : 0ull) + inc - v;
+}
+
+// the same over SegOp values (C2's tile-local segmented scan)
+IXG_DEV SegOp::T cta_seg_exclusive(SegOp::T a, SegOp::T* s_seg, SegOp::T* total) {
+  const int lane = lane_id(), w = warp_id();
+  const SegOp::T inc = warp_inclusive<SegOp>(a);
+  SegOp::T lex = SegOp::shfl_up(inc, 1);
+  if (lane == 0) lex = SegOp::identity();
+  if (lane == 31) s_seg[w] = inc;
+  bar_sync(1, kBT);
+  SegOp::T x = lane < kBW ? s_seg[lane] : SegOp::identity();
+#pragma unroll
+  for (int d = 1; d < kBW; d <<= 1) {
+    const SegOp::T o = SegOp::shfl_up(x, d);
+    if (lane >= d) x = SegOp::op(o, x);
+  }
+  SegOp::T pre = SegOp::shfl(x, (w + 31) & 31);
+  if (w == 0) pre = SegOp::identity();
+  *total = SegOp::shfl(x, kBW - 1);
+  return SegOp::op(pre, lex);
 }
 IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) & 0x1fffffull); }
 
@@ -128,6 +164,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   __shared__ SegOp::T s_seg[kBW];
   __shared__ unsigned long long s_w[kBW];
   __shared__ int s_cnt;
+  __shared__ int s_lovf;
   __shared__ long long s_excl;
 
   const long long tile = blockIdx.x;
@@ -135,6 +172,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   const int t = threadIdx.x;
   if (warp_id() == kBW) {  // look-back warp
     long long ex = 0;
+    if (kSeg && lane_id() == 0) s_lovf = 0;  // read after the workers' barriers
     if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
     if (lane_id() == 0) s_excl = ex;
     IXG_TR_LANE0(3);
@@ -170,13 +208,14 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     }
     cp_async_wait_all();
   } else {
+    const Selector<T> sel(p);
     cp_async_wait_all();
 #pragma unroll
     for (int c = 0; c < B::CH; ++c) {
       T x[kSItems];
       big_read<T>(buf, c, t, x);
       const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
-      m[c] = select_mask<T>(p, x) & valid_mask(g, n);
+      m[c] = sel.mask(x) & valid_mask(g, n);
       packed |= (unsigned long long)__popc(m[c]) << (21 * c);
     }
   }
@@ -224,11 +263,11 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     T x[kSItems];
     big_read<T>(buf, c, t, x);
     bar_sync(1, kBT);
-    int idx = shift + before[c];
+    T* dst = buf + shift + before[c];
+    const uint32_t mc = m[c];
 #pragma unroll
     for (int j = 0; j < kSItems; ++j) {
-      if ((m[c] >> j) & 1u) buf[idx] = x[j];
-      idx += (m[c] >> j) & 1u;
+      if (mc & (1u << j)) *dst++ = x[j];
     }
   }
   bar_sync(1, kBT);
@@ -248,32 +287,50 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     const int last = fw ? 63 - __clzll(fw) : 0;
     long long s = 0;
     for (int j = last; j < len; ++j) s += (long long)buf[shift + q0 + j];
-    const SegOp::T a{s, fw != 0};
-    SegOp::T inc = warp_inclusive<SegOp>(a);
-    SegOp::T lex = SegOp::shfl_up(inc, 1);
-    if (lane_id() == 0) lex = SegOp::identity();
-    if (lane_id() == 31) s_seg[warp_id()] = inc;
-    bar_sync(1, kBT);  // also: every thread has finished storing ys from buf
-    SegOp::T pre = SegOp::identity(), tagg = SegOp::identity();
-#pragma unroll
-    for (int w = 0; w < kBW; ++w) {
-      if (w < warp_id()) pre = SegOp::op(pre, s_seg[w]);
-      tagg = SegOp::op(tagg, s_seg[w]);
+    // tile-local exclusive prefix of the piece (its barrier also orders
+    // every thread's ys stores from buf before zs overwrites it)
+    SegOp::T tagg;
+    const SegOp::T init = cta_seg_exclusive(SegOp::T{s, fw != 0}, s_seg, &tagg);
+    // pass 2: zs in place of ys.  Values at or after the tile's first flag
+    // are final; earlier ones still lack the carry of preceding tiles, which
+    // the fix-up adds (and range-checks exactly: a tile-local overflow there
+    // is reported through bit 1 of meta.f rather than as a narrowing).
+    Z* zbuf = reinterpret_cast<Z*>(buf) + shift + q0;
+    const int jf = init.f ? 0 : (fw ? __ffsll((long long)fw) - 1 : len);
+    uint64_t fb = fw;
+    int j = 0;
+    if constexpr (sizeof(Z) == 4) {
+      // 32-bit modular run; a final value leaves int32 iff its add overflows
+      // (the run since the last reset is exact while no overflow occurred)
+      int32_t r = (int32_t)init.v;
+      uint32_t ov_local = 0, ov_final = 0;
+      auto step = [&](uint32_t& acc) {
+        const int32_t x = (int32_t)zbuf[j];
+        const int32_t rr = (fb & 1ull) ? 0 : r;
+        const int32_t nr = (int32_t)((uint32_t)rr + (uint32_t)x);
+        acc |= (uint32_t)((rr ^ nr) & (x ^ nr));
+        zbuf[j] = (Z)nr;
+        r = nr;
+        fb >>= 1;
+        ++j;
+      };
+      const int jm = jf < len ? jf : len;
+#pragma unroll 4
+      while (j < jm) step(ov_local);
+#pragma unroll 4
+      while (j < len) step(ov_final);
+      if ((int32_t)ov_final < 0 && st) atomicOr(&st->flags, IXG_F_NARROW);
+      if ((int32_t)ov_local < 0) s_lovf = 1;
+    } else {
+      long long r = init.v;
+      for (; j < len; ++j, fb >>= 1) {
+        r = ((fb & 1ull) ? 0LL : r) + (long long)zbuf[j];
+        zbuf[j] = (Z)r;
+      }
     }
-    // pass 2: zs in place of ys
-    long long run = SegOp::op(pre, lex).v;
-    bool narrow = false;
-    Z* zbuf = reinterpret_cast<Z*>(buf);
-    for (int j = 0; j < len; ++j) {
-      const long long x = (long long)buf[shift + q0 + j];
-      run = (((fw >> j) & 1ull) ? 0LL : run) + x;
-      if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
-      zbuf[shift + q0 + j] = (Z)run;
-    }
-    if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
-    if (t == 0) meta[tile] = SegTileMeta{tagg.v, (long long)tagg.f, base, (long long)cnt};
     bar_sync(1, kBT);
-    store_aligned<Z, kBT>(zs, base, cnt, zbuf);
+    if (t == 0) meta[tile] = SegTileMeta{tagg.v, (long long)(tagg.f ? 1 : 0) | (s_lovf ? 2 : 0), base, (long long)cnt};
+    store_aligned<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(buf));
   }
 }
 

@@ -88,29 +88,34 @@ IXG_DEV uint32_t valid_mask(long long i0, long long n) {
   return valid <= 0 ? 0u : (valid >= kSItems ? 0xffffu : ((1u << valid) - 1u));
 }
 
-// selection mask of 16 elements; the predicate kind is hoisted (uniform)
+// The predicate of a kernel, decoded once per thread: the comparison kinds
+// become an interval test (common.cuh PredRange), HASH keeps its seed.
+template <typename T>
+struct Selector {
+  int kind;  // IXG_PRED_LT..NE -> range test
+  PredRange<T> r;
+  uint64_t seed;
+  IXG_DEV explicit Selector(const ixg_pred& p) : kind(p.kind), r(pred_range<T>(p)), seed(p.seed) {}
+  // selection mask of 16 elements; the kind is uniform, so no divergence
+  IXG_DEV uint32_t mask(const T (&x)[kSItems]) const {
+    uint32_t m = 0;
+    if (kind <= IXG_PRED_NE) {
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j) m |= (uint32_t)r.test(x[j]) << j;
+      return (m & r.keep) ^ r.flip;
+    }
+    if (kind == IXG_PRED_HASH) {
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j) m |= (uint32_t)(mix64((uint64_t)(long long)x[j] ^ seed) >> 63) << j;
+      return m;
+    }
+    return kind == IXG_PRED_TRUE ? 0xffffu : 0u;
+  }
+};
+
 template <typename T>
 IXG_DEV uint32_t select_mask(const ixg_pred& p, const T (&x)[kSItems]) {
-  uint32_t m = 0;
-  const long long t = p.thr;
-#define IXG_SEL(expr)                                    \
-  _Pragma("unroll") for (int j = 0; j < kSItems; ++j) {  \
-    const long long v = (long long)x[j];                 \
-    m |= (uint32_t)(expr) << j;                          \
-  }
-  switch (p.kind) {
-    case IXG_PRED_LT: IXG_SEL(v < t) break;
-    case IXG_PRED_GT: IXG_SEL(v > t) break;
-    case IXG_PRED_LE: IXG_SEL(v <= t) break;
-    case IXG_PRED_GE: IXG_SEL(v >= t) break;
-    case IXG_PRED_EQ: IXG_SEL(v == t) break;
-    case IXG_PRED_NE: IXG_SEL(v != t) break;
-    case IXG_PRED_HASH: IXG_SEL((mix64((uint64_t)v ^ p.seed) >> 63) != 0) break;
-    case IXG_PRED_TRUE: m = 0xffffu; break;
-    default: m = 0; break;
-  }
-#undef IXG_SEL
-  return m;
+  return Selector<T>(p).mask(x);
 }
 
 // CTA-wide exclusive prefix of per-thread counts; returns the thread's
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(1024) k_seg_tile_scan(SegTileMeta* __restrict_
   for (long long b = 0; b < ntiles; b += blockDim.x) {
     const long long t = b + threadIdx.x;
     SegOp::T x = SegOp::identity();
-    if (t < ntiles) x = SegOp::T{meta[t].v, (int)meta[t].f};
+    if (t < ntiles) x = SegOp::T{meta[t].v, (int)(meta[t].f & 1)};
     SegOp::T inc = warp_inclusive<SegOp>(x);
     if (lane_id() == 31) s_w[warp_id()] = inc;
     __syncthreads();
@@ -557,15 +562,19 @@ __global__ void __launch_bounds__(1024) k_seg_tile_scan(SegTileMeta* __restrict_
 }
 
 // Pass 2: zs[q] += carry(tile) for q in [base, first flag of the tile).
-template <typename Z>
+// meta.f bit 1 (set by k_filter_b<kSeg>): a tile-local prefix value before
+// the first flag left Z's range, so zs there holds it modulo 2^32 and the
+// exact value carry + sum ys[base..q] is range-checked from ys instead.
+template <typename Z, typename T>
 __global__ void __launch_bounds__(256) k_seg_fixup(const SegTileMeta* __restrict__ meta, long long ntiles,
                                                    const uint32_t* __restrict__ segbits, long long out_base,
-                                                   Z* __restrict__ zs, ixg_status* st) {
+                                                   Z* __restrict__ zs, const T* __restrict__ ys, ixg_status* st) {
   __shared__ long long s_stop;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const long long c = meta[t].v;
     const long long base = meta[t].base, cnt = meta[t].cnt;
-    if (c == 0 || cnt == 0) continue;  // uniform per CTA
+    const bool lovf = (meta[t].f & 2) != 0;
+    if ((c == 0 && !lovf) || cnt == 0) continue;  // uniform per CTA
     if (warp_id() == 0) {  // first set flag bit in [base, base + cnt)
       long long stop = base + cnt;
       for (long long q = base; q < base + cnt; q += 32 * 32) {
@@ -591,9 +600,23 @@ __global__ void __launch_bounds__(256) k_seg_fixup(const SegTileMeta* __restrict
     __syncthreads();
     const long long stop = s_stop;
     bool narrow = false;
+    if (lovf && warp_id() == 0) {  // rare: exact values from ys, one warp
+      long long run = c;
+      for (long long q = base; q < stop; q += 32) {
+        const bool in = q + lane_id() < stop;
+        long long x = in ? (long long)ys[q + lane_id()] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const long long o = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane_id() >= d) x += o;
+        }
+        if (in && run + x != (long long)(int)(run + x)) narrow = true;
+        run += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
     for (long long q = base + threadIdx.x; q < stop; q += blockDim.x) {
       const long long v = (long long)zs[q] + c;
-      if (sizeof(Z) == 4 && v != (long long)(int)v) narrow = true;
+      if (sizeof(Z) == 4 && !lovf && v != (long long)(int)v) narrow = true;
       zs[q] = (Z)v;
     }
     if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);

@@ -83,6 +83,62 @@ def test_filter(cuda, n, dtype, variant):
     assert np.array_equal(_np(gys)[:k].astype(np.int64), want)
 
 
+EDGE_THR = [-(1 << 63), -(1 << 31) - 1, -(1 << 31), -1, 0, 1, (1 << 31) - 1, 1 << 31, (1 << 63) - 1]
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_filter_pred_edges(cuda, dtype):
+    """comparison predicates with thresholds at and beyond the element
+    type's range (the kernels test them as a clamped interval in T's width)."""
+    from paper_2506_23058_b200 import ops
+    from paper_2506_23058_b200 import pred as P
+
+    n = 100_000  # several full tiles + a ragged one
+    info = np.iinfo(dtype)
+    xs = gen.uniform(77, n, int(info.min), int(info.max), dtype)
+    xs[:12] = [info.min, info.min + 1, -2, -1, 0, 1, 2, info.max - 1, info.max, -(1 << 31), (1 << 31) - 1, 0]
+    for kind in (P.LT, P.GT, P.LE, P.GE, P.EQ, P.NE):
+        for thr in EDGE_THR + [int(xs[500]), int(info.min), int(info.max)]:
+            p = Pred(kind, thr)
+            want = O.filter_(p, xs)
+            st = ops.Status(cuda)
+            gys, dk = ops.filter(_t(xs, cuda), p, L.VARIANT_ELIDED, st)
+            k = int(dk.item())
+            assert k == len(want), (kind, thr)
+            assert np.array_equal(_np(gys)[:k].astype(np.int64), want), (kind, thr)
+            nt, ys = O.partition2(p, xs)
+            gys, dnt = ops.partition2(_t(xs, cuda), p, L.VARIANT_ELIDED, st)
+            assert int(dnt.item()) == nt and np.array_equal(_np(gys).astype(np.int64), ys), (kind, thr)
+
+
+@pytest.mark.parametrize("head", [-(1 << 20), 0])
+def test_c2_narrow_exact(cuda, head):
+    """int32 zs: NARROW is raised iff an exact sgmSum value leaves int32.  A
+    segment crossing a tile boundary whose tile-local prefix overflows while
+    the exact value (with the preceding tile's carry) stays in range must
+    not raise it (head < 0); with no negative head it must (head = 0)."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    tile = 3 * 8192  # k_filter_b<int32> tile
+    n = 3 * tile + 100
+    xs = np.zeros(n, np.int32)
+    xs[:2047] = head
+    xs[tile:tile + 2100] = 1 << 20
+    shape = np.array([30_000, n - 30_000], np.int64)
+    want_ys, want_zs = O.c2(Pred(7), xs, shape)
+    st = ops.Status(cuda)
+    ys, zs, dk = ops.c2(_t(xs, cuda), Pred(7), _t(shape, cuda), L.VARIANT_ELIDED, st, z_dtype=torch.int32)
+    s = st.read()
+    assert s.ok
+    overflow = bool(np.any(want_zs != want_zs.astype(np.int32)))
+    assert overflow == (head == 0)
+    assert s.narrow == overflow
+    if not overflow:
+        assert np.array_equal(_np(zs).astype(np.int64), want_zs)
+
+
 @pytest.mark.parametrize("n", SIZES + [1 << 21])
 @pytest.mark.parametrize("zdt", ["i32", "i64"])
 @pytest.mark.parametrize("variant", VARIANTS + [0x2000])  # 0x2000: only mkFlags' conflict check on
