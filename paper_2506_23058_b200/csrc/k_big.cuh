@@ -97,6 +97,45 @@ IXG_DEV void big_read(const T* buf, int c, int t, T (&x)[kSItems]) {
   }
 }
 
+// Store the run buf[0 .. cnt) (tile-local slots, 16-byte aligned buffer) to
+// out[base ..]: thread j writes the j-th 16-byte chunk of out the run
+// touches.  With base not chunk-aligned the chunk's elements straddle two
+// aligned chunks of buf; the word offset is CTA-uniform, so the funnel is a
+// uniform switch.  Consecutive lanes read consecutive 16-byte chunks of buf
+// (conflict-free) and write consecutive 16-byte chunks of out.
+template <typename E, int NT>
+IXG_DEV void store_run(E* __restrict__ out, long long base, int cnt, const E* buf) {
+  constexpr int EP = 16 / (int)sizeof(E);
+  if (cnt <= 0) return;
+  const long long c0 = base / EP;
+  const int s = (int)(base - c0 * EP);                    // misalignment in elements
+  const int nch = (int)((base + cnt - 1) / EP - c0) + 1;  // chunks of out touched
+  const int sw = ((EP - s) % EP) * (int)sizeof(E) / 4;    // word offset of l in its aligned chunk
+  for (int j = threadIdx.x; j < nch; j += NT) {
+    const int l = j * EP - s;  // local index of the chunk's first element
+    E* dst = out + (c0 + j) * EP;
+    if (l >= 0 && l + EP <= cnt) {
+      uint4 v;
+      if (sw == 0) {
+        v = *reinterpret_cast<const uint4*>(buf + l);
+      } else {
+        const uint4 a = *reinterpret_cast<const uint4*>(buf + l - (EP - s));
+        const uint4 b = *reinterpret_cast<const uint4*>(buf + l + s);
+        if (sw == 1) v = make_uint4(a.y, a.z, a.w, b.x);
+        else if (sw == 2) v = make_uint4(a.z, a.w, b.x, b.y);
+        else v = make_uint4(a.w, b.x, b.y, b.z);
+      }
+      asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(v.x), "r"(v.y),
+                   "r"(v.z), "r"(v.w)
+                   : "memory");
+    } else {
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (l + e >= 0 && l + e < cnt) dst[e] = buf[l + e];
+    }
+  }
+}
+
 // CTA-wide exclusive scan of up to 3 per-thread counts (< 2^21 each) packed
 // into one 64-bit value; one named barrier over the kBT workers.
 IXG_DEV unsigned long long cta_exclusive3(unsigned long long v, unsigned long long* s_w, unsigned long long* total) {
@@ -233,13 +272,29 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     s_cnt = cnt;
     lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
   }
-  bar_sync(2, kBT + 32);
+  // in-place stable compaction to TILE-LOCAL slots, chunk by chunk, while
+  // the look-back warp resolves the tile's global base: output slot r of an
+  // element never exceeds its input slot PAD + i, and chunk c's outputs end
+  // before chunk c+1's inputs begin
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    T x[kSItems];
+    big_read<T>(buf, c, t, x);
+    bar_sync(1, kBT);
+    T* dst = buf + before[c];
+    const uint32_t mc = m[c];
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) {
+      if (mc & (1u << j)) *dst++ = x[j];
+    }
+  }
+  IXG_TR(7);
+  bar_sync(2, kBT + 32);  // base resolved; every worker's compaction done
   IXG_TR(4);
   const long long base = s_excl;
-  const int shift = (int)(base % B::PAD);
-  // kSeg: thread t later scans the output piece [q0, q1) of odd length L
-  // (L <= 49 outputs: its flags span <= 3 bitmap words); the L2 loads of
-  // those words are issued now and land during the compaction
+  // kSeg: thread t scans the output piece [q0, q1) of odd length L (L <= 49
+  // outputs: its flags span <= 3 bitmap words); the L2 loads of those words
+  // are issued now and land during the ys stores
   int L = 0, q0 = 0, q1 = 0;
   long long g0 = 0;
   uint32_t bw0 = 0, bw1 = 0, bw2 = 0;
@@ -255,25 +310,8 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
       bw2 = __ldg(&segbits[wd + 2]);
     }
   }
-  // in-place stable compaction, chunk by chunk: output slot shift + r of
-  // an element never exceeds its input slot PAD + i, and chunk c's outputs
-  // end before chunk c+1's inputs begin
-#pragma unroll
-  for (int c = 0; c < B::CH; ++c) {
-    T x[kSItems];
-    big_read<T>(buf, c, t, x);
-    bar_sync(1, kBT);
-    T* dst = buf + shift + before[c];
-    const uint32_t mc = m[c];
-#pragma unroll
-    for (int j = 0; j < kSItems; ++j) {
-      if (mc & (1u << j)) *dst++ = x[j];
-    }
-  }
-  bar_sync(1, kBT);
-  // store buf[shift .. shift + cnt) to ys[base ..] (same convention as store_aligned)
   IXG_TR(5);
-  store_aligned<T, kBT>(ys, base, cnt, buf);
+  store_run<T, kBT>(ys, base, cnt, buf);
   IXG_TR(6);
   if constexpr (kSeg) {
     // thread t scans the run piece [q0, q1) of odd length L (odd stride:
@@ -286,7 +324,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     // pass 1: the piece's segmented aggregate
     const int last = fw ? 63 - __clzll(fw) : 0;
     long long s = 0;
-    for (int j = last; j < len; ++j) s += (long long)buf[shift + q0 + j];
+    for (int j = last; j < len; ++j) s += (long long)buf[q0 + j];
     // tile-local exclusive prefix of the piece (its barrier also orders
     // every thread's ys stores from buf before zs overwrites it)
     SegOp::T tagg;
@@ -295,7 +333,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     // are final; earlier ones still lack the carry of preceding tiles, which
     // the fix-up adds (and range-checks exactly: a tile-local overflow there
     // is reported through bit 1 of meta.f rather than as a narrowing).
-    Z* zbuf = reinterpret_cast<Z*>(buf) + shift + q0;
+    Z* zbuf = reinterpret_cast<Z*>(buf) + q0;
     const int jf = init.f ? 0 : (fw ? __ffsll((long long)fw) - 1 : len);
     uint64_t fb = fw;
     int j = 0;
@@ -330,7 +368,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     }
     bar_sync(1, kBT);
     if (t == 0) meta[tile] = SegTileMeta{tagg.v, (long long)(tagg.f ? 1 : 0) | (s_lovf ? 2 : 0), base, (long long)cnt};
-    store_aligned<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(buf));
+    store_run<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(buf));
   }
 }
 
