@@ -9,20 +9,22 @@
 // 8192-element chunks per tile (96 KB of int32) with ONE look-back per tile,
 // resolved by a dedicated warp while the copies land.
 //
-//   k_filter_b   filter / filter_by: count pass over the staged chunks, one
-//                CTA-wide scan of the packed per-chunk counts, stable
-//                compaction IN PLACE in shared memory (an element's output
-//                slot never lies after its input slot), aligned 256-bit
-//                stores of the run.
+//   k_filter_b   filter / filter_by [+ C2's sgmSum]: "quad" layout (below),
+//                count pass, warp-packed scans of per-piece counts, stable
+//                compaction IN PLACE to tile-local slots (an element's output
+//                slot never lies after its input slot) while the look-back
+//                resolves the base, then 16-byte stores of the run.
 //   k_segsum_b   sgmSum over an array (C2's zs = sgmSum flags ys): flags are
 //                bits of the mkFlags bitmap at the element's own position, so
 //                they are fetched together with the data; the segmented
 //                aggregate of the tile takes the look-back; every thread
 //                writes its 16 results with two 256-bit stores.
 //
-// Shared-memory layout of a thread's 16 elements: one 16*sizeof(T)-byte
-// block per chunk, its 16-byte pieces XOR-swizzled by the thread index so
-// that the LDS.128 reads of a quarter-warp hit 8 distinct bank groups.
+// k_segsum_b's shared-memory layout gives a thread 16 consecutive elements:
+// one 16*sizeof(T)-byte block per chunk, its 16-byte pieces XOR-swizzled by
+// the thread index so that the LDS.128 reads of a quarter-warp hit 8
+// distinct bank groups (the copies into it still cost ~7x the ideal
+// wavefronts; k_filter_b's quad layout avoids that).
 #pragma once
 #include "k_stream.cuh"
 
@@ -97,6 +99,129 @@ IXG_DEV void big_read(const T* buf, int c, int t, T (&x)[kSItems]) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// "Quad" layout of a tile (k_filter_b): in chunk c, warp w owns elements
+// [512w, 512w + 512); its lane l holds P = 16/EP pieces of EP = 16/sizeof(T)
+// consecutive elements, piece k at 512w + k*32*EP + l*EP.  Every warp-wide
+// cp.async / LDS.128 of piece k then covers 512 contiguous bytes: 16 full
+// sectors from L2 and 4 shared-memory wavefronts, with no swizzle (the
+// blocked 16-per-lane layout cost 7x the wavefronts on the copy side).  The
+// compaction stores of a warp for one (piece, element) land ~EP/2 words
+// apart instead of ~8, i.e. <= 2-way bank conflicts.
+template <typename T>
+struct Quad {
+  static constexpr int EP = 16 / (int)sizeof(T);
+  static constexpr int P = kSItems / EP;
+  // per-piece counts, 8 bits each (a warp's piece total is <= 32*EP <= 128)
+  using PK = typename std::conditional<(P <= 4), uint32_t, unsigned long long>::type;
+  IXG_DEV static int off(int w, int k, int l) { return w * (32 * kSItems) + k * (32 * EP) + l * EP; }
+  IXG_DEV static PK counts(uint32_t m) {
+    PK v = 0;
+#pragma unroll
+    for (int k = 0; k < P; ++k) v |= (PK)__popc((m >> (k * EP)) & ((1u << EP) - 1u)) << (8 * k);
+    return v;
+  }
+  IXG_DEV static int field(PK v, int k) { return (int)((v >> (8 * k)) & 0xff); }
+  IXG_DEV static int field_sum(PK v) {
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < P; ++k) s += field(v, k);
+    return s;
+  }
+};
+
+template <typename T>
+IXG_DEV void quad_issue(T* buf, const T* __restrict__ xs, long long n, long long tile_base, int w, int l, bool full) {
+  using B = Big<T>;
+  using Q = Quad<T>;
+  const int o0 = Q::off(w, 0, l);
+  if (full) {
+    const T* src = xs + tile_base + o0;
+    const uint32_t s0 = smem_u32(buf + B::PAD + o0);
+#pragma unroll
+    for (int c = 0; c < B::CH; ++c)
+#pragma unroll
+      for (int k = 0; k < Q::P; ++k)
+        cp_async16_full(s0 + (uint32_t)((c * kBChunk + k * 32 * Q::EP) * (int)sizeof(T)),
+                        src + c * kBChunk + k * 32 * Q::EP);
+  } else {
+#pragma unroll
+    for (int c = 0; c < B::CH; ++c)
+#pragma unroll
+      for (int k = 0; k < Q::P; ++k) {
+        const int o = c * kBChunk + o0 + k * 32 * Q::EP;
+        long long valid = (n - (tile_base + o)) * (long long)sizeof(T);
+        valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+        cp_async16(buf + B::PAD + o, valid ? (const void*)(xs + tile_base + o) : (const void*)xs, (int)valid);
+      }
+  }
+  cp_async_commit();
+}
+
+template <typename T>
+IXG_DEV void quad_read(const T* buf, int c, int w, int l, T (&x)[kSItems]) {
+  using B = Big<T>;
+  using Q = Quad<T>;
+#pragma unroll
+  for (int k = 0; k < Q::P; ++k) {
+    const uint4 v = *reinterpret_cast<const uint4*>(buf + B::PAD + c * kBChunk + Q::off(w, k, l));
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int q = 0; q < Q::EP; ++q) x[k * Q::EP + q] = e[q];
+  }
+}
+
+// valid bits of the lane's pieces (g0 = global index of its piece 0)
+template <int EP>
+IXG_DEV uint32_t quad_valid(long long n, long long g0) {
+  uint32_t vm = 0;
+#pragma unroll
+  for (int k = 0; k < kSItems / EP; ++k) {
+    const long long r = n - (g0 + k * 32 * EP);
+    const int v = r <= 0 ? 0 : (r >= EP ? EP : (int)r);
+    vm |= ((1u << v) - 1u) << (k * EP);
+  }
+  return vm;
+}
+
+// filter_by: bit k*EP + e = (cs[g0 + k*32*EP + e] != 0), bounds-checked
+template <int EP>
+IXG_DEV uint32_t quad_cs_mask(const uint8_t* __restrict__ cs, long long n, long long g0, bool full) {
+  uint32_t mm = 0;
+#pragma unroll
+  for (int k = 0; k < kSItems / EP; ++k) {
+    const long long g = g0 + k * 32 * EP;
+    uint32_t b = 0;
+    if (full && ((reinterpret_cast<uintptr_t>(cs + g) & (EP - 1)) == 0)) {
+      b = EP == 4 ? *reinterpret_cast<const uint32_t*>(cs + g) : (uint32_t)*reinterpret_cast<const uint16_t*>(cs + g);
+    } else {
+#pragma unroll
+      for (int e = 0; e < EP; ++e) b |= (g + e < n) ? (uint32_t)cs[g + e] << (8 * e) : 0u;
+    }
+#pragma unroll
+    for (int e = 0; e < EP; ++e) mm |= (uint32_t)(((b >> (8 * e)) & 0xffu) != 0) << (k * EP + e);
+  }
+  return mm;
+}
+
+// CTA-wide exclusive scan of warp-uniform packed counts (3 x 21 bits):
+// returns the exclusive prefix of the calling warp, *total = CTA totals
+IXG_DEV unsigned long long cta_warp_exclusive3(unsigned long long v, unsigned long long* s_w,
+                                               unsigned long long* total) {
+  const int lane = lane_id(), w = warp_id();
+  if (lane == 0) s_w[w] = v;
+  bar_sync(1, kBT);
+  unsigned long long x = lane < kBW ? s_w[lane] : 0ull;
+#pragma unroll
+  for (int d = 1; d < kBW; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += o;
+  }
+  const unsigned long long pre = __shfl_sync(0xffffffffu, x, (w + 31) & 31);
+  *total = __shfl_sync(0xffffffffu, x, kBW - 1);
+  return w ? pre : 0ull;
+}
+
 // Store the run buf[0 .. cnt) (tile-local slots, 16-byte aligned buffer) to
 // out[base ..]: thread j writes the j-th 16-byte chunk of out the run
 // touches.  With base not chunk-aligned the chunk's elements straddle two
@@ -136,31 +261,8 @@ IXG_DEV void store_run(E* __restrict__ out, long long base, int cnt, const E* bu
   }
 }
 
-// CTA-wide exclusive scan of up to 3 per-thread counts (< 2^21 each) packed
-// into one 64-bit value; one named barrier over the kBT workers.
-IXG_DEV unsigned long long cta_exclusive3(unsigned long long v, unsigned long long* s_w, unsigned long long* total) {
-  const int lane = lane_id(), w = warp_id();
-  unsigned long long inc = v;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= d) inc += o;
-  }
-  if (lane == 31) s_w[w] = inc;
-  bar_sync(1, kBT);
-  // every warp scans the kBW warp totals itself (lanes >= kBW hold 0)
-  unsigned long long x = lane < kBW ? s_w[lane] : 0ull;
-#pragma unroll
-  for (int d = 1; d < kBW; d <<= 1) {
-    const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
-    if (lane >= d) x += o;
-  }
-  const unsigned long long pre = __shfl_sync(0xffffffffu, x, (w + 31) & 31);  // lane w-1 (lane 31 = 0 for w = 0)
-  *total = __shfl_sync(0xffffffffu, x, kBW - 1);
-  return (w ? pre : 0ull) + inc - v;
-}
-
-// the same over SegOp values (C2's tile-local segmented scan)
+// CTA-wide exclusive scan over SegOp values (C2's tile-local segmented scan);
+// one named barrier over the kBT workers, *total = the CTA aggregate
 IXG_DEV SegOp::T cta_seg_exclusive(SegOp::T a, SegOp::T* s_seg, SegOp::T* total) {
   const int lane = lane_id(), w = warp_id();
   const SegOp::T inc = warp_inclusive<SegOp>(a);
@@ -179,6 +281,7 @@ IXG_DEV SegOp::T cta_seg_exclusive(SegOp::T a, SegOp::T* s_seg, SegOp::T* total)
   *total = SegOp::shfl(x, kBW - 1);
   return SegOp::op(pre, lex);
 }
+
 IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) & 0x1fffffull); }
 
 // ---------------------------------------------------------------------------
@@ -214,7 +317,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     if (kSeg && lane_id() == 0) s_lovf = 0;  // read after the workers' barriers
     if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
     if (lane_id() == 0) s_excl = ex;
-    IXG_TR_LANE0(3);
+    IXG_TR_LANE0(5);
     bar_sync(2, kBT + 32);
     if (lane_id() == 0) {
       const int cnt = s_cnt;
@@ -224,27 +327,15 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     return;
   }
   IXG_TR(0);
-  big_issue<T>(buf, xs, n, tile_base, t);
-  // selection masks of the thread's blocks (filter_by: read cs meanwhile)
+  using Q = Quad<T>;
+  const int w = warp_id(), l = lane_id();
+  const bool full = tile_base + B::TILE <= n;
+  quad_issue<T>(buf, xs, n, tile_base, w, l, full);
+  // selection masks of the lane's pieces (bit k*EP + e), filter_by reads cs meanwhile
   uint32_t m[B::CH];
-  unsigned long long packed = 0;
   if (kByCs) {
 #pragma unroll
-    for (int c = 0; c < B::CH; ++c) {
-      const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
-      uint32_t mm = 0;
-      if (g + kSItems <= n) {
-        const uint4 v = *reinterpret_cast<const uint4*>(cs + g);
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < kSItems; ++j) mm |= (uint32_t)(((w4[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0) << j;
-      } else {
-#pragma unroll
-        for (int j = 0; j < kSItems; ++j) mm |= (uint32_t)((g + j < n) && cs[g + j] != 0) << j;
-      }
-      m[c] = mm;
-      packed |= (unsigned long long)__popc(mm) << (21 * c);
-    }
+    for (int c = 0; c < B::CH; ++c) m[c] = quad_cs_mask<Q::EP>(cs, n, tile_base + c * kBChunk + Q::off(w, 0, l), full);
     cp_async_wait_all();
   } else {
     const Selector<T> sel(p);
@@ -252,20 +343,36 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
 #pragma unroll
     for (int c = 0; c < B::CH; ++c) {
       T x[kSItems];
-      big_read<T>(buf, c, t, x);
-      const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
-      m[c] = sel.mask(x) & valid_mask(g, n);
-      packed |= (unsigned long long)__popc(m[c]) << (21 * c);
+      quad_read<T>(buf, c, w, l, x);
+      m[c] = sel.mask(x);
+      if (!full) m[c] &= quad_valid<Q::EP>(n, tile_base + c * kBChunk + Q::off(w, 0, l));
     }
   }
-  unsigned long long tot;
   IXG_TR(1);
-  const unsigned long long ex3 = cta_exclusive3(packed, s_w, &tot);
+  // per-piece counts packed 8 bits per piece, scanned across the warp:
+  // order within a chunk is (warp, piece, lane)
+  typename Q::PK ex[B::CH], wt[B::CH];
+  unsigned long long packed = 0;
+#pragma unroll
+  for (int c = 0; c < B::CH; ++c) {
+    const typename Q::PK v = Q::counts(m[c]);
+    typename Q::PK inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const typename Q::PK o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (l >= d) inc += o;
+    }
+    wt[c] = __shfl_sync(0xffffffffu, inc, 31);
+    ex[c] = inc - v;
+    packed |= (unsigned long long)Q::field_sum(wt[c]) << (21 * c);
+  }
+  unsigned long long tot;
+  const unsigned long long exw = cta_warp_exclusive3(packed, s_w, &tot);
   IXG_TR(2);
   int cnt = 0, before[B::CH];
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
-    before[c] = cnt + field21(ex3, c);
+    before[c] = cnt + field21(exw, c);
     cnt += field21(tot, c);
   }
   if (t == 0) {
@@ -279,16 +386,21 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     T x[kSItems];
-    big_read<T>(buf, c, t, x);
+    quad_read<T>(buf, c, w, l, x);
     bar_sync(1, kBT);
-    T* dst = buf + before[c];
     const uint32_t mc = m[c];
+    int pre = before[c];  // + totals of the warp's earlier pieces
 #pragma unroll
-    for (int j = 0; j < kSItems; ++j) {
-      if (mc & (1u << j)) *dst++ = x[j];
+    for (int k = 0; k < Q::P; ++k) {
+      T* dst = buf + pre + Q::field(ex[c], k);
+      pre += Q::field(wt[c], k);
+#pragma unroll
+      for (int e = 0; e < Q::EP; ++e) {
+        if (mc & (1u << (k * Q::EP + e))) *dst++ = x[k * Q::EP + e];
+      }
     }
   }
-  IXG_TR(7);
+  IXG_TR(3);
   bar_sync(2, kBT + 32);  // base resolved; every worker's compaction done
   IXG_TR(4);
   const long long base = s_excl;
@@ -310,7 +422,6 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
       bw2 = __ldg(&segbits[wd + 2]);
     }
   }
-  IXG_TR(5);
   store_run<T, kBT>(ys, base, cnt, buf);
   IXG_TR(6);
   if constexpr (kSeg) {

@@ -45,11 +45,13 @@ def main():
     a = a[:tiles]
     t0 = a[:, 0].min()
     a[:, :7] -= t0
-    names = ["load", "cta_scan", "lb_done", "bar2", "stage", "store"]
+    # k_filter_b slots: 0 start, 1 counted, 2 CTA scan, 3 compacted,
+    # 4 base known (bar 2), 5 look-back warp done, 6 stores done
     print(f"tiles {tiles}, kernel span {a[:, 6].max() / 1e3:.1f} us")
-    for i, nm in enumerate(names):
-        d = a[:, i + 1] - a[:, i]
-        print(f"  {nm:9s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
+    for nm, i, j in (("load+count", 0, 1), ("cta_scan", 1, 2), ("compact", 2, 3), ("wait_base", 3, 4),
+                     ("store(+seg)", 4, 6), ("lookback", 0, 5)):
+        d = a[:, j] - a[:, i]
+        print(f"  {nm:11s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
     life = a[:, 6] - a[:, 0]
     print(f"  life      median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
     # CTAs in flight at the middle of the kernel
