@@ -200,7 +200,7 @@ inline bool seg_split_mode() {
 template <typename T, bool kByCs, bool kSeg = false, typename Z = T>
 int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, LBChan ch,
                     long long* d_count, cudaStream_t s, Z* zs = nullptr, const uint32_t* segbits = nullptr,
-                    long long out_base = 0, SegTileMeta* meta = nullptr, ixg_status* st = nullptr) {
+                    long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr}, ixg_status* st = nullptr) {
   auto kern = k_filter_b<T, kByCs, kSeg, Z>;
   static bool attr = false;
   if (!attr) {
@@ -209,7 +209,7 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
   }
   TimedLaunch tl(IXG_K_FILTER_FUSED, s);
   kern<<<(unsigned)tiles_of(n, Big<T>::TILE), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(),
-                                                                           d_count, zs, segbits, out_base, meta, st);
+                                                                           d_count, zs, segbits, out_base, ch2, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -373,11 +373,9 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     if (big_mode()) {
       if constexpr (sizeof(Z) == sizeof(T)) {
         if (!seg_split_mode()) {
-          // one pass: filter + tile-local sgmSum in shared memory, then the
-          // carry fix-up across tiles (k_seg_tile_scan + k_seg_fixup)
-          if ((rc = launch_filter_b<T, false, true, Z>(xs, nullptr, n, pp, ys, c0, d_k, s, zs, bits, 0, meta, st)))
-            return rc;
-          return launch_seg_fixup<Z, T>(meta, n, bits, 0, zs, ys, 0, 0, st, s, Big<T>::TILE);
+          // one pass: filter + sgmSum in shared memory; the carry across
+          // tiles takes a second look-back chain (channel 1)
+          return launch_filter_b<T, false, true, Z>(xs, nullptr, n, pp, ys, c0, d_k, s, zs, bits, 0, c1, st);
         }
       }
       // two passes: ys = filter p xs, then zs = sgmSum flags ys over the k

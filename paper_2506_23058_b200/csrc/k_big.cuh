@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
                                                           uint32_t nonce, long long* d_count,
                                                           Z* __restrict__ zs = nullptr,
                                                           const uint32_t* __restrict__ segbits = nullptr,
-                                                          long long out_base = 0, SegTileMeta* meta = nullptr,
+                                                          long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr},
                                                           ixg_status* st = nullptr) {
   static_assert(!kSeg || sizeof(Z) == sizeof(T), "zs is computed in place of ys");
   using B = Big<T>;
@@ -306,15 +306,14 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   __shared__ SegOp::T s_seg[kBW];
   __shared__ unsigned long long s_w[kBW];
   __shared__ int s_cnt;
-  __shared__ int s_lovf;
   __shared__ long long s_excl;
+  __shared__ SegOp::T s_tagg, s_carry;
 
   const long long tile = blockIdx.x;
   const long long tile_base = tile * B::TILE;
   const int t = threadIdx.x;
   if (warp_id() == kBW) {  // look-back warp
     long long ex = 0;
-    if (kSeg && lane_id() == 0) s_lovf = 0;  // read after the workers' barriers
     if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
     if (lane_id() == 0) s_excl = ex;
     IXG_TR_LANE0(5);
@@ -323,6 +322,16 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
       const int cnt = s_cnt;
       if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
       if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
+    }
+    if constexpr (kSeg) {
+      // second chain: the sgmSum carry into the tile (SegOp over the tiles'
+      // segmented aggregates), polled while the workers store ys and scan
+      SegOp::T carry = SegOp::identity();
+      if (tile > 0) carry = lb_lookback<SegOp>(ch2, nonce, tile);
+      if (lane_id() == 0) s_carry = carry;
+      bar_sync(3, kBT + 32);
+      const SegOp::T a = s_tagg;
+      if (lane_id() == 0 && tile > 0 && !a.f) lb_publish<SegOp>(ch2, nonce, tile, SegOp::op(carry, a), true);
     }
     return;
   }
@@ -440,36 +449,44 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     // every thread's ys stores from buf before zs overwrites it)
     SegOp::T tagg;
     const SegOp::T init = cta_seg_exclusive(SegOp::T{s, fw != 0}, s_seg, &tagg);
+    if (t == 0) {  // a tile with a flag knows its inclusive value already
+      s_tagg = tagg;
+      lb_publish<SegOp>(ch2, nonce, tile, tagg, tile == 0 || tagg.f);
+    }
     // pass 2: zs in place of ys.  Values at or after the tile's first flag
-    // are final; earlier ones still lack the carry of preceding tiles, which
-    // the fix-up adds (and range-checks exactly: a tile-local overflow there
-    // is reported through bit 1 of meta.f rather than as a narrowing).
+    // are final; the earlier ones (j < jm) are tile-local until the carry of
+    // the preceding tiles arrives, so they run exactly in 64 bits and keep
+    // their range [lo, hi] for the check once the carry is known.
     Z* zbuf = reinterpret_cast<Z*>(buf) + q0;
     const int jf = init.f ? 0 : (fw ? __ffsll((long long)fw) - 1 : len);
-    uint64_t fb = fw;
-    int j = 0;
+    const int jm = jf < len ? jf : len;
+    uint64_t fb = fw >> jm;
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    {
+      long long r = init.v;
+      for (int j = 0; j < jm; ++j) {  // no flags here
+        r += (long long)zbuf[j];
+        lo = r < lo ? r : lo;
+        hi = r > hi ? r : hi;
+        zbuf[j] = (Z)r;
+      }
+    }
+    int j = jm;
     if constexpr (sizeof(Z) == 4) {
-      // 32-bit modular run; a final value leaves int32 iff its add overflows
-      // (the run since the last reset is exact while no overflow occurred)
+      // 32-bit modular run from the first flag on (or from an exact final
+      // init): a value leaves int32 iff its add overflows
       int32_t r = (int32_t)init.v;
-      uint32_t ov_local = 0, ov_final = 0;
-      auto step = [&](uint32_t& acc) {
+      uint32_t ov = 0;
+#pragma unroll 4
+      for (; j < len; ++j, fb >>= 1) {
         const int32_t x = (int32_t)zbuf[j];
         const int32_t rr = (fb & 1ull) ? 0 : r;
         const int32_t nr = (int32_t)((uint32_t)rr + (uint32_t)x);
-        acc |= (uint32_t)((rr ^ nr) & (x ^ nr));
+        ov |= (uint32_t)((rr ^ nr) & (x ^ nr));
         zbuf[j] = (Z)nr;
         r = nr;
-        fb >>= 1;
-        ++j;
-      };
-      const int jm = jf < len ? jf : len;
-#pragma unroll 4
-      while (j < jm) step(ov_local);
-#pragma unroll 4
-      while (j < len) step(ov_final);
-      if ((int32_t)ov_final < 0 && st) atomicOr(&st->flags, IXG_F_NARROW);
-      if ((int32_t)ov_local < 0) s_lovf = 1;
+      }
+      if ((int32_t)ov < 0 && st) atomicOr(&st->flags, IXG_F_NARROW);
     } else {
       long long r = init.v;
       for (; j < len; ++j, fb >>= 1) {
@@ -477,8 +494,14 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
         zbuf[j] = (Z)r;
       }
     }
+    bar_sync(3, kBT + 32);  // carry of the preceding tiles
+    if (jm > 0) {
+      const long long cv = s_carry.v;
+      if (sizeof(Z) == 4 && st && (cv + lo < (long long)INT32_MIN || cv + hi > (long long)INT32_MAX))
+        atomicOr(&st->flags, IXG_F_NARROW);
+      for (int q = 0; q < jm; ++q) zbuf[q] = (Z)((unsigned long long)zbuf[q] + (unsigned long long)cv);
+    }
     bar_sync(1, kBT);
-    if (t == 0) meta[tile] = SegTileMeta{tagg.v, (long long)(tagg.f ? 1 : 0) | (s_lovf ? 2 : 0), base, (long long)cnt};
     store_run<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(buf));
   }
 }
