@@ -55,6 +55,30 @@ IXG_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
 IXG_DEV void cp_async16_full(uint32_t saddr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
 }
+// mbarrier + 1-D bulk copy (TMA engine, SASS UBLKCP) helpers
+IXG_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+IXG_DEV void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+IXG_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+IXG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+IXG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
 IXG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 IXG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -308,6 +332,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   __shared__ int s_cnt;
   __shared__ long long s_excl;
   __shared__ SegOp::T s_tagg, s_carry;
+  __shared__ __align__(8) uint64_t s_mbar[B::CH];
 
   const long long tile = blockIdx.x;
   const long long tile_base = tile * B::TILE;
@@ -339,18 +364,36 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   using Q = Quad<T>;
   const int w = warp_id(), l = lane_id();
   const bool full = tile_base + B::TILE <= n;
-  quad_issue<T>(buf, xs, n, tile_base, w, l, full);
+  // full tiles: one bulk (TMA) copy per chunk issued by one thread, landing
+  // on the chunk's mbarrier (no per-lane copies, no LSU wavefronts); the
+  // ragged last tile uses per-lane cp.async with zero fill
+  if (full) {
+    if (t == 0) {
+#pragma unroll
+      for (int c = 0; c < B::CH; ++c) mbar_init(&s_mbar[c], 1);
+      mbar_fence_init();
+#pragma unroll
+      for (int c = 0; c < B::CH; ++c) {
+        mbar_expect_tx(&s_mbar[c], kBChunk * (uint32_t)sizeof(T));
+        bulk_g2s(buf + B::PAD + c * kBChunk, xs + tile_base + c * kBChunk, kBChunk * (uint32_t)sizeof(T), &s_mbar[c]);
+      }
+    }
+    bar_sync(1, kBT);  // the mbarriers are initialised
+  } else {
+    quad_issue<T>(buf, xs, n, tile_base, w, l, false);
+  }
   // selection masks of the lane's pieces (bit k*EP + e), filter_by reads cs meanwhile
   uint32_t m[B::CH];
   if (kByCs) {
 #pragma unroll
     for (int c = 0; c < B::CH; ++c) m[c] = quad_cs_mask<Q::EP>(cs, n, tile_base + c * kBChunk + Q::off(w, 0, l), full);
-    cp_async_wait_all();
+    if (!full) cp_async_wait_all();
   } else {
     const Selector<T> sel(p);
-    cp_async_wait_all();
+    if (!full) cp_async_wait_all();
 #pragma unroll
     for (int c = 0; c < B::CH; ++c) {
+      if (full) mbar_wait(&s_mbar[c], 0);
       T x[kSItems];
       quad_read<T>(buf, c, w, l, x);
       m[c] = sel.mask(x);
@@ -394,6 +437,7 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   // before chunk c+1's inputs begin
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
+    if (kByCs && full) mbar_wait(&s_mbar[c], 0);
     T x[kSItems];
     quad_read<T>(buf, c, w, l, x);
     bar_sync(1, kBT);

@@ -1,6 +1,6 @@
-# GPU tests + per-kernel timings (development loop)
-python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-python tools/kbench.py ${1:-28} > gpurun_out/kbench.json 2>&1
+# GPU tests + per-kernel timings (development loop); each step under its own timeout
+timeout 600 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python tools/kbench.py ${1:-28} > gpurun_out/kbench.json 2>&1
 python - <<'PY'
 import json
 d = json.load(open("gpurun_out/kbench.json"))
