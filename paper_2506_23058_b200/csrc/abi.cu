@@ -4,6 +4,7 @@
 // allocator (the same code path sizes it for ixg_ws_bytes), picks the fused
 // ELIDED kernel or the materialising CHECKED sequence from the site bits,
 // and enqueues everything on the caller's stream.  No host synchronisation.
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -197,19 +198,21 @@ inline bool seg_split_mode() {
   return mode == 1;
 }
 
-template <typename T, bool kByCs, bool kSeg = false, typename Z = T>
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1>
 int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, LBChan ch,
                     long long* d_count, cudaStream_t s, Z* zs = nullptr, const uint32_t* segbits = nullptr,
-                    long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr}, ixg_status* st = nullptr) {
-  auto kern = k_filter_b<T, kByCs, kSeg, Z>;
+                    long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr}, ixg_status* st = nullptr,
+                    const ixg_pred& q = ixg_pred{}) {
+  auto kern = k_filter_b<T, kByCs, kSeg, Z, NS>;
   static bool attr = false;
   if (!attr) {
     allow_smem(kern, Big<T>::SMEM);
     attr = true;
   }
-  TimedLaunch tl(IXG_K_FILTER_FUSED, s);
-  kern<<<(unsigned)tiles_of(n, Big<T>::TILE), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(),
-                                                                           d_count, zs, segbits, out_base, ch2, st);
+  TimedLaunch tl(NS > 1 ? IXG_K_PLACE : IXG_K_FILTER_FUSED, s);
+  const long long seg_tiles = tiles_of(n, Big<T>::TILE);
+  kern<<<(unsigned)(NS * seg_tiles), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(), d_count, zs,
+                                                                  segbits, out_base, ch2, st, q, seg_tiles);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -296,10 +299,21 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
   const int cgrid = grid_for(n / (16 / (int)sizeof(T)) + 1);
   long long* partials = (long long*)ws.take((size_t)cgrid * 2 * 8);
   if (fused) {
-    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
+    const long long lb_tiles = std::max(tiles_of(n, kSTile), kClasses * tiles_of(n, Big<T>::TILE));
+    LBChan c0 = ws.chan(0, lb_tiles);
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
+    if (big_mode()) {
+      // one pass: kClasses segments of big tiles on one look-back chain
+      int rc = launch_filter_b<T, false, false, T, kClasses>(xs, nullptr, n, pp, ys, c0, d_tot, s, nullptr, nullptr,
+                                                             0, LBChan{nullptr, nullptr}, nullptr, qq);
+      if (rc || kClasses == 2) return rc;
+      k_sub_first<<<1, 1, 0, s>>>(d_tot);  // d_tot[1] held m1 + m2
+      LAUNCHED();
+      CHECK_LAUNCH();
+      return IXG_OK;
+    }
     {
       TimedLaunch tl(IXG_K_CLASS_COUNT, s);
       k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);

@@ -315,14 +315,22 @@ IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) 
 // the mkFlags bitmap) and a TILE-LOCAL carry; the tile's segmented aggregate
 // goes to meta[tile] for the fix-up pass (k_seg_tile_scan + k_seg_fixup)
 // that adds the carry of earlier tiles before each tile's first segment.
-template <typename T, bool kByCs, bool kSeg = false, typename Z = T>
+//
+// NS > 1 (partition2 / partition3, ELIDED): the grid is NS segments of
+// seg_tiles tiles over the same xs, segment s selecting class s (p; not p
+// [and q]; not p and not q), all on ONE look-back chain -- so the chain's
+// prefix is the class's output position and the whole stable partition is
+// a single pass writing each element once (d_count[s] = the prefix at the
+// end of segment s, for s < NS - 1).
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1>
 __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
                                                           long long n, ixg_pred p, T* __restrict__ ys, LBChan ch,
                                                           uint32_t nonce, long long* d_count,
                                                           Z* __restrict__ zs = nullptr,
                                                           const uint32_t* __restrict__ segbits = nullptr,
                                                           long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr},
-                                                          ixg_status* st = nullptr) {
+                                                          ixg_status* st = nullptr, ixg_pred q = ixg_pred{},
+                                                          long long seg_tiles = 0) {
   static_assert(!kSeg || sizeof(Z) == sizeof(T), "zs is computed in place of ys");
   using B = Big<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -334,8 +342,9 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
   __shared__ SegOp::T s_tagg, s_carry;
   __shared__ __align__(8) uint64_t s_mbar[B::CH];
 
-  const long long tile = blockIdx.x;
-  const long long tile_base = tile * B::TILE;
+  const long long tile = blockIdx.x;  // position on the look-back chain
+  const int seg = NS > 1 ? (int)(tile / seg_tiles) : 0;
+  const long long tile_base = (NS > 1 ? tile - seg * seg_tiles : tile) * B::TILE;
   const int t = threadIdx.x;
   if (warp_id() == kBW) {  // look-back warp
     long long ex = 0;
@@ -346,7 +355,8 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
     if (lane_id() == 0) {
       const int cnt = s_cnt;
       if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
-      if (tile == (long long)gridDim.x - 1) *d_count = ex + cnt;
+      if (NS == 1 ? tile == (long long)gridDim.x - 1 : (seg < NS - 1 && tile == (seg + 1) * seg_tiles - 1))
+        d_count[seg] = ex + cnt;
     }
     if constexpr (kSeg) {
       // second chain: the sgmSum carry into the tile (SegOp over the tiles'
@@ -397,6 +407,14 @@ __global__ void __launch_bounds__(kBT + 32, 2) k_filter_b(const T* __restrict__ 
       T x[kSItems];
       quad_read<T>(buf, c, w, l, x);
       m[c] = sel.mask(x);
+      if constexpr (NS == 2) {
+        if (seg == 1) m[c] ^= 0xffffu;
+      } else if constexpr (NS == 3) {
+        if (seg > 0) {
+          const uint32_t mq = Selector<T>(q).mask(x);
+          m[c] = ~m[c] & (seg == 1 ? mq : ~mq) & 0xffffu;
+        }
+      }
       if (!full) m[c] &= quad_valid<Q::EP>(n, tile_base + c * kBChunk + Q::off(w, 0, l));
     }
   }
@@ -713,5 +731,8 @@ __global__ void __launch_bounds__(256) k_add_prefix(Z* __restrict__ zs, const un
   }
   if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
 }
+
+// partition3's single pass leaves the prefix at the end of segment 1 (m1 + m2)
+__global__ void k_sub_first(long long* d_tot) { d_tot[1] -= d_tot[0]; }
 
 }  // namespace ixg

@@ -260,12 +260,12 @@ def partition2(xs: torch.Tensor, p: Pred, variant: int, status: Status, ys=None,
     return ys, d_nt
 
 
-def partition3(xs: torch.Tensor, p: Pred, q: Pred, variant: int, status: Status):
+def partition3(xs: torch.Tensor, p: Pred, q: Pred, variant: int, status: Status, ys=None, d_m=None):
     """partition3 p q xs (corpus partition3.ixl); returns (ys, device (m1, m2))."""
     xs = _contig(xs)
     n = xs.numel()
-    ys = torch.empty(n, dtype=xs.dtype, device=xs.device)
-    d_m = torch.empty(2, dtype=torch.int64, device=xs.device)
+    ys = torch.empty(n, dtype=xs.dtype, device=xs.device) if ys is None else ys
+    d_m = torch.empty(2, dtype=torch.int64, device=xs.device) if d_m is None else d_m
     ws, wsb = _ws(L.OP_PARTITION3, n, 0, xs.device)
     cp, cq = _c_pred(p), _c_pred(q)
     L.check(

@@ -83,7 +83,12 @@ def main():
     out["place_kernel"] = {"ms": ktime(L.K_PLACE, f)}
     out["count_kernel"] = {"ms": ktime(L.K_CLASS_COUNT, f)}
     out["place_kernel"]["algoGBps"] = 8 * n / out["place_kernel"]["ms"] / 1e6
-    out["count_kernel"]["GBps"] = 4 * n / out["count_kernel"]["ms"] / 1e6
+    out["count_kernel"]["GBps"] = 4 * n / max(out["count_kernel"]["ms"], 1e-9) / 1e6
+    dm = torch.empty(2, dtype=torch.int64, device=dev)
+    for name, var in (("elided", L.VARIANT_ELIDED), ("checked", L.VARIANT_CHECKED)):
+        f = lambda var=var: ops.partition3(xs2, Pred.lt(-(1 << 30)), Pred.hash(7), var, st, ys=ys, d_m=dm)  # noqa: E731
+        ms = timeit(f, reps=10)
+        out[f"partition3_{name}"] = {"ms": ms, "Gelem/s": n / ms / 1e6, "algoGBps": 8 * n / ms / 1e6}
 
     # library reference points (CUB via torch): stream compaction and scan
     mask = xs >= 0
