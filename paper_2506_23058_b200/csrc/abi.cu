@@ -82,6 +82,7 @@ inline int grid_for(long long work, int per_block = kGThreads) {
 }
 inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+inline bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
 #define LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
 #define CHECK_LAUNCH()                          \
@@ -140,7 +141,11 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
   }
   {
     TimedLaunch tl(IXG_K_SCATTER, s);
-    k_scatter<E><<<grid_for(m), kGThreads, 0, s>>>(out, ndst, d_ndst, is, vs, m, check ? 1 : 0, claim, hdr);
+    if (aligned32(is) && aligned32(vs))
+      k_scatter_v<E><<<grid_for(m / 8 + 1, 256), 256, 0, s>>>(out, ndst, d_ndst, is, vs, m, check ? 1 : 0, claim,
+                                                               hdr);
+    else
+      k_scatter<E><<<grid_for(m), kGThreads, 0, s>>>(out, ndst, d_ndst, is, vs, m, check ? 1 : 0, claim, hdr);
   }
   LAUNCHED();
   CHECK_LAUNCH();
@@ -723,8 +728,8 @@ int ixg_csr_gather(int dt, const void* x, int64_t num_cols, const void* values, 
   if (!aligned16(values) || !aligned16(indices) || !aligned16(out)) return IXG_BADARG;
   const int check = (IXG_SITE_BITS(variant, 0) & IXG_V_BOUNDS) ? 1 : 0;
   cudaStream_t s = S(stream);
-  const long long work = nnz / 4 + 1;
   TimedLaunch tl(IXG_K_CSR_GATHER, s);
+  const long long work = nnz / 4 + 1;
   if (dt == IXG_I32)
     k_csr_gather<int32_t><<<grid_for(work), kGThreads, 0, s>>>((const int32_t*)x, num_cols, (const int32_t*)values,
                                                                 (const long long*)indices, nnz, (int32_t*)out, check,

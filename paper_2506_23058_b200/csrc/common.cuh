@@ -189,13 +189,14 @@ struct Vec<long long> {
 // compaction kernels (thread 0 of the first 2^17 CTAs); read with
 // ixg_trace_read().  Compiled out otherwise.
 #ifdef IXG_TRACE
-__device__ unsigned long long g_trace[(1 << 17) * 8];
+#define IXG_TRS 16  // trace slots per CTA
+__device__ unsigned long long g_trace[(1 << 17) * IXG_TRS];
 #define IXG_TR(slot)                                                        \
   do {                                                                      \
     if (threadIdx.x == 0 && blockIdx.x < (1u << 17)) {                      \
       unsigned long long t__;                                               \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));               \
-      g_trace[blockIdx.x * 8 + (slot)] = t__;                               \
+      g_trace[blockIdx.x * IXG_TRS + (slot)] = t__;                               \
     }                                                                       \
   } while (0)
 #define IXG_TR_LANE0(slot)                                                  \
@@ -203,7 +204,7 @@ __device__ unsigned long long g_trace[(1 << 17) * 8];
     if ((threadIdx.x & 31) == 0 && blockIdx.x < (1u << 17)) {               \
       unsigned long long t__;                                               \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));               \
-      g_trace[blockIdx.x * 8 + (slot)] = t__;                               \
+      g_trace[blockIdx.x * IXG_TRS + (slot)] = t__;                               \
     }                                                                       \
   } while (0)
 #else

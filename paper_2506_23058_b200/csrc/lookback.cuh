@@ -205,7 +205,8 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long ti
     pred -= 32 * kPerLane;
   }
 #ifdef IXG_TRACE
-  if (lane == 0 && blockIdx.x < (1u << 17)) g_trace[blockIdx.x * 8 + 7] = ((unsigned long long)tr_rounds << 32) | tr_spins;
+  if (lane == 0 && blockIdx.x < (1u << 17)) g_trace[blockIdx.x * IXG_TRS + (std::is_same<M, SegOp>::value ? 13 : 7)] =
+      ((unsigned long long)tr_rounds << 32) | tr_spins;
 #endif
   return excl;
 }

@@ -36,15 +36,16 @@ def main():
             ops.filter(xs, Pred.ge(0), 0, st, ys=ys, d_count=dk)
     torch.cuda.synchronize()
     lib = L.load()
-    cnt = (1 << 17) * 8
+    cnt = (1 << 17) * 16
     buf = (ctypes.c_ulonglong * cnt)()
     L.check(lib.ixg_trace_read(buf, cnt), "trace")
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8).astype(np.int64)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 16).astype(np.int64)
     tile = int(os.environ.get("IXG_TILE", "8192"))
     tiles = min((n + tile - 1) // tile, a.shape[0])
     a = a[:tiles]
     t0 = a[:, 0].min()
     a[:, :7] -= t0
+    a[:, 8:13] -= t0
     # k_filter_b slots: 0 start, 1 counted, 2 CTA scan, 3 compacted,
     # 4 base known (bar 2), 5 look-back warp done, 6 stores done
     print(f"tiles {tiles}, kernel span {a[:, 6].max() / 1e3:.1f} us")
@@ -54,11 +55,21 @@ def main():
         print(f"  {nm:11s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
     life = a[:, 6] - a[:, 0]
     print(f"  life      median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
+    if what == "c2":  # 8 seg scanned, 9 pass 2 done, 10 carry known, 11 zs stored, 12 lb warp carry done
+        for nm, i, j in (("seg_p1+scan", 6, 8), ("seg_pass2", 8, 9), ("wait_carry", 9, 10), ("zs_store", 10, 11),
+                         ("lb_carry", 4, 12)):
+            d = a[:, j] - a[:, i]
+            print(f"  {nm:11s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
+        life = a[:, 11] - a[:, 0]
+        print(f"  c2 life   median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
+        r2 = a[:, 13] >> 32
+        print(f"  seg look-back rounds mean {r2.mean():.2f}, spins mean {(a[:, 13] & 0xFFFFFFFF).mean():.1f}")
     # CTAs in flight at the middle of the kernel
     mid = a[:, 6].max() / 2
     print("  in flight at mid:", int(((a[:, 0] <= mid) & (a[:, 6] >= mid)).sum()))
     starts = np.sort(a[:, 0])
     print(f"  start interval (median over tiles) {np.median(np.diff(starts)):.1f} ns")
+    mid = a[:, 6].max() / 2
     rounds, spins = a[:, 7] >> 32, a[:, 7] & 0xFFFFFFFF
     print(f"  look-back rounds mean {rounds.mean():.2f} max {rounds.max()}, first-slot spins mean {spins.mean():.1f} p90 {np.percentile(spins, 90):.0f}")
 
