@@ -804,155 +804,5 @@ __global__ void __launch_bounds__(256) k_scatter_v(E* __restrict__ out, long lon
   if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
 }
 
-// partition3's single pass leaves the prefix at the end of segment 1 (m1 + m2)
-__global__ void k_sub_first(long long* d_tot) { d_tot[1] -= d_tot[0]; }
-
-// ---------------------------------------------------------------------------
-// Vectorised scatter (C3 and every fused-away-free scatter site): 8 source
-// elements per thread-iteration, indices and values as 256-bit streaming
-// loads (96 B in flight per thread for i64 indices + i32 values), then 8
-// independent stores; CHECKED adds the claim-bitmap atomics exactly as
-// k_scatter (k_generic.cuh).  Needs 32-byte aligned is / vs.
-template <typename E>
-__global__ void __launch_bounds__(256) k_scatter_v(E* __restrict__ out, long long ndst,
-                                                   const long long* __restrict__ d_ndst,
-                                                   const long long* __restrict__ is, const E* __restrict__ vs,
-                                                   long long m, int check, uint32_t* __restrict__ claim,
-                                                   LBHeader* hdr) {
-  if (d_ndst) ndst = *d_ndst;
-  const long long nv = m >> 3;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  bool dup = false;
-  for (long long k = tid; k < nv; k += stride) {
-    uint32_t a[8], b[8];
-    ld256(is + 8 * k, a);
-    ld256(is + 8 * k + 4, b);
-    E x[8];
-    if constexpr (sizeof(E) == 4) {
-      uint32_t c[8];
-      ld256(vs + 8 * k, c);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = (E)c[j];
-    } else {
-      uint32_t c[8], e[8];
-      ld256(vs + 8 * k, c);
-      ld256(vs + 8 * k + 4, e);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        x[j] = (E)(((unsigned long long)c[2 * j + 1] << 32) | c[2 * j]);
-        x[4 + j] = (E)(((unsigned long long)e[2 * j + 1] << 32) | e[2 * j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t lo = j < 4 ? a[2 * j] : b[2 * (j - 4)];
-      const uint32_t hi = j < 4 ? a[2 * j + 1] : b[2 * (j - 4) + 1];
-      const long long d = (long long)(((unsigned long long)hi << 32) | lo);
-      if ((unsigned long long)d < (unsigned long long)ndst) {
-        if (check) {
-          const uint32_t bit = 1u << (d & 31);
-          if (atomicOr(&claim[d >> 5], bit) & bit) dup = true;
-        }
-        out[d] = x[j];
-      }
-    }
-  }
-  for (long long i = nv * 8 + tid; i < m; i += stride) {
-    const long long d = is[i];
-    if ((unsigned long long)d < (unsigned long long)ndst) {
-      if (check) {
-        const uint32_t bit = 1u << (d & 31);
-        if (atomicOr(&claim[d >> 5], bit) & bit) dup = true;
-      }
-      out[d] = vs[i];
-    }
-  }
-  if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
-}
-
-// Vectorised CSR flat gather (C4): 8 nnz per thread-iteration (values and
-// indices as 256-bit streaming loads), then 8 independent reads of x (L2
-// resident at C4) and one 256-bit store of the products.
-template <typename E, int kXMode = 0>
-__global__ void __launch_bounds__(256) k_csr_gather_v(const E* __restrict__ x, long long num_cols,
-                                                      const E* __restrict__ values,
-                                                      const long long* __restrict__ indices, long long nnz,
-                                                      E* __restrict__ out, int check, ixg_status* st) {
-  const long long nv = nnz >> 3;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  bool narrow = false;
-  auto one = [&](long long i, long long c, long long v) -> E {
-    if (check && (unsigned long long)c >= (unsigned long long)num_cols) {
-      status_fail(st, IXG_OOB, 0, i, 0);
-      return E(0);
-    }
-    E xv;
-    if constexpr (kXMode == 1) {
-      if constexpr (sizeof(E) == 4) {
-        int32_t r;
-        asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(x + c));
-        xv = (E)r;
-      } else {
-        long long r;
-        asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(r) : "l"(x + c));
-        xv = (E)r;
-      }
-    } else {
-      xv = __ldg(&x[c]);
-    }
-    const long long prod = v * (long long)xv;
-    if (sizeof(E) == 4 && prod != (long long)(int)prod) narrow = true;
-    return (E)prod;
-  };
-  for (long long k = tid; k < nv; k += stride) {
-    uint32_t a[8], b[8];
-    ld256(indices + 8 * k, a);
-    ld256(indices + 8 * k + 4, b);
-    long long v[8];
-    if constexpr (sizeof(E) == 4) {
-      uint32_t c[8];
-      ld256(values + 8 * k, c);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = (long long)(int32_t)c[j];
-    } else {
-      uint32_t c[8], e[8];
-      ld256(values + 8 * k, c);
-      ld256(values + 8 * k + 4, e);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        v[j] = (long long)(((unsigned long long)c[2 * j + 1] << 32) | c[2 * j]);
-        v[4 + j] = (long long)(((unsigned long long)e[2 * j + 1] << 32) | e[2 * j]);
-      }
-    }
-    E o[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t lo = j < 4 ? a[2 * j] : b[2 * (j - 4)];
-      const uint32_t hi = j < 4 ? a[2 * j + 1] : b[2 * (j - 4) + 1];
-      o[j] = one(8 * k + j, (long long)(((unsigned long long)hi << 32) | lo), v[j]);
-    }
-    if constexpr (sizeof(E) == 4) {
-      uint32_t r[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = (uint32_t)o[j];
-      st256(out + 8 * k, r);
-    } else {
-      uint32_t r[8], q[8];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        r[2 * j] = (uint32_t)(unsigned long long)o[j];
-        r[2 * j + 1] = (uint32_t)((unsigned long long)o[j] >> 32);
-        q[2 * j] = (uint32_t)(unsigned long long)o[4 + j];
-        q[2 * j + 1] = (uint32_t)((unsigned long long)o[4 + j] >> 32);
-      }
-      st256(out + 8 * k, r);
-      st256(out + 8 * k + 4, q);
-    }
-  }
-  for (long long i = nv * 8 + tid; i < nnz; i += stride) out[i] = one(i, indices[i], (long long)values[i]);
-  if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
-}
 
 }  // namespace ixg
