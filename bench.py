@@ -280,9 +280,11 @@ class C1:
         self.N = ((1 << 24) if quick else (1 << 32) // ws) if big else (1 << 20)
         self.p = Pred.lt(0)
         self.xs_h = None if big else gen.uniform(0, self.N, -(1 << 31), (1 << 31) - 1, np.int32, offset=rank * self.N)
-        self.big, self.rank = big, rank
+        self.big, self.rank, self.ws = big, rank, ws
         self.workload = (f"partition2 (x < 0), N=2^{self.N.bit_length() - 1} int32 uniform over int32"
-                         + (" per GPU (2^32 total)" if big else ""))
+                         + (" per GPU (2^32 total)" if big else "")
+                         + (f"; {ws} contiguous shards, all-gather of per-shard true counts -> each shard's two "
+                            "output runs of the global result" if ws > 1 else ""))
 
     def setup_device(self):
         import torch
@@ -298,6 +300,11 @@ class C1:
         self.dnt = torch.empty(1, dtype=torch.int64, device=dev)
         self.st = ops.Status(dev)
         self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if not self.big else None
+        if self.ws > 1:
+            from paper_2506_23058_b200 import dist as D
+
+            self.local = D.GpuPart2Local(self.xs, self.p)
+            self.local.ys, self.local.dnt, self.local.st = self.ys, self.dnt, self.st
 
     def pre_step(self):
         """between timed steps, outside the timed region: a 256 MB write
@@ -308,6 +315,11 @@ class C1:
     def step(self, variant):
         from paper_2506_23058_b200 import ops
 
+        if self.ws > 1:
+            from paper_2506_23058_b200 import dist as D
+
+            self.nt_global, self.runs = D.partition2_sharded(self.local)
+            return
         ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
 
     def check(self, want):
@@ -341,7 +353,12 @@ class C1:
 
         xs_p, ys_p, variant = bufs
         self.xs.copy_(xs_p, non_blocking=True)
-        ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
+        if self.ws > 1:
+            from paper_2506_23058_b200 import dist as D
+
+            D.partition2_sharded(self.local)
+        else:
+            ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
         ys_p.copy_(self.ys, non_blocking=True)
         int(self.dnt.item())
         return 4 * self.N, 4 * self.N + 8

@@ -111,6 +111,28 @@ def partition2_sharded(local, group=None):
 
 
 # ----------------------------------------------------------------- GPU backend
+class GpuPart2Local:
+    """partition2 on one GPU's contiguous shard (the single-pass ixg_partition2
+    kernel); partition2_sharded turns its true count into the shard's two
+    output runs of the global result."""
+
+    def __init__(self, xs, pred):
+        import torch
+
+        from . import _lib as L
+        from . import ops
+
+        self.ops, self.L = ops, L
+        self.xs, self.pred = xs, pred
+        self.ys = torch.empty_like(xs)
+        self.dnt = torch.empty(1, dtype=torch.int64, device=xs.device)
+        self.st = ops.Status(xs.device)
+
+    def partition2(self):
+        self.ops.partition2(self.xs, self.pred, self.L.VARIANT_ELIDED, self.st, ys=self.ys, d_nt=self.dnt)
+        return int(self.dnt.item()), self.xs.numel()
+
+
 class GpuC2Local:
     """C2 on one GPU's shard with the CUDA kernels (ixg_filter, ixg_flag_bitmap,
     ixg_segsum, ixg_seg_carry).  `shape` is the GLOBAL segment shape."""

@@ -43,3 +43,34 @@ def test_c2_sharded_kernels(cuda, G, n, m):
     assert np.array_equal(zs, want_zs)
     for loc in locs:
         assert loc.st.read().ok
+
+
+@pytest.mark.parametrize("G,n", [(2, 100_000), (4, 1_000_003), (8, 3_000_001), (3, 50)])
+def test_partition2_sharded_kernels(cuda, G, n):
+    """dist.GpuPart2Local per simulated rank + dist.partition2_runs: each
+    shard's [trues | falses] lands at its global runs; the assembly equals
+    the single-process partition2."""
+    import torch
+
+    xs = gen.uniform(G * 7 + n, n, -(1 << 31), (1 << 31) - 1, np.int32)
+    p = Pred.lt(0)
+    want_nt, want = O.partition2(p, xs)
+    locs, tc, sizes = [], [], []
+    for r in range(G):
+        lo, hi = r * n // G, (r + 1) * n // G
+        loc = D.GpuPart2Local(torch.from_numpy(xs[lo:hi].copy()).to(cuda), p)
+        t, size = loc.partition2()
+        locs.append(loc)
+        tc.append(t)
+        sizes.append(size)
+    out = np.zeros(n, np.int64)
+    for r, loc in enumerate(locs):
+        nt, runs = D.partition2_runs(tc, sizes, r)
+        assert nt == want_nt
+        ys = loc.ys.cpu().numpy().astype(np.int64)
+        off = 0
+        for s, ln in zip(runs.starts, runs.lengths):
+            out[s:s + ln] = ys[off:off + ln]
+            off += ln
+        assert loc.st.read().ok
+    assert np.array_equal(out, want)
