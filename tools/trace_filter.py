@@ -1,8 +1,13 @@
-"""Per-CTA timeline of the compaction kernel (development tool).
+"""Per-CTA timeline of the big-tile compaction kernel (development tool).
 
 Needs a library built with -DIXG_TRACE (IXGPU_LIB=...):
-    python tools/trace_filter.py <filter|c2|partition2> [log2n]
+    IXG_TILE=24576 python tools/trace_filter.py <filter|c2> [log2n]
 Prints per-phase durations (ns) over CTAs and the number of CTAs in flight.
+k_filter_b trace slots: 0 start, 1 counted, 2 CTA scan, 3 compacted, 4 base
+known (bar 2), 5 look-back warp done, 6 stores done (filter), 7 look-back
+rounds/spins; C2: 6 ys stored, 8 seg pass 1 + scan, 9 pass 2 done, 10 carry
+known (bar 3), 11 zs stored, 12 look-back warp carry done, 13 seg look-back
+rounds/spins.
 """
 
 import ctypes
@@ -16,6 +21,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2506_23058_b200 import _lib as L  # noqa: E402
 from paper_2506_23058_b200 import gen, ops  # noqa: E402
 from paper_2506_23058_b200.pred import Pred  # noqa: E402
+
+SLOTS = 16
+
+
+def phase(a, nm, i, j):
+    d = a[:, j] - a[:, i]
+    print(f"  {nm:11s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
 
 
 def main():
@@ -36,42 +48,43 @@ def main():
             ops.filter(xs, Pred.ge(0), 0, st, ys=ys, d_count=dk)
     torch.cuda.synchronize()
     lib = L.load()
-    cnt = (1 << 17) * 16
+    cnt = (1 << 17) * SLOTS
     buf = (ctypes.c_ulonglong * cnt)()
     L.check(lib.ixg_trace_read(buf, cnt), "trace")
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 16).astype(np.int64)
-    tile = int(os.environ.get("IXG_TILE", "8192"))
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, SLOTS).astype(np.int64)
+    tile = int(os.environ.get("IXG_TILE", "24576"))
     tiles = min((n + tile - 1) // tile, a.shape[0])
     a = a[:tiles]
     t0 = a[:, 0].min()
-    a[:, :7] -= t0
-    a[:, 8:13] -= t0
-    # k_filter_b slots: 0 start, 1 counted, 2 CTA scan, 3 compacted,
-    # 4 base known (bar 2), 5 look-back warp done, 6 stores done
-    print(f"tiles {tiles}, kernel span {a[:, 6].max() / 1e3:.1f} us")
-    for nm, i, j in (("load+count", 0, 1), ("cta_scan", 1, 2), ("compact", 2, 3), ("wait_base", 3, 4),
-                     ("store(+seg)", 4, 6), ("lookback", 0, 5)):
-        d = a[:, j] - a[:, i]
-        print(f"  {nm:11s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
-    life = a[:, 6] - a[:, 0]
-    print(f"  life      median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
-    if what == "c2":  # 8 seg scanned, 9 pass 2 done, 10 carry known, 11 zs stored, 12 lb warp carry done
-        for nm, i, j in (("seg_p1+scan", 6, 8), ("seg_pass2", 8, 9), ("wait_carry", 9, 10), ("zs_store", 10, 11),
-                         ("lb_carry", 4, 12)):
-            d = a[:, j] - a[:, i]
-            print(f"  {nm:11s} median {np.median(d):8.0f} ns  p90 {np.percentile(d, 90):8.0f}  mean {d.mean():8.0f}")
-        life = a[:, 11] - a[:, 0]
-        print(f"  c2 life   median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
+    for c in (0, 1, 2, 3, 4, 5, 6, 8, 9, 10, 11, 12):
+        a[:, c] -= t0
+    end = 11 if what == "c2" else 6
+    print(f"tiles {tiles}, kernel span {a[:, end].max() / 1e3:.1f} us")
+    phase(a, "load+count", 0, 1)
+    phase(a, "cta_scan", 1, 2)
+    phase(a, "compact", 2, 3)
+    phase(a, "wait_base", 3, 4)
+    phase(a, "lookback", 0, 5)
+    if what == "c2":
+        phase(a, "ys_store", 4, 6)
+        phase(a, "seg_p1+scan", 6, 8)
+        phase(a, "seg_pass2", 8, 9)
+        phase(a, "wait_carry", 9, 10)
+        phase(a, "zs_store", 10, 11)
+        phase(a, "lb_carry", 4, 12)
         r2 = a[:, 13] >> 32
         print(f"  seg look-back rounds mean {r2.mean():.2f}, spins mean {(a[:, 13] & 0xFFFFFFFF).mean():.1f}")
-    # CTAs in flight at the middle of the kernel
-    mid = a[:, 6].max() / 2
-    print("  in flight at mid:", int(((a[:, 0] <= mid) & (a[:, 6] >= mid)).sum()))
+    else:
+        phase(a, "store", 4, 6)
+    life = a[:, end] - a[:, 0]
+    print(f"  life        median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
+    mid = a[:, end].max() / 2
+    print("  in flight at mid:", int(((a[:, 0] <= mid) & (a[:, end] >= mid)).sum()))
     starts = np.sort(a[:, 0])
     print(f"  start interval (median over tiles) {np.median(np.diff(starts)):.1f} ns")
-    mid = a[:, 6].max() / 2
     rounds, spins = a[:, 7] >> 32, a[:, 7] & 0xFFFFFFFF
-    print(f"  look-back rounds mean {rounds.mean():.2f} max {rounds.max()}, first-slot spins mean {spins.mean():.1f} p90 {np.percentile(spins, 90):.0f}")
+    print(f"  look-back rounds mean {rounds.mean():.2f} max {rounds.max()}, "
+          f"first-slot spins mean {spins.mean():.1f} p90 {np.percentile(spins, 90):.0f}")
 
 
 if __name__ == "__main__":
