@@ -661,7 +661,7 @@ def run_ours(args):
     units_total = wl.units() * ws
     value = units_total / (ms * 1e-3) / 1e9
     achieved = (kbytes / (kms * 1e-3) / 1e9) if kms else None
-    traffic = _ncu_traffic(wl.name)
+    traffic = _ncu_traffic(wl.name, wl.units())
     line = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -726,14 +726,18 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _ncu_traffic(name):
+def _ncu_traffic(name, units=None):
     """dram bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/ncu_<name>_full.json), else null."""
+    --set full capture (profiles/ncu_<name>_full.json; scaled by the units of
+    this run when the capture was taken at another size), else null."""
     try:
         with open(os.path.join(ROOT, "profiles", f"ncu_{name}_full.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
     except Exception:
         return None
+    if units and d.get("dram_bytes_per_unit") and d.get("units") != units:
+        return round(d["dram_bytes_per_unit"] * units)
+    return d.get("dram_bytes_per_launch")
 
 
 def cpu_baseline(wl, args):
