@@ -438,7 +438,8 @@ class C3:
     def kernel(self):
         from paper_2506_23058_b200 import _lib as L
 
-        return L.K_SCATTER, 16 * self.N, "k_scatter<int32> (is i64 + vs i32 read, dst i32 written)"
+        return (L.K_SCATTER, 16 * self.N,
+                "k_scatter_t<int32> (TMA-staged 4096-element tiles, striped stores; is i64 + vs i32 read, dst i32 written)")
 
     def e2e_bufs(self, variant):
         import torch
@@ -697,6 +698,8 @@ def run_ours(args):
             "achieved": round(achieved, 1) if achieved else None,
             "peak": hbm,
             "peak_kind": peak_kind,
+            "peak_note": ("MEASURED_PEAKS hbm_gbs is a copy (50 % read / 50 % write); a read-heavy kernel can "
+                          "exceed it -- ncu's dram__throughput pct_of_peak is the device-limit reference"),
             "unit": "GB/s",
             "frac": round(achieved / hbm, 4) if achieved else None,
             "traffic": traffic,

@@ -141,7 +141,23 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
   }
   {
     TimedLaunch tl(IXG_K_SCATTER, s);
-    if (aligned32(is) && aligned32(vs))
+    static int mode = -1;
+    if (mode < 0) {
+      const char* e = getenv("IXG_SCATTER");
+      mode = e ? atoi(e) : 0;
+    }
+    // ELIDED: TMA-staged striped scatter.  CHECKED keeps the blocked
+    // kernel: striped lanes would all hit the same claim word (a warp's 32
+    // sources are ~2 destination runs), serialising the atomics.
+    if (mode == 0 && !check && aligned16(is) && aligned16(vs)) {
+      static bool attr = false;
+      if (!attr) {
+        allow_smem(k_scatter_t<E>, ScSmem<E>::BYTES);
+        attr = true;
+      }
+      k_scatter_t<E><<<(unsigned)tiles_of(m, kScTile), 256, ScSmem<E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m,
+                                                                                 check ? 1 : 0, claim, hdr);
+    } else if (aligned32(is) && aligned32(vs))
       k_scatter_v<E><<<grid_for(m / 8 + 1, 256), 256, 0, s>>>(out, ndst, d_ndst, is, vs, m, check ? 1 : 0, claim,
                                                                hdr);
     else

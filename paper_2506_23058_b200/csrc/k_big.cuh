@@ -805,4 +805,61 @@ __global__ void __launch_bounds__(256) k_scatter_v(E* __restrict__ out, long lon
 }
 
 
+// ---------------------------------------------------------------------------
+// TMA-staged scatter: one CTA per 4096-element tile; thread 0 bulk-copies the
+// tile's indices and values to shared memory (48 KB for i64 indices + i32
+// values: 4 CTAs per SM keep ~190 KB of reads in flight without LSU work),
+// then the warps walk the tile STRIPED -- lane l takes element 32k + l -- so
+// each warp-wide store covers 32 consecutive sources, i.e. the few
+// contiguous destination runs of an index-array permutation (C3: two
+// streams) land in a handful of sectors.  CHECKED adds the claim-bitmap
+// atomics exactly as k_scatter (k_generic.cuh).
+constexpr int kScTile = 4096;
+template <typename E>
+struct ScSmem {
+  static constexpr int BYTES = kScTile * (8 + (int)sizeof(E));
+};
+
+template <typename E>
+__global__ void __launch_bounds__(256) k_scatter_t(E* __restrict__ out, long long ndst,
+                                                   const long long* __restrict__ d_ndst,
+                                                   const long long* __restrict__ is, const E* __restrict__ vs,
+                                                   long long m, int check, uint32_t* __restrict__ claim,
+                                                   LBHeader* hdr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  long long* s_is = reinterpret_cast<long long*>(smem_raw);
+  E* s_vs = reinterpret_cast<E*>(smem_raw + kScTile * 8);
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (d_ndst) ndst = *d_ndst;
+  const long long base = (long long)blockIdx.x * kScTile;
+  const int t = threadIdx.x;
+  const bool full = base + kScTile <= m;
+  bool dup = false;
+  auto one = [&](long long d, E v) {
+    if ((unsigned long long)d < (unsigned long long)ndst) {
+      if (check) {
+        const uint32_t bit = 1u << (d & 31);
+        if (atomicOr(&claim[d >> 5], bit) & bit) dup = true;
+      }
+      out[d] = v;
+    }
+  };
+  if (full) {
+    if (t == 0) {
+      mbar_init(&s_mbar, 1);
+      mbar_fence_init();
+      mbar_expect_tx(&s_mbar, (uint32_t)ScSmem<E>::BYTES);
+      bulk_g2s(s_is, is + base, kScTile * 8u, &s_mbar);
+      bulk_g2s(s_vs, vs + base, kScTile * (uint32_t)sizeof(E), &s_mbar);
+    }
+    __syncthreads();  // the mbarrier is initialised
+    mbar_wait(&s_mbar, 0);
+#pragma unroll 4
+    for (int k = t; k < kScTile; k += 256) one(s_is[k], s_vs[k]);
+  } else {
+    for (long long i = base + t; i < m; i += 256) one(is[i], vs[i]);
+  }
+  if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
+}
+
 }  // namespace ixg
