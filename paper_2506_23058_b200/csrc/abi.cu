@@ -82,6 +82,11 @@ inline int grid_for(long long work, int per_block = kGThreads) {
 }
 inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+// look-back slots for the compaction kernels: enough for the register-tiled
+// (kSTile) and the big-tile kernels of either element width
+inline long long lb_tiles(long long n) {
+  return std::max(tiles_of(n, kSTile), tiles_of(n, std::min(Big<int32_t>::TILE, Big<long long>::TILE)));
+}
 inline bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
 #define LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
@@ -280,7 +285,7 @@ int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T*
   const bool fused = (sb & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;  // Sc1 proved
   ixg_pred pp = p ? *p : ixg_pred{IXG_PRED_TRUE, 0, 0, 0};
   if (fused) {
-    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));  // >= tiles of either kernel
+    LBChan c0 = ws.chan(0, lb_tiles(n));
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
@@ -320,8 +325,7 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
   const int cgrid = grid_for(n / (16 / (int)sizeof(T)) + 1);
   long long* partials = (long long*)ws.take((size_t)cgrid * 2 * 8);
   if (fused) {
-    const long long lb_tiles = std::max(tiles_of(n, kSTile), kClasses * tiles_of(n, Big<T>::TILE));
-    LBChan c0 = ws.chan(0, lb_tiles);
+    LBChan c0 = ws.chan(0, std::max(lb_tiles(n), kClasses * tiles_of(n, Big<long long>::TILE)));
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
@@ -395,8 +399,8 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     // segment start (no conflict check), starts >= k are never read.
     uint32_t* bits = (uint32_t*)ws.take(bitmap_bytes(n));
     LBChan cs = ws.chan(2, tiles_of(m, kGTile));
-    LBChan c0 = ws.chan(0, tiles_of(n, kSTile));
-    LBChan c1 = ws.chan(1, tiles_of(n, kSTile));
+    LBChan c0 = ws.chan(0, lb_tiles(n));
+    LBChan c1 = ws.chan(1, lb_tiles(n));
     SegTileMeta* meta = (SegTileMeta*)ws.take((size_t)tiles_of(n, kSTile) * sizeof(SegTileMeta) + 64);
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_k, 0, sizeof(long long), s));

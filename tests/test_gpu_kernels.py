@@ -121,7 +121,7 @@ def test_c2_narrow_exact(cuda, head):
 
     from paper_2506_23058_b200 import ops
 
-    tile = 3 * 8192  # k_filter_b<int32> tile
+    tile = 3 * 8192  # a multiple of the k_filter_b<int32> tile (12288 or 24576 elements)
     n = 3 * tile + 100
     xs = np.zeros(n, np.int32)
     xs[:2047] = head

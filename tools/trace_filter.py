@@ -1,7 +1,7 @@
 """Per-CTA timeline of the big-tile compaction kernel (development tool).
 
 Needs a library built with -DIXG_TRACE (IXGPU_LIB=...):
-    IXG_TILE=24576 python tools/trace_filter.py <filter|c2> [log2n]
+    IXG_TILE=12288 python tools/trace_filter.py <filter|c2> [log2n]
 Prints per-phase durations (ns) over CTAs and the number of CTAs in flight.
 k_filter_b trace slots: 0 start, 1 counted, 2 CTA scan, 3 compacted, 4 base
 known (bar 2), 5 look-back warp done, 6 stores done (filter), 7 look-back
@@ -52,7 +52,7 @@ def main():
     buf = (ctypes.c_ulonglong * cnt)()
     L.check(lib.ixg_trace_read(buf, cnt), "trace")
     a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, SLOTS).astype(np.int64)
-    tile = int(os.environ.get("IXG_TILE", "24576"))
+    tile = int(os.environ.get("IXG_TILE", "12288"))
     tiles = min((n + tile - 1) // tile, a.shape[0])
     a = a[:tiles]
     t0 = a[:, 0].min()
