@@ -82,11 +82,8 @@ inline int grid_for(long long work, int per_block = kGThreads) {
 }
 inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
-// look-back slots for the compaction kernels: enough for the register-tiled
-// (kSTile) and the big-tile kernels of either element width
-inline long long lb_tiles(long long n) {
-  return std::max(tiles_of(n, kSTile), tiles_of(n, std::min(Big<int32_t>::TILE, Big<long long>::TILE)));
-}
+// look-back slots for the big-tile kernels of either element width
+inline long long lb_tiles(long long n) { return tiles_of(n, std::min(Big<int32_t>::TILE, Big<long long>::TILE)); }
 inline bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
 #define LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
@@ -179,41 +176,6 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
 }
 
 // --------------------------------------------------------------- filter
-// Persistent streaming compaction (k_stream.cuh).  All CTAs must be
-// co-resident (they wait on each other's look-back slots): the grid is the
-// occupancy-derived resident capacity, never more.
-template <typename T, typename Z, bool kByCs, bool kSeg>
-int launch_filter_p(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, Z* zs,
-                    const uint32_t* segbits, long long out_base, LBChan ch, long long* d_count, SegTileMeta* meta,
-                    ixg_status* st, cudaStream_t s) {
-  const int smem = (kSTile + 32 / (int)sizeof(T)) * (int)sizeof(T) +
-                   (kSeg ? (kSTile + 32 / (int)sizeof(Z)) * (int)sizeof(Z) : 0);
-  const long long tiles = tiles_of(n, kSTile);
-  TimedLaunch tl(IXG_K_FILTER_FUSED, s);
-  auto kern = k_filter_s<T, Z, kByCs, kSeg>;
-  static bool attr = false;
-  if (!attr) {
-    allow_smem(kern, smem);
-    attr = true;
-  }
-  kern<<<(unsigned)tiles, kNT + 32, smem, s>>>(xs, cs, n, p, ys, zs, segbits, out_base, ch, next_nonce(), d_count,
-                                                meta, st);
-  LAUNCHED();
-  CHECK_LAUNCH();
-  return IXG_OK;
-}
-
-// Big-tile kernels (k_big.cuh) are the default; IXG_BIG=0 selects the
-// register-tiled kernels of k_stream.cuh (kept for A/B measurements).
-inline bool big_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("IXG_BIG");
-    mode = (e && e[0] == '0') ? 0 : 1;
-  }
-  return mode == 1;
-}
-
 // IXG_SEG_SPLIT=1: C2 as two passes (filter, then sgmSum over ys) for A/B
 inline bool seg_split_mode() {
   static int mode = -1;
@@ -263,20 +225,6 @@ int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32
   return IXG_OK;
 }
 
-// tiles' carries for the segmented sum (k_stream.cuh fix-up), then the fix-up
-template <typename Z, typename T>
-int launch_seg_fixup(SegTileMeta* meta, long long n, const uint32_t* segbits, long long out_base, Z* zs, const T* ys,
-                     long long carry_v, int carry_f, ixg_status* st, cudaStream_t s, int tile = kSTile) {
-  const long long tiles = tiles_of(n, tile);
-  k_seg_tile_scan<<<1, 1024, 0, s>>>(meta, tiles, carry_v, carry_f);
-  LAUNCHED();
-  CHECK_LAUNCH();
-  k_seg_fixup<Z, T><<<grid_for(tiles * 256), 256, 0, s>>>(meta, tiles, segbits, out_base, zs, ys, st);
-  LAUNCHED();
-  CHECK_LAUNCH();
-  return IXG_OK;
-}
-
 // filter / filter_by on element type T.  Sites: 0 = offs[n-1], 1 = scatter.
 template <typename T>
 int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T* ys, long long* d_count,
@@ -289,14 +237,8 @@ int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T*
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
-    if (big_mode()) {
-      if (cs) return launch_filter_b<T, true>(xs, cs, n, pp, ys, c0, d_count, s);
-      return launch_filter_b<T, false>(xs, cs, n, pp, ys, c0, d_count, s);
-    }
-    if (cs) return launch_filter_p<T, T, true, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, d_count,
-                                                       nullptr, st, s);
-    return launch_filter_p<T, T, false, false>(xs, cs, n, pp, ys, (T*)nullptr, nullptr, 0, c0, d_count, nullptr,
-                                                st, s);
+    if (cs) return launch_filter_b<T, true>(xs, cs, n, pp, ys, c0, d_count, s);
+    return launch_filter_b<T, false>(xs, cs, n, pp, ys, c0, d_count, s);
   }
   // CHECKED: offs/inds materialised (filter.ixl:10-12), then the scatter
   // into `replicate count 0` with the dynamic checks (filter.ixl:13-14).
@@ -329,33 +271,11 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
     if (!aligned16(xs) || !aligned16(ys)) return IXG_BADARG;
-    if (big_mode()) {
-      // one pass: kClasses segments of big tiles on one look-back chain
-      int rc = launch_filter_b<T, false, false, T, kClasses>(xs, nullptr, n, pp, ys, c0, d_tot, s, nullptr, nullptr,
-                                                             0, LBChan{nullptr, nullptr}, nullptr, qq);
-      if (rc || kClasses == 2) return rc;
-      k_sub_first<<<1, 1, 0, s>>>(d_tot);  // d_tot[1] held m1 + m2
-      LAUNCHED();
-      CHECK_LAUNCH();
-      return IXG_OK;
-    }
-    {
-      TimedLaunch tl(IXG_K_CLASS_COUNT, s);
-      k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
-    }
-    LAUNCHED();
-    CHECK_LAUNCH();
-    auto kern = k_place_s<T, kClasses>;
-    const int smem = kClasses * (kSTile + 32 / (int)sizeof(T)) * (int)sizeof(T);
-    static bool attr = false;
-    if (!attr) {
-      allow_smem(kern, smem);
-      attr = true;
-    }
-    {
-      TimedLaunch tl(IXG_K_PLACE, s);
-      kern<<<(unsigned)tiles_of(n, kSTile), kNT + 32, smem, s>>>(xs, n, pp, qq, ys, d_tot, c0, next_nonce());
-    }
+    // one pass: kClasses segments of big tiles on one look-back chain
+    int rc = launch_filter_b<T, false, false, T, kClasses>(xs, nullptr, n, pp, ys, c0, d_tot, s, nullptr, nullptr, 0,
+                                                           LBChan{nullptr, nullptr}, nullptr, qq);
+    if (rc || kClasses == 2) return rc;
+    k_sub_first<<<1, 1, 0, s>>>(d_tot);  // d_tot[1] held m1 + m2
     LAUNCHED();
     CHECK_LAUNCH();
     return IXG_OK;
@@ -401,7 +321,6 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     LBChan cs = ws.chan(2, tiles_of(m, kGTile));
     LBChan c0 = ws.chan(0, lb_tiles(n));
     LBChan c1 = ws.chan(1, lb_tiles(n));
-    SegTileMeta* meta = (SegTileMeta*)ws.take((size_t)tiles_of(n, kSTile) * sizeof(SegTileMeta) + 64);
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_k, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys) || !aligned16(zs)) return IXG_BADARG;
@@ -409,22 +328,17 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     LAUNCHED();
     int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
     if (rc) return rc;
-    if (big_mode()) {
-      if constexpr (sizeof(Z) == sizeof(T)) {
-        if (!seg_split_mode()) {
-          // one pass: filter + sgmSum in shared memory; the carry across
-          // tiles takes a second look-back chain (channel 1)
-          return launch_filter_b<T, false, true, Z>(xs, nullptr, n, pp, ys, c0, d_k, s, zs, bits, 0, c1, st);
-        }
+    if constexpr (sizeof(Z) == sizeof(T)) {
+      if (!seg_split_mode()) {
+        // one pass: filter + sgmSum in shared memory; the carry across
+        // tiles takes a second look-back chain (channel 1)
+        return launch_filter_b<T, false, true, Z>(xs, nullptr, n, pp, ys, c0, d_k, s, zs, bits, 0, c1, st);
       }
-      // two passes: ys = filter p xs, then zs = sgmSum flags ys over the k
-      // outputs (the flag of output j is bit j of the bitmap)
-      if ((rc = launch_filter_b<T, false>(xs, nullptr, n, pp, ys, c0, d_k, s))) return rc;
-      return launch_segsum_b<T, Z>(ys, n, d_k, bits, 0, zs, c1, 0, 0, nullptr, st, s);
     }
-    if ((rc = launch_filter_p<T, Z, false, true>(xs, nullptr, n, pp, ys, zs, bits, 0, c0, d_k, meta, st, s)))
-      return rc;
-    return launch_seg_fixup<Z, T>(meta, n, bits, 0, zs, ys, 0, 0, st, s);
+    // two passes: ys = filter p xs, then zs = sgmSum flags ys over the k
+    // outputs (the flag of output j is bit j of the bitmap)
+    if ((rc = launch_filter_b<T, false>(xs, nullptr, n, pp, ys, c0, d_k, s))) return rc;
+    return launch_segsum_b<T, Z>(ys, n, d_k, bits, 0, zs, c1, 0, 0, nullptr, st, s);
   }
   // CHECKED: filter (checked), mkFlags with materialised ind/flags arrays
   // and the checked scatter of `replicate m 1`, sgmSum as a 2-ary scan.

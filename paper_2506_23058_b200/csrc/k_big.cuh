@@ -320,9 +320,10 @@ IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) 
 // kSeg (C2, Z the width of zs == sizeof(T)): after ys is stored, the
 // compacted run still in shared memory is scanned again for zs = sgmSum
 // flags ys with flags at the output positions (bits out_base + base + q of
-// the mkFlags bitmap) and a TILE-LOCAL carry; the tile's segmented aggregate
-// goes to meta[tile] for the fix-up pass (k_seg_tile_scan + k_seg_fixup)
-// that adds the carry of earlier tiles before each tile's first segment.
+// the mkFlags bitmap), first with a TILE-LOCAL carry; the tile's segmented
+// aggregate goes on a second look-back chain, whose result (the carry of
+// the preceding tiles) is added to the values before the tile's first flag
+// just before zs is stored.
 //
 // NS > 1 (partition2 / partition3, ELIDED): the grid is NS segments of
 // seg_tiles tiles over the same xs, segment s selecting class s (p; not p
