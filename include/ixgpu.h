@@ -139,6 +139,11 @@ unsigned long long ixg_launch_count(void);
 int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, int64_t* out,
                  void* ws, size_t ws_bytes, void* stream);
 
+/* total of `scan (+) 0 xs` -- the last element of oracle.py:281-293's inclusive
+ * scan -- written to *out (device int64).  The sharded scan (dist.py) needs it
+ * before the seeded local scan; dt in {I32, I64, U8}. */
+int ixg_reduce_add(int dt, const void* xs, int64_t n, int64_t* out, void* stream);
+
 /* 2-ary scan with the segmented-sum operator (the k-ary scan
  * of oracle.py:281-293 with \f1 v1 f2 v2 -> (f1 || f2, if f2 then v2 else v1+v2),
  * ne = (f0, v0)): out_v[i] = value component; out_f (nullable, u8) = flag

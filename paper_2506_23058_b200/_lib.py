@@ -65,6 +65,7 @@ SIGNATURES = {
     "ixg_status_init": (_I, [_P, _P]),
     "ixg_launch_count": (ctypes.c_ulonglong, []),
     "ixg_scan_add": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _SZ, _P]),
+    "ixg_reduce_add": (_I, [_I, _P, _I64, _P, _P]),
     "ixg_segscan_add": (_I, [_I, _P, _I, _P, _I64, _I, _I64, _P, _P, _P, _SZ, _P]),
     "ixg_scatter": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _U32, _I, _I, _P, _P, _SZ, _P]),
     "ixg_gather": (_I, [_I, _P, _I64, _P, _I64, _P, _U32, _I, _I, _P, _P]),

@@ -489,6 +489,23 @@ int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, i
   return launch_scan<SumOp>(n, SrcArrT<long long>{(const long long*)xs}, epi, c, S(stream));
 }
 
+int ixg_reduce_add(int dt, const void* xs, int64_t n, int64_t* out, void* stream) {
+  if (n < 0 || !out || (n > 0 && !xs)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  int rc = cuda_rc(cudaMemsetAsync(out, 0, 8, s));
+  if (rc || n == 0) return rc;
+  unsigned long long* o = reinterpret_cast<unsigned long long*>(out);
+  if (dt == IXG_I32)
+    k_reduce_add<int32_t><<<grid_for(n / 4 + 1), kGThreads, 0, s>>>((const int32_t*)xs, n, o);
+  else if (dt == IXG_U8)
+    k_reduce_add<uint8_t><<<grid_for(n / 16 + 1), kGThreads, 0, s>>>((const uint8_t*)xs, n, o);
+  else
+    k_reduce_add<long long><<<grid_for(n / 2 + 1), kGThreads, 0, s>>>((const long long*)xs, n, o);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
 int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64_t n, int f0, int64_t v0,
                     int64_t* out_v, uint8_t* out_f, void* ws, size_t ws_bytes, void* stream) {
   if (n < 0 || (n > 0 && (!flags || !xs || !out_v))) return IXG_BADARG;

@@ -368,6 +368,30 @@ __global__ void __launch_bounds__(kGThreads) k_eq_gather(const long long* __rest
   }
 }
 
+// ---------------------------------------------------------------- reduce
+// sum of xs into *out (int64, zeroed by the caller): 16-byte loads, warp
+// shuffles, one atomic per warp (integer: order-independent, exact)
+template <typename E>
+__global__ void __launch_bounds__(kGThreads) k_reduce_add(const E* __restrict__ xs, long long n,
+                                                          unsigned long long* __restrict__ out) {
+  constexpr int V = 16 / (int)sizeof(E);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long s = 0;
+  const bool vec = (((uintptr_t)xs) & 15) == 0;
+  const long long nv = vec ? n / V : 0;
+  for (long long k = tid; k < nv; k += stride) {
+    const int4 v = ld_stream_v4(xs + k * V);
+    const E* e = reinterpret_cast<const E*>(&v);
+#pragma unroll
+    for (int q = 0; q < V; ++q) s += (long long)e[q];
+  }
+  for (long long i = nv * V + tid; i < n; i += stride) s += (long long)xs[i];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  if (lane_id() == 0 && s != 0) atomicAdd(out, (unsigned long long)s);
+}
+
 // ---------------------------------------------------------------- hist
 __global__ void __launch_bounds__(kGThreads) k_hist(int op, long long dlen, const long long* __restrict__ is,
                                                      const long long* __restrict__ vs, long long m,

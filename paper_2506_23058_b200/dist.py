@@ -7,6 +7,12 @@ all-gathers of per-rank totals -- the data never moves:
 * partition2 (C5): all-gather of each rank's true-count; rank r's local
   result [its trues | its falses] is exactly two runs of the global result,
   at [T_<r, T_<r + T_r) and [NT + F_<r, NT + F_<r + F_r).
+* partition3 / filter: the same with per-class counts (partition_runs).
+* scan (+): each rank's total (ixg_reduce_add) is all-gathered first; the
+  rank then runs ONE seeded scan with ne + the totals of the ranks before it.
+* hist: each rank builds the table of its shard; an all-reduce with the
+  hist operator (min / max / sum) combines them (ne seeds rank 0 only for sum).
+* CSR gather / map: shards by nnz range with `x` replicated; no exchange.
 * C2 (filter + mkFlags + sgmSum): all-gather of each rank's filter count k_r
   gives its output offset K_r; the mkFlags bitmap is built from the global
   segment shape on every rank; each rank's segmented sum starts with carry
@@ -64,6 +70,18 @@ def partition2_runs(true_counts: Sequence[int], sizes: Sequence[int], rank: int)
     return nt, Runs([t_before, nt + f_before], [true_counts[rank], falses[rank]])
 
 
+def partition_runs(counts: Sequence[Sequence[int]], rank: int) -> Tuple[List[int], Runs]:
+    """counts[r][c] = rank r's class-c count, classes in output order.  Class c
+    of the global result starts at G_c (the totals of the classes before it);
+    rank r's class-c run at G_c + the class-c counts of the ranks before r.
+    Returns (class totals, Runs of rank r's local [class 0 | class 1 | ...])."""
+    k = len(counts[0])
+    totals = [sum(int(row[c]) for row in counts) for c in range(k)]
+    G = exclusive_offsets(totals)
+    starts = [G[c] + sum(int(counts[q][c]) for q in range(rank)) for c in range(k)]
+    return totals, Runs(starts, [int(counts[rank][c]) for c in range(k)])
+
+
 # ----------------------------------------------------------------- collectives
 def all_gather_ints(values: Sequence[int], group=None) -> List[List[int]]:
     """All-gather a few int64 per rank (NCCL needs device tensors)."""
@@ -110,7 +128,114 @@ def partition2_sharded(local, group=None):
     return partition2_runs([r[0] for r in rows], [r[1] for r in rows], rank)
 
 
+def partition3_sharded(local, group=None):
+    """Sharded partition3.  `local.partition3()` -> (m1, m2, size) of the shard;
+    returns ((M1, M2) global, Runs of this rank's local [c0 | c1 | c2])."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    m1, m2, size = local.partition3()
+    rows = all_gather_ints([m1, m2, size], group)
+    totals, runs = partition_runs([[r[0], r[1], r[2] - r[0] - r[1]] for r in rows], rank)
+    return (totals[0], totals[1]), runs
+
+
+def filter_sharded(local, group=None):
+    """Sharded filter / filter_by.  `local.filter()` -> k of the shard; returns
+    (k_total, Runs): the shard's outputs are global [K_r, K_r + k_r)."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    k = local.filter()
+    ks = [row[0] for row in all_gather_ints([k], group)]
+    return sum(ks), Runs([exclusive_offsets(ks)[rank]], [k])
+
+
+def scan_sharded(local, ne: int = 0, exclusive: bool = False, group=None) -> int:
+    """Sharded scan (+) ne xs.  `local.total()` -> the shard's sum;
+    `local.scan(seed, exclusive)` runs the seeded local scan.  Returns the
+    global total (ne + sum of all shards)."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    ts = [row[0] for row in all_gather_ints([local.total()], group)]
+    local.scan(ne + exclusive_offsets(ts)[rank], exclusive)
+    return ne + sum(ts)
+
+
+HIST_OPS = {"min": "MIN", "max": "MAX", "add": "SUM"}
+
+
+def hist_sharded(local, op: str, ne: int, group=None):
+    """Sharded hist op ne dlen is vs (oracle.py:306-316) over a contiguous
+    shard of (is, vs): local tables, then one all-reduce with the operator.
+    For `add` only rank 0 folds ne in."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    table = local.hist(ne if (op != "add" or rank == 0) else 0)
+    dist.all_reduce(table, op=getattr(dist.ReduceOp, HIST_OPS[op]), group=group)
+    return table
+
+
 # ----------------------------------------------------------------- GPU backend
+class GpuScanLocal:
+    """scan (+) on one GPU's shard: ixg_reduce_add for the total, then one
+    seeded ixg_scan_add."""
+
+    def __init__(self, xs):
+        from . import ops
+
+        self.ops, self.xs = ops, xs
+        self.out = None
+
+    def total(self) -> int:
+        return int(self.ops.reduce_add(self.xs).item())
+
+    def scan(self, seed: int, exclusive: bool) -> None:
+        self.out = self.ops.scan_add(self.xs, seed, exclusive=exclusive)
+
+
+class GpuFilterLocal:
+    def __init__(self, xs, pred):
+        from . import _lib as L
+        from . import ops
+
+        self.ops, self.L, self.xs, self.pred = ops, L, xs, pred
+        self.st = ops.Status(xs.device)
+        self.ys = None
+
+    def filter(self) -> int:
+        self.ys, dk = self.ops.filter(self.xs, self.pred, self.L.VARIANT_ELIDED, self.st)
+        return int(dk.item())
+
+
+class GpuPart3Local:
+    def __init__(self, xs, p, q):
+        from . import _lib as L
+        from . import ops
+
+        self.ops, self.L, self.xs, self.p, self.q = ops, L, xs, p, q
+        self.st = ops.Status(xs.device)
+        self.ys = None
+
+    def partition3(self):
+        self.ys, dm = self.ops.partition3(self.xs, self.p, self.q, self.L.VARIANT_ELIDED, self.st)
+        m1, m2 = dm.cpu().tolist()
+        return m1, m2, self.xs.numel()
+
+
+class GpuHistLocal:
+    def __init__(self, op: int, dlen: int, is_, vs):
+        from . import ops
+
+        self.ops, self.op, self.dlen, self.is_, self.vs = ops, op, dlen, is_, vs
+
+    def hist(self, ne: int):
+        return self.ops.hist(self.op, ne, self.dlen, self.is_, self.vs)
+
+
+# ----------------------------------------------------------------- GPU backend (C5 / C2)
 class GpuPart2Local:
     """partition2 on one GPU's contiguous shard (the single-pass ixg_partition2
     kernel); partition2_sharded turns its true count into the shard's two

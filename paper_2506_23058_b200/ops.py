@@ -146,6 +146,14 @@ def scan_add(xs: torch.Tensor, ne: int = 0, exclusive: bool = False, out=None) -
     return out
 
 
+def reduce_add(xs: torch.Tensor, out=None) -> torch.Tensor:
+    """total of scan (+) 0 xs (its last element) as a device int64 scalar."""
+    xs = _contig(xs)
+    out = torch.empty(1, dtype=torch.int64, device=xs.device) if out is None else out
+    L.check(_lib().ixg_reduce_add(_dt(xs), _ptr(xs), xs.numel(), _ptr(out), _stream()), "reduce_add")
+    return out
+
+
 def segscan_add(flags: torch.Tensor, xs: torch.Tensor, want_flags: bool = False):
     """sgmSum's 2-ary scan; returns values (and flags)."""
     flags, xs = _contig(flags), _contig(xs)

@@ -120,3 +120,112 @@ def test_sharded_c2_and_partition2_gloo(world, n, m):
         pr.join(120)
         assert pr.exitcode == 0
     assert q.get() == (True, True, True, True)
+
+
+# ------------------------------------------------------------------ scan / filter / partition3 / hist
+class NpScanLocal:
+    def __init__(self, xs):
+        self.xs = xs
+
+    def total(self):
+        return int(self.xs.sum())
+
+    def scan(self, seed, exclusive):
+        inc = seed + np.cumsum(self.xs, dtype=np.int64)
+        self.out = inc - self.xs if exclusive else inc
+
+
+class NpFilterLocal:
+    def __init__(self, xs, pred):
+        self.xs, self.pred = xs, pred
+
+    def filter(self):
+        self.ys = O.filter_(self.pred, self.xs)
+        return len(self.ys)
+
+
+class NpPart3Local:
+    def __init__(self, xs, p, q):
+        self.xs, self.p, self.q = xs, p, q
+
+    def partition3(self):
+        m1, m2, self.ys = O.partition3(self.p, self.q, self.xs)
+        return m1, m2, len(self.xs)
+
+
+class NpHistLocal:
+    def __init__(self, op, dlen, is_, vs):
+        self.op, self.dlen, self.is_, self.vs = op, dlen, is_, vs
+
+    def hist(self, ne):
+        import torch
+
+        return torch.from_numpy(O.hist(self.op, ne, self.dlen, self.is_, self.vs).astype(np.int64))
+
+
+def _worker2(rank, world, port, n, q):
+    import torch.distributed as dist
+
+    from paper_2506_23058_b200 import _lib as L
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = rank * n // world, (rank + 1) * n // world
+        xs = gen.uniform(11, n, -50, 50, np.int64)
+        res = {}
+        for exclusive in (False, True):
+            sc = NpScanLocal(xs[lo:hi])
+            tot = D.scan_sharded(sc, ne=7, exclusive=exclusive)
+            parts = [None] * world
+            dist.all_gather_object(parts, sc.out.tolist())
+            want = O.scan_add(xs, 7)
+            if exclusive:
+                want = want - xs
+            res[f"scan{int(exclusive)}"] = (tot == 7 + int(xs.sum())
+                                            and np.array_equal(np.concatenate([np.array(p, np.int64) for p in parts]),
+                                                               want))
+        fl = NpFilterLocal(xs[lo:hi], Pred.ge(3))
+        kt, runs = D.filter_sharded(fl)
+        parts = [None] * world
+        dist.all_gather_object(parts, (runs.starts, fl.ys.tolist()))
+        out = np.zeros(kt, np.int64)
+        for (s,), ys_r in parts:
+            out[s:s + len(ys_r)] = ys_r
+        res["filter"] = np.array_equal(out, O.filter_(Pred.ge(3), xs))
+        p3 = NpPart3Local(xs[lo:hi], Pred.lt(-10), Pred.hash(5))
+        (M1, M2), runs = D.partition3_sharded(p3)
+        parts = [None] * world
+        dist.all_gather_object(parts, (runs.starts, runs.lengths, p3.ys.tolist()))
+        out = np.zeros(n, np.int64)
+        for starts, lengths, ys_r in parts:
+            off = 0
+            for s, ln in zip(starts, lengths):
+                out[s:s + ln] = ys_r[off:off + ln]
+                off += ln
+        wm1, wm2, wys = O.partition3(Pred.lt(-10), Pred.hash(5), xs)
+        res["partition3"] = (M1, M2) == (wm1, wm2) and np.array_equal(out, wys)
+        is_ = gen.uniform(12, n, -3, 40, np.int64)
+        for op_name, op in (("min", L.HIST_MIN), ("max", L.HIST_MAX), ("add", L.HIST_ADD)):
+            ne = {"min": 1 << 40, "max": -(1 << 40), "add": 5}[op_name]
+            table = D.hist_sharded(NpHistLocal(op, 37, is_[lo:hi], xs[lo:hi]), op_name, ne)
+            res[f"hist_{op_name}"] = np.array_equal(table.numpy(), O.hist(op, ne, 37, is_, xs))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1001), (3, 2500)])
+def test_sharded_scan_filter_partition3_hist_gloo(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker2, args=(r, world, port, n, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(180)
+        assert pr.exitcode == 0
+    res = q.get()
+    assert all(res.values()), res

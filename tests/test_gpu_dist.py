@@ -74,3 +74,49 @@ def test_partition2_sharded_kernels(cuda, G, n):
             off += ln
         assert loc.st.read().ok
     assert np.array_equal(out, want)
+
+
+@pytest.mark.parametrize("G,n", [(2, 100_000), (4, 1_000_003), (3, 50)])
+def test_sharded_scan_filter_partition3_kernels(cuda, G, n):
+    """the per-rank GPU locals of dist.scan_sharded / filter_sharded /
+    partition3_sharded, driven rank by rank with the same offset arithmetic."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    xs = gen.uniform(G + n, n, -1000, 1000, np.int64)
+    bounds = [(r * n // G, (r + 1) * n // G) for r in range(G)]
+    # reduce_add == the shard sums (i32 / i64 / u8 inputs)
+    for dt in (np.int32, np.int64, np.uint8):
+        a = (xs % 200).astype(dt) if dt == np.uint8 else xs.astype(dt)
+        assert int(ops.reduce_add(torch.from_numpy(a).to(cuda)).item()) == int(a.astype(np.int64).sum())
+    # scan: totals first, then one seeded scan per rank
+    locs = [D.GpuScanLocal(torch.from_numpy(xs[lo:hi].copy()).to(cuda)) for lo, hi in bounds]
+    ts = [loc.total() for loc in locs]
+    for exclusive in (False, True):
+        for loc, seed in zip(locs, D.exclusive_offsets(ts)):
+            loc.scan(-3 + seed, exclusive)
+        got = np.concatenate([loc.out.cpu().numpy() for loc in locs])
+        want = O.scan_add(xs, -3) - (xs if exclusive else 0)
+        assert np.array_equal(got, want)
+    # filter
+    fl = [D.GpuFilterLocal(torch.from_numpy(xs[lo:hi].copy()).to(cuda), Pred.gt(100)) for lo, hi in bounds]
+    ks = [f.filter() for f in fl]
+    got = np.concatenate([f.ys[:k].cpu().numpy() for f, k in zip(fl, ks)])
+    assert np.array_equal(got, O.filter_(Pred.gt(100), xs))
+    # partition3
+    p, q = Pred.lt(-300), Pred.hash(17)
+    pl = [D.GpuPart3Local(torch.from_numpy(xs[lo:hi].copy()).to(cuda), p, q) for lo, hi in bounds]
+    rows = [loc.partition3() for loc in pl]
+    counts = [[m1, m2, size - m1 - m2] for m1, m2, size in rows]
+    out = np.zeros(n, np.int64)
+    for r, loc in enumerate(pl):
+        totals, runs = D.partition_runs(counts, r)
+        ys = loc.ys.cpu().numpy()
+        off = 0
+        for s, ln in zip(runs.starts, runs.lengths):
+            out[s:s + ln] = ys[off:off + ln]
+            off += ln
+    wm1, wm2, wys = O.partition3(p, q, xs)
+    assert totals[:2] == [wm1, wm2]
+    assert np.array_equal(out, wys)
