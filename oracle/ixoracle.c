@@ -401,3 +401,87 @@ int ixo_csrg(const int64_t* x, int64_t num_cols, const int64_t* values, const in
   }
   return IXO_OK;
 }
+
+/* partition2L -- corpus/partition2l.ixl, statement by
+ * statement.  II = mkII shp has length L = sum shp; the reference's sgmSum
+ * scans L elements of fs (so L <= n, else its scan raises IndexError). */
+int ixo_partition2l(const int64_t* shp, int64_t m, const int64_t* cs, const int64_t* xs, int64_t n,
+                    int64_t* ys) {
+  int64_t L = 0;
+  for (int64_t k = 0; k < m; ++k) L += shp[k] > 0 ? shp[k] : 0;
+  if (L > n) return IXO_BADARG;
+  int64_t cap = L > 0 ? L : 1;
+  int64_t *II = ALLOC(int64_t, cap), *offs = ALLOC(int64_t, m > 0 ? m : 1), *ones = ALLOC(int64_t, m > 0 ? m : 1);
+  int64_t *descr = ALLOC(int64_t, cap), *fl = ALLOC(int64_t, cap), *tb = ALLOC(int64_t, cap);
+  int64_t *rtot = ALLOC(int64_t, m > 0 ? m : 1), *inds = ALLOC(int64_t, n > 0 ? n : 1), *zeros = ALLOC(int64_t, n > 0 ? n : 1);
+  int64_t len = 0;
+  int rc = IXO_NOMEM;
+  if (!II || !offs || !ones || !descr || !fl || !tb || !rtot || !inds || !zeros) goto out;
+  if ((rc = ixo_mkii(shp, m, II, cap, &len))) goto out;                          /* :32 */
+  int64_t acc = 0;                                                                /* :33-34 */
+  for (int64_t k = 0; k < m; ++k) {
+    acc += k == 0 ? 0 : shp[k - 1];
+    offs[k] = acc;
+    ones[k] = 1;                                                                  /* :35 */
+  }
+  if ((rc = ixo_mksgmdescr(shp, ones, m, descr, cap, &len))) goto out;          /* :36 */
+  for (int64_t i = 0; i < len; ++i) fl[i] = descr[i] > 0;                         /* :37 */
+  if ((rc = ixo_sgmsum(fl, cs, len, tb))) goto out;                               /* :38-39: fs = cs as 0/1 */
+  for (int64_t k = 0; k < m; ++k) {                                               /* :40 */
+    if (shp[k] > 0) {
+      const int64_t j = offs[k] + shp[k] - 1;
+      if (j < 0 || j >= len) { rc = IXO_OOB; goto out; }
+      rtot[k] = tb[j];
+    } else {
+      rtot[k] = 0;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) {                                               /* :41 */
+    if (i >= len) { rc = IXO_OOB; goto out; }                                     /* II[i] */
+    inds[i] = cs[i] ? offs[II[i]] + tb[i] - 1 : i + rtot[II[i]] - tb[i];
+  }
+  for (int64_t i = 0; i < n; ++i) zeros[i] = 0;
+  rc = ixo_scatter(zeros, n, inds, n, xs, n, ys);                                 /* :42 */
+out:
+  free(II); free(offs); free(ones); free(descr); free(fl); free(tb); free(rtot); free(inds); free(zeros);
+  return rc;
+}
+
+/* filter_seg -- corpus/filter_seg.ixl: filter.ixl's compaction, then the new
+ * row sizes from the running count at each row's ends (statement order: all
+ * `before` gathers, then all `upto` gathers). */
+int ixo_filter_seg(const int64_t* shp, int64_t m, const int64_t* cs, const int64_t* xs, int64_t n,
+                   int64_t* newshp, int64_t* ys, int64_t* count) {
+  int64_t *offs = ALLOC(int64_t, n > 0 ? n : 1), *starts = ALLOC(int64_t, m > 0 ? m : 1);
+  int64_t *before = ALLOC(int64_t, m > 0 ? m : 1), *upto = ALLOC(int64_t, m > 0 ? m : 1);
+  int rc = IXO_NOMEM;
+  if (!offs || !starts || !before || !upto) goto out;
+  int64_t acc = 0;
+  for (int64_t i = 0; i < n; ++i) offs[i] = (acc += cs[i] ? 1 : 0);                /* :9-10 */
+  if ((rc = ixo_filter_by(cs, xs, n, ys, count))) goto out;                          /* :11-13 */
+  acc = 0;
+  for (int64_t k = 0; k < m; ++k) starts[k] = (acc += k == 0 ? 0 : shp[k - 1]);     /* :14-15 */
+  for (int64_t k = 0; k < m; ++k) {                                                  /* :16 */
+    const int64_t st = starts[k];
+    if (st > 0) {
+      if (st - 1 >= n) { rc = IXO_OOB; goto out; }
+      before[k] = offs[st - 1];
+    } else {
+      before[k] = 0;
+    }
+  }
+  for (int64_t k = 0; k < m; ++k) {                                                  /* :17 */
+    if (shp[k] > 0) {
+      const int64_t j = starts[k] + shp[k] - 1;
+      if (j < 0 || j >= n) { rc = IXO_OOB; goto out; }
+      upto[k] = offs[j];
+    } else {
+      upto[k] = 0;
+    }
+  }
+  for (int64_t k = 0; k < m; ++k) newshp[k] = shp[k] > 0 ? upto[k] - before[k] : 0;  /* :18 */
+  rc = IXO_OK;
+out:
+  free(offs); free(starts); free(before); free(upto);
+  return rc;
+}

@@ -85,6 +85,13 @@ int ixo_kmeans_ker(int64_t row, const int64_t* pointers, int64_t np1,
                    const int64_t* indices, int64_t nnz, double* out, ixo_status* st);
 int ixo_csrg(const int64_t* x, int64_t num_cols, const int64_t* values, const int64_t* indices,
              int64_t nnz, int64_t* out, int64_t* first_bad);
+/* the jagged programs corpus/partition2l.ixl and corpus/filter_seg.ixl.
+ * Inputs with sum shp > n make the reference's own k-ary scan index past the
+ * shorter array (an uncaught IndexError): IXO_BADARG here. */
+int ixo_partition2l(const int64_t* shp, int64_t m, const int64_t* cs, const int64_t* xs, int64_t n,
+                    int64_t* ys);
+int ixo_filter_seg(const int64_t* shp, int64_t m, const int64_t* cs, const int64_t* xs, int64_t n,
+                   int64_t* newshp, int64_t* ys, int64_t* count);
 
 /* ---- multi-threaded restatements used only as the timed CPU baseline
  *      (bench.py cpu_baseline / --impl reference).  Same results as the

@@ -266,3 +266,22 @@ def par_partition2_i32(p, xs, nthreads=0):
     _ok(lib().ixo_par_partition2_i32(ctypes.byref(cp), _p(xs), ctypes.c_int64(len(xs)), ctypes.byref(nt), _p(ys),
                                      int(nthreads)))
     return nt.value, ys[: len(xs)]
+
+
+def partition2l(shp, cs, xs):
+    """corpus/partition2l.ixl (ixo_partition2l)."""
+    shp, cs, xs = _i64(shp), _i64(cs), _i64(xs)
+    ys = np.empty_like(xs)
+    _ok(lib().ixo_partition2l(_p(shp), ctypes.c_int64(len(shp)), _p(cs), _p(xs), ctypes.c_int64(len(xs)), _p(ys)))
+    return ys
+
+
+def filter_seg(shp, cs, xs):
+    """corpus/filter_seg.ixl (ixo_filter_seg) -> (new row sizes, filtered values)."""
+    shp, cs, xs = _i64(shp), _i64(cs), _i64(xs)
+    newshp = np.empty_like(shp)
+    ys = np.empty_like(xs)
+    cnt = ctypes.c_int64(0)
+    _ok(lib().ixo_filter_seg(_p(shp), ctypes.c_int64(len(shp)), _p(cs), _p(xs), ctypes.c_int64(len(xs)), _p(newshp),
+                             _p(ys), ctypes.byref(cnt)))
+    return newshp, ys[: cnt.value].copy()

@@ -139,6 +139,13 @@ def big_cases(fun):
             out.append([gen.uniform(seed + 6, ncols, -300, 300, np.int64).tolist(),
                         gen.uniform(seed + 7, n, -300, 300, np.int64).tolist(),
                         gen.uniform(seed + 8, n, 0, ncols - 1, np.int64).tolist()])
+        elif fun in ("partition2L", "filter_seg"):
+            m = n // 16
+            shp = gen.uniform(seed + 10, m, 0, 31, np.int64)
+            shp[::7] = 0  # empty rows
+            nn = int(shp.sum())
+            cs = [bool(c) for c in (gen.uniform(seed + 11, nn, 0, 2, np.int64) == 0)]
+            out.append([shp.tolist(), cs, gen.uniform(seed + 12, nn, -500, 500, np.int64).tolist()])
         elif fun == "get_smallest_pairs":
             nv = 50
             es = gen.uniform(seed + 9, 200, 0, nv - 1, np.int64).tolist()
@@ -186,6 +193,12 @@ DEMOS = {
     ("ref:partition2.ixl", "partition2"): [[Pred(LT, 5), [5, 4, 2, 8, 7, 3]]],
     ("ref:mksgmdescr.ixl", "mkSgmDescr"): [[[0, 2, 1, 0, 3], [1, 2, 3, 4, 5]]],
     ("own:mkii.ixl", "mkII"): [[[0, 2, 1, 0, 3]]],
+    ("own:partition2l.ixl", "partition2L"): [[[3, 0, 2, 4], [True, False, True, False, True, False, False, True,
+                                                               True], [10, 11, 12, 13, 14, 15, 16, 17, 18]],
+                                             [[2, 1], [True, False, True, False], [1, 2, 3, 4]]],  # n != sum shp
+    ("own:filter_seg.ixl", "filter_seg"): [[[3, 0, 2, 4], [True, False, True, False, True, False, False, True,
+                                                             True], [10, 11, 12, 13, 14, 15, 16, 17, 18]],
+                                           [[4], [True, False], [1, 2]]],  # n != sum shp
 }
 
 
@@ -204,7 +217,16 @@ def main():
         for f in prog.defs:
             rng = random.Random(hash((key, f.name)) & 0xFFFF if False else sum(map(ord, key + f.name)))
             draws = []
-            if f.name != "kmeans_ker":
+            if f.name in ("partition2L", "filter_seg"):
+                # jagged inputs need n == sum shp, which the language cannot
+                # state (gen_args would draw unrelated lengths; with sum shp > n
+                # the reference's own scan indexes past the shorter array)
+                for _ in range(40):
+                    shp = [rng.randint(0, 4) for _ in range(rng.randint(0, 5))]
+                    nn = sum(shp)
+                    draws.append(("jagged", [shp, [rng.random() < 0.5 for _ in range(nn)],
+                                             [rng.randint(-9, 9) for _ in range(nn)]]))
+            elif f.name != "kmeans_ker":
                 for _ in range(40):
                     a = gen_args(f, rng, interp)
                     if a is not None:

@@ -111,6 +111,15 @@ def test_vm_compiles_corpus_lambdas():
     for key, d in PROGRAMS.items():
         prog = ir.from_json(d["program"])
         for f in prog.defs:
+            lets = set()
+
+            def collect(e):
+                if ir.kind(e) == "Let":
+                    lets.update(e.names)
+                for c in ir.children(e):
+                    collect(c)
+            collect(f.body)
+
             def walk(e):
                 nonlocal n
                 if ir.kind(e) == "App" and ir.kind(e.fun) == "VarE" and e.fun.name == "map" and ir.kind(e.args[0]) == "Lambda":
@@ -122,6 +131,8 @@ def test_vm_compiles_corpus_lambdas():
                     for nm in ("num_true", "m1", "m2", "count", "len"):
                         env.setdefault(nm, ("scalar", 1))
                     for nm in ("H", "shape", "x"):
+                        env.setdefault(nm, ("array", object()))
+                    for nm in lets:  # let-bound names of the body (arrays, except the scalars above)
                         env.setdefault(nm, ("array", object()))
                     arrs = [object() for _ in lam.params]
                     c = vm.compile_map(lam, arrs, env)

@@ -76,13 +76,18 @@ def run_oracle(fun, a):
         return ints(O.csrg(a[0], a[1], a[2]))
     if fun == "kmeans_ker":
         return O.kmeans_ker(a[0], a[1], a[2], a[3], a[4])
+    if fun == "partition2L":
+        return ints(O.partition2l(a[0], [int(c) for c in a[1]], a[2]))
+    if fun == "filter_seg":
+        newshp, ys = O.filter_seg(a[0], [int(c) for c in a[1]], a[2])
+        return (ints(newshp), ints(ys))
     raise KeyError(fun)
 
 
 def test_golden_file_covers_corpus():
     funs = {c["fun"] for c in CASES}
     assert {"partition2", "partition3", "filter", "filter_by", "get_smallest_pairs", "mkSgmDescr", "kmeans_ker",
-            "c2", "mkFlags", "sgmSum", "mkII", "sc_any", "csrg_any"} <= funs
+            "c2", "mkFlags", "sgmSum", "mkII", "sc_any", "csrg_any", "partition2L", "filter_seg"} <= funs
     assert any("error" in c for c in CASES)
     assert len(CASES) > 500
 
