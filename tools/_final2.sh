@@ -1,0 +1,8 @@
+# bench all configs + ncu of the C2 fused kernel and partition kernel (bw8)
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
+for c in c2 c1 c3 c4 c5; do timeout 600 python bench.py --config $c > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "$c rc=$?"; done
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+B="python bench.py --steps 3 --warmup 3 --no-cpu"
+timeout 600 $B > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv $B > /dev/null 2>&1; echo "launches rc=$?"
+bash tools/_prof4.sh
+timeout 300 python tools/prof_run.py partition2 28 2 > /dev/null && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_filter_b -s 1 -c 1 -o gpurun_out/part2_full python tools/prof_run.py partition2 28 2 > /dev/null 2>&1; echo "p2 rc=$?"
