@@ -283,8 +283,9 @@ class C1:
         self.big, self.rank, self.ws = big, rank, ws
         self.workload = (f"partition2 (x < 0), N=2^{self.N.bit_length() - 1} int32 uniform over int32"
                          + (" per GPU (2^32 total)" if big else "")
-                         + (f"; {ws} contiguous shards, all-gather of per-shard true counts -> each shard's two "
-                            "output runs of the global result" if ws > 1 else ""))
+                         + (f"; {ws} contiguous shards: all-gather of per-shard true counts -> each shard's two "
+                            "output runs of the global result, moved to the shards owning their positions "
+                            "(one NCCL all-to-all per class)" if ws > 1 else ""))
 
     def setup_device(self):
         import torch
@@ -318,7 +319,7 @@ class C1:
         if self.ws > 1:
             from paper_2506_23058_b200 import dist as D
 
-            self.nt_global, self.runs = D.partition2_sharded(self.local)
+            self.nt_global, self.runs, self.mine = D.partition2_sharded(self.local, exchange=True)
             return
         ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
 
@@ -356,7 +357,7 @@ class C1:
         if self.ws > 1:
             from paper_2506_23058_b200 import dist as D
 
-            D.partition2_sharded(self.local)
+            D.partition2_sharded(self.local, exchange=True)
         else:
             ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
         ys_p.copy_(self.ys, non_blocking=True)

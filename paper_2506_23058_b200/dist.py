@@ -117,15 +117,59 @@ def c2_sharded(local, group=None):
     return K[rank], k, k_total
 
 
-def partition2_sharded(local, group=None):
+def partition2_sharded(local, group=None, exchange: bool = False):
     """Sharded partition2 (C5).  `local.partition2()` -> (true count, size);
-    returns (num_true_global, Runs of this rank's local [trues | falses])."""
+    returns (num_true_global, Runs of this rank's local [trues | falses]).
+    With `exchange`, the runs are then moved to the shards owning their
+    global positions and the third result is this rank's contiguous slice
+    of the global output (exchange_runs; NCCL all-to-all on the GPU box)."""
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
     t, size = local.partition2()
     rows = all_gather_ints([t, size], group)
-    return partition2_runs([r[0] for r in rows], [r[1] for r in rows], rank)
+    nt, runs = partition2_runs([r[0] for r in rows], [r[1] for r in rows], rank)
+    if not exchange:
+        return nt, runs
+    return nt, runs, exchange_runs(local.ys_tensor(), [[r[0], r[1] - r[0]] for r in rows], rank, group)
+
+
+def shard_bounds(n_total: int, world: int, rank: int) -> Tuple[int, int]:
+    """contiguous destination shard [lo, hi) of rank r (the input split rule)."""
+    return rank * n_total // world, (rank + 1) * n_total // world
+
+
+def _overlap(a0: int, a1: int, b0: int, b1: int) -> int:
+    return max(0, min(a1, b1) - max(a0, b0))
+
+
+def exchange_runs(ys, all_counts: Sequence[Sequence[int]], rank: int, group=None):
+    """Move each rank's class runs to the shards that own their global
+    positions ('scatter destinations remapped per shard').
+    `ys` holds this rank's local [class 0 | class 1 | ...]; all_counts[r][c]
+    are every rank's class counts (already all-gathered).  One all-to-all per
+    class: a class run's positions increase with the source rank, so the
+    received pieces arrive in global order and the result is this rank's
+    contiguous slice [lo, hi) of the global output (same tensor type/device)."""
+    import torch
+    import torch.distributed as dist
+
+    world = len(all_counts)
+    k = len(all_counts[0])
+    n_total = sum(sum(int(x) for x in row) for row in all_counts)
+    runs = [partition_runs(all_counts, q)[1] for q in range(world)]
+    lo, hi = shard_bounds(n_total, world, rank)
+    outs, off = [], 0
+    for c in range(k):
+        s0, ln = runs[rank].starts[c], runs[rank].lengths[c]
+        send = [_overlap(s0, s0 + ln, *shard_bounds(n_total, world, r)) for r in range(world)]
+        recv = [_overlap(runs[q].starts[c], runs[q].starts[c] + runs[q].lengths[c], lo, hi) for q in range(world)]
+        out = torch.empty(sum(recv), dtype=ys.dtype, device=ys.device)
+        dist.all_to_all_single(out, ys[off:off + ln].contiguous(), output_split_sizes=recv, input_split_sizes=send,
+                               group=group)
+        outs.append(out)
+        off += ln
+    return torch.cat(outs)
 
 
 def partition3_sharded(local, group=None):
@@ -256,6 +300,9 @@ class GpuPart2Local:
     def partition2(self):
         self.ops.partition2(self.xs, self.pred, self.L.VARIANT_ELIDED, self.st, ys=self.ys, d_nt=self.dnt)
         return int(self.dnt.item()), self.xs.numel()
+
+    def ys_tensor(self):
+        return self.ys
 
 
 class GpuC2Local:

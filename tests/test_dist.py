@@ -59,6 +59,11 @@ class NpPart2Local:
         self.ys = ys
         return nt, len(self.xs)
 
+    def ys_tensor(self):
+        import torch
+
+        return torch.from_numpy(np.asarray(self.ys, dtype=np.int64))
+
 
 def _worker(rank, world, port, n, m, q):
     import torch.distributed as dist
@@ -77,7 +82,9 @@ def _worker(rank, world, port, n, m, q):
         zs_all = [None] * world
         dist.all_gather_object(zs_all, (K, loc.ys.tolist(), loc.zs.tolist()))
         p2 = NpPart2Local(xs[lo:hi], Pred.lt(3))
-        nt, runs = D.partition2_sharded(p2)
+        nt, runs, mine = D.partition2_sharded(p2, exchange=True)
+        slices = [None] * world
+        dist.all_gather_object(slices, mine.tolist())
         parts = [None] * world
         dist.all_gather_object(parts, (runs.starts, runs.lengths, p2.ys.tolist()))
         if rank == 0:
@@ -94,8 +101,10 @@ def _worker(rank, world, port, n, m, q):
                     p_out[s:s + ln] = ys_r[off:off + ln]
                     off += ln
             want_nt, want_p = O.partition2(Pred.lt(3), xs)
+            exchanged = np.concatenate([np.array(x, np.int64) for x in slices])
             q.put((np.array_equal(ys_g, want_ys), np.array_equal(zs_g, want_zs), nt == want_nt,
-                   np.array_equal(p_out, want_p)))
+                   np.array_equal(p_out, want_p) and np.array_equal(exchanged, want_p)
+                   and all(len(slices[r]) == (r + 1) * n // world - r * n // world for r in range(world))))
     finally:
         dist.destroy_process_group()
 
