@@ -306,6 +306,17 @@ class C1:
 
             self.local = D.GpuPart2Local(self.xs, self.p)
             self.local.ys, self.local.dnt, self.local.st = self.ys, self.dnt, self.st
+            # default: the exchange fused into the partition kernel (peer
+            # stores into IPC-mapped shards); IXG_C5_EXCHANGE=nccl selects the
+            # NCCL all-to-all after the local partition
+            self.peer = None
+            self.exchange = os.environ.get("IXG_C5_EXCHANGE", "fused")
+            if self.exchange == "fused":
+                try:
+                    self.peer = D.GpuPart2PeerLocal(self.xs, self.p)
+                except Exception as e:  # no CUDA IPC between the ranks' GPUs
+                    self.exchange = f"nccl (fused setup failed: {type(e).__name__})"
+            self.workload += f"; exchange: {self.exchange}"
 
     def pre_step(self):
         """between timed steps, outside the timed region: a 256 MB write
@@ -319,7 +330,10 @@ class C1:
         if self.ws > 1:
             from paper_2506_23058_b200 import dist as D
 
-            self.nt_global, self.runs, self.mine = D.partition2_sharded(self.local, exchange=True)
+            if self.peer is not None:
+                self.nt_global = self.peer.step()
+            else:
+                self.nt_global, self.runs, self.mine = D.partition2_sharded(self.local, exchange=True)
             return
         ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
 
@@ -350,6 +364,8 @@ class C1:
         return (torch.from_numpy(xs_h).pin_memory(), torch.empty(self.N, dtype=torch.int32).pin_memory(), variant)
 
     def e2e_step(self, bufs):
+        import torch
+
         from paper_2506_23058_b200 import ops
 
         xs_p, ys_p, variant = bufs
@@ -357,9 +373,15 @@ class C1:
         if self.ws > 1:
             from paper_2506_23058_b200 import dist as D
 
-            D.partition2_sharded(self.local, exchange=True)
-        else:
-            ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
+            if self.peer is not None:
+                self.peer.step()
+                ys_p.copy_(self.peer.out, non_blocking=True)
+            else:
+                _, _, mine = D.partition2_sharded(self.local, exchange=True)
+                ys_p[:mine.numel()].copy_(mine, non_blocking=True)
+            torch.cuda.synchronize()
+            return 4 * self.N, 4 * self.N
+        ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
         ys_p.copy_(self.ys, non_blocking=True)
         int(self.dnt.item())
         return 4 * self.N, 4 * self.N + 8

@@ -187,6 +187,29 @@ int ixg_filter_by(int dt, const uint8_t* cs, const void* xs, int64_t n, void* ys
                   int64_t* d_count, uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Sharded partition2 (BASELINE configs[4]) with the exchange
+ * fused into the kernel.  ixg_partition_counts: class totals of the shard
+ * (d_tot[0] = trues; classes 3 adds d_tot[1] = class 1), the all-gather input.
+ * ixg_partition2_peer: the single-pass partition of this rank's shard whose
+ * runs are stored straight to their global positions of the output sharded
+ * over `ranks` GPUs (`shard` elements each, shard % (16 / elem size) == 0):
+ * dst[r] = rank r's shard, mapped with ixg_ipc_open for r != this rank (peer
+ * stores over NVLink); true_base / false_base = this rank's first global
+ * position of each class (T_<r and NT + F_<r), local_true = its true count.
+ * Replaces partition2.ixl's scatter (:17) for the sharded case. */
+int ixg_partition_counts(int dt, const void* xs, int64_t n, const ixg_pred* p, const ixg_pred* q, int classes,
+                         int64_t* d_tot, void* ws, size_t ws_bytes, void* stream);
+int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, void* const* dst, int ranks,
+                        int64_t shard, int64_t true_base, int64_t false_base, int64_t local_true, void* ws,
+                        size_t ws_bytes, void* stream);
+/* device buffers shared between the ranks' processes (CUDA IPC):
+ * handle = 64 opaque bytes, exchanged by the host (torch.distributed). */
+int ixg_dev_alloc(size_t bytes, void** out);
+int ixg_dev_free(void* p);
+int ixg_ipc_handle(const void* p, void* handle);
+int ixg_ipc_open(const void* handle, void** out);
+int ixg_ipc_close(void* p);
+
 /* partition2 (corpus/partition2.ixl:4-19; sites: 0 = indicesT[n-1],
  * 1 = scatter).  ys: length n; *d_num_true. */
 int ixg_partition2(int dt, const void* xs, int64_t n, const ixg_pred* p, void* ys,

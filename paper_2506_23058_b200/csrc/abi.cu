@@ -186,12 +186,12 @@ inline bool seg_split_mode() {
   return mode == 1;
 }
 
-template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1>
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false>
 int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, LBChan ch,
                     long long* d_count, cudaStream_t s, Z* zs = nullptr, const uint32_t* segbits = nullptr,
                     long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr}, ixg_status* st = nullptr,
-                    const ixg_pred& q = ixg_pred{}) {
-  auto kern = k_filter_b<T, kByCs, kSeg, Z, NS>;
+                    const ixg_pred& q = ixg_pred{}, const PeerOut<T>& po = PeerOut<T>{}) {
+  auto kern = k_filter_b<T, kByCs, kSeg, Z, NS, kPeer>;
   static bool attr = false;
   if (!attr) {
     allow_smem(kern, Big<T>::SMEM);
@@ -200,7 +200,7 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
   TimedLaunch tl(NS > 1 ? IXG_K_PLACE : IXG_K_FILTER_FUSED, s);
   const long long seg_tiles = tiles_of(n, Big<T>::TILE);
   kern<<<(unsigned)(NS * seg_tiles), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(), d_count, zs,
-                                                                  segbits, out_base, ch2, st, q, seg_tiles);
+                                                                  segbits, out_base, ch2, st, q, seg_tiles, po);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -610,6 +610,104 @@ int ixg_filter_by(int dt, const uint8_t* cs, const void* xs, int64_t n, void* ys
   return do_filter<int64_t>((const int64_t*)xs, cs, n, nullptr, (int64_t*)ys, (long long*)d_count, variant, st, w,
                             S(stream));
 }
+
+// ---- sharded partition2 with the exchange fused into the kernel (C5) ----
+int ixg_partition_counts(int dt, const void* xs, int64_t n, const ixg_pred* p, const ixg_pred* q, int classes,
+                         int64_t* d_tot, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !p || !d_tot || (classes != 2 && classes != 3) || (n > 0 && !xs)) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_PARTITION2, n, 0)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  if (n == 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(int64_t) * (classes - 1), s));
+  WS w(ws);
+  const int cgrid = grid_for(n / 4 + 1);
+  long long* partials = (long long*)w.take((size_t)cgrid * 2 * 8);
+  const ixg_pred qq = q ? *q : ixg_pred{IXG_PRED_FALSE, 0, 0, 0};
+  TimedLaunch tl(IXG_K_CLASS_COUNT, s);
+  if (dt == IXG_I32) {
+    if (classes == 2)
+      k_class_count<int32_t, 2><<<cgrid, kSThreads, 0, s>>>((const int32_t*)xs, n, *p, qq, partials, w.hdr(5),
+                                                           (long long*)d_tot);
+    else
+      k_class_count<int32_t, 3><<<cgrid, kSThreads, 0, s>>>((const int32_t*)xs, n, *p, qq, partials, w.hdr(5),
+                                                           (long long*)d_tot);
+  } else {
+    if (classes == 2)
+      k_class_count<long long, 2><<<cgrid, kSThreads, 0, s>>>((const long long*)xs, n, *p, qq, partials, w.hdr(5),
+                                                             (long long*)d_tot);
+    else
+      k_class_count<long long, 3><<<cgrid, kSThreads, 0, s>>>((const long long*)xs, n, *p, qq, partials, w.hdr(5),
+                                                             (long long*)d_tot);
+  }
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, void* const* dst, int ranks,
+                        int64_t shard, int64_t true_base, int64_t false_base, int64_t local_true, void* ws,
+                        size_t ws_bytes, void* stream) {
+  if (n < 0 || !p || !dst || ranks < 1 || ranks > 8 || shard <= 0 || (n > 0 && !xs)) return IXG_BADARG;
+  const int ep = dt == IXG_I32 ? 4 : 2;
+  if (shard % ep) return IXG_BADARG;  // a 16-byte chunk never straddles two shards
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_PARTITION2, n, 0)) return IXG_BADARG;
+  if (n == 0) return IXG_OK;
+  for (int r = 0; r < ranks; ++r)
+    if (!dst[r] || !aligned16(dst[r])) return IXG_BADARG;
+  if (!aligned16(xs)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  WS w(ws);
+  LBChan c0 = w.chan(0, std::max(lb_tiles(n), 2 * tiles_of(n, Big<long long>::TILE)));
+  long long* scratch = (long long*)w.take(64);
+  const ixg_pred pp = *p;
+  if (dt == IXG_I32) {
+    PeerOut<int32_t> po{};
+    for (int r = 0; r < ranks; ++r) po.dst[r] = (int32_t*)dst[r];
+    po.shard = shard;
+    po.seg_base[0] = true_base;
+    po.seg_base[1] = false_base;
+    po.seg_local[0] = 0;
+    po.seg_local[1] = local_true;
+    po.ranks = ranks;
+    return launch_filter_b<int32_t, false, false, int32_t, 2, true>((const int32_t*)xs, nullptr, n, pp, nullptr, c0,
+                                                                    scratch, s, nullptr, nullptr, 0,
+                                                                    LBChan{nullptr, nullptr}, nullptr, ixg_pred{},
+                                                                    po);
+  }
+  PeerOut<long long> po{};
+  for (int r = 0; r < ranks; ++r) po.dst[r] = (long long*)dst[r];
+  po.shard = shard;
+  po.seg_base[0] = true_base;
+  po.seg_base[1] = false_base;
+  po.seg_local[0] = 0;
+  po.seg_local[1] = local_true;
+  po.ranks = ranks;
+  return launch_filter_b<long long, false, false, long long, 2, true>((const long long*)xs, nullptr, n, pp, nullptr,
+                                                                      c0, scratch, s, nullptr, nullptr, 0,
+                                                                      LBChan{nullptr, nullptr}, nullptr, ixg_pred{},
+                                                                      po);
+}
+
+// ---- device memory shared across processes (CUDA IPC over NVLink) ----
+int ixg_dev_alloc(size_t bytes, void** out) {
+  if (!out) return IXG_BADARG;
+  return cuda_rc(cudaMalloc(out, bytes ? bytes : 16));
+}
+int ixg_dev_free(void* p) { return cuda_rc(cudaFree(p)); }
+int ixg_ipc_handle(const void* p, void* handle) {
+  if (!p || !handle) return IXG_BADARG;
+  cudaIpcMemHandle_t h;
+  int rc = cuda_rc(cudaIpcGetMemHandle(&h, const_cast<void*>(p)));
+  if (rc) return rc;
+  memcpy(handle, &h, sizeof(h));
+  return IXG_OK;
+}
+int ixg_ipc_open(const void* handle, void** out) {
+  if (!handle || !out) return IXG_BADARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_rc(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+}
+int ixg_ipc_close(void* p) { return cuda_rc(cudaIpcCloseMemHandle(p)); }
 
 int ixg_partition2(int dt, const void* xs, int64_t n, const ixg_pred* p, void* ys, int64_t* d_num_true,
                    uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {

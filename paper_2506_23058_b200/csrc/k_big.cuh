@@ -236,6 +236,58 @@ IXG_DEV uint32_t quad_cs_mask(const uint8_t* __restrict__ cs, long long n, long 
   return mm;
 }
 
+// Fused partition + exchange (sharded C5): the global output is sharded
+// contiguously over `ranks` GPUs, `shard` elements each; dst[r] is rank r's
+// shard (a peer pointer mapped over NVLink for r != this rank).  A class
+// segment s of this rank's tiles starts at global seg_base[s]; seg_local[s]
+// is its start on the local look-back chain.
+template <typename T>
+struct PeerOut {
+  T* dst[8];
+  long long shard;
+  long long seg_base[3];
+  long long seg_local[3];
+  int ranks;
+};
+
+// store_run to the global positions [gbase, gbase + cnt) of a sharded
+// output: every 16-byte chunk lies in one shard (shard % EP == 0) and goes
+// to dst[g / shard] + g % shard -- a peer store when another GPU owns it
+template <typename E, int NT>
+IXG_DEV void store_run_peer(const PeerOut<E>& po, long long gbase, int cnt, const E* buf) {
+  constexpr int EP = 16 / (int)sizeof(E);
+  if (cnt <= 0) return;
+  const long long c0 = gbase / EP;
+  const int s = (int)(gbase - c0 * EP);
+  const int nch = (int)((gbase + cnt - 1) / EP - c0) + 1;
+  const int sw = ((EP - s) % EP) * (int)sizeof(E) / 4;
+  for (int j = threadIdx.x; j < nch; j += NT) {
+    const int l = j * EP - s;
+    const long long g = (c0 + j) * EP;
+    const long long r = g / po.shard;
+    E* dst = po.dst[r] + (g - r * po.shard);
+    if (l >= 0 && l + EP <= cnt) {
+      uint4 v;
+      if (sw == 0) {
+        v = *reinterpret_cast<const uint4*>(buf + l);
+      } else {
+        const uint4 a = *reinterpret_cast<const uint4*>(buf + l - (EP - s));
+        const uint4 b = *reinterpret_cast<const uint4*>(buf + l + s);
+        if (sw == 1) v = make_uint4(a.y, a.z, a.w, b.x);
+        else if (sw == 2) v = make_uint4(a.z, a.w, b.x, b.y);
+        else v = make_uint4(a.w, b.x, b.y, b.z);
+      }
+      asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(v.x), "r"(v.y),
+                   "r"(v.z), "r"(v.w)
+                   : "memory");
+    } else {
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (l + e >= 0 && l + e < cnt) dst[e] = buf[l + e];
+    }
+  }
+}
+
 // CTA-wide exclusive scan of warp-uniform packed counts (3 x 21 bits):
 // returns the exclusive prefix of the calling warp, *total = CTA totals
 IXG_DEV unsigned long long cta_warp_exclusive3(unsigned long long v, unsigned long long* s_w,
@@ -331,7 +383,7 @@ IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) 
 // prefix is the class's output position and the whole stable partition is
 // a single pass writing each element once (d_count[s] = the prefix at the
 // end of segment s, for s < NS - 1).
-template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1>
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false>
 __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
                                                           long long n, ixg_pred p, T* __restrict__ ys, LBChan ch,
                                                           uint32_t nonce, long long* d_count,
@@ -339,7 +391,7 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_filter_b(const T* __r
                                                           const uint32_t* __restrict__ segbits = nullptr,
                                                           long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr},
                                                           ixg_status* st = nullptr, ixg_pred q = ixg_pred{},
-                                                          long long seg_tiles = 0) {
+                                                          long long seg_tiles = 0, PeerOut<T> po = PeerOut<T>{}) {
   static_assert(!kSeg || sizeof(Z) == sizeof(T), "zs is computed in place of ys");
   using B = Big<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -503,7 +555,11 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_filter_b(const T* __r
       bw2 = __ldg(&segbits[wd + 2]);
     }
   }
-  store_run<T, kBT>(ys, base, cnt, buf);
+  if constexpr (kPeer) {
+    store_run_peer<T, kBT>(po, po.seg_base[seg] + (base - po.seg_local[seg]), cnt, buf);
+  } else {
+    store_run<T, kBT>(ys, base, cnt, buf);
+  }
   IXG_TR(6);
   if constexpr (kSeg) {
     // thread t scans the run piece [q0, q1) of odd length L (odd stride:

@@ -305,6 +305,67 @@ class GpuPart2Local:
         return self.ys
 
 
+class GpuPart2PeerLocal:
+    """Sharded partition2 (C5) with the exchange fused into the kernel: the
+    global output is sharded contiguously (`shard` elements per rank, in a
+    cudaMalloc'd buffer whose IPC handle every rank maps); a count pass and an
+    all-gather of the counts give this rank's class bases, then ONE
+    partition kernel stores each run straight to the owning shards (local or
+    peer stores over NVLink) -- no separate all-to-all pass."""
+
+    def __init__(self, xs, pred, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import ops
+
+        self.ops, self.xs, self.pred, self.group = ops, xs, pred, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        sizes = [r[0] for r in all_gather_ints([xs.numel()], group)]
+        if len(set(sizes)) != 1:
+            raise ValueError("GpuPart2PeerLocal needs equal shards")
+        self.sizes = sizes
+        self.shard = sizes[0]
+        self.buf = ops.DeviceBuffer(self.shard, xs.dtype, xs.device)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.buf.ipc_handle(), group=group)
+        self.opened = []
+        self.ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(self.buf.ptr)
+            else:
+                ptr = ops.ipc_open(h)
+                self.opened.append(ptr)
+                self.ptrs.append(ptr)
+        self.d_tot = torch.empty(1, dtype=torch.int64, device=xs.device)
+
+    @property
+    def out(self):
+        """this rank's contiguous slice of the global result"""
+        return self.buf.tensor
+
+    def step(self) -> int:
+        import torch
+        import torch.distributed as dist
+
+        t = int(self.ops.partition_counts(self.xs, self.pred, d_tot=self.d_tot).item())
+        ts = [r[0] for r in all_gather_ints([t], self.group)]
+        nt = sum(ts)
+        tb = exclusive_offsets(ts)[self.rank]
+        fb = exclusive_offsets([n - x for n, x in zip(self.sizes, ts)])[self.rank]
+        self.ops.partition2_peer(self.xs, self.pred, self.ptrs, self.shard, tb, nt + fb, t)
+        torch.cuda.synchronize()  # this rank's peer stores are done ...
+        dist.barrier(group=self.group)  # ... and so are everyone else's into our shard
+        return nt
+
+    def close(self):
+        for ptr in self.opened:
+            self.ops.ipc_close(ptr)
+        self.opened = []
+        self.buf.free()
+
+
 class GpuC2Local:
     """C2 on one GPU's shard with the CUDA kernels (ixg_filter, ixg_flag_bitmap,
     ixg_segsum, ixg_seg_carry).  `shape` is the GLOBAL segment shape."""

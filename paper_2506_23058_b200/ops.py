@@ -268,6 +268,71 @@ def partition2(xs: torch.Tensor, p: Pred, variant: int, status: Status, ys=None,
     return ys, d_nt
 
 
+def partition_counts(xs: torch.Tensor, p: Pred, q: Optional[Pred] = None, d_tot=None) -> torch.Tensor:
+    """class totals of xs for partition2 (q None: [trues]) or partition3
+    ([class 0, class 1]) as a device int64 tensor."""
+    xs = _contig(xs)
+    classes = 2 if q is None else 3
+    d_tot = torch.empty(classes - 1, dtype=torch.int64, device=xs.device) if d_tot is None else d_tot
+    ws, wsb = _ws(L.OP_PARTITION2, xs.numel(), 0, xs.device)
+    cp = _c_pred(p)
+    cq = _c_pred(q) if q is not None else None
+    L.check(_lib().ixg_partition_counts(_dt(xs), _ptr(xs), xs.numel(), ctypes.byref(cp),
+                                        ctypes.byref(cq) if cq is not None else None, classes, _ptr(d_tot), ws, wsb,
+                                        _stream()), "partition_counts")
+    return d_tot
+
+
+def partition2_peer(xs: torch.Tensor, p: Pred, dst_ptrs, shard: int, true_base: int, false_base: int,
+                    local_true: int) -> None:
+    """this rank's partition2 runs stored straight into the sharded global
+    output (dst_ptrs[r] = rank r's shard, peer-mapped; see ixg_partition2_peer)."""
+    xs = _contig(xs)
+    n = xs.numel()
+    ws, wsb = _ws(L.OP_PARTITION2, n, 0, xs.device)
+    cp = _c_pred(p)
+    arr = (ctypes.c_void_p * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
+    L.check(_lib().ixg_partition2_peer(_dt(xs), _ptr(xs), n, ctypes.byref(cp), arr, len(dst_ptrs), shard, true_base,
+                                       false_base, local_true, ws, wsb, _stream()), "partition2_peer")
+
+
+class DeviceBuffer:
+    """cudaMalloc'd buffer (exactly its own IPC allocation) viewed as a tensor."""
+
+    def __init__(self, n: int, dtype=torch.int32, device=None):
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.nbytes = n * torch.empty(0, dtype=dtype).element_size()
+        ptr = ctypes.c_void_p()
+        L.check(_lib().ixg_dev_alloc(self.nbytes, ctypes.byref(ptr)), "dev_alloc")
+        self.ptr = ptr.value
+        typestr = {torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (self.ptr, False), "version": 2}
+
+        self.tensor = torch.as_tensor(_View(), device=dev)
+
+    def ipc_handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        L.check(_lib().ixg_ipc_handle(self.ptr, h), "ipc_handle")
+        return h.raw
+
+    def free(self):
+        if self.ptr:
+            L.check(_lib().ixg_dev_free(self.ptr), "dev_free")
+            self.ptr = None
+
+
+def ipc_open(handle: bytes) -> int:
+    ptr = ctypes.c_void_p()
+    L.check(_lib().ixg_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)), "ipc_open")
+    return ptr.value
+
+
+def ipc_close(ptr: int) -> None:
+    L.check(_lib().ixg_ipc_close(ptr), "ipc_close")
+
+
 def partition3(xs: torch.Tensor, p: Pred, q: Pred, variant: int, status: Status, ys=None, d_m=None):
     """partition3 p q xs (corpus partition3.ixl); returns (ys, device (m1, m2))."""
     xs = _contig(xs)

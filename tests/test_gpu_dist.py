@@ -120,3 +120,81 @@ def test_sharded_scan_filter_partition3_kernels(cuda, G, n):
     wm1, wm2, wys = O.partition3(p, q, xs)
     assert totals[:2] == [wm1, wm2]
     assert np.array_equal(out, wys)
+
+
+@pytest.mark.parametrize("G,per", [(2, 100_000), (4, 300_000), (8, 40_000), (3, 4)])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_partition2_peer_kernel(cuda, G, per, dtype):
+    """ixg_partition2_peer for G simulated ranks in one process: every rank's
+    kernel stores its runs straight into the G destination shards (the
+    pointer table a rank gets from CUDA IPC); the shards concatenate to the
+    single-process partition2."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    n = G * per
+    xs = gen.uniform(G * 31 + per, n, -(1 << 31), (1 << 31) - 1, dtype)
+    p = Pred.lt(0)
+    want_nt, want = O.partition2(p, xs)
+    tdt = torch.int32 if dtype == np.int32 else torch.int64
+    bufs = [torch.full((per,), -7, dtype=tdt, device=cuda) for _ in range(G)]
+    ptrs = [b.data_ptr() for b in bufs]
+    shards = [torch.from_numpy(xs[r * per:(r + 1) * per].copy()).to(cuda) for r in range(G)]
+    ts = [int(ops.partition_counts(x, p).item()) for x in shards]
+    assert sum(ts) == want_nt
+    tb = D.exclusive_offsets(ts)
+    fb = D.exclusive_offsets([per - t for t in ts])
+    for r in range(G):
+        ops.partition2_peer(shards[r], p, ptrs, per, tb[r], want_nt + fb[r], ts[r])
+    got = torch.cat(bufs).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, want)
+
+
+def _ipc_worker(rank, world, port, per, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = world * per
+        xs = gen.uniform(99, n, -(1 << 31), (1 << 31) - 1, np.int32)
+        loc = D.GpuPart2PeerLocal(torch.from_numpy(xs[rank * per:(rank + 1) * per].copy()).cuda(), Pred.lt(0))
+        nt = loc.step()
+        want_nt, want = O.partition2(Pred.lt(0), xs)
+        ok = nt == want_nt and np.array_equal(loc.out.cpu().numpy().astype(np.int64), want[rank * per:(rank + 1) * per])
+        dist.barrier()
+        loc.close()
+        oks = [None] * world
+        dist.all_gather_object(oks, bool(ok))
+        if rank == 0:
+            q.put(all(oks))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition2_peer_ipc_two_processes(cuda):
+    """the CUDA-IPC plumbing of GpuPart2PeerLocal: two processes on one GPU
+    map each other's shard and store into it (the kernels never wait on each
+    other; the host barrier orders the reads)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, 200_000, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(300)
+        assert pr.exitcode == 0
+    assert q.get() is True
