@@ -41,6 +41,9 @@ constexpr int kBW = IXG_BW;             // worker warps
 constexpr int kBT = kBW * 32;           // worker threads
 constexpr int kBChunk = kBT * kSItems;  // elements per chunk
 constexpr int kBMinBlocks = kBW >= 16 ? 2 : 4;  // resident CTAs per SM the registers must allow
+#ifndef IXG_SEGSUM_MINB
+#define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
+#endif
 
 template <typename T>
 struct Big {
@@ -128,6 +131,35 @@ IXG_DEV void big_read(const T* buf, int c, int t, T (&x)[kSItems]) {
     const T* e = reinterpret_cast<const T*>(&v);
 #pragma unroll
     for (int q = 0; q < B::EP; ++q) x[j * B::EP + q] = e[q];
+  }
+}
+
+// Thread t's 16 consecutive int32 of chunk c from a LINEAR (TMA-loaded)
+// buffer without bank conflicts: step j reads piece j ^ r, r = (t >> 1) & 3
+// (the XOR swizzle of big_issue moved from the copy to the read address, so
+// a quarter-warp's LDS.128 hit 8 distinct bank groups), then two conditional
+// swap stages put piece k back at k.
+IXG_DEV void lin_read_xor(const int32_t* buf, int c, int t, int32_t (&x)[kSItems]) {
+  const int r = (t >> 1) & 3;
+  const int32_t* b = buf + Big<int32_t>::PAD + c * kBChunk + kSItems * t;
+  uint4 v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const uint4*>(b + 4 * (j ^ r));
+  auto cswap = [](bool p, uint4& a, uint4& d) {
+    const uint4 a0 = a, d0 = d;
+    a = make_uint4(p ? d0.x : a0.x, p ? d0.y : a0.y, p ? d0.z : a0.z, p ? d0.w : a0.w);
+    d = make_uint4(p ? a0.x : d0.x, p ? a0.y : d0.y, p ? a0.z : d0.z, p ? a0.w : d0.w);
+  };
+  cswap(r & 1, v[0], v[1]);
+  cswap(r & 1, v[2], v[3]);
+  cswap(r & 2, v[0], v[2]);
+  cswap(r & 2, v[1], v[3]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    x[4 * k] = (int32_t)v[k].x;
+    x[4 * k + 1] = (int32_t)v[k].y;
+    x[4 * k + 2] = (int32_t)v[k].z;
+    x[4 * k + 3] = (int32_t)v[k].w;
   }
 }
 
@@ -642,7 +674,7 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_filter_b(const T* __r
 // zs = sgmSum flags vs over n elements; flag of element i = bit (flag_base + i)
 // of `bits` (mkFlags' bitmap over output positions).  Z: zs storage.
 template <typename T, typename Z>
-__global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_segsum_b(const T* __restrict__ vs, long long n,
+__global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T* __restrict__ vs, long long n,
                                                           const long long* __restrict__ d_n,
                                                           const uint32_t* __restrict__ bits, long long flag_base,
                                                           Z* __restrict__ zs, LBChan ch, uint32_t nonce,
@@ -654,6 +686,7 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_segsum_b(const T* __r
   __shared__ SegOp::T s_w[B::CH][kBW];
   __shared__ SegOp::T s_agg;
   __shared__ SegOp::T s_carry;
+  __shared__ __align__(8) uint64_t s_mbar[B::CH];
 
   if (d_n) n = *d_n;  // length known only on the device (C2: k = filter's count)
   const long long ntiles = (n + B::TILE - 1) / B::TILE;
@@ -673,7 +706,24 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_segsum_b(const T* __r
     }
     return;
   }
-  big_issue<T>(buf, vs, n, tile_base, t);
+  // int32 full tiles: one TMA bulk copy per chunk into a linear buffer
+  // (read back with lin_read_xor); otherwise swizzled per-lane cp.async
+  const bool tma = sizeof(T) == 4 && tile_base + B::TILE <= n;
+  if (tma) {
+    if (t == 0) {
+#pragma unroll
+      for (int c = 0; c < B::CH; ++c) mbar_init(&s_mbar[c], 1);
+      mbar_fence_init();
+#pragma unroll
+      for (int c = 0; c < B::CH; ++c) {
+        mbar_expect_tx(&s_mbar[c], kBChunk * (uint32_t)sizeof(T));
+        bulk_g2s(buf + B::PAD + c * kBChunk, vs + tile_base + c * kBChunk, kBChunk * (uint32_t)sizeof(T), &s_mbar[c]);
+      }
+    }
+    bar_sync(1, kBT);  // the mbarriers are initialised
+  } else {
+    big_issue<T>(buf, vs, n, tile_base, t);
+  }
   // the thread's 16 flag bits per chunk (positions are known up front)
   uint32_t fl[B::CH];
 #pragma unroll
@@ -685,12 +735,21 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_segsum_b(const T* __r
     if (g < n) f = (uint32_t)((((uint64_t)__ldg(&bits[wd + 1]) << 32) | (uint64_t)__ldg(&bits[wd])) >> (pos & 31));
     fl[c] = f & valid_mask(g, n);
   }
-  cp_async_wait_all();
+  if (!tma) cp_async_wait_all();
   SegOp::T a[B::CH];
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     T x[kSItems];
-    big_read<T>(buf, c, t, x);
+    if constexpr (sizeof(T) == 4) {
+      if (tma) {
+        mbar_wait(&s_mbar[c], 0);
+        lin_read_xor(reinterpret_cast<const int32_t*>(buf), c, t, reinterpret_cast<int32_t(&)[kSItems]>(x));
+      } else {
+        big_read<T>(buf, c, t, x);
+      }
+    } else {
+      big_read<T>(buf, c, t, x);
+    }
     const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
     const uint32_t vm = valid_mask(g, n);
     const uint32_t tail = fl[c] ? (vm & ~((1u << (31 - __clz(fl[c]))) - 1u)) : vm;
@@ -730,7 +789,12 @@ __global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_segsum_b(const T* __r
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     T x[kSItems];
-    big_read<T>(buf, c, t, x);
+    if constexpr (sizeof(T) == 4) {
+      if (tma) lin_read_xor(reinterpret_cast<const int32_t*>(buf), c, t, reinterpret_cast<int32_t(&)[kSItems]>(x));
+      else big_read<T>(buf, c, t, x);
+    } else {
+      big_read<T>(buf, c, t, x);
+    }
     const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
     long long run = SegOp::op(carry, chunk_pre[c]).v;
     Z z[kSItems];

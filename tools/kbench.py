@@ -72,6 +72,11 @@ def main():
     f = lambda: ops.filter(xs, p, 0, st, ys=ys, d_count=dk)  # noqa: E731
     kms = ktime(L.K_FILTER_FUSED, f)
     out["filter_kernel"] = {"ms": kms, "algoGBps": (4 * n + 4 * k) / kms / 1e6}
+    # the sharded / split C2's sgmSum pass over the filtered ys (k elements)
+    bits = ops.flag_bitmap(shape, k)
+    tot = torch.empty(2, dtype=torch.int64, device=dev)
+    kms = ktime(L.K_SEGSUM, lambda: ops.segsum(ys, k, bits, 0, zs, 0, False, tot, st))
+    out["segsum_kernel"] = {"ms": kms, "algoGBps": 8 * k / kms / 1e6}
 
     xs2 = ops.gen_uniform(n, -(1 << 31), (1 << 31) - 1, 1, torch.int32, device=dev)
     dnt = torch.empty(1, dtype=torch.int64, device=dev)
