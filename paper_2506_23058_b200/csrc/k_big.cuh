@@ -41,6 +41,15 @@ constexpr int kBW = IXG_BW;             // worker warps
 constexpr int kBT = kBW * 32;           // worker threads
 constexpr int kBChunk = kBT * kSItems;  // elements per chunk
 constexpr int kBMinBlocks = kBW >= 16 ? 2 : 4;  // resident CTAs per SM the registers must allow
+#ifndef IXG_CH64
+#define IXG_CH64 2  // chunks per int64 tile (64 KB, 3 CTAs/SM): filter i64 0.347 -> 0.290 ms at 2^27
+#endif
+// resident CTAs per SM of a big-tile kernel over T (shared memory: 4 x 48 KB
+// for int32; int64 tiles of IXG_CH64 x 32 KB)
+template <typename T>
+constexpr int big_min_blocks() {
+  return sizeof(T) == 4 ? kBMinBlocks : (IXG_CH64 == 1 ? kBMinBlocks : 3);
+}
 #ifndef IXG_SEGSUM_MINB
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
 #endif
@@ -49,7 +58,7 @@ template <typename T>
 struct Big {
   static constexpr int P = (int)sizeof(T);           // 16-byte pieces per thread block (16 elements)
   static constexpr int EP = 16 / (int)sizeof(T);     // elements per piece
-  static constexpr int CH = sizeof(T) == 4 ? 3 : 1;  // chunks per tile (96 KB / 64 KB)
+  static constexpr int CH = sizeof(T) == 4 ? 3 : IXG_CH64;  // chunks per tile (48 KB int32 / 32-64 KB int64)
   static constexpr int PAD = 32 / (int)sizeof(T);    // >= the 32-byte store phase
   static constexpr int TILE = CH * kBChunk;
   static constexpr int SMEM = (PAD + TILE) * (int)sizeof(T);
@@ -416,7 +425,7 @@ IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) 
 // a single pass writing each element once (d_count[s] = the prefix at the
 // end of segment s, for s < NS - 1).
 template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false>
-__global__ void __launch_bounds__(kBT + 32, kBMinBlocks) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
+__global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
                                                           long long n, ixg_pred p, T* __restrict__ ys, LBChan ch,
                                                           uint32_t nonce, long long* d_count,
                                                           Z* __restrict__ zs = nullptr,

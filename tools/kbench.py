@@ -95,6 +95,17 @@ def main():
         ms = timeit(f, reps=10)
         out[f"partition3_{name}"] = {"ms": ms, "Gelem/s": n / ms / 1e6, "algoGBps": 8 * n / ms / 1e6}
 
+    # the drop-in path's element type: int64 (the language's i64), 2^27 elements = 1 GiB
+    n64 = n // 2
+    x64s = ops.gen_uniform(n64, -128, 127, 0, torch.int64, device=dev)
+    y64 = torch.empty(n64, dtype=torch.int64, device=dev)
+    kms = ktime(L.K_FILTER_FUSED, lambda: ops.filter(x64s, p, 0, st, ys=y64, d_count=dk))
+    k64 = int(dk.item())
+    out["filter_i64_kernel"] = {"ms": kms, "algoGBps": (8 * n64 + 8 * k64) / kms / 1e6}
+    kms = ktime(L.K_PLACE, lambda: ops.partition2(x64s, Pred.lt(0), 0, st, ys=y64, d_nt=dnt))
+    out["partition2_i64_kernel"] = {"ms": kms, "algoGBps": 16 * n64 / kms / 1e6}
+    del x64s, y64
+
     # library reference points (CUB via torch): stream compaction and scan
     mask = xs >= 0
     out["torch_masked_select"] = {"ms": timeit(lambda: torch.masked_select(xs, mask), reps=5)}
