@@ -41,6 +41,9 @@ constexpr int kBW = IXG_BW;             // worker warps
 constexpr int kBT = kBW * 32;           // worker threads
 constexpr int kBChunk = kBT * kSItems;  // elements per chunk
 constexpr int kBMinBlocks = kBW >= 16 ? 2 : 4;  // resident CTAs per SM the registers must allow
+#ifndef IXG_CH32
+#define IXG_CH32 3  // chunks per int32 tile (48 KB, 4 CTAs/SM)
+#endif
 #ifndef IXG_CH64
 #define IXG_CH64 2  // chunks per int64 tile (64 KB, 3 CTAs/SM): filter i64 0.347 -> 0.290 ms at 2^27
 #endif
@@ -48,7 +51,7 @@ constexpr int kBMinBlocks = kBW >= 16 ? 2 : 4;  // resident CTAs per SM the regi
 // for int32; int64 tiles of IXG_CH64 x 32 KB)
 template <typename T>
 constexpr int big_min_blocks() {
-  return sizeof(T) == 4 ? kBMinBlocks : (IXG_CH64 == 1 ? kBMinBlocks : 3);
+  return sizeof(T) == 4 ? (IXG_CH32 <= 3 ? kBMinBlocks : 3) : (IXG_CH64 == 1 ? kBMinBlocks : 3);
 }
 #ifndef IXG_SEGSUM_MINB
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
@@ -58,7 +61,7 @@ template <typename T>
 struct Big {
   static constexpr int P = (int)sizeof(T);           // 16-byte pieces per thread block (16 elements)
   static constexpr int EP = 16 / (int)sizeof(T);     // elements per piece
-  static constexpr int CH = sizeof(T) == 4 ? 3 : IXG_CH64;  // chunks per tile (48 KB int32 / 32-64 KB int64)
+  static constexpr int CH = sizeof(T) == 4 ? IXG_CH32 : IXG_CH64;  // chunks per tile
   static constexpr int PAD = 32 / (int)sizeof(T);    // >= the 32-byte store phase
   static constexpr int TILE = CH * kBChunk;
   static constexpr int SMEM = (PAD + TILE) * (int)sizeof(T);
@@ -407,7 +410,13 @@ IXG_DEV SegOp::T cta_seg_exclusive(SegOp::T a, SegOp::T* s_seg, SegOp::T* total)
   return SegOp::op(pre, lex);
 }
 
-IXG_DEV int field21(unsigned long long v, int c) { return (int)((v >> (21 * c)) & 0x1fffffull); }
+// per-chunk counts packed into 64 bits: CH fields of 64 / CH bits (a chunk's
+// CTA total is <= kBChunk = 4096 < 2^16)
+template <int CH>
+IXG_DEV int fieldc(unsigned long long v, int c) {
+  constexpr int W = 64 / CH;
+  return (int)((v >> (W * c)) & (W >= 64 ? ~0ull : ((1ull << W) - 1ull)));
+}
 
 // ---------------------------------------------------------------------------
 // kSeg (C2, Z the width of zs == sizeof(T)): after ys is stored, the
@@ -537,7 +546,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     }
     wt[c] = __shfl_sync(0xffffffffu, inc, 31);
     ex[c] = inc - v;
-    packed |= (unsigned long long)Q::field_sum(wt[c]) << (21 * c);
+    packed |= (unsigned long long)Q::field_sum(wt[c]) << ((64 / B::CH) * c);
   }
   unsigned long long tot;
   const unsigned long long exw = cta_warp_exclusive3(packed, s_w, &tot);
@@ -545,8 +554,8 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   int cnt = 0, before[B::CH];
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
-    before[c] = cnt + field21(exw, c);
-    cnt += field21(tot, c);
+    before[c] = cnt + fieldc<B::CH>(exw, c);
+    cnt += fieldc<B::CH>(tot, c);
   }
   if (t == 0) {
     s_cnt = cnt;
