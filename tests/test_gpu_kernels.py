@@ -393,3 +393,34 @@ def test_workspace_reuse(cuda):
         gys, dnt = ops.partition2(_t(xs, cuda), Pred.lt(0), L.VARIANT_ELIDED, st)
         nt, ys = O.partition2(Pred.lt(0), xs)
         assert int(dnt.item()) == nt and np.array_equal(_np(gys).astype(np.int64), ys)
+
+
+@pytest.mark.parametrize("pred", [Pred(7), Pred(8), Pred.ge(120)])  # all, none, ~3 %
+@pytest.mark.parametrize("seg", ["one", "unit", "sparse"])
+def test_c2_extremes(cuda, pred, seg):
+    """C2 at 2^22 with the selectivity and flag density at their extremes:
+    every element kept / none / few; one segment, every output its own
+    segment (all flags set), or a few long segments."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    n = 1 << 22
+    xs = gen.uniform(71, n, -128, 127, np.int32)
+    k = len(O.filter_(pred, xs))
+    if seg == "one":
+        shape = np.array([k], np.int64)
+    elif seg == "unit":
+        shape = np.ones(k, np.int64)
+    else:
+        shape = gen.segment_shape(5, 3, k)
+    want_ys, want_zs = O.c2(pred, xs, shape)
+    for zt in (torch.int32, torch.int64):
+        st = ops.Status(cuda)
+        ys, zs, dk = ops.c2(_t(xs, cuda), pred, _t(shape, cuda), L.VARIANT_ELIDED, st, z_dtype=zt)
+        kk = int(dk.item())
+        assert kk == k
+        assert np.array_equal(_np(ys)[:kk].astype(np.int64), want_ys)
+        assert np.array_equal(_np(zs)[:kk].astype(np.int64), want_zs)
+        s = st.read()
+        assert s.ok and not s.narrow
