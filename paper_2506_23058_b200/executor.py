@@ -312,7 +312,7 @@ class Interp:
         raise NotImplementedError(f"{k} outside a registered pipeline: {ir.expr_str(e)}")
 
     def _app(self, e, env, f, fs):
-        from . import vm
+        from . import jit, vm
 
         name = e.fun.name if ir.kind(e.fun) == "VarE" else None
         ev = lambda x: self._eval(x, env, f, fs)  # noqa: E731
@@ -327,12 +327,21 @@ class Interp:
                 cenv = {"%p": ("pred", ev(e.args[0]))}
             else:
                 cenv = self._captured(env)
-            comp = vm.compile_map(lam, arrs, cenv, lambda node: self._bits(fs, node))
             st = ops.Status(self.dev)
-            out = ops.map_vm(comp, n, st, device=self.dev)
+            bits = lambda node: self._bits(fs, node)  # noqa: E731
+            out = None
+            if jit.enabled():  # the lambda compiled to its own kernel (NVRTC, cached)
+                try:
+                    out, sites = jit.map_jit(lam, arrs, cenv, bits, n, st, device=self.dev)
+                except vm.Unsupported:
+                    out = None
+            if out is None:  # the register VM
+                comp = vm.compile_map(lam, arrs, cenv, bits)
+                out = ops.map_vm(comp, n, st, device=self.dev)
+                sites = comp.sites
             s = st.read()
             if not s.ok:
-                node = comp.sites[s.site]
+                node = sites[s.site]
                 raise errors.OutOfBounds(ir.expr_str(node), node.pos)
             return out.to(torch.bool) if _is_bool_expr(lam.body) else out
         if name == "scan":

@@ -11,6 +11,7 @@ import pytest
 from paper_2506_23058_b200 import _lib as L
 from paper_2506_23058_b200 import ir, vm
 from paper_2506_23058_b200 import select as sel
+from paper_2506_23058_b200.pred import Pred
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROGRAMS = json.load(open(os.path.join(ROOT, "paper_2506_23058_b200", "data", "programs.json")))
@@ -162,3 +163,51 @@ def test_errors_mirror():
     e = errors.OutOfBounds("xs[i]", (3, 4))
     assert str(e) == "out of bounds: xs[i]" and e.site == "xs[i]" and e.pos == (3, 4)
     assert isinstance(errors.NonIdempotentScatter((1, 2)), errors.OracleError)
+
+
+def test_jit_generates_and_compiles_corpus_lambdas():
+    """Every map lambda of the corpus becomes a CUDA kernel that NVRTC
+    compiles for sm_100a (no GPU needed to compile)."""
+    import torch
+
+    from paper_2506_23058_b200 import jit
+
+    nvrtc = pytest.importorskip("cuda.bindings.nvrtc")
+    seen = set()
+    for key, d in PROGRAMS.items():
+        prog = ir.from_json(d["program"])
+        for f in prog.defs:
+            lets = set()
+
+            def collect(e):
+                if ir.kind(e) == "Let":
+                    lets.update(e.names)
+                for c in ir.children(e):
+                    collect(c)
+            collect(f.body)
+
+            def walk(e):
+                if ir.kind(e) == "App" and ir.kind(e.fun) == "VarE" and e.fun.name == "map" and ir.kind(e.args[0]) == "Lambda":
+                    lam = e.args[0]
+                    env = {}
+                    for p in f.params:
+                        env[p.name] = ("pred", Pred.lt(3)) if ir.kind(p.type) == "TFun" else ("array", torch.zeros(4, dtype=torch.int64))
+                    env.update({s: ("scalar", 3) for s in f.sizes})
+                    for nm in ("num_true", "m1", "m2", "count", "len"):
+                        env.setdefault(nm, ("scalar", 1))
+                    for nm in ("H", "shape", "x"):
+                        env.setdefault(nm, ("array", torch.zeros(4, dtype=torch.int64)))
+                    for nm in lets:
+                        env.setdefault(nm, ("array", torch.zeros(4, dtype=torch.int64)))
+                    arrs = [torch.zeros(4, dtype=torch.int64) for _ in lam.params]
+                    src, spec = jit.generate(lam, arrs, env)
+                    if src not in seen:
+                        seen.add(src)
+                        err, prog_ = nvrtc.nvrtcCreateProgram(src.encode(), b"m.cu", 0, [], [])
+                        opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device"]
+                        (err,) = nvrtc.nvrtcCompileProgram(prog_, len(opts), opts)
+                        assert int(err) == 0, src
+                for c in ir.children(e):
+                    walk(c)
+            walk(f.body)
+    assert len(seen) >= 15
