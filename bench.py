@@ -111,8 +111,16 @@ def dist_init():
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # IXG_DIST_BACKEND=gloo: a functional check of the multi-rank path
+        # with fewer GPUs than ranks (ranks share devices round-robin; no
+        # kernel waits on another rank, only host collectives)
+        backend = os.environ.get("IXG_DIST_BACKEND", "nccl")
+        dev = local % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return rank, ws, local
@@ -124,7 +132,7 @@ def max_over_ranks(x: float, ws: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
