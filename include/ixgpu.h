@@ -139,6 +139,15 @@ unsigned long long ixg_launch_count(void);
 int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, int64_t* out,
                  void* ws, size_t ws_bytes, void* stream);
 
+/* partition2L's scatter destinations (corpus/partition2l.ixl:41, PAPER.md:
+ * 3250-3261) for a jagged array with sum shp == n: bits = row starts (the
+ * mkFlags bitmap of shp over n positions, ixg_flag_bitmap), cs = the
+ * per-element predicate (u8), tb = the per-row inclusive count of cs
+ * (ixg_segsum of cs).  dest[i] = row start + trues before i in its row for
+ * a true element, i + trues after i in its row for a false one. */
+int ixg_jagged_dest(const uint32_t* bits, int64_t n, const uint8_t* cs, const int64_t* tb, int64_t* dest,
+                    void* stream);
+
 /* total of `scan (+) 0 xs` -- the last element of oracle.py:281-293's inclusive
  * scan -- written to *out (device int64).  The sharded scan (dist.py) needs it
  * before the seeded local scan; dt in {I32, I64, U8}. */

@@ -66,6 +66,7 @@ SIGNATURES = {
     "ixg_launch_count": (ctypes.c_ulonglong, []),
     "ixg_scan_add": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _SZ, _P]),
     "ixg_reduce_add": (_I, [_I, _P, _I64, _P, _P]),
+    "ixg_jagged_dest": (_I, [_P, _I64, _P, _P, _P, _P]),
     "ixg_partition_counts": (_I, [_I, _P, _I64, _P, _P, _I, _P, _P, _SZ, _P]),
     "ixg_partition2_peer": (_I, [_I, _P, _I64, _P, _P, _I, _I64, _I64, _I64, _I64, _P, _SZ, _P]),
     "ixg_dev_alloc": (_I, [_SZ, _P]),

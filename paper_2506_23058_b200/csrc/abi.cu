@@ -506,6 +506,16 @@ int ixg_reduce_add(int dt, const void* xs, int64_t n, int64_t* out, void* stream
   return IXG_OK;
 }
 
+int ixg_jagged_dest(const uint32_t* bits, int64_t n, const uint8_t* cs, const int64_t* tb, int64_t* dest,
+                    void* stream) {
+  if (n < 0 || (n > 0 && (!bits || !cs || !tb || !dest))) return IXG_BADARG;
+  if (n == 0) return IXG_OK;
+  k_jagged_dest<<<grid_for(n), kGThreads, 0, S(stream)>>>(bits, n, cs, (const long long*)tb, (long long*)dest);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
 int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64_t n, int f0, int64_t v0,
                     int64_t* out_v, uint8_t* out_f, void* ws, size_t ws_bytes, void* stream) {
   if (n < 0 || (n > 0 && (!flags || !xs || !out_v))) return IXG_BADARG;

@@ -392,6 +392,38 @@ __global__ void __launch_bounds__(kGThreads) k_reduce_add(const E* __restrict__ 
   if (lane_id() == 0 && s != 0) atomicAdd(out, (unsigned long long)s);
 }
 
+// ---------------------------------------------------------------- jagged
+// partition2L's destinations (corpus/partition2l.ixl:41) for a jagged array
+// whose row starts are the set bits of `bits` (mkFlags over n positions,
+// sum shp == n): tb = the segmented inclusive count of cs per row.  A true
+// element goes to its row start + the trues before it in its row, a false
+// one to its own index + the trues after it in its row.
+// Row start / end come from the nearest set bits (rows average tens of
+// elements: a word or two of the bitmap).
+__global__ void __launch_bounds__(kGThreads) k_jagged_dest(const uint32_t* __restrict__ bits, long long n,
+                                                           const uint8_t* __restrict__ cs,
+                                                           const long long* __restrict__ tb,
+                                                           long long* __restrict__ dest) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    long long w = i >> 5;
+    uint32_t m = bits[w] & (0xffffffffu >> (31 - (int)(i & 31)));  // starts <= i
+    while (m == 0) m = bits[--w];  // position 0 starts the first non-empty row
+    const long long rs = (w << 5) + (31 - __clz(m));
+    long long re = n;  // one past the row's last element: the next start, or n
+    const long long j = i + 1;
+    if (j < n) {
+      long long w2 = j >> 5;
+      uint32_t m2 = bits[w2] & (0xffffffffu << (int)(j & 31));
+      while (m2 == 0 && ((w2 + 1) << 5) < n) m2 = bits[++w2];
+      if (m2) re = (w2 << 5) + (__ffs(m2) - 1);
+      if (re > n) re = n;
+    }
+    const long long t = tb[i];
+    dest[i] = cs[i] ? rs + t - 1 : i + (tb[re - 1] - t);
+  }
+}
+
 // ---------------------------------------------------------------- hist
 __global__ void __launch_bounds__(kGThreads) k_hist(int op, long long dlen, const long long* __restrict__ is,
                                                      const long long* __restrict__ vs, long long m,

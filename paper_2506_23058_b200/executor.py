@@ -66,6 +66,7 @@ _PIPELINES = {
     "csrg": ("csrg", ()),
     "csrg_any": ("csrg", ()),
     "kmeans_ker": ("kmeans", ()),
+    "partition2L": ("partition2l", ("mkII", "mkSgmDescr", "sgmSum")),
 }
 
 
@@ -88,6 +89,20 @@ def registry() -> dict:
                 reg.setdefault(fp, Entry(pipe, {c: funs[c] for c in callees}))
         _REGISTRY = reg
     return _REGISTRY
+
+
+# `\c -> if c then 1 else 0` (partition2l.ixl:38), compiled by jit_map
+_ONE_IF_TRUE = ir.Lambda(("c",), ir.If(ir.VarE("c"), ir.Const(1), ir.Const(0)), (0, 0))
+
+
+def jit_map(lam, arrs, env, bits, n, st, device=None):
+    """a map through the NVRTC kernel, or the register VM when IXG_JIT=0"""
+    from . import jit, vm
+
+    if jit.enabled():
+        return jit.map_jit(lam, arrs, env, bits, n, st, device=device)
+    comp = vm.compile_map(lam, arrs, env, bits)
+    return ops.map_vm(comp, n, st, device=device), comp.sites
 
 
 # ----------------------------------------------------------------- marshal
@@ -440,6 +455,41 @@ class Interp:
         k = int(dk.item())
         self._raise(st, f)
         return self._out(ys, k)
+
+    def _p_partition2l(self, f, a):
+        """corpus/partition2l.ixl as one GPU pipeline: row-start bitmap (the
+        mkFlags bitmap of shp), the per-row inclusive count of csL (sgmSum),
+        the destinations of :41 (k_jagged_dest) and the scatter of :42 --
+        CHECKED, as the verifier proves nothing here (mkSgmDescr is
+        unanalyzable).  Its preconditions shp >= 0 and sum shp == n are
+        checked first; inputs outside them take the generic executor, which
+        raises exactly what the program as written raises."""
+        shp, cs, xs = _dev_i64(a[0], self.dev), _dev_u8(a[1], self.dev), _dev_i64(a[2], self.dev)
+        n, m = cs.numel(), shp.numel()
+        ok = xs.numel() == n
+        if ok and m:
+            neg = int(ops.partition_counts(shp, Pred.lt(0)).item())
+            ok = neg == 0 and int(ops.reduce_add(shp).item()) == n
+        elif ok:
+            ok = n == 0
+        if not ok:
+            return self._generic(f, a)
+        if n == 0:
+            return self._out(torch.empty(0, dtype=torch.int64, device=self.dev))
+        st = ops.Status(self.dev)
+        bits = ops.flag_bitmap(shp, n)                                               # :36-37 row starts
+        fs, _ = jit_map(_ONE_IF_TRUE, [cs], {}, lambda node: 0, n, st, device=self.dev)  # :38
+        tb = torch.empty(n, dtype=torch.int64, device=self.dev)
+        tot = torch.empty(2, dtype=torch.int64, device=self.dev)
+        ops.segsum(fs, n, bits, 0, tb, 0, False, tot, st)                            # :39
+        dest = ops.jagged_dest(bits, cs, tb)                                         # :40-41
+        out = torch.zeros(n, dtype=torch.int64, device=self.dev)                     # :42 replicate n 0
+        sb = self._sel(f).sites[-1].bits                                             # the scatter site
+        ops.scatter(out, dest, xs, sb, st, stmt=0, site=len(self._sel(f).sites) - 1)
+        s = st.read()
+        if not s.ok:  # cannot happen under the checked preconditions; keep the reference's answer
+            return self._generic(f, a)
+        return self._out(out)
 
     def _p_partition2(self, f, a):
         p, xs = _pred(a[0]), _dev_i64(a[1], self.dev)

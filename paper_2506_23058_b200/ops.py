@@ -154,6 +154,15 @@ def reduce_add(xs: torch.Tensor, out=None) -> torch.Tensor:
     return out
 
 
+def jagged_dest(bits: torch.Tensor, cs: torch.Tensor, tb: torch.Tensor, out=None) -> torch.Tensor:
+    """partition2L's scatter destinations (ixg_jagged_dest)."""
+    cs, tb = _contig(cs), _contig(tb)
+    n = cs.numel()
+    out = torch.empty(n, dtype=torch.int64, device=cs.device) if out is None else out
+    L.check(_lib().ixg_jagged_dest(_ptr(bits), n, _ptr(cs), _ptr(tb), _ptr(out), _stream()), "jagged_dest")
+    return out
+
+
 def segscan_add(flags: torch.Tensor, xs: torch.Tensor, want_flags: bool = False):
     """sgmSum's 2-ary scan; returns values (and flags)."""
     flags, xs = _contig(flags), _contig(xs)
