@@ -72,3 +72,24 @@ def test_opaque_callable_rejected(cuda):
     prog = program("ref:filter.ixl")
     with pytest.raises(TypeError):
         eval_program(prog, "filter", [lambda x: x < 3, [1, 2, 5]])
+
+
+@pytest.mark.parametrize("m", [1, 1000, 40_000])
+def test_partition2l_pipeline_large(cuda, m):
+    """partition2L's registered pipeline at up to ~1.2M elements against the
+    C restatement (oracle/ixoracle.c ixo_partition2l)."""
+    import numpy as np
+
+    from oracle import ixoracle as O
+    from paper_2506_23058_b200 import gen
+    from paper_2506_23058_b200.executor import eval_program
+
+    prog = ir.from_json(PROGRAMS["own:partition2l.ixl"]["program"])
+    shp = gen.uniform(m, m, 0, 60, np.int64)
+    shp[::5] = 0
+    n = int(shp.sum())
+    cs = gen.uniform(m + 1, n, 0, 2, np.int64) == 0
+    xs = gen.uniform(m + 2, n, -1000, 1000, np.int64)
+    want = O.partition2l(shp, cs.astype(np.int64), xs)
+    got = eval_program(prog, "partition2L", [shp.tolist(), cs.tolist(), xs.tolist()], as_tensors=True)
+    assert np.array_equal(got.cpu().numpy(), want)
