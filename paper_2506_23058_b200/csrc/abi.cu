@@ -483,6 +483,16 @@ int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, i
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, n, 0)) return IXG_BADARG;
   WS w(ws);
   LBChan c = w.chan(0, tiles_of(n, kGTile));
+  // inclusive scans of int32 / int64: the big-tile sgmSum kernel without
+  // flags (TMA-loaded 48 KB int32 tiles, one look-back per tile), `ne` as the
+  // carry into the first tile; exclusive / u8 keep the generic k_scan
+  if (!exclusive && n > 0 && (dt == IXG_I32 || dt == IXG_I64) && aligned16(xs) && aligned16(out)) {
+    if (dt == IXG_I32)
+      return launch_segsum_b<int32_t, long long>((const int32_t*)xs, n, nullptr, nullptr, 0, (long long*)out, c, ne,
+                                                 0, nullptr, nullptr, S(stream));
+    return launch_segsum_b<long long, long long>((const long long*)xs, n, nullptr, nullptr, 0, (long long*)out, c, ne,
+                                                 0, nullptr, nullptr, S(stream));
+  }
   const EpiScanOut epi{ne, exclusive, (long long*)out};
   if (dt == IXG_I32) return launch_scan<SumOp>(n, SrcArrT<int32_t>{(const int32_t*)xs}, epi, c, S(stream));
   if (dt == IXG_U8) return launch_scan<SumOp>(n, SrcArrT<uint8_t>{(const uint8_t*)xs}, epi, c, S(stream));

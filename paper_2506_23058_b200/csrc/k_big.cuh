@@ -750,7 +750,8 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     const long long pos = flag_base + g;
     const long long wd = pos >> 5;
     uint32_t f = 0;
-    if (g < n) f = (uint32_t)((((uint64_t)__ldg(&bits[wd + 1]) << 32) | (uint64_t)__ldg(&bits[wd])) >> (pos & 31));
+    if (g < n && bits)  // bits == nullptr: no flags -- a plain inclusive scan (ixg_scan_add)
+      f = (uint32_t)((((uint64_t)__ldg(&bits[wd + 1]) << 32) | (uint64_t)__ldg(&bits[wd])) >> (pos & 31));
     fl[c] = f & valid_mask(g, n);
   }
   if (!tma) cp_async_wait_all();

@@ -110,6 +110,10 @@ def main():
     mask = xs >= 0
     out["torch_masked_select"] = {"ms": timeit(lambda: torch.masked_select(xs, mask), reps=5)}
     out["torch_cumsum_i32"] = {"ms": timeit(lambda: torch.cumsum(xs, 0, dtype=torch.int64), reps=5)}
+    so32 = torch.empty(n, dtype=torch.int64, device=dev)
+    ms = timeit(lambda: ops.scan_add(xs, 0, out=so32))
+    out["scan_i32"] = {"ms": ms, "GBps": 12 * n / ms / 1e6}
+    del so32
     x64 = xs.to(torch.int64)
     so = torch.empty(n, dtype=torch.int64, device=dev)
     ms = timeit(lambda: ops.scan_add(x64, 0, out=so))
