@@ -285,3 +285,68 @@ def filter_seg(shp, cs, xs):
     _ok(lib().ixo_filter_seg(_p(shp), ctypes.c_int64(len(shp)), _p(cs), _p(xs), ctypes.c_int64(len(xs)), _p(newshp),
                              _p(ys), ctypes.byref(cnt)))
     return newshp, ys[: cnt.value].copy()
+
+
+# ---------------------------------------------------------------------------
+# corpus/scanops.ixl: scan / hist with other operators.  Pure-Python loops
+# (small cases only) restating the reference's folds: scan seeds the
+# accumulators with the neutrals once and folds left to right
+# (oracle.py:281-293); hist fills [ne] * dlen and applies the operator to each
+# in-bounds bin in index order (oracle.py:306-316).
+def fold_scan(op, nes, arrs):
+    k = len(nes)
+    acc = list(nes)
+    n = len(arrs[0])
+    outs = [[] for _ in range(k)]
+    for i in range(n):
+        r = op(*acc, *[a[i] for a in arrs])
+        acc = list(r) if k > 1 else [r]
+        for j in range(k):
+            outs[j].append(acc[j])
+    return tuple(outs) if k > 1 else outs[0]
+
+
+def fold_hist(op, ne, dlen, is_, vs):
+    dst = [ne] * dlen
+    for i, v in zip(is_, vs):
+        if 0 <= i < dlen:
+            dst[i] = op(dst[i], v)
+    return dst
+
+
+def _lookup(tbl):
+    def op(a, b):
+        if not 0 <= b < len(tbl):
+            raise OracleFail(OOB, site=0)
+        return a + tbl[b]
+    return op
+
+
+def scanops(fun, a):
+    """One corpus/scanops.ixl function on Python lists."""
+    if fun == "scan_min":
+        return fold_scan(lambda x, y: x if x < y else y, [7], [a[0]])
+    if fun == "scan_max":
+        return fold_scan(lambda x, y: x if y <= x else y, [-1], [a[0]])
+    if fun == "scan_mul":
+        return fold_scan(lambda x, y: x * y, [1], [a[0]])
+    if fun == "scan_and":
+        return fold_scan(lambda x, y: bool(x) and bool(y), [True], [a[0]])
+    if fun == "scan_pair":
+        return fold_scan(lambda a1, a2, b1, b2: (a1 + b1, a2 if a2 > b2 else b2), [3, -100], [a[0], a[1]])
+    if fun == "scan_segmax":
+        return fold_scan(lambda f1, v1, f2, v2: (bool(f1) or bool(f2), v2 if f2 else (v2 if v1 < v2 else v1)),
+                         [False, -50], [a[0], a[1]])[1]
+    if fun == "scan_clip":
+        return fold_scan(lambda x, y: y if x > 20 else x + y, [0], [a[0]])
+    if fun == "scan_lookup":
+        return fold_scan(_lookup(a[0]), [0], [a[1]])
+    if fun == "hist_mul":
+        return fold_hist(lambda x, y: x * y, 1, a[0], a[1], a[2])
+    if fun == "hist_lmin":
+        return fold_hist(lambda x, y: y if y < x else x, 9, a[0], a[1], a[2])
+    if fun == "hist_last":
+        return fold_hist(lambda x, y: y, 0, a[0], a[1], a[2])
+    if fun == "hist_horner":
+        return fold_hist(lambda x, y: x * 3 + y, 0, a[0], a[1], a[2])
+    raise KeyError(fun)

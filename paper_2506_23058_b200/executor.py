@@ -32,7 +32,7 @@ from typing import Callable, Optional
 import torch
 
 from . import _lib as L
-from . import errors, ir, ops
+from . import errors, ir, jit_fold, ops
 from . import select as sel
 from .pred import Pred
 
@@ -372,7 +372,7 @@ class Interp:
                     raise errors.OracleError("scan: value array shorter than flags")
                 v, fl = ops.segscan_add(arrs[0].to(torch.uint8), arrs[1][:n], want_flags=True)
                 return (fl.to(torch.bool), v)
-            raise NotImplementedError(f"scan operator {ir.expr_str(op) if ir.kind(op) == 'Lambda' else op}")
+            return self._scan_generic(e, op, nes, arrs, env, fs)
         if name == "scatter":
             dst, is_, vs = ev(e.args[0]), ev(e.args[1]), ev(e.args[2])
             bits = self._bits(fs, e)
@@ -388,9 +388,17 @@ class Interp:
             op, ne, dlen, is_, vs = (ev(a) for a in e.args)
             code = {"i64.min": L.HIST_MIN, "i64.max": L.HIST_MAX}.get(op) if isinstance(op, str) else (
                 L.HIST_ADD if _is_add(op) else None)
-            if code is None:
-                raise NotImplementedError("hist operator")
-            return ops.hist(code, int(ne), int(dlen), is_, vs)
+            if code is None and ir.kind(op) == "Lambda" and vs.dtype != torch.bool:
+                code = {"add": L.HIST_ADD, "min": L.HIST_MIN, "max": L.HIST_MAX}.get(jit_fold.classify_hist(op))
+            if code is not None:
+                return ops.hist(code, int(ne), int(dlen), is_, vs.to(torch.int64))
+            if ir.kind(op) != "Lambda":
+                raise NotImplementedError(f"hist operator {op}")
+            st = ops.Status(self.dev)
+            dst, sites, _ = jit_fold.hist(op, int(ne), int(dlen), is_, vs, self._captured(env),
+                                          lambda node: self._bits(fs, node), st)
+            self._raise_site(st, sites)
+            return dst.to(torch.bool) if _is_bool_expr(op.body) else dst
         if name == "iota":
             return ops.iota(int(ev(e.args[0])), self.dev)
         if name == "replicate":
@@ -411,6 +419,32 @@ class Interp:
         if isinstance(fn, Pred):
             return fn(*[ev(a) for a in e.args])
         raise NotImplementedError(f"application {ir.expr_str(e)}")
+
+    def _scan_generic(self, e, op, nes, arrs, env, fs):
+        """scan with any other operator (oracle.py:281-293): the tiled
+        parallel scan when the operator is recognisably associative, else
+        the in-order fold on the device (jit_fold.py)."""
+        if isinstance(op, str) and op in ("i64.min", "i64.max"):
+            op = ir.Lambda(("a", "b"), ir.If(ir.BinOp("<" if op == "i64.min" else ">", ir.VarE("a"), ir.VarE("b")),
+                                             ir.VarE("a"), ir.VarE("b")))
+        if ir.kind(op) != "Lambda":
+            raise NotImplementedError(f"scan operator {op}")
+        n = arrs[0].numel()
+        if any(a.numel() < n for a in arrs[1:]):
+            raise errors.OracleError("scan: operand shorter than the first array")
+        st = ops.Status(self.dev)
+        outs, sites, _ = jit_fold.scan(op, nes, arrs, self._captured(env), lambda node: self._bits(fs, node), st,
+                                       device=self.dev)
+        self._raise_site(st, sites)
+        kk = len(nes)
+        res = [o.to(torch.bool) if _scan_comp_is_bool(op, j, nes, arrs) else o for j, o in enumerate(outs)]
+        return tuple(res) if kk > 1 else res[0]
+
+    def _raise_site(self, st, sites):
+        s = st.read()
+        if not s.ok:
+            node = sites[s.site]
+            raise errors.OutOfBounds(ir.expr_str(node), node.pos)
 
     def _captured(self, env):
         out = {}
@@ -623,6 +657,55 @@ def _is_segsum(op) -> bool:
     ok_v = (getattr(th, "name", None) == v2 and ir.kind(el) == "BinOp" and el.op == "+"
             and {getattr(res(el.lhs), "name", None), getattr(res(el.rhs), "name", None)} == {v1, v2})
     return ok_f and ok_v
+
+
+def _scan_comp_is_bool(op, j: int, nes: list, arrs: list) -> bool:
+    """Is component j of a k-ary scan operator's result a bool?  Resolved
+    through let-bound temporaries; a parameter is bool when its neutral
+    (accumulator) or its array (element) is."""
+    k = len(nes)
+    binds = {}
+
+    def collect(x):
+        if ir.kind(x) == "Let" and len(x.names) == 1:
+            binds.setdefault(x.names[0], x.rhs)
+        for f in ("lhs", "rhs", "arg", "cond", "then", "els", "body"):
+            y = getattr(x, f, None)
+            if y is not None and not isinstance(y, (str, int, float, bool)):
+                collect(y)
+        for y in getattr(x, "items", ()) or ():
+            collect(y)
+
+    collect(op.body)
+    params = list(op.params)
+
+    def is_bool(x, depth=0):
+        if depth > 64:
+            return False
+        kx = ir.kind(x)
+        if kx == "VarE":
+            if x.name in binds:
+                return is_bool(binds[x.name], depth + 1)
+            if x.name in params:
+                i = params.index(x.name)
+                return isinstance(nes[i], bool) if i < k else arrs[i - k].dtype == torch.bool
+            return False
+        if kx == "Let":
+            return is_bool(x.body, depth + 1)
+        if kx == "If":
+            return is_bool(x.then, depth + 1) and is_bool(x.els, depth + 1)
+        return _is_bool_expr(x)
+
+    body = op.body
+    while ir.kind(body) == "Let":
+        body = body.body
+    if ir.kind(body) == "VarE" and body.name in binds and k > 1:
+        body = binds[body.name]
+    if k == 1:
+        return is_bool(op.body)
+    if ir.kind(body) == "TupleE":
+        return is_bool(body.items[j])
+    return isinstance(nes[j], bool)
 
 
 def _is_bool_expr(e) -> bool:

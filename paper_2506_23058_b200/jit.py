@@ -80,6 +80,8 @@ class _Gen:
         self.ntmp = 0
         self.depth = 2
         self._arr_slot: dict = {}
+        # what a failed CHECKED index site does after recording the failure
+        self.on_fail = "goto next;"
 
     def line(self, s: str):
         self.body.append("  " * self.depth + s)
@@ -181,7 +183,7 @@ class _Gen:
             site = len(self.spec.sites)
             self.spec.sites.append(e)
             if self.site_bits(e) & L.V_BOUNDS:
-                self.line(f"if ((u64){i} >= (u64)len{slot}) {{ fail_oob(st, stmt, i, {site}); goto next; }}")
+                self.line(f"if ((u64){i} >= (u64)len{slot}) {{ fail_oob(st, stmt, i, {site}); {self.on_fail} }}")
             return self.new(f"(long long)a{slot}[{i}]")
         if k == "App" and ir.kind(e.fun) == "VarE":
             b = self.env.get(e.fun.name)
@@ -197,6 +199,40 @@ class _Gen:
                 if b is not None and b[0] == "array":
                     return f"len{self.array_slot(b[1])}"
         raise Unsupported(f"{k} inside a lambda: {ir.expr_str(e)}")
+
+    def tuple_expr(self, e, scope: dict, k: int) -> list:
+        """The k components of a tuple-valued body (a k-ary scan operator,
+        oracle.py:286-290), evaluated left to right like TupleE
+        (oracle.py:199-200); Let and If may wrap the tuple."""
+        if k == 1:
+            return [self.expr(e, scope)]
+        kd = ir.kind(e)
+        if kd == "TupleE":
+            if len(e.items) != k:
+                raise Unsupported("operator result arity")
+            return [self.new(self.expr(x, scope)) for x in e.items]
+        if kd == "Let":
+            if len(e.names) != 1:
+                raise Unsupported("tuple let inside a lambda")
+            v = self.new(self.expr(e.rhs, scope))
+            inner = dict(scope)
+            if e.names[0] != "_":
+                inner[e.names[0]] = v
+            return self.tuple_expr(e.body, inner, k)
+        if kd == "If":
+            c = self.expr(e.cond, scope)
+            rs = [self.tmp() for _ in range(k)]
+            self.line("long long " + ", ".join(rs) + ";")
+            self.line(f"if (({c}) != 0) {{")
+            for branch in (e.then, e.els):
+                self.depth += 1
+                vs = self.tuple_expr(branch, scope, k)
+                for r, v in zip(rs, vs):
+                    self.line(f"{r} = {v};")
+                self.depth -= 1
+                self.line("} else {" if branch is e.then else "}")
+            return rs
+        raise Unsupported(f"{kd} as a tuple-valued operator body")
 
 
 def _ctype(t: torch.Tensor) -> str:
@@ -235,7 +271,7 @@ def generate(lam, arrays: list, env: dict, site_bits=lambda node: L.V_BOUNDS, ou
 
 
 class _Kernel:
-    def __init__(self, src: str):
+    def __init__(self, src: str, names=("ixg_jit_map",)):
         from cuda.bindings import driver, nvrtc
 
         err, prog = nvrtc.nvrtcCreateProgram(src.encode(), b"ixg_jit_map.cu", 0, [], [])
@@ -246,7 +282,7 @@ class _Kernel:
             _, size = nvrtc.nvrtcGetProgramLogSize(prog)
             log = b" " * size
             nvrtc.nvrtcGetProgramLog(prog, log)
-            raise RuntimeError("NVRTC failed on a generated map kernel:\n" + log.decode(errors="replace") + "\n" + src)
+            raise RuntimeError("NVRTC failed on a generated kernel:\n" + log.decode(errors="replace") + "\n" + src)
         err, size = nvrtc.nvrtcGetCUBINSize(prog)
         _ok(err, "nvrtcGetCUBINSize")
         cubin = b" " * size
@@ -257,8 +293,11 @@ class _Kernel:
         _ok(err, "cuInit")
         err, self.module = driver.cuModuleLoadData(cubin)
         _ok(err, "cuModuleLoadData")
-        err, self.fn = driver.cuModuleGetFunction(self.module, b"ixg_jit_map")
-        _ok(err, "cuModuleGetFunction")
+        self.fns = {}
+        for name in names:
+            err, self.fns[name] = driver.cuModuleGetFunction(self.module, name.encode())
+            _ok(err, "cuModuleGetFunction")
+        self.fn = self.fns[names[0]]
 
 
 def _ok(err, what):

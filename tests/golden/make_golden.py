@@ -146,6 +146,23 @@ def big_cases(fun):
             nn = int(shp.sum())
             cs = [bool(c) for c in (gen.uniform(seed + 11, nn, 0, 2, np.int64) == 0)]
             out.append([shp.tolist(), cs, gen.uniform(seed + 12, nn, -500, 500, np.int64).tolist()])
+        elif fun in ("scan_min", "scan_max", "scan_clip"):
+            out.append([xs])
+        elif fun == "scan_mul":
+            out.append([[1 if v >= 0 else -1 for v in xs]])  # bounded products
+        elif fun == "scan_and":
+            out.append([[bool(c) for c in (gen.uniform(seed + 13, n, 0, 300, np.int64) != 0)]])
+        elif fun == "scan_pair":
+            out.append([xs, gen.uniform(seed + 14, n, -900, 900, np.int64).tolist()])
+        elif fun == "scan_segmax":
+            out.append([[bool(c) for c in (gen.uniform(seed + 15, n, 0, 9, np.int64) == 0)], xs])
+        elif fun == "scan_lookup":
+            out.append([gen.uniform(seed + 16, 97, -50, 50, np.int64).tolist(),
+                        gen.uniform(seed + 17, n, 0, 96, np.int64).tolist()])
+        elif fun in ("hist_mul", "hist_lmin", "hist_last", "hist_horner"):
+            bins = n // 4 if fun != "hist_horner" else 2 * n
+            out.append([bins, gen.uniform(seed + 18, n, -3, bins + 2, np.int64).tolist(),
+                        gen.uniform(seed + 19, n, -3, 3, np.int64).tolist()])
         elif fun == "get_smallest_pairs":
             nv = 50
             es = gen.uniform(seed + 9, 200, 0, nv - 1, np.int64).tolist()
@@ -186,6 +203,10 @@ def error_cases(fun):
         return [[[3, -3, 4, 1], [1, 2, 3, 4]]]                           # negative shape -> conflict
     if fun == "get_smallest_pairs":
         return [[3, 99, [0, 5, 1], [4, 2, 7]]]                           # H[i] OOB
+    if fun == "scan_lookup":
+        return [[[1, 2, 3], [0, 2, 5, 1, 9]],                            # tbl[5] at element 2 (first)
+                [[1, 2], [-1]],                                          # negative index
+                [[4] * 40, list(range(40)) + [40]]]                      # last element only
     return []
 
 

@@ -211,3 +211,75 @@ def test_jit_generates_and_compiles_corpus_lambdas():
                     walk(c)
             walk(f.body)
     assert len(seen) >= 15
+
+
+def _scanops_lambdas():
+    prog = ir.from_json(PROGRAMS["own:scanops.ixl"]["program"])
+    out = {}
+    for f in prog.defs:
+        def walk(e):
+            if ir.kind(e) == "App" and ir.kind(e.fun) == "VarE" and e.fun.name in ("scan", "hist"):
+                out[f.name] = (e.fun.name, e.args[0], (len(e.args) - 1) // 2)
+            for c in ir.children(e):
+                walk(c)
+        walk(f.body)
+    return out
+
+
+def test_fold_classifier():
+    """jit_fold's structural classifier: associative scan operators take the
+    tiled parallel scan, commutative+associative hist operators the CAS loop,
+    everything else the in-order device fold (oracle.py:281-316)."""
+    from paper_2506_23058_b200 import jit_fold
+
+    lams = _scanops_lambdas()
+    par = {name for name, (kind, lam, k) in lams.items() if kind == "scan" and jit_fold.classify_scan(lam, k)}
+    assert par == {"scan_min", "scan_max", "scan_mul", "scan_and", "scan_pair", "scan_segmax"}
+    hk = {name: jit_fold.classify_hist(lam) for name, (kind, lam, k) in lams.items() if kind == "hist"}
+    assert hk == {"hist_mul": "mul", "hist_lmin": "min", "hist_last": None, "hist_horner": None}
+    # the corpus' own (+) and segmented (+) are associative too
+    c2 = ir.from_json(PROGRAMS["own:c2_filter_sgmsum.ixl"]["program"])
+    seg = [e for f in c2.defs if f.name == "sgmSum" for e in [f.body]][0]
+    while ir.kind(seg) == "Let":
+        seg = seg.rhs
+    assert jit_fold.classify_scan(seg.args[0], 2)
+    # min / max / projections from every comparison
+    for op, want in (("<", "min"), ("<=", "min"), (">", "max"), (">=", "max")):
+        lam = ir.Lambda(("a", "b"), ir.If(ir.BinOp(op, ir.VarE("a"), ir.VarE("b")), ir.VarE("a"), ir.VarE("b")))
+        assert jit_fold.classify_hist(lam) == want
+        lam2 = ir.Lambda(("a", "b"), ir.If(ir.BinOp(op, ir.VarE("b"), ir.VarE("a")), ir.VarE("a"), ir.VarE("b")))
+        assert jit_fold.classify_hist(lam2) == {"min": "max", "max": "min"}[want]
+    lam = ir.Lambda(("a", "b"), ir.BinOp("-", ir.VarE("a"), ir.VarE("b")))
+    assert not jit_fold.classify_scan(lam, 1) and jit_fold.classify_hist(lam) is None
+
+
+def test_fold_kernels_compile():
+    """Every scanops operator's generated kernels (parallel and in-order
+    forms) compile with NVRTC for sm_100a (no GPU needed)."""
+    import torch
+
+    from paper_2506_23058_b200 import jit_fold
+
+    nvrtc = pytest.importorskip("cuda.bindings.nvrtc")
+
+    def compile_ok(src):
+        err, prog_ = nvrtc.nvrtcCreateProgram(src.encode(), b"f.cu", 0, [], [])
+        opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device"]
+        (err,) = nvrtc.nvrtcCompileProgram(prog_, len(opts), opts)
+        if err != nvrtc.nvrtcResult.NVRTC_SUCCESS:
+            _, size = nvrtc.nvrtcGetProgramLogSize(prog_)
+            log = b" " * size
+            nvrtc.nvrtcGetProgramLog(prog_, log)
+            raise AssertionError(log.decode() + "\n" + src)
+
+    env = {"tbl": ("array", torch.zeros(4, dtype=torch.int64))}
+    for name, (kind, lam, k) in _scanops_lambdas().items():
+        if kind == "scan":
+            types = ["long long"] * k
+            if jit_fold.classify_scan(lam, k):
+                compile_ok(jit_fold._par_scan_source(lam, k, types)[0])
+            compile_ok(jit_fold._seq_scan_source(lam, k, types, env, lambda node: L.V_BOUNDS)[0])
+        else:
+            if jit_fold.classify_hist(lam):
+                compile_ok(jit_fold._hist_cas_source(lam, "long long"))
+            compile_ok(jit_fold._hist_seq_source(lam, "long long", env, lambda node: L.V_BOUNDS)[0])

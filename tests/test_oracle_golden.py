@@ -81,13 +81,16 @@ def run_oracle(fun, a):
     if fun == "filter_seg":
         newshp, ys = O.filter_seg(a[0], [int(c) for c in a[1]], a[2])
         return (ints(newshp), ints(ys))
+    if fun.startswith(("scan_", "hist_")):
+        return O.scanops(fun, a)
     raise KeyError(fun)
 
 
 def test_golden_file_covers_corpus():
     funs = {c["fun"] for c in CASES}
     assert {"partition2", "partition3", "filter", "filter_by", "get_smallest_pairs", "mkSgmDescr", "kmeans_ker",
-            "c2", "mkFlags", "sgmSum", "mkII", "sc_any", "csrg_any", "partition2L", "filter_seg"} <= funs
+            "c2", "mkFlags", "sgmSum", "mkII", "sc_any", "csrg_any", "partition2L", "filter_seg", "scan_min",
+            "scan_pair", "scan_segmax", "scan_lookup", "hist_mul", "hist_last", "hist_horner"} <= funs
     assert any("error" in c for c in CASES)
     assert len(CASES) > 500
 
