@@ -324,6 +324,8 @@ class Interp:
             return e
         if k == "App":
             return self._app(e, env, f, fs)
+        if k == "Loop":
+            return self._loop_device(e, env, fs)
         raise NotImplementedError(f"{k} outside a registered pipeline: {ir.expr_str(e)}")
 
     def _app(self, e, env, f, fs):
@@ -347,18 +349,16 @@ class Interp:
             out = None
             if jit.enabled():  # the lambda compiled to its own kernel (NVRTC, cached)
                 try:
-                    out, sites = jit.map_jit(lam, arrs, cenv, bits, n, st, device=self.dev)
+                    out, sites = jit.map_jit(lam, arrs, cenv, bits, n, st, device=self.dev, funs=self.funs,
+                                             bits_for=self._bits_for_caller(fs), loop_cap=self.budget)
                 except vm.Unsupported:
                     out = None
             if out is None:  # the register VM
                 comp = vm.compile_map(lam, arrs, cenv, bits)
                 out = ops.map_vm(comp, n, st, device=self.dev)
                 sites = comp.sites
-            s = st.read()
-            if not s.ok:
-                node = sites[s.site]
-                raise errors.OutOfBounds(ir.expr_str(node), node.pos)
-            return out.to(torch.bool) if _is_bool_expr(lam.body) else out
+            self._raise_site(st, sites)
+            return out.to(torch.bool) if _is_bool_expr(lam.body, self.funs) else out
         if name == "scan":
             kk = (len(e.args) - 1) // 2
             op = ev(e.args[0])
@@ -395,8 +395,11 @@ class Interp:
             if ir.kind(op) != "Lambda":
                 raise NotImplementedError(f"hist operator {op}")
             st = ops.Status(self.dev)
-            dst, sites, _ = jit_fold.hist(op, int(ne), int(dlen), is_, vs, self._captured(env),
-                                          lambda node: self._bits(fs, node), st)
+            try:
+                dst, sites, _ = jit_fold.hist(op, ne, int(dlen), is_, vs, self._captured(env),
+                                              lambda node: self._bits(fs, node), st)
+            except jit_fold.Unsupported as ex:
+                raise NotImplementedError(f"hist operator: {ex}") from ex
             self._raise_site(st, sites)
             return dst.to(torch.bool) if _is_bool_expr(op.body) else dst
         if name == "iota":
@@ -413,6 +416,8 @@ class Interp:
             sub = Interp.__new__(Interp)
             sub.__dict__.update(self.__dict__)
             sub.as_tensors = True  # arrays stay on the device between calls
+            if fs.status != "verified":  # see _callee_sel
+                sub.variant = "checked"
             vals = [ev(a) for a in e.args]
             return sub.call(name, vals)
         fn = ev(e.fun) if ir.kind(e.fun) != "Lambda" else e.fun
@@ -433,18 +438,57 @@ class Interp:
         if any(a.numel() < n for a in arrs[1:]):
             raise errors.OracleError("scan: operand shorter than the first array")
         st = ops.Status(self.dev)
-        outs, sites, _ = jit_fold.scan(op, nes, arrs, self._captured(env), lambda node: self._bits(fs, node), st,
-                                       device=self.dev)
+        try:
+            outs, sites, _ = jit_fold.scan(op, nes, arrs, self._captured(env), lambda node: self._bits(fs, node), st,
+                                           device=self.dev)
+        except jit_fold.Unsupported as ex:
+            raise NotImplementedError(f"scan operator: {ex}") from ex
         self._raise_site(st, sites)
         kk = len(nes)
         res = [o.to(torch.bool) if _scan_comp_is_bool(op, j, nes, arrs) else o for j, o in enumerate(outs)]
         return tuple(res) if kk > 1 else res[0]
 
     def _raise_site(self, st, sites):
+        from . import jit
+
         s = st.read()
         if not s.ok:
+            if s.site == jit.BUDGET_SITE:
+                raise errors.StepBudgetExceeded(f"loop ran past the step budget ({self.budget})")
             node = sites[s.site]
             raise errors.OutOfBounds(ir.expr_str(node), node.pos)
+
+    def _callee_sel(self, caller_fs, name):
+        """A callee's verdicts hold only where the verifier also showed its
+        preconditions at the call, i.e. in a caller it verified; from any
+        other caller the callee runs with every site CHECKED."""
+        if caller_fs is not None and caller_fs.status == "verified":
+            return self._sel(self.funs[name])
+        return sel.checked_selection(self.funs[name])
+
+    def _bits_for_caller(self, caller_fs):
+        def bits_for(name):
+            fs = self._callee_sel(caller_fs, name)
+            return lambda node: self._bits(fs, node)
+        return bits_for
+
+    def _loop_device(self, e, env, fs):
+        """A loop at function level (oracle.py:242-262), e.g. kmeans_ker's
+        row loop called directly: compiled with its captured scalars and
+        arrays into a one-thread kernel (jit.py) and run on the device."""
+        from . import jit
+
+        k = len(e.params)
+        st = ops.Status(self.dev)
+        lam = ir.Lambda((), e)
+        try:
+            out, sites = jit.map_jit(lam, [], self._captured(env), lambda node: self._bits(fs, node), 1, st, device=self.dev, funs=self.funs,
+                                     bits_for=self._bits_for_caller(fs), loop_cap=self.budget, k_out=k)
+        except jit.Unsupported as ex:
+            raise NotImplementedError(f"loop: {ex}") from ex
+        self._raise_site(st, sites)
+        vals = [o.item() for o in (out if k > 1 else [out])]
+        return tuple(vals) if k > 1 else vals[0]
 
     def _captured(self, env):
         out = {}
@@ -455,6 +499,8 @@ class Interp:
                 out[k] = ("pred", v)
             elif isinstance(v, (bool, int)):
                 out[k] = ("scalar", int(v))
+            elif isinstance(v, float):
+                out[k] = ("scalar", float(v))
         return out
 
     def _out(self, t: torch.Tensor, n: Optional[int] = None):
@@ -708,10 +754,13 @@ def _scan_comp_is_bool(op, j: int, nes: list, arrs: list) -> bool:
     return isinstance(nes[j], bool)
 
 
-def _is_bool_expr(e) -> bool:
+def _is_bool_expr(e, funs=None) -> bool:
     k = ir.kind(e)
     if k == "Let":
-        return _is_bool_expr(e.body)
+        return _is_bool_expr(e.body, funs)
+    if k == "App" and funs and ir.kind(e.fun) == "VarE" and e.fun.name in funs:
+        rt = funs[e.fun.name].result_type
+        return ir.kind(rt) == "TBase" and rt.name == "bool"
     if k == "BinOp":
         return e.op in ("==", "!=", "<", "<=", ">", ">=", "&&", "||")
     if k == "NotE":
@@ -721,7 +770,7 @@ def _is_bool_expr(e) -> bool:
     if k == "App":
         return ir.kind(e.fun) == "VarE" and e.fun.name not in ("map", "scan", "iota", "replicate", "length")
     if k == "If":
-        return _is_bool_expr(e.then) and _is_bool_expr(e.els)
+        return _is_bool_expr(e.then, funs) and _is_bool_expr(e.els, funs)
     return False
 
 

@@ -37,7 +37,7 @@ import torch
 
 from . import _lib as L
 from . import ir
-from .jit import _CACHE, _CT, _PRELUDE, LAUNCHES, _ctype, _Gen, _Kernel, _ok
+from .jit import _CACHE, _PRELUDE, LAUNCHES, _ctype, _Gen, _Kernel, _ok, _scalar_param, scalar_args
 from .vm import Unsupported
 
 _CMPS = ("<", "<=", ">", ">=", "==", "!=")
@@ -172,6 +172,7 @@ def _op_function(lam, k):
     g = _Gen({}, lambda node: 0)
     g.depth = 1
     res = g.tuple_expr(lam.body, _params_scope(lam, k), k)
+    _ints_only(g, res)
     lines = ["__device__ __forceinline__ V op(const V& A_, const V& B_) {",
              "  const long long* A = A_.c; const long long* B = B_.c; (void)A; (void)B;"]
     lines += g.body
@@ -309,11 +310,12 @@ def _seq_scan_source(lam, k, in_types, env, site_bits):
         if p != "_":
             scope[p] = f"acc{j}" if j < k else f"el{j - k}"
     res = g.tuple_expr(lam.body, scope, k)
+    _ints_only(g, res)
     ins = [f"const {t}* __restrict__ in{j}" for j, t in enumerate(in_types)]
     params = ins + [f"const {_ctype(t)}* __restrict__ a{j}, long long len{j}" for j, t in enumerate(g.spec.arrays)]
     params += [f"long long* __restrict__ out{j}" for j in range(k)]
     params += ["long long n", "int stmt", "ixg_status* st"] + [f"long long ne{j}" for j in range(k)]
-    params += [f"long long s{j}" for j in range(len(g.spec.scalars))]
+    params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
     load = "\n".join(f"      sm[{j}][q] = (long long)in{j}[base + q];" for j in range(k))
     els = "\n".join(f"        const long long el{j} = sm[{j}][q];" for j in range(k))
@@ -368,10 +370,11 @@ def _hist_seq_source(lam, v_type, env, site_bits):
     if b != "_":
         scope[b] = "v"
     res = g.expr(lam.body, scope)
+    _ints_only(g, [res])
     params = [f"const long long* __restrict__ is", f"const {v_type}* __restrict__ vs"]
     params += [f"const {_ctype(t)}* __restrict__ a{j}, long long len{j}" for j, t in enumerate(g.spec.arrays)]
     params += ["long long* __restrict__ dst", "long long dlen", "long long m", "int stmt", "ixg_status* st"]
-    params += [f"long long s{j}" for j in range(len(g.spec.scalars))]
+    params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
     src = _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__(256) ixg_hist_seq({", ".join(params)}) {{
@@ -410,6 +413,7 @@ def _hist_cas_source(lam, v_type):
     g = _Gen({}, lambda node: 0)
     g.depth = 3
     res = g.expr(lam.body, {a: "cur", b: "v"})
+    _ints_only(g, [res])
     return _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__(256) ixg_hist_cas(const long long* __restrict__ is,
     const {v_type}* __restrict__ vs, long long* __restrict__ dst, long long dlen, long long m) {{
@@ -463,10 +467,13 @@ def _captures(spec):
 
 
 def _tail(spec):
-    vals = [ctypes.c_longlong(v) for v in spec.scalars]
-    for p in spec.preds:
-        vals += [ctypes.c_int(p.kind), ctypes.c_longlong(p.thr), ctypes.c_ulonglong(p.seed & ((1 << 64) - 1))]
-    return vals
+    return scalar_args(spec)
+
+
+def _ints_only(g, res):
+    """The fold kernels carry int64 state: float operators are not lowered."""
+    if any(g.is_f(r) for r in res):
+        raise Unsupported("floating-point scan / hist operator")
 
 
 def _elem(t: torch.Tensor) -> torch.Tensor:
@@ -481,6 +488,8 @@ def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None
     dev = device or arrays[0].device
     n = arrays[0].numel()
     ins = [_elem(a)[:n] for a in arrays]
+    if any(t.is_floating_point() for t in ins) or any(isinstance(v, float) for v in nes):
+        raise Unsupported("floating-point scan")
     in_types = [_ctype(t) for t in ins]
     outs = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(k)]
     nev = [ctypes.c_longlong(int(v)) for v in nes]
@@ -516,8 +525,10 @@ def hist(lam, ne: int, dlen: int, is_: torch.Tensor, vs: torch.Tensor, env: dict
 
     dev = is_.device
     m = min(is_.numel(), vs.numel())
-    dst = ops.fill(max(int(dlen), 0), int(ne), torch.int64, dev)
     iss, vss = is_.contiguous()[:m], _elem(vs)[:m]
+    if vss.is_floating_point() or isinstance(ne, float):
+        raise Unsupported("floating-point hist")
+    dst = ops.fill(max(int(dlen), 0), int(ne), torch.int64, dev)
     v_type = _ctype(vss)
     if not force_seq and classify_hist(lam) is not None:
         src = _hist_cas_source(lam, v_type)

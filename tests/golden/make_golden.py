@@ -163,6 +163,17 @@ def big_cases(fun):
             bins = n // 4 if fun != "hist_horner" else 2 * n
             out.append([bins, gen.uniform(seed + 18, n, -3, bins + 2, np.int64).tolist(),
                         gen.uniform(seed + 19, n, -3, 3, np.int64).tolist()])
+        elif fun in ("all_rows", "row_corr"):
+            rng = np.random.default_rng(seed + 20)
+            rows = n // 16
+            ptr = [0] + np.cumsum(rng.integers(0, 40, rows)).tolist()
+            nnz, m = ptr[-1], 37
+            args = [ptr, [round(float(v), 3) for v in rng.uniform(-4, 9, m)],
+                    [round(float(v), 3) for v in rng.uniform(-4, 9, nnz)], rng.integers(0, m, nnz).tolist()]
+            if fun == "all_rows":
+                out.append(args)
+            else:
+                out += [[r] + args for r in (0, rows // 2, rows - 1)]
         elif fun == "get_smallest_pairs":
             nv = 50
             es = gen.uniform(seed + 9, 200, 0, nv - 1, np.int64).tolist()
@@ -203,6 +214,12 @@ def error_cases(fun):
         return [[[3, -3, 4, 1], [1, 2, 3, 4]]]                           # negative shape -> conflict
     if fun == "get_smallest_pairs":
         return [[3, 99, [0, 5, 1], [4, 2, 7]]]                           # H[i] OOB
+    if fun == "all_rows":
+        return [[[0, 2, 5], [1.5, 2.0], [0.5, 1.0, 2.0, 3.0], [0, 1, 1, 0]],     # vals[lo + j] OOB in row 1
+                [[0, 1, 3], [1.5], [0.5, 1.0, 2.0], [0, 0, 4]]]                  # cl[cols[lo + j]] OOB
+    if fun == "row_corr":
+        return [[2, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],                  # ptr[row + 1] OOB
+                [0, [0, 3], [1.0], [0.5, 1.0, 2.0], [0, 0, 0]]]                  # vals[lo + j] OOB at j = 2
     if fun == "scan_lookup":
         return [[[1, 2, 3], [0, 2, 5, 1, 9]],                            # tbl[5] at element 2 (first)
                 [[1, 2], [-1]],                                          # negative index

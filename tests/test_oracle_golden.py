@@ -81,6 +81,10 @@ def run_oracle(fun, a):
     if fun == "filter_seg":
         newshp, ys = O.filter_seg(a[0], [int(c) for c in a[1]], a[2])
         return (ints(newshp), ints(ys))
+    if fun == "row_corr":
+        return O.kmeans_ker(a[0], a[1], a[2], a[3], a[4])
+    if fun == "all_rows":
+        return [O.kmeans_ker(r, a[0], a[1], a[2], a[3]) for r in range(len(a[0]) - 1)]
     if fun.startswith(("scan_", "hist_")):
         return O.scanops(fun, a)
     raise KeyError(fun)
@@ -109,8 +113,10 @@ def test_oracle_matches_reference(idx):
         return
     got = run_oracle(case["fun"], a)
     want = dec(case["result"])
-    if isinstance(want, float) or case["fun"] == "kmeans_ker":
+    if isinstance(want, float) or case["fun"] in ("kmeans_ker", "row_corr"):
         assert float(got).hex() == float(want).hex()
+    elif case["fun"] == "all_rows":
+        assert [float(x).hex() for x in got] == [float(x).hex() for x in want]
     else:
         assert got == want
 
