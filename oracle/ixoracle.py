@@ -20,6 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libixoracle.so")
 
 OK, OOB, CONFLICT, LENGTH, BADARG, NOMEM, OVERFLOW = range(7)
+BUDGET = 100  # StepBudgetExceeded (oracle.py:118-125); Python-side cases only
 HIST_MIN, HIST_MAX, HIST_ADD = 0, 1, 2
 
 

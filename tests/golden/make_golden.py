@@ -74,9 +74,9 @@ def enc(v):
     raise TypeError(type(v))
 
 
-def run(program, fun, args):
+def run(program, fun, args, budget=BUDGET):
     try:
-        return {"result": enc(eval_program(program, fun, args, BUDGET))}
+        return {"result": enc(eval_program(program, fun, args, budget))}
     except OracleError as e:
         d = {"error": type(e).__name__}
         if hasattr(e, "site"):
@@ -163,6 +163,8 @@ def big_cases(fun):
             bins = n // 4 if fun != "hist_horner" else 2 * n
             out.append([bins, gen.uniform(seed + 18, n, -3, bins + 2, np.int64).tolist(),
                         gen.uniform(seed + 19, n, -3, 3, np.int64).tolist()])
+        elif fun == "countdown":
+            out.append([gen.uniform(seed + 21, n, 0, 3000, np.int64).tolist()])
         elif fun in ("all_rows", "row_corr"):
             rng = np.random.default_rng(seed + 20)
             rows = n // 16
@@ -220,6 +222,8 @@ def error_cases(fun):
     if fun == "row_corr":
         return [[2, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],                  # ptr[row + 1] OOB
                 [0, [0, 3], [1.0], [0.5, 1.0, 2.0], [0, 0, 0]]]                  # vals[lo + j] OOB at j = 2
+    if fun == "countdown":
+        return [[[3, -1, 5]], [[0] * 40 + [-2]]]                         # never-ending while loop
     if fun == "scan_lookup":
         return [[[1, 2, 3], [0, 2, 5, 1, 9]],                            # tbl[5] at element 2 (first)
                 [[1, 2], [-1]],                                          # negative index
@@ -276,7 +280,8 @@ def main():
             draws += [("demo", a) for a in DEMOS.get((key, f.name), [])]
             for origin_kind, a in draws:
                 rec = {"program": key, "fun": f.name, "kind": origin_kind, "args": enc(a)}
-                rec.update(run(prog, f.name, a))
+                # a never-ending loop is cut by the default budget (oracle.py:118)
+                rec.update(run(prog, f.name, a, 10**6 if (f.name, origin_kind) == ("countdown", "error") else BUDGET))
                 cases.append(rec)
     data = os.path.join(ROOT, "paper_2506_23058_b200", "data")
     os.makedirs(data, exist_ok=True)

@@ -83,6 +83,10 @@ def run_oracle(fun, a):
         return (ints(newshp), ints(ys))
     if fun == "row_corr":
         return O.kmeans_ker(a[0], a[1], a[2], a[3], a[4])
+    if fun == "countdown":
+        if any(x < 0 for x in a[0]):
+            raise O.OracleFail(O.BUDGET)
+        return list(a[0])
     if fun == "all_rows":
         return [O.kmeans_ker(r, a[0], a[1], a[2], a[3]) for r in range(len(a[0]) - 1)]
     if fun.startswith(("scan_", "hist_")):
@@ -106,7 +110,7 @@ def test_oracle_matches_reference(idx):
     if "error" in case:
         with pytest.raises(O.OracleFail) as ei:
             run_oracle(case["fun"], a)
-        want = {"OutOfBounds": O.OOB, "NonIdempotentScatter": O.CONFLICT}[case["error"]]
+        want = {"OutOfBounds": O.OOB, "NonIdempotentScatter": O.CONFLICT, "StepBudgetExceeded": O.BUDGET}[case["error"]]
         assert ei.value.code == want
         if case["fun"] == "kmeans_ker":
             assert KMEANS_SITES[ei.value.site] == case["site"]
