@@ -53,6 +53,12 @@ template <typename T>
 constexpr int big_min_blocks() {
   return sizeof(T) == 4 ? (IXG_CH32 <= 3 ? kBMinBlocks : 3) : (IXG_CH64 == 1 ? kBMinBlocks : 3);
 }
+#ifndef IXG_BULK_ST
+#define IXG_BULK_ST 1  // C2: ys / zs leave as bulk (TMA) stores of the phase-shifted run (0.502 -> 0.481 ms)
+#endif
+#ifndef IXG_BULK_ALL
+#define IXG_BULK_ALL 0  // int32 filter / partition too (measured 1 % slower; int64 always: 1 % faster)
+#endif
 #ifndef IXG_SEGSUM_MINB
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
 #endif
@@ -92,6 +98,19 @@ IXG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// 1-D bulk store shared -> global (TMA engine): both addresses 16-byte
+// aligned, size a multiple of 16.  The writing threads' generic-proxy smem
+// stores must be fenced into the async proxy before the issuing barrier, and
+// the issuer must wait for the engine's smem reads before the buffer is
+// rewritten or the CTA exits.
+IXG_DEV void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+IXG_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+IXG_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+IXG_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 IXG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
   do {
@@ -389,6 +408,61 @@ IXG_DEV void store_run(E* __restrict__ out, long long base, int cnt, const E* bu
   }
 }
 
+// Move the run buf[0 .. cnt) up by s < EP slots (s = the output base's
+// misalignment in elements), so that run element j sits at buf + s + j and
+// shares its 16-byte phase with out + base + j: the aligned middle of the run
+// can then leave in one bulk store.  New 16-byte chunk c is old chunks c-1
+// and c funnelled by s; rounds of 2 * NT chunks run from the top down, each
+// reading (before its barrier) everything it overwrites and the old chunk
+// below it, which the next round rewrites only after that barrier.
+template <typename T, int NT>
+IXG_DEV void shift_run_up(T* buf, int cnt, int s) {
+  constexpr int EP = 16 / (int)sizeof(T);
+  constexpr int PER = 2;
+  const int nnew = (cnt + s + EP - 1) / EP;  // chunks of the moved run
+  uint4* b4 = reinterpret_cast<uint4*>(buf);
+  const int sw = s * (int)sizeof(T) / 4;  // word shift 1..3
+  for (int top = nnew; top > 0; top -= PER * NT) {
+    uint4 v[PER];
+    int cidx[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int c = top - PER * NT + i * NT + (int)threadIdx.x;
+      cidx[i] = c;
+      if (c >= 0) {
+        const uint4 hi = b4[c];
+        const uint4 lo = c > 0 ? b4[c - 1] : make_uint4(0u, 0u, 0u, 0u);
+        if (sw == 1) v[i] = make_uint4(lo.w, hi.x, hi.y, hi.z);
+        else if (sw == 2) v[i] = make_uint4(lo.z, lo.w, hi.x, hi.y);
+        else v[i] = make_uint4(lo.y, lo.z, lo.w, hi.x);
+      }
+    }
+    bar_sync(1, NT);
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (cidx[i] >= 0) b4[cidx[i]] = v[i];
+  }
+}
+
+// Store run[0 .. cnt) (run = buf + s, phase-matched to out + base) to
+// out[base ..]: the aligned middle as one bulk store issued by thread 0
+// (after every thread's fence + the caller's barrier), the <= EP-1 head and
+// tail elements by plain stores.  Returns with the bulk store in flight.
+template <typename E, int NT>
+IXG_DEV void store_run_bulk(E* __restrict__ out, long long base, int cnt, const E* run) {
+  constexpr int EP = 16 / (int)sizeof(E);
+  if (cnt <= 0) return;
+  const int a0 = min(cnt, (int)((EP - (base & (EP - 1))) & (EP - 1)));  // first aligned element
+  const int a1 = max(a0, (int)(((base + cnt) & ~(long long)(EP - 1)) - base));  // end of the aligned part
+  const int t = (int)threadIdx.x;
+  if (t == 0 && a1 > a0) {
+    bulk_s2g(out + base + a0, run + a0, (uint32_t)(a1 - a0) * (uint32_t)sizeof(E));
+    bulk_commit();
+  }
+  if (t >= 32 && t < 32 + a0) out[base + (t - 32)] = run[t - 32];
+  if (t >= 64 && t < 64 + (cnt - a1)) out[base + a1 + (t - 64)] = run[a1 + (t - 64)];
+}
+
 // CTA-wide exclusive scan over SegOp values (C2's tile-local segmented scan);
 // one named barrier over the kBT workers, *total = the CTA aggregate
 IXG_DEV SegOp::T cta_seg_exclusive(SegOp::T a, SegOp::T* s_seg, SegOp::T* total) {
@@ -605,8 +679,23 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       bw2 = __ldg(&segbits[wd + 2]);
     }
   }
+  // kSeg + IXG_BULK_ST: the ys run is phase-shifted to base and leaves as
+  // one bulk (TMA) store that drains while the workers scan zs
+  constexpr bool kBulk = (kSeg && IXG_BULK_ST) || (!kSeg && !kPeer && (IXG_BULK_ALL || sizeof(T) == 8));
+  const bool bulk = kBulk && ((((uintptr_t)ys) | (kSeg ? (uintptr_t)zs : (uintptr_t)0)) & 15) == 0;  // 16-byte aligned outputs
+  T* run = buf;
   if constexpr (kPeer) {
     store_run_peer<T, kBT>(po, po.seg_base[seg] + (base - po.seg_local[seg]), cnt, buf);
+  } else if (bulk) {
+    const int sh0 = (int)(base & (B::EP - 1));
+    if (sh0) {
+      shift_run_up<T, kBT>(buf, cnt, sh0);
+      run = buf + sh0;
+    }
+    fence_async_smem();
+    bar_sync(1, kBT);
+    store_run_bulk<T, kBT>(ys, base, cnt, run);
+    if (!kSeg && t == 0) bulk_wait_read0();  // before the CTA's smem is released
   } else {
     store_run<T, kBT>(ys, base, cnt, buf);
   }
@@ -622,9 +711,11 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     // pass 1: the piece's segmented aggregate
     const int last = fw ? 63 - __clzll(fw) : 0;
     long long s = 0;
-    for (int j = last; j < len; ++j) s += (long long)buf[q0 + j];
+    for (int j = last; j < len; ++j) s += (long long)run[q0 + j];
     // tile-local exclusive prefix of the piece (its barrier also orders
-    // every thread's ys stores from buf before zs overwrites it)
+    // every thread's ys stores from buf -- and the bulk store's smem reads,
+    // waited for by its issuer -- before zs overwrites it)
+    if (bulk && t == 0) bulk_wait_read0();
     SegOp::T tagg;
     const SegOp::T init = cta_seg_exclusive(SegOp::T{s, fw != 0}, s_seg, &tagg);
     IXG_TR(8);
@@ -636,7 +727,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     // are final; the earlier ones (j < jm) are tile-local until the carry of
     // the preceding tiles arrives, so they run exactly in 64 bits and keep
     // their range [lo, hi] for the check once the carry is known.
-    Z* zbuf = reinterpret_cast<Z*>(buf) + q0;
+    Z* zbuf = reinterpret_cast<Z*>(run) + q0;
     const int jf = init.f ? 0 : (fw ? __ffsll((long long)fw) - 1 : len);
     const int jm = jf < len ? jf : len;
     uint64_t fb = fw >> jm;
@@ -682,8 +773,15 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
         atomicOr(&st->flags, IXG_F_NARROW);
       for (int q = 0; q < jm; ++q) zbuf[q] = (Z)((unsigned long long)zbuf[q] + (unsigned long long)cv);
     }
-    bar_sync(1, kBT);
-    store_run<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(buf));
+    if (bulk) {
+      fence_async_smem();
+      bar_sync(1, kBT);
+      store_run_bulk<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(run));
+      if (t == 0) bulk_wait_read0();  // the engine has read the run before the CTA's smem is released
+    } else {
+      bar_sync(1, kBT);
+      store_run<Z, kBT>(zs, base, cnt, reinterpret_cast<Z*>(buf));
+    }
     IXG_TR(11);
   }
 }
