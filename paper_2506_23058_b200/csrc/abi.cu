@@ -73,7 +73,9 @@ struct WS {
 };
 
 inline long long tiles_of(long long n, int tile) { return (n + tile - 1) / tile; }
-inline size_t bitmap_bytes(long long nbits) { return (size_t)((nbits + 31) / 32 + 2 + 128) * 4; }
+// + slack: readers fetch whole windows past the last word (k_filter_b kSeg
+// bulk-loads TILE/32 + 12 words from the tile's first flag word)
+inline size_t bitmap_bytes(long long nbits) { return (size_t)((nbits + 31) / 32 + 2 + 512) * 4; }
 inline int grid_for(long long work, int per_block = kGThreads) {
   long long g = (work + per_block - 1) / per_block;
   long long cap = (long long)num_sms() * 8;

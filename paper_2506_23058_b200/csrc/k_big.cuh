@@ -526,15 +526,36 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   __shared__ long long s_excl;
   __shared__ SegOp::T s_tagg, s_carry;
   __shared__ __align__(8) uint64_t s_mbar[B::CH];
+  // kSeg: the mkFlags bitmap words of the tile's output range, fetched by
+  // the look-back warp the moment the base is known
+  constexpr int kBitsW = kSeg ? ((B::TILE + 31) / 32 + 8 + 3) & ~3 : 4;
+  __shared__ __align__(16) uint32_t s_bits[kBitsW];
+  __shared__ __align__(8) uint64_t s_mbar_bits;
+  __shared__ long long s_wbase;
 
   const long long tile = blockIdx.x;  // position on the look-back chain
   const int seg = NS > 1 ? (int)(tile / seg_tiles) : 0;
   const long long tile_base = (NS > 1 ? tile - seg * seg_tiles : tile) * B::TILE;
   const int t = threadIdx.x;
   if (warp_id() == kBW) {  // look-back warp
+    if (kSeg && lane_id() == 0) {
+      mbar_init(&s_mbar_bits, 1);
+      mbar_fence_init();
+    }
     long long ex = 0;
     if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
-    if (lane_id() == 0) s_excl = ex;
+    if (lane_id() == 0) {
+      s_excl = ex;
+      if constexpr (kSeg) {
+        // bitmap words [wb, wb + kBitsW) cover flags out_base + ex .. + TILE
+        // (bitmap_bytes() pads the bitmap past its last word)
+        const long long wb = ((out_base + ex) >> 5) & ~3LL;
+        s_wbase = wb;
+        mbar_expect_tx(&s_mbar_bits, kBitsW * 4u);
+        bulk_g2s(s_bits, segbits + wb, kBitsW * 4u, &s_mbar_bits);
+      }
+    }
+    __syncwarp();
     IXG_TR_LANE0(5);
     bar_sync(2, kBT + 32);
     if (lane_id() == 0) {
@@ -666,18 +687,11 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   // are issued now and land during the ys stores
   int L = 0, q0 = 0, q1 = 0;
   long long g0 = 0;
-  uint32_t bw0 = 0, bw1 = 0, bw2 = 0;
   if constexpr (kSeg) {
     L = ((cnt + kBT - 1) / kBT) | 1;
     q0 = min(t * L, cnt);
     q1 = min(q0 + L, cnt);
     g0 = out_base + base + q0;
-    if (q1 > q0) {
-      const long long wd = g0 >> 5;
-      bw0 = __ldg(&segbits[wd]);
-      bw1 = __ldg(&segbits[wd + 1]);
-      bw2 = __ldg(&segbits[wd + 2]);
-    }
   }
   // kSeg + IXG_BULK_ST: the ys run is phase-shifted to base and leaves as
   // one bulk (TMA) store that drains while the workers scan zs
@@ -692,8 +706,10 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       shift_run_up<T, kBT>(buf, cnt, sh0);
       run = buf + sh0;
     }
+    IXG_TR(14);
     fence_async_smem();
     bar_sync(1, kBT);
+    IXG_TR(15);
     store_run_bulk<T, kBT>(ys, base, cnt, run);
     if (!kSeg && t == 0) bulk_wait_read0();  // before the CTA's smem is released
   } else {
@@ -703,6 +719,14 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   if constexpr (kSeg) {
     // thread t scans the run piece [q0, q1) of odd length L (odd stride:
     // the scalar shared-memory reads of a warp hit 32 distinct banks)
+    uint32_t bw0 = 0, bw1 = 0, bw2 = 0;
+    mbar_wait(&s_mbar_bits, 0);  // the look-back warp's bitmap window has landed
+    if (q1 > q0) {
+      const int wd = (int)((g0 >> 5) - s_wbase);
+      bw0 = s_bits[wd];
+      bw1 = s_bits[wd + 1];
+      bw2 = s_bits[wd + 2];
+    }
     const int sh = (int)(g0 & 31);
     uint64_t fw = ((((uint64_t)bw1 << 32) | bw0) >> sh) | (sh ? ((uint64_t)bw2 << (64 - sh)) : 0ull);
     const int len = q1 - q0;
