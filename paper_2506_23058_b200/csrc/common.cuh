@@ -59,6 +59,9 @@ IXG_DEV uint32_t lanemask_lt() {
 IXG_DEV void bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+IXG_DEV void bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 IXG_DEV int lane_id() { return threadIdx.x & 31; }
 IXG_DEV int warp_id() { return threadIdx.x >> 5; }
 
@@ -189,13 +192,18 @@ struct Vec<long long> {
 // compaction kernels (thread 0 of the first 2^17 CTAs); read with
 // ixg_trace_read().  Compiled out otherwise.
 #ifdef IXG_TRACE
-#define IXG_TRS 16  // trace slots per CTA
+#define IXG_TRS 20  // trace slots per CTA
+#ifdef IXG_TRACE_CLK  // SM cycle counter: exact within a CTA, not across SMs
+#define IXG_TR_NOW(t) asm volatile("mov.u64 %0, %%clock64;" : "=l"(t))
+#else
+#define IXG_TR_NOW(t) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t))
+#endif
 __device__ unsigned long long g_trace[(1 << 17) * IXG_TRS];
 #define IXG_TR(slot)                                                        \
   do {                                                                      \
     if (threadIdx.x == 0 && blockIdx.x < (1u << 17)) {                      \
       unsigned long long t__;                                               \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));               \
+      IXG_TR_NOW(t__);                                                      \
       g_trace[blockIdx.x * IXG_TRS + (slot)] = t__;                               \
     }                                                                       \
   } while (0)
@@ -203,7 +211,7 @@ __device__ unsigned long long g_trace[(1 << 17) * IXG_TRS];
   do {                                                                      \
     if ((threadIdx.x & 31) == 0 && blockIdx.x < (1u << 17)) {               \
       unsigned long long t__;                                               \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));               \
+      IXG_TR_NOW(t__);                                                      \
       g_trace[blockIdx.x * IXG_TRS + (slot)] = t__;                               \
     }                                                                       \
   } while (0)

@@ -40,7 +40,10 @@ namespace ixg {
 constexpr int kBW = IXG_BW;             // worker warps
 constexpr int kBT = kBW * 32;           // worker threads
 constexpr int kBChunk = kBT * kSItems;  // elements per chunk
-constexpr int kBMinBlocks = kBW >= 16 ? 2 : 4;  // resident CTAs per SM the registers must allow
+#ifndef IXG_MINB
+#define IXG_MINB (kBW >= 16 ? 2 : 4)
+#endif
+constexpr int kBMinBlocks = IXG_MINB;  // resident CTAs per SM the registers must allow
 #ifndef IXG_CH32
 #define IXG_CH32 3  // chunks per int32 tile (48 KB, 4 CTAs/SM)
 #endif
@@ -58,6 +61,9 @@ constexpr int big_min_blocks() {
 #endif
 #ifndef IXG_BULK_ALL
 #define IXG_BULK_ALL 0  // int32 filter / partition too (measured 1 % slower; int64 always: 1 % faster)
+#endif
+#ifndef IXG_LB_DEFER
+#define IXG_LB_DEFER 1  // look-back polling deferred until it can succeed: C2 0.463 -> 0.458 ms, filter -0.7 %
 #endif
 #ifndef IXG_SEGSUM_MINB
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
@@ -422,6 +428,7 @@ IXG_DEV void shift_run_up(T* buf, int cnt, int s) {
   const int nnew = (cnt + s + EP - 1) / EP;  // chunks of the moved run
   uint4* b4 = reinterpret_cast<uint4*>(buf);
   const int sw = s * (int)sizeof(T) / 4;  // word shift 1..3
+  IXG_TR(16);
   for (int top = nnew; top > 0; top -= PER * NT) {
     uint4 v[PER];
     int cidx[PER];
@@ -438,6 +445,7 @@ IXG_DEV void shift_run_up(T* buf, int cnt, int s) {
       }
     }
     bar_sync(1, NT);
+    IXG_TR(17);
 #pragma unroll
     for (int i = 0; i < PER; ++i)
       if (cidx[i] >= 0) b4[cidx[i]] = v[i];
@@ -543,6 +551,10 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       mbar_fence_init();
     }
     long long ex = 0;
+    // IXG_LB_DEFER: start polling once this tile's own count is published
+    // (its predecessors' are then mostly published too: fewer spins
+    // stealing issue slots from the workers)
+    if (IXG_LB_DEFER && sizeof(T) == 4) bar_sync(4, 64);  // int64: measured 0.5 % slower
     if (tile > 0) ex = lb_lookback<SumOp>(ch, nonce, tile).v;
     if (lane_id() == 0) {
       s_excl = ex;
@@ -568,6 +580,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       // second chain: the sgmSum carry into the tile (SegOp over the tiles'
       // segmented aggregates), polled while the workers store ys and scan
       SegOp::T carry = SegOp::identity();
+      if (IXG_LB_DEFER) bar_sync(5, kBT + 32);  // the workers' pass 1 is done
       if (tile > 0) carry = lb_lookback<SegOp>(ch2, nonce, tile);
       if (lane_id() == 0) s_carry = carry;
       IXG_TR_LANE0(12);
@@ -655,6 +668,10 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   if (t == 0) {
     s_cnt = cnt;
     lb_publish<SumOp>(ch, nonce, tile, SumOp::T{cnt}, tile == 0);
+  }
+  if (IXG_LB_DEFER && sizeof(T) == 4 && w == 0) {
+    __syncwarp();
+    bar_arrive(4, 64);
   }
   // in-place stable compaction to TILE-LOCAL slots, chunk by chunk, while
   // the look-back warp resolves the tile's global base: output slot r of an
@@ -746,6 +763,10 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     if (t == 0) {  // a tile with a flag knows its inclusive value already
       s_tagg = tagg;
       lb_publish<SegOp>(ch2, nonce, tile, tagg, tile == 0 || tagg.f);
+    }
+    if (IXG_LB_DEFER) {
+      __syncwarp();
+      bar_arrive(5, kBT + 32);
     }
     // pass 2: zs in place of ys.  Values at or after the tile's first flag
     // are final; the earlier ones (j < jm) are tile-local until the carry of
