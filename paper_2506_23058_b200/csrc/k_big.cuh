@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     for (int c = 0; c < B::CH; ++c) m[c] = quad_cs_mask<Q::EP>(cs, n, tile_base + c * kBChunk + Q::off(w, 0, l), full);
     if (!full) cp_async_wait_all();
   } else {
-    const Selector<T> sel(p);
+    const Selector<T, (NS < 3)> sel(p);  // partition3: the sign test measured 3 % slower
     if (!full) cp_async_wait_all();
 #pragma unroll
     for (int c = 0; c < B::CH; ++c) {
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
         if (seg == 1) m[c] ^= 0xffffu;
       } else if constexpr (NS == 3) {
         if (seg > 0) {
-          const uint32_t mq = Selector<T>(q).mask(x);
+          const uint32_t mq = Selector<T, false>(q).mask(x);
           m[c] = ~m[c] & (seg == 1 ? mq : ~mq) & 0xffffu;
         }
       }

@@ -32,15 +32,44 @@ IXG_DEV uint32_t valid_mask(long long i0, long long n) {
 
 // The predicate of a kernel, decoded once per thread: the comparison kinds
 // become an interval test (common.cuh PredRange), HASH keeps its seed.
+// sign bits of 16 int32 (bit j set iff x[j] < 0): the four top bytes of a
+// 16-byte piece gathered with two-level byte permutes, their sign bits packed
+// into a nibble by one multiply (bits 7/15/23/31 -> 28..31, no carries)
 template <typename T>
+IXG_DEV uint32_t sign16(const T (&x)[kSItems]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < kSItems / 4; ++k) {
+    const uint32_t a = __byte_perm((uint32_t)x[4 * k], (uint32_t)x[4 * k + 1], 0x0073);
+    const uint32_t b = __byte_perm((uint32_t)x[4 * k + 2], (uint32_t)x[4 * k + 3], 0x0073);
+    const uint32_t w = __byte_perm(a, b, 0x5410);
+    m |= (((w & 0x80808080u) * 0x00204081u) >> 28) << (4 * k);
+  }
+  return m;
+}
+
+#ifndef IXG_SIGN_SEL
+#define IXG_SIGN_SEL 1
+#endif
+template <typename T, bool kSign = true>
 struct Selector {
   int kind;  // IXG_PRED_LT..NE -> range test
   PredRange<T> r;
   uint64_t seed;
-  IXG_DEV explicit Selector(const ixg_pred& p) : kind(p.kind), r(pred_range<T>(p)), seed(p.seed) {}
+  int sgn;  // int32 half ranges [INT_MIN, -1] (1) / [0, INT_MAX] (2): a sign-bit test
+  IXG_DEV explicit Selector(const ixg_pred& p) : kind(p.kind), r(pred_range<T>(p)), seed(p.seed) {
+    sgn = (kSign && IXG_SIGN_SEL && sizeof(T) == 4 && kind <= IXG_PRED_NE && r.keep && (unsigned long long)r.span == 0x7fffffffull &&
+           ((unsigned long long)r.lo == 0ull || (unsigned long long)r.lo == 0x80000000ull))
+              ? ((unsigned long long)r.lo ? 1 : 2)
+              : 0;
+  }
   // selection mask of 16 elements; the kind is uniform, so no divergence
   IXG_DEV uint32_t mask(const T (&x)[kSItems]) const {
     uint32_t m = 0;
+    if (kSign && sizeof(T) == 4 && sgn) {
+      m = sign16(x);
+      return (sgn == 1 ? m : (~m & 0xffffu)) ^ r.flip;
+    }
     if (kind <= IXG_PRED_NE) {
 #pragma unroll
       for (int j = 0; j < kSItems; ++j) m |= (uint32_t)r.test(x[j]) << j;
