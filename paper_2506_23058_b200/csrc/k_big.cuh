@@ -62,6 +62,13 @@ constexpr int big_min_blocks() {
 #ifndef IXG_BULK_ALL
 #define IXG_BULK_ALL 0  // int32 filter / partition too (measured 1 % slower; int64 always: 1 % faster)
 #endif
+#ifndef IXG_P1_UNROLL
+#define IXG_P1_UNROLL 4
+#endif
+#ifndef IXG_P2_UNROLL
+#define IXG_P2_UNROLL 8  // measured 0.5 % faster than 4 on C2
+#endif
+constexpr int kP1Unroll = IXG_P1_UNROLL, kP2Unroll = IXG_P2_UNROLL;
 #ifndef IXG_LB_DEFER
 #define IXG_LB_DEFER 1  // look-back polling deferred until it can succeed: C2 0.463 -> 0.458 ms, filter -0.7 %
 #endif
@@ -752,6 +759,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     // pass 1: the piece's segmented aggregate
     const int last = fw ? 63 - __clzll(fw) : 0;
     long long s = 0;
+#pragma unroll kP1Unroll
     for (int j = last; j < len; ++j) s += (long long)run[q0 + j];
     // tile-local exclusive prefix of the piece (its barrier also orders
     // every thread's ys stores from buf -- and the bulk store's smem reads,
@@ -792,7 +800,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       // init): a value leaves int32 iff its add overflows
       int32_t r = (int32_t)init.v;
       uint32_t ov = 0;
-#pragma unroll 4
+#pragma unroll kP2Unroll
       for (; j < len; ++j, fb >>= 1) {
         const int32_t x = (int32_t)zbuf[j];
         const int32_t rr = (fb & 1ull) ? 0 : r;
