@@ -22,7 +22,7 @@ from paper_2506_23058_b200 import _lib as L  # noqa: E402
 from paper_2506_23058_b200 import gen, ops  # noqa: E402
 from paper_2506_23058_b200.pred import Pred  # noqa: E402
 
-SLOTS = 16
+SLOTS = 20
 
 
 def phase(a, nm, i, j):
@@ -71,6 +71,10 @@ def main():
             a[:, 14] -= t0
             a[:, 15] -= t0
             phase(a, " shift", 4, 14)
+            a[:, 16] -= t0
+            a[:, 17] -= t0
+            phase(a, "  pre-shift", 4, 16)
+            phase(a, "  to last round bar", 16, 17)
             phase(a, " fence+bar", 14, 15)
             phase(a, " bulk issue", 15, 6)
         phase(a, "seg_p1+scan", 6, 8)
@@ -82,10 +86,10 @@ def main():
         print(f"  seg look-back rounds mean {r2.mean():.2f}, spins mean {(a[:, 13] & 0xFFFFFFFF).mean():.1f}")
     else:
         phase(a, "store", 4, 6)
-    cum = {c: int(np.median(a[:, c] - a[:, 0])) for c in range(1, 16) if a[:, c].any() and c not in (7, 13)}
+    cum = {c: int(np.median(a[:, c] - a[:, 0])) for c in range(1, 18) if a[:, c].any() and c not in (7, 13)}
     print("  cumulative medians from start (slot: ns):", cum)
     for r in (100, 5000, 15000):
-        print(f"  tile {r}:", {c: int(a[r, c] - a[r, 0]) for c in (1, 2, 3, 4, 5, 6, 14, 15)})
+        print(f"  tile {r}:", {c: int(a[r, c] - a[r, 0]) for c in (1, 2, 3, 4, 5, 6, 14, 15, 16, 17)})
     print("  frac slot5 > slot4:", float(np.mean(a[:, 5] > a[:, 4])))
     life = a[:, end] - a[:, 0]
     print(f"  life        median {np.median(life):8.0f} ns  p90 {np.percentile(life, 90):8.0f}")
