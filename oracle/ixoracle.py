@@ -342,6 +342,16 @@ def scanops(fun, a):
         return fold_scan(lambda x, y: y if x > 20 else x + y, [0], [a[0]])
     if fun == "scan_lookup":
         return fold_scan(_lookup(a[0]), [0], [a[1]])
+    if fun == "scan_fsum":
+        return fold_scan(lambda x, y: x + y, [0.5], [a[0]])
+    if fun == "scan_fmax":
+        return fold_scan(lambda x, y: y if x < y else x, [0.0 - 100.0], [a[0]])
+    if fun == "scan_decay":
+        return fold_scan(lambda x, y: x * 0.5 + y, [0], [a[0]])
+    if fun == "hist_fadd":
+        return fold_hist(lambda x, y: x + y, 0.25, a[0], a[1], a[2])
+    if fun == "hist_fmin":
+        return fold_hist(lambda x, y: min(x, y), 100.0, a[0], a[1], a[2])
     if fun == "hist_mul":
         return fold_hist(lambda x, y: x * y, 1, a[0], a[1], a[2])
     if fun == "hist_lmin":

@@ -364,9 +364,10 @@ class Interp:
             op = ev(e.args[0])
             nes = [ev(a) for a in e.args[1:1 + kk]]
             arrs = [ev(a) for a in e.args[1 + kk:]]
-            if kk == 1 and _is_add(op):
+            ints = not any(a.is_floating_point() for a in arrs) and not any(isinstance(v, float) for v in nes)
+            if kk == 1 and _is_add(op) and ints:
                 return ops.scan_add(arrs[0], int(nes[0]))
-            if kk == 2 and _is_segsum(op) and not nes[0] and nes[1] == 0:
+            if kk == 2 and ints and _is_segsum(op) and not nes[0] and nes[1] == 0:
                 n = arrs[0].numel()
                 if arrs[1].numel() < n:
                     raise errors.OracleError("scan: value array shorter than flags")
@@ -386,9 +387,12 @@ class Interp:
             return out
         if name == "hist":
             op, ne, dlen, is_, vs = (ev(a) for a in e.args)
+            if vs.is_floating_point() or isinstance(ne, float):  # float folds keep the index order
+                op = _named_lambda(op) if isinstance(op, str) else op
             code = {"i64.min": L.HIST_MIN, "i64.max": L.HIST_MAX}.get(op) if isinstance(op, str) else (
-                L.HIST_ADD if _is_add(op) else None)
-            if code is None and ir.kind(op) == "Lambda" and vs.dtype != torch.bool:
+                L.HIST_ADD if _is_add(op) and not vs.is_floating_point() and not isinstance(ne, float) else None)
+            if code is None and ir.kind(op) == "Lambda" and vs.dtype != torch.bool and not (
+                    vs.is_floating_point() or isinstance(ne, float)):
                 code = {"add": L.HIST_ADD, "min": L.HIST_MIN, "max": L.HIST_MAX}.get(jit_fold.classify_hist(op))
             if code is not None:
                 return ops.hist(code, int(ne), int(dlen), is_, vs.to(torch.int64))
@@ -430,8 +434,7 @@ class Interp:
         parallel scan when the operator is recognisably associative, else
         the in-order fold on the device (jit_fold.py)."""
         if isinstance(op, str) and op in ("i64.min", "i64.max"):
-            op = ir.Lambda(("a", "b"), ir.If(ir.BinOp("<" if op == "i64.min" else ">", ir.VarE("a"), ir.VarE("b")),
-                                             ir.VarE("a"), ir.VarE("b")))
+            op = _named_lambda(op)
         if ir.kind(op) != "Lambda":
             raise NotImplementedError(f"scan operator {op}")
         n = arrs[0].numel()
@@ -703,6 +706,15 @@ def _is_segsum(op) -> bool:
     ok_v = (getattr(th, "name", None) == v2 and ir.kind(el) == "BinOp" and el.op == "+"
             and {getattr(res(el.lhs), "name", None), getattr(res(el.rhs), "name", None)} == {v1, v2})
     return ok_f and ok_v
+
+
+def _named_lambda(op: str):
+    """i64.min / i64.max (oracle.py:110-114: Python min / max) as lambdas:
+    min(a, b) is a unless b < a, max(a, b) is a unless b > a."""
+    if op not in ("i64.min", "i64.max"):
+        raise NotImplementedError(f"operator {op}")
+    return ir.Lambda(("a", "b"), ir.If(ir.BinOp("<" if op == "i64.min" else ">", ir.VarE("b"), ir.VarE("a")),
+                                       ir.VarE("b"), ir.VarE("a")))
 
 
 def _scan_comp_is_bool(op, j: int, nes: list, arrs: list) -> bool:

@@ -298,10 +298,33 @@ extern "C" __global__ void __launch_bounds__(256) ixg_scan_down({ins}, {outs}, l
 """), ipt
 
 
-_SEQ_TILE = 1024
+_SEQ_TILE = 512
+_CT2 = {"f": "double", "i": "long long"}
 
 
-def _seq_scan_source(lam, k, in_types, env, site_bits):
+def fold_types(lam, k: int, in_f: list, ne_f: list, env=None) -> list:
+    """'i' | 'f' per accumulator of an in-order fold: a float neutral or
+    element makes it a double, so does an operator that turns it into one
+    (Python's int -> float promotion, fixed point over the parameters)."""
+    g = _Gen(env or {}, lambda node: 0)
+    tys = ["f" if (in_f[j] or ne_f[j]) else "i" for j in range(k)]
+    for _ in range(k + 2):
+        tenv = {}
+        for j, p in enumerate(lam.params):
+            tenv[p] = tys[j] if j < k else ("f" if in_f[j - k] else "i")
+        r = g.infer(lam.body, tenv)
+        rs = r if isinstance(r, list) else [r]
+        new = ["f" if "f" in (a, b) else "i" for a, b in zip(tys, rs)]
+        if new == tys:
+            break
+        tys = new
+    return tys
+
+
+def _seq_scan_source(lam, k, in_types, env, site_bits, acc_tys=None):
+    """The exact in-order fold (oracle.py:288-292) on one thread over
+    shared-memory-staged tiles; accumulators typed int64 or double."""
+    acc_tys = acc_tys or ["i"] * k
     g = _Gen(env, site_bits)
     g.depth = 4
     g.on_fail = "failed = 1; goto done;"
@@ -309,26 +332,32 @@ def _seq_scan_source(lam, k, in_types, env, site_bits):
     for j, p in enumerate(lam.params):
         if p != "_":
             scope[p] = f"acc{j}" if j < k else f"el{j - k}"
+    for j in range(k):
+        if acc_tys[j] == "f":
+            g.fty.add(f"acc{j}")
+        if in_types[j] == "double":
+            g.fty.add(f"el{j}")
     res = g.tuple_expr(lam.body, scope, k)
-    _ints_only(g, res)
+    ein = ["double" if t == "double" else "long long" for t in in_types]
     ins = [f"const {t}* __restrict__ in{j}" for j, t in enumerate(in_types)]
     params = ins + [f"const {_ctype(t)}* __restrict__ a{j}, long long len{j}" for j, t in enumerate(g.spec.arrays)]
-    params += [f"long long* __restrict__ out{j}" for j in range(k)]
-    params += ["long long n", "int stmt", "ixg_status* st"] + [f"long long ne{j}" for j in range(k)]
+    params += [f"{_CT2[acc_tys[j]]}* __restrict__ out{j}" for j in range(k)]
+    params += ["long long n", "int stmt", "ixg_status* st"] + [f"{_CT2[acc_tys[j]]} ne{j}" for j in range(k)]
     params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
-    load = "\n".join(f"      sm[{j}][q] = (long long)in{j}[base + q];" for j in range(k))
-    els = "\n".join(f"        const long long el{j} = sm[{j}][q];" for j in range(k))
-    wr = "\n".join(f"        sm[{j}][q] = acc{j};" for j in range(k))
-    store = "\n".join(f"      out{j}[base + q] = sm[{j}][q];" for j in range(k))
+    decl = "\n".join(f"  __shared__ {ein[j]} si{j}[{_SEQ_TILE}];\n  __shared__ {_CT2[acc_tys[j]]} so{j}[{_SEQ_TILE}];"
+                     for j in range(k))
+    load = "\n".join(f"      si{j}[q] = ({ein[j]})in{j}[base + q];" for j in range(k))
+    els = "\n".join(f"        const {ein[j]} el{j} = si{j}[q];" for j in range(k))
     # results are staged in temporaries before any acc is overwritten
-    upd_tmp = "\n".join(f"        const long long r{j} = {r};" for j, r in enumerate(res))
-    upd = "\n".join(f"        acc{j} = r{j};" for j in range(k))
+    upd_tmp = "\n".join(f"        const {_CT2[acc_tys[j]]} r{j} = {g.conv(r, acc_tys[j])};" for j, r in enumerate(res))
+    upd = "\n".join(f"        acc{j} = r{j};\n        so{j}[q] = r{j};" for j in range(k))
+    store = "\n".join(f"      out{j}[base + q] = so{j}[q];" for j in range(k))
     src = _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__(256) ixg_scan_seq({", ".join(params)}) {{
-  __shared__ long long sm[{k}][{_SEQ_TILE}];
+{decl}
   __shared__ int failed;
-  {" ".join(f"long long acc{j} = ne{j};" for j in range(k))}
+  {" ".join(f"{_CT2[acc_tys[j]]} acc{j} = ne{j};" for j in range(k))}
   if (threadIdx.x == 0) failed = 0;
   for (long long base = 0; base < n; base += {_SEQ_TILE}) {{
     const int cnt = (int)min((long long){_SEQ_TILE}, n - base);
@@ -343,7 +372,6 @@ extern "C" __global__ void __launch_bounds__(256) ixg_scan_seq({", ".join(params
 {chr(10).join(g.body)}
 {upd_tmp}
 {upd}
-{wr}
       }}
       done:;
     }}
@@ -359,7 +387,9 @@ extern "C" __global__ void __launch_bounds__(256) ixg_scan_seq({", ".join(params
     return src, g.spec
 
 
-def _hist_seq_source(lam, v_type, env, site_bits):
+def _hist_seq_source(lam, v_type, env, site_bits, acc_ty="i"):
+    """hist in index order (oracle.py:313-315) on one thread; the
+    destination is filled with ne by the kernel itself."""
     g = _Gen(env, site_bits)
     g.depth = 4
     g.on_fail = "failed = 1; goto done;"
@@ -369,23 +399,32 @@ def _hist_seq_source(lam, v_type, env, site_bits):
         scope[a] = "cur"
     if b != "_":
         scope[b] = "v"
+    if acc_ty == "f":
+        g.fty.add("cur")
+    vf = v_type == "double"
+    if vf:
+        g.fty.add("v")
     res = g.expr(lam.body, scope)
-    _ints_only(g, [res])
-    params = [f"const long long* __restrict__ is", f"const {v_type}* __restrict__ vs"]
+    ct = _CT2[acc_ty]
+    vt = "double" if vf else "long long"
+    params = ["const long long* __restrict__ is", f"const {v_type}* __restrict__ vs"]
     params += [f"const {_ctype(t)}* __restrict__ a{j}, long long len{j}" for j, t in enumerate(g.spec.arrays)]
-    params += ["long long* __restrict__ dst", "long long dlen", "long long m", "int stmt", "ixg_status* st"]
+    params += [f"{ct}* __restrict__ dst", "long long dlen", "long long m", "int stmt", "ixg_status* st", f"{ct} ne"]
     params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
     src = _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__(256) ixg_hist_seq({", ".join(params)}) {{
-  __shared__ long long si[{_SEQ_TILE}], sv[{_SEQ_TILE}];
+  __shared__ long long si[{_SEQ_TILE}];
+  __shared__ {vt} sv[{_SEQ_TILE}];
   __shared__ int failed;
   if (threadIdx.x == 0) failed = 0;
+  for (long long q = threadIdx.x; q < dlen; q += blockDim.x) dst[q] = ne;
+  __syncthreads();
   for (long long base = 0; base < m; base += {_SEQ_TILE}) {{
     const int cnt = (int)min((long long){_SEQ_TILE}, m - base);
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {{
       si[q] = is[base + q];
-      sv[q] = (long long)vs[base + q];
+      sv[q] = ({vt})vs[base + q];
     }}
     __syncthreads();
     if (threadIdx.x == 0) {{
@@ -393,10 +432,11 @@ extern "C" __global__ void __launch_bounds__(256) ixg_hist_seq({", ".join(params
         const long long i = base + q;
         const long long bin = si[q];
         if ((unsigned long long)bin >= (unsigned long long)dlen) continue;
-        const long long cur = dst[bin], v = sv[q];
+        const {ct} cur = dst[bin];
+        const {vt} v = sv[q];
         (void)cur; (void)v;
 {chr(10).join(g.body)}
-        dst[bin] = {res};
+        dst[bin] = {g.conv(res, acc_ty)};
       }}
       done:;
     }}
@@ -481,19 +521,19 @@ def _elem(t: torch.Tensor) -> torch.Tensor:
 
 
 def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None, force_seq=False):
-    """scan lam nes... arrays... -> (list of k int64 tensors, sites, parallel?).
-    Output length = len(arrays[0]) (oracle.py:286); the caller checks that
-    the other operands are at least as long."""
+    """scan lam nes... arrays... -> (list of k tensors (int64, or float64 for
+    a float accumulator), sites, parallel?).  Output length = len(arrays[0])
+    (oracle.py:286); the caller checks that the other operands are at least
+    as long.  Float folds are never re-associated: the in-order kernel."""
     k = len(nes)
     dev = device or arrays[0].device
     n = arrays[0].numel()
     ins = [_elem(a)[:n] for a in arrays]
-    if any(t.is_floating_point() for t in ins) or any(isinstance(v, float) for v in nes):
-        raise Unsupported("floating-point scan")
     in_types = [_ctype(t) for t in ins]
-    outs = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(k)]
-    nev = [ctypes.c_longlong(int(v)) for v in nes]
-    par = not force_seq and classify_scan(lam, k)
+    acc_tys = fold_types(lam, k, [t.is_floating_point() for t in ins], [isinstance(v, float) for v in nes], env)
+    outs = [torch.empty(n, dtype=torch.float64 if ty == "f" else torch.int64, device=dev) for ty in acc_tys]
+    nev = [ctypes.c_double(float(v)) if ty == "f" else ctypes.c_longlong(int(v)) for v, ty in zip(nes, acc_tys)]
+    par = not force_seq and "f" not in acc_tys and classify_scan(lam, k)
     if par:
         src, ipt = _par_scan_source(lam, k, in_types)
         if n == 0:
@@ -507,7 +547,7 @@ def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None
         _launch(kern, "ixg_scan_down", tiles, 256,
                 [_p(t) for t in ins] + [_p(o) for o in outs] + [ctypes.c_longlong(n), _p(carry)], dev)
         return outs, [], True
-    src, spec = _seq_scan_source(lam, k, in_types, env, site_bits)
+    src, spec = _seq_scan_source(lam, k, in_types, env, site_bits, acc_tys)
     if n == 0:
         return outs, spec.sites, False
     kern = _kernel(src, ("ixg_scan_seq",))
@@ -517,32 +557,35 @@ def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None
     return outs, spec.sites, False
 
 
-def hist(lam, ne: int, dlen: int, is_: torch.Tensor, vs: torch.Tensor, env: dict, site_bits, status,
+def hist(lam, ne, dlen: int, is_: torch.Tensor, vs: torch.Tensor, env: dict, site_bits, status,
          force_seq=False):
-    """hist lam ne dlen is vs -> (int64 tensor [max(dlen,0)], sites, kind)
-    with kind 'cas' | 'seq' (the named fast paths are the caller's)."""
+    """hist lam ne dlen is vs -> (tensor [max(dlen,0)] int64 or float64,
+    sites, kind) with kind 'cas' | 'seq' (the named fast paths are the
+    caller's).  Float accumulations keep the index order (no CAS)."""
     from . import ops
 
     dev = is_.device
     m = min(is_.numel(), vs.numel())
     iss, vss = is_.contiguous()[:m], _elem(vs)[:m]
-    if vss.is_floating_point() or isinstance(ne, float):
-        raise Unsupported("floating-point hist")
-    dst = ops.fill(max(int(dlen), 0), int(ne), torch.int64, dev)
     v_type = _ctype(vss)
-    if not force_seq and classify_hist(lam) is not None:
+    acc_ty = fold_types(lam, 1, [vss.is_floating_point()], [isinstance(ne, float)], env)[0]
+    nd = max(int(dlen), 0)
+    if not force_seq and acc_ty == "i" and classify_hist(lam) is not None:
+        dst = ops.fill(nd, int(ne), torch.int64, dev)
         src = _hist_cas_source(lam, v_type)
-        if m and dst.numel():
+        if m and nd:
             kern = _kernel(src, ("ixg_hist_cas",))
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             grid = max(1, min((m + 255) // 256, sms * 8))
             _launch(kern, "ixg_hist_cas", grid, 256,
-                    [_p(iss), _p(vss), _p(dst), ctypes.c_longlong(dst.numel()), ctypes.c_longlong(m)], dev)
+                    [_p(iss), _p(vss), _p(dst), ctypes.c_longlong(nd), ctypes.c_longlong(m)], dev)
         return dst, [], "cas"
-    src, spec = _hist_seq_source(lam, v_type, env, site_bits)
-    if m and dst.numel():
+    dst = torch.empty(nd, dtype=torch.float64 if acc_ty == "f" else torch.int64, device=dev)
+    src, spec = _hist_seq_source(lam, v_type, env, site_bits, acc_ty)
+    if nd:
         kern = _kernel(src, ("ixg_hist_seq",))
+        nev = ctypes.c_double(float(ne)) if acc_ty == "f" else ctypes.c_longlong(int(ne))
         vals = [_p(iss), _p(vss)] + _captures(spec)
-        vals += [_p(dst), ctypes.c_longlong(dst.numel()), ctypes.c_longlong(m), ctypes.c_int(0), _p(status.t)]
+        vals += [_p(dst), ctypes.c_longlong(nd), ctypes.c_longlong(m), ctypes.c_int(0), _p(status.t), nev]
         _launch(kern, "ixg_hist_seq", 1, 256, vals + _tail(spec), dev)
     return dst, spec.sites, "seq"

@@ -159,6 +159,13 @@ def big_cases(fun):
         elif fun == "scan_lookup":
             out.append([gen.uniform(seed + 16, 97, -50, 50, np.int64).tolist(),
                         gen.uniform(seed + 17, n, 0, 96, np.int64).tolist()])
+        elif fun in ("scan_fsum", "scan_fmax"):
+            out.append([[round(float(v), 3) for v in np.random.default_rng(seed + 22).uniform(-50, 50, n)]])
+        elif fun == "scan_decay":
+            out.append([xs])
+        elif fun in ("hist_fadd", "hist_fmin"):
+            out.append([n // 4, gen.uniform(seed + 23, n, -3, n // 4 + 2, np.int64).tolist(),
+                        [round(float(v), 3) for v in np.random.default_rng(seed + 24).uniform(-9, 9, n)]])
         elif fun in ("hist_mul", "hist_lmin", "hist_last", "hist_horner"):
             bins = n // 4 if fun != "hist_horner" else 2 * n
             out.append([bins, gen.uniform(seed + 18, n, -3, bins + 2, np.int64).tolist(),

@@ -245,9 +245,14 @@ def test_fold_classifier():
 
     lams = _scanops_lambdas()
     par = {name for name, (kind, lam, k) in lams.items() if kind == "scan" and jit_fold.classify_scan(lam, k)}
-    assert par == {"scan_min", "scan_max", "scan_mul", "scan_and", "scan_pair", "scan_segmax"}
+    # (structural: a float accumulator still takes the in-order fold at run time, jit_fold.scan)
+    assert par == {"scan_min", "scan_max", "scan_mul", "scan_and", "scan_pair", "scan_segmax", "scan_fsum",
+                   "scan_fmax"}
     hk = {name: jit_fold.classify_hist(lam) for name, (kind, lam, k) in lams.items() if kind == "hist"}
-    assert hk == {"hist_mul": "mul", "hist_lmin": "min", "hist_last": None, "hist_horner": None}
+    assert hk == {"hist_mul": "mul", "hist_lmin": "min", "hist_last": None, "hist_horner": None, "hist_fadd": "add",
+                  "hist_fmin": None}
+    assert jit_fold.fold_types(lams["scan_decay"][1], 1, [False], [False]) == ["f"]  # int ne, float operator
+    assert jit_fold.fold_types(lams["scan_min"][1], 1, [False], [False]) == ["i"]
     # the corpus' own (+) and segmented (+) are associative too
     c2 = ir.from_json(PROGRAMS["own:c2_filter_sgmsum.ixl"]["program"])
     seg = [e for f in c2.defs if f.name == "sgmSum" for e in [f.body]][0]
@@ -285,6 +290,8 @@ def test_fold_kernels_compile():
 
     env = {"tbl": ("array", torch.zeros(4, dtype=torch.int64))}
     for name, (kind, lam, k) in _scanops_lambdas().items():
+        if ir.kind(lam) != "Lambda":
+            continue  # a named operator (i64.min): the executor builds its lambda
         if kind == "scan":
             types = ["long long"] * k
             if jit_fold.classify_scan(lam, k):
