@@ -352,6 +352,15 @@ def scanops(fun, a):
         return fold_hist(lambda x, y: x + y, 0.25, a[0], a[1], a[2])
     if fun == "hist_fmin":
         return fold_hist(lambda x, y: min(x, y), 100.0, a[0], a[1], a[2])
+    if fun == "pairs":
+        return [(x * 2, x > 3) for x in a[0]]
+    if fun == "unpair":
+        return [p[0] - p[1] for p in a[0]]
+    if fun == "pair_pick":
+        if not 0 <= a[1] < len(a[0]):
+            raise OracleFail(OOB, site=0)
+        x = a[0][a[1]]
+        return (x + 1, x < 0)
     if fun == "hist_mul":
         return fold_hist(lambda x, y: x * y, 1, a[0], a[1], a[2])
     if fun == "hist_lmin":

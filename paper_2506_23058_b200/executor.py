@@ -215,9 +215,17 @@ class Interp:
         return self._result(val)
 
     def _marshal(self, t, v):
+        from . import jit
+
         k = ir.kind(t)
         if k == "TFun":
             return _pred(v)
+        if k == "TArray" and ir.kind(t.elem) == "TTuple":  # list of tuples -> columns
+            if isinstance(v, jit.TupleCols):
+                return v
+            items = t.elem.items
+            rows = list(v)
+            return jit.TupleCols([self._marshal(ir.TArray(None, it), [r[j] for r in rows]) for j, it in enumerate(items)])
         if k == "TArray":
             ek = ir.kind(t.elem)
             if ek == "TBase" and t.elem.name == "bool":
@@ -248,8 +256,14 @@ class Interp:
                         break
 
     def _result(self, v):
+        from . import jit
+
         if isinstance(v, tuple):
             return tuple(self._result(x) for x in v)
+        if isinstance(v, jit.TupleCols):  # a list of tuples, as the reference's map returns
+            if self.as_tensors:
+                return v
+            return list(zip(*[self._result(c) for c in v.cols]))
         if isinstance(v, torch.Tensor):
             if self.as_tensors:
                 return v
@@ -308,8 +322,14 @@ class Interp:
         if k == "TupleE":
             return tuple(self._eval(x, env, f, fs) for x in e.items)
         if k == "IndexE":
+            from . import jit
+
             arr = self._eval(e.arr, env, f, fs)
             idx = self._eval(e.idx, env, f, fs)
+            if isinstance(arr, jit.TupleCols):
+                if not 0 <= idx < arr.numel():
+                    raise errors.OutOfBounds(ir.expr_str(e), e.pos)
+                return tuple((bool(c[idx].item()) if c.dtype == torch.bool else c[idx].item()) for c in arr.cols)
             if not isinstance(arr, torch.Tensor):
                 raise errors.OracleError(f"indexing a non-array: {ir.expr_str(e)}")
             n = arr.numel()
@@ -346,6 +366,23 @@ class Interp:
                 cenv = self._captured(env)
             st = ops.Status(self.dev)
             bits = lambda node: self._bits(fs, node)  # noqa: E731
+            kt = jit.tuple_arity(lam.body, self.funs) if ir.kind(lam) == "Lambda" else 1
+            if kt > 1 or any(isinstance(a, jit.TupleCols) for a in arrs):
+                # tuple-valued lambdas / arrays of tuples: NVRTC path only
+                try:
+                    out, sites = jit.map_jit(lam, arrs, cenv, bits, n, st, device=self.dev, funs=self.funs,
+                                             bits_for=self._bits_for_caller(fs), loop_cap=self.budget, k_out=kt)
+                except vm.Unsupported as ex:
+                    raise NotImplementedError(f"map: {ex}") from ex
+                self._raise_site(st, sites)
+                if kt == 1:
+                    return out.to(torch.bool) if _is_bool_expr(lam.body, self.funs) else out
+                body = lam.body
+                while ir.kind(body) == "Let":
+                    body = body.body
+                items = body.items if ir.kind(body) == "TupleE" else [None] * kt
+                return jit.TupleCols([o.to(torch.bool) if it is not None and _is_bool_expr(it, self.funs) else o
+                                      for o, it in zip(out, items)])
             out = None
             if jit.enabled():  # the lambda compiled to its own kernel (NVRTC, cached)
                 try:

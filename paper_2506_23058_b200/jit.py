@@ -173,7 +173,8 @@ class _Gen:
 
     # ------------------------------------------------------------ inference
     def _tenv(self, scope: dict) -> dict:
-        return {n: ("f" if self.is_f(c) else "i") for n, c in scope.items()}
+        return {n: ([("f" if self.is_f(x) else "i") for x in c] if isinstance(c, list) else
+                    ("f" if self.is_f(c) else "i")) for n, c in scope.items()}
 
     def infer(self, e, tenv: dict, env=None):
         """'i' | 'f' of a scalar expression, a list of those for a tuple."""
@@ -260,6 +261,8 @@ class _Gen:
             return f"{int(e.value)}LL"
         if k == "VarE":
             if e.name in scope:
+                if isinstance(scope[e.name], list):
+                    raise Unsupported(f"tuple {e.name} in a scalar position")
                 return scope[e.name]
             b = self.env.get(e.name)
             if b is None:
@@ -372,9 +375,13 @@ class _Gen:
         oracle.py:286-290, a multi-parameter loop, a tuple-returning
         function), evaluated left to right like TupleE (oracle.py:199-200);
         Let and If may wrap the tuple."""
+        kd = ir.kind(e)
+        if kd == "VarE" and isinstance(scope.get(e.name), list):  # an element of an array of tuples
+            if len(scope[e.name]) != k:
+                raise Unsupported("tuple arity")
+            return list(scope[e.name])
         if k == 1:
             return [self.expr(e, scope)]
-        kd = ir.kind(e)
         if kd == "TupleE":
             if len(e.items) != k:
                 raise Unsupported("operator result arity")
@@ -497,6 +504,38 @@ class _Gen:
             self.env, self.site_bits = saved
 
 
+class TupleCols:
+    """An array of k-tuples (`map` with a tuple-valued lambda, oracle.py:280
+    returns a list of tuples) held as k device columns."""
+
+    def __init__(self, cols: list):
+        self.cols = list(cols)
+
+    def numel(self) -> int:
+        return self.cols[0].numel() if self.cols else 0
+
+    def __len__(self) -> int:
+        return self.numel()
+
+
+def tuple_arity(e, funs=None) -> int:
+    """k of a tuple-valued expression (TupleE, through let / if / loops /
+    calls of tuple-returning functions), 1 for a scalar."""
+    k = ir.kind(e)
+    if k == "TupleE":
+        return len(e.items)
+    if k == "Let":
+        return tuple_arity(e.body, funs)
+    if k == "If":
+        return tuple_arity(e.then, funs)
+    if k == "Loop":
+        return len(e.params)
+    if k == "App" and ir.kind(e.fun) == "VarE" and funs and e.fun.name in funs:
+        rt = funs[e.fun.name].result_type
+        return len(rt.items) if ir.kind(rt) == "TTuple" else 1
+    return 1
+
+
 def _ctype(t: torch.Tensor) -> str:
     if t.dtype not in _CT:
         raise Unsupported(f"element type {t.dtype}")
@@ -517,18 +556,26 @@ def generate(lam, arrays: list, env: dict, site_bits=lambda node: L.V_BOUNDS, ou
     if len(lam.params) != len(arrays):
         raise Unsupported("lambda arity")
     g = _Gen(env, site_bits, funs, bits_for, loop_cap)
-    g.spec.inputs = list(arrays)
+    flat = []  # per-element input columns (an array of tuples contributes one per component)
     scope = {}
     loads = []
-    for j, (p, t) in enumerate(zip(lam.params, arrays)):
-        ct = _ctype(t)
-        if t.is_floating_point():
-            loads.append(f"    const double x{j} = in{j}[i];")
-            g.fty.add(f"x{j}")
-        else:
-            loads.append(f"    const long long x{j} = (long long)in{j}[i];")
+    for p, a in zip(lam.params, arrays):
+        cols = a.cols if isinstance(a, TupleCols) else [a]
+        names = []
+        for t in cols:
+            j = len(flat)
+            flat.append(t)
+            _ctype(t)
+            if t.is_floating_point():
+                loads.append(f"    const double x{j} = in{j}[i];")
+                g.fty.add(f"x{j}")
+            else:
+                loads.append(f"    const long long x{j} = (long long)in{j}[i];")
+            names.append(f"x{j}")
         if p != "_":
-            scope[p] = f"x{j}"
+            scope[p] = names if isinstance(a, TupleCols) else names[0]
+    arrays = flat
+    g.spec.inputs = list(flat)
     res = g.tuple_expr(lam.body, scope, k_out)
     tys = ["f" if g.is_f(r) else "i" for r in res]
     if out_dtype is not None and k_out == 1:

@@ -159,6 +159,12 @@ def big_cases(fun):
         elif fun == "scan_lookup":
             out.append([gen.uniform(seed + 16, 97, -50, 50, np.int64).tolist(),
                         gen.uniform(seed + 17, n, 0, 96, np.int64).tolist()])
+        elif fun == "pairs":
+            out.append([xs])
+        elif fun == "unpair":
+            out.append([list(zip(xs, gen.uniform(seed + 25, n, -500, 500, np.int64).tolist()))])
+        elif fun == "pair_pick":
+            out += [[xs, 0], [xs, n - 1], [xs, n // 3]]
         elif fun in ("scan_fsum", "scan_fmax"):
             out.append([[round(float(v), 3) for v in np.random.default_rng(seed + 22).uniform(-50, 50, n)]])
         elif fun == "scan_decay":
@@ -229,6 +235,8 @@ def error_cases(fun):
     if fun == "row_corr":
         return [[2, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],                  # ptr[row + 1] OOB
                 [0, [0, 3], [1.0], [0.5, 1.0, 2.0], [0, 0, 0]]]                  # vals[lo + j] OOB at j = 2
+    if fun == "pair_pick":
+        return [[[1, 2, 3], 3], [[1, 2, 3], -1], [[], 0]]
     if fun == "countdown":
         return [[[3, -1, 5]], [[0] * 40 + [-2]]]                         # never-ending while loop
     if fun == "scan_lookup":

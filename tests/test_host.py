@@ -107,10 +107,12 @@ def test_expr_str_matches_reference_sites():
 
 
 def _calls_program_function(e, prog):
-    """loops and calls of program functions inside a lambda are compiled by
-    the NVRTC path only (jit.py), not the register VM"""
+    """loops, tuples and calls of program functions inside a lambda are
+    compiled by the NVRTC path only (jit.py), not the register VM"""
     names = {f.name for f in prog.defs}
-    if ir.kind(e) == "Loop" or (ir.kind(e) == "App" and ir.kind(e.fun) == "VarE" and e.fun.name in names):
+    if ir.kind(e) in ("Loop", "TupleE") or (ir.kind(e) == "App" and ir.kind(e.fun) == "VarE" and e.fun.name in names):
+        return True
+    if ir.kind(e) == "Let" and len(e.names) > 1:
         return True
     return any(_calls_program_function(c, prog) for c in ir.children(e))
 

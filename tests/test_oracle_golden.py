@@ -89,7 +89,7 @@ def run_oracle(fun, a):
         return list(a[0])
     if fun == "all_rows":
         return [O.kmeans_ker(r, a[0], a[1], a[2], a[3]) for r in range(len(a[0]) - 1)]
-    if fun.startswith(("scan_", "hist_")):
+    if fun.startswith(("scan_", "hist_")) or fun in ("pairs", "unpair", "pair_pick"):
         return O.scanops(fun, a)
     raise KeyError(fun)
 
