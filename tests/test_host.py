@@ -212,8 +212,18 @@ def test_jit_generates_and_compiles_corpus_lambdas():
                         env.setdefault(nm, ("array", torch.zeros(4, dtype=torch.int64)))
                     for nm in lets:
                         env.setdefault(nm, ("array", torch.zeros(4, dtype=torch.int64)))
-                    arrs = [torch.zeros(4, dtype=torch.int64) for _ in lam.params]
-                    src, spec = jit.generate(lam, arrs, env, funs={g.name: g for g in prog.defs})
+                    funs = {g.name: g for g in prog.defs}
+                    tup = {}  # parameters destructured by a tuple let: arrays of tuples
+
+                    def find(x):
+                        if ir.kind(x) == "Let" and len(x.names) > 1 and ir.kind(x.rhs) == "VarE":
+                            tup[x.rhs.name] = len(x.names)
+                        for c in ir.children(x):
+                            find(c)
+                    find(lam.body)
+                    arrs = [jit.TupleCols([torch.zeros(4, dtype=torch.int64)] * tup[p]) if p in tup else
+                            torch.zeros(4, dtype=torch.int64) for p in lam.params]
+                    src, spec = jit.generate(lam, arrs, env, funs=funs, k_out=jit.tuple_arity(lam.body, funs))
                     if src not in seen:
                         seen.add(src)
                         err, prog_ = nvrtc.nvrtcCreateProgram(src.encode(), b"m.cu", 0, [], [])
