@@ -52,6 +52,9 @@ constexpr uint32_t kNonceMask = 0xffffffu;
 #endif
 constexpr int kSlotStride = IXG_SLOT_STRIDE;
 constexpr int kPerLane = IXG_LB_PER_LANE;
+#ifndef IXG_LB_SLEEP
+#define IXG_LB_SLEEP 0  // ns between re-polls of unready slots (0: 32 tight spins, then 16 ns)
+#endif
 
 IXG_DEV ulonglong2* slot_at(const LBChan& ch, long long tile) { return ch.slot + tile * kSlotStride; }
 
@@ -172,7 +175,11 @@ IXG_DEV typename M::T lb_lookback(const LBChan& ch, uint32_t nonce, long long ti
 #ifdef IXG_TRACE
       ++tr_spins;
 #endif
-      if (++spins > 32) __nanosleep(16);
+      if (IXG_LB_SLEEP) {
+        __nanosleep(IXG_LB_SLEEP);
+      } else if (++spins > 32) {
+        __nanosleep(16);
+      }
 #pragma unroll
       for (int j = 0; j < kPerLane; ++j) {
         const long long idx = pred - (lane * kPerLane + j);
