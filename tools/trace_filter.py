@@ -44,6 +44,8 @@ def main():
     for _ in range(3):
         if what == "c2":
             ops.c2(xs, Pred.ge(0), shape, 0, st, ys=ys, zs=zs, d_k=dk)
+        elif what == "part2":
+            ops.partition2(xs, Pred.lt(0), 0, st, ys=ys, d_nt=dk)
         else:
             ops.filter(xs, Pred.ge(0), 0, st, ys=ys, d_count=dk)
     torch.cuda.synchronize()
@@ -88,7 +90,7 @@ def main():
         phase(a, "store", 4, 6)
     cum = {c: int(np.median(a[:, c] - a[:, 0])) for c in range(1, 18) if a[:, c].any() and c not in (7, 13)}
     print("  cumulative medians from start (slot: ns):", cum)
-    for r in (100, 5000, 15000):
+    for r in [x for x in (100, 5000, 15000) if x < tiles]:
         print(f"  tile {r}:", {c: int(a[r, c] - a[r, 0]) for c in (1, 2, 3, 4, 5, 6, 14, 15, 16, 17)})
     print("  frac slot5 > slot4:", float(np.mean(a[:, 5] > a[:, 4])))
     life = a[:, end] - a[:, 0]
