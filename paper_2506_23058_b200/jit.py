@@ -627,6 +627,7 @@ class _Kernel:
         nvrtc.nvrtcDestroyProgram(prog)
         (err,) = driver.cuInit(0)
         _ok(err, "cuInit")
+        torch.cuda.synchronize()  # the runtime's primary context is current on this thread
         err, self.module = driver.cuModuleLoadData(cubin)
         _ok(err, "cuModuleLoadData")
         self.fns = {}
