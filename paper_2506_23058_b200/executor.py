@@ -118,6 +118,8 @@ def _dev_i64(a, dev) -> torch.Tensor:
 
 def _dev_u8(a, dev) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
+        if a.dtype == torch.bool and a.device == dev and a.is_contiguous():
+            return a.view(torch.uint8)
         return (a != 0).to(device=dev, dtype=torch.uint8).contiguous()
     return torch.tensor([1 if bool(x) else 0 for x in a], dtype=torch.uint8, device=dev)
 
@@ -229,7 +231,7 @@ class Interp:
         if k == "TArray":
             ek = ir.kind(t.elem)
             if ek == "TBase" and t.elem.name == "bool":
-                return _dev_u8(v, self.dev).to(torch.bool)
+                return _dev_u8(v, self.dev).view(torch.bool)
             if ek == "TBase" and t.elem.name in ("f32", "f64"):
                 return _dev_f64(v, self.dev)
             return _dev_i64(v, self.dev)
@@ -376,18 +378,20 @@ class Interp:
                     raise NotImplementedError(f"map: {ex}") from ex
                 self._raise_site(st, sites)
                 if kt == 1:
-                    return out.to(torch.bool) if _is_bool_expr(lam.body, self.funs) else out
+                    return _as_bool(out) if _is_bool_expr(lam.body, self.funs) else out
                 body = lam.body
                 while ir.kind(body) == "Let":
                     body = body.body
                 items = body.items if ir.kind(body) == "TupleE" else [None] * kt
-                return jit.TupleCols([o.to(torch.bool) if it is not None and _is_bool_expr(it, self.funs) else o
+                return jit.TupleCols([_as_bool(o) if it is not None and _is_bool_expr(it, self.funs) else o
                                       for o, it in zip(out, items)])
             out = None
+            is_bool = _is_bool_expr(lam.body, self.funs)
             if jit.enabled():  # the lambda compiled to its own kernel (NVRTC, cached)
                 try:
                     out, sites = jit.map_jit(lam, arrs, cenv, bits, n, st, device=self.dev, funs=self.funs,
-                                             bits_for=self._bits_for_caller(fs), loop_cap=self.budget)
+                                             bits_for=self._bits_for_caller(fs), loop_cap=self.budget,
+                                             out_dtype=torch.uint8 if is_bool else None)
                 except vm.Unsupported:
                     out = None
             if out is None:  # the register VM
@@ -395,7 +399,7 @@ class Interp:
                 out = ops.map_vm(comp, n, st, device=self.dev)
                 sites = comp.sites
             self._raise_site(st, sites)
-            return out.to(torch.bool) if _is_bool_expr(lam.body, self.funs) else out
+            return _as_bool(out) if is_bool else out
         if name == "scan":
             kk = (len(e.args) - 1) // 2
             op = ev(e.args[0])
@@ -408,8 +412,8 @@ class Interp:
                 n = arrs[0].numel()
                 if arrs[1].numel() < n:
                     raise errors.OracleError("scan: value array shorter than flags")
-                v, fl = ops.segscan_add(arrs[0].to(torch.uint8), arrs[1][:n], want_flags=True)
-                return (fl.to(torch.bool), v)
+                v, fl = ops.segscan_add(_u8(arrs[0]), arrs[1][:n], want_flags=True)
+                return (_as_bool(fl), v)
             return self._scan_generic(e, op, nes, arrs, env, fs)
         if name == "scatter":
             dst, is_, vs = ev(e.args[0]), ev(e.args[1]), ev(e.args[2])
@@ -442,13 +446,13 @@ class Interp:
             except jit_fold.Unsupported as ex:
                 raise NotImplementedError(f"hist operator: {ex}") from ex
             self._raise_site(st, sites)
-            return dst.to(torch.bool) if _is_bool_expr(op.body) else dst
+            return _as_bool(dst) if _is_bool_expr(op.body) else dst
         if name == "iota":
             return ops.iota(int(ev(e.args[0])), self.dev)
         if name == "replicate":
             n, v = ev(e.args[0]), ev(e.args[1])
             if isinstance(v, bool):
-                return ops.fill(n, int(v), torch.uint8, self.dev).to(torch.bool)
+                return ops.fill(n, int(v), torch.uint8, self.dev).view(torch.bool)
             return ops.fill(n, int(v), torch.int64, self.dev)
         if name == "length":
             a = ev(e.args[0])
@@ -485,7 +489,7 @@ class Interp:
             raise NotImplementedError(f"scan operator: {ex}") from ex
         self._raise_site(st, sites)
         kk = len(nes)
-        res = [o.to(torch.bool) if _scan_comp_is_bool(op, j, nes, arrs) else o for j, o in enumerate(outs)]
+        res = [_as_bool(o) if _scan_comp_is_bool(op, j, nes, arrs) else o for j, o in enumerate(outs)]
         return tuple(res) if kk > 1 else res[0]
 
     def _raise_site(self, st, sites):
@@ -534,7 +538,7 @@ class Interp:
         out = {}
         for k, v in env.items():
             if isinstance(v, torch.Tensor):
-                out[k] = ("array", v if v.dtype != torch.bool else v.to(torch.uint8))
+                out[k] = ("array", _u8(v) if v.dtype == torch.bool else v)
             elif isinstance(v, Pred):
                 out[k] = ("pred", v)
             elif isinstance(v, (bool, int)):
@@ -743,6 +747,18 @@ def _is_segsum(op) -> bool:
     ok_v = (getattr(th, "name", None) == v2 and ir.kind(el) == "BinOp" and el.op == "+"
             and {getattr(res(el.lhs), "name", None), getattr(res(el.rhs), "name", None)} == {v1, v2})
     return ok_f and ok_v
+
+
+def _u8(t: torch.Tensor) -> torch.Tensor:
+    """bool -> uint8 without a copy (same 1-byte 0/1 storage)."""
+    return t.view(torch.uint8) if t.dtype == torch.bool else t.to(torch.uint8)
+
+
+def _as_bool(t: torch.Tensor) -> torch.Tensor:
+    """A 0/1 array as bool: a view when it is already one byte per element."""
+    if t.dtype == torch.bool:
+        return t
+    return t.view(torch.bool) if t.dtype == torch.uint8 else t.ne(0)
 
 
 def _named_lambda(op: str):

@@ -517,7 +517,7 @@ def _ints_only(g, res):
 
 
 def _elem(t: torch.Tensor) -> torch.Tensor:
-    return t.to(torch.uint8) if t.dtype == torch.bool else t.contiguous()
+    return t.view(torch.uint8) if t.dtype == torch.bool else t.contiguous()
 
 
 def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None, force_seq=False):

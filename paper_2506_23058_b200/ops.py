@@ -248,7 +248,7 @@ def filter(xs: torch.Tensor, p: Pred, variant: int, status: Status, ys=None, d_c
 
 def filter_by(cs: torch.Tensor, xs: torch.Tensor, variant: int, status: Status):
     """filter_by cs xs (maxmatching.ixl:1-9)."""
-    cs, xs = _contig(cs.to(torch.uint8)), _contig(xs)
+    cs, xs = _contig(cs.view(torch.uint8) if cs.dtype == torch.bool else cs.to(torch.uint8)), _contig(xs)
     n = xs.numel()
     ys = torch.empty(n, dtype=xs.dtype, device=xs.device)
     d_count = torch.empty(1, dtype=torch.int64, device=xs.device)
