@@ -1,7 +1,7 @@
 """Summarise an ncu report (development tool).
 
 python tools/ncu_summary.py rep.ncu-rep [...]
-python tools/ncu_summary.py --json profiles/ncu_c2_full.json --source "..." rep.ncu-rep
+python tools/ncu_summary.py --json profiles/ncu_c2_full.json --source "..." [--units N] rep.ncu-rep
     also writes {kernel, dram_bytes_per_launch, ...} for the first kernel in
     the report (bench.py reads `dram_bytes_per_launch` as roofline.traffic).
 """
@@ -49,12 +49,15 @@ def main(path):
         print("  top stalls:", ", ".join(f"{n}={x:.2f}" for x, n in stalls[:6]))
 
 
-def write_json(path, out, source):
+def write_json(path, out, source, units=None):
     h, u, v = next(iter(kernels(path)))
     rd, wr = value(h, u, v, "dram__bytes_read.sum"), value(h, u, v, "dram__bytes_write.sum")
     t = value(h, u, v, "gpu__time_duration.sum")
     doc = {"kernel": v[h.index("Kernel Name")][:120], "dram_bytes_read": rd, "dram_bytes_write": wr,
            "dram_bytes_per_launch": rd + wr, "gpu_time_s": t, "dram_gbs": (rd + wr) / t / 1e9, "source": source}
+    if units:
+        doc["units"] = units
+        doc["dram_bytes_per_unit"] = (rd + wr) / units
     with open(out, "w") as f:
         json.dump(doc, f, indent=1)
     print("wrote", out, doc)
@@ -63,11 +66,13 @@ def write_json(path, out, source):
 if __name__ == "__main__":
     args = sys.argv[1:]
     if args and args[0] == "--json":
-        out, src = args[1], ""
+        out, src, units = args[1], "", None
         args = args[2:]
         if args[0] == "--source":
             src, args = args[1], args[2:]
-        write_json(args[0], out, src)
+        if args[0] == "--units":
+            units, args = int(args[1]), args[2:]
+        write_json(args[0], out, src, units)
     else:
         for p in args:
             main(p)
