@@ -330,8 +330,8 @@ class C1:
         self.workload = (f"partition2 (x < 0), N=2^{self.N.bit_length() - 1} int32 uniform over int32"
                          + (" per GPU (2^32 total)" if big else "")
                          + (f"; {ws} contiguous shards: all-gather of per-shard true counts -> each shard's two "
-                            "output runs of the global result, moved to the shards owning their positions "
-                            "(one NCCL all-to-all per class)" if ws > 1 else ""))
+                            "output runs of the global result, moved to the shards owning their positions"
+                            if ws > 1 else ""))
 
     def setup_device(self):
         import torch
@@ -362,7 +362,9 @@ class C1:
                     self.peer = D.GpuPart2PeerLocal(self.xs, self.p)
                 except Exception as e:  # no CUDA IPC between the ranks' GPUs
                     self.exchange = f"nccl (fused setup failed: {type(e).__name__})"
-            self.workload += f"; exchange: {self.exchange}"
+            self.workload += ("; exchange: peer stores over NVLink fused into the partition kernel (CUDA IPC)"
+                              if self.exchange == "fused" else f"; exchange: one NCCL all-to-all per class "
+                              f"({self.exchange})")
 
     def pre_step(self):
         """between timed steps, outside the timed region: a 256 MB write
