@@ -95,3 +95,39 @@ def test_partition2l_pipeline_large(cuda, m):
     want = O.partition2l(shp, cs.astype(np.int64), xs)
     got = eval_program(prog, "partition2L", [shp.tolist(), cs.tolist(), xs.tolist()], as_tensors=True)
     assert np.array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("mode", ["selected", "checked", "generic"])
+def test_drop_in_at_scale(cuda, mode):
+    """The drop-in eval_program on the reference's own corpus at 2^22 int64
+    elements (device tensors in, device tensors out), every execution mode
+    against the C restatement: partition2, filter, partition3, C2."""
+    import numpy as np
+    import torch
+
+    from oracle import ixoracle as O
+    from paper_2506_23058_b200 import gen
+    from paper_2506_23058_b200.executor import eval_program
+    from paper_2506_23058_b200.pred import Pred
+
+    n = 1 << 22
+    xs_h = gen.uniform(41, n, -(1 << 40), 1 << 40, np.int64)
+    xs = torch.from_numpy(xs_h).to(cuda)
+    kw = {"variant": "checked" if mode == "checked" else "selected", "generic_only": mode == "generic",
+          "as_tensors": True}
+    p, q = Pred.lt(0), Pred.hash(0xC0FFEE)
+    nt, ys = eval_program(program("ref:partition2.ixl"), "partition2", [p, xs], **kw)
+    wnt, wys = O.partition2(p, xs_h)
+    assert nt == wnt and np.array_equal(ys.cpu().numpy(), wys)
+    ys = eval_program(program("ref:filter.ixl"), "filter", [q, xs], **kw)
+    assert np.array_equal(ys.cpu().numpy(), O.filter_(q, xs_h))
+    m1, m2, ys = eval_program(program("ref:partition3.ixl"), "partition3", [p, q, xs], **kw)
+    w1, w2, wys = O.partition3(p, q, xs_h)
+    assert (m1, m2) == (w1, w2) and np.array_equal(ys.cpu().numpy(), wys)
+    small = gen.uniform(42, n, -128, 127, np.int64)
+    k = int(np.count_nonzero(small >= 0))
+    shape = gen.segment_shape(43, 1 << 14, k)
+    ys, zs = eval_program(program("own:c2_filter_sgmsum.ixl"), "c2",
+                          [Pred.ge(0), torch.from_numpy(small).to(cuda), torch.from_numpy(shape).to(cuda)], **kw)
+    wys, wzs = O.c2(Pred.ge(0), small, shape)
+    assert np.array_equal(ys.cpu().numpy(), wys) and np.array_equal(zs.cpu().numpy(), wzs)
