@@ -575,8 +575,15 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       }
     }
     __syncwarp();
-    IXG_TR_LANE0(5);
+#ifdef IXG_TRACE
+    unsigned long long t5__;
+    IXG_TR_NOW(t5__);  // every lane: a divergent trace store here would let the warp's other lanes
+                       // complete the (per-warp counted) barrier early
+#endif
     bar_sync(2, kBT + 32);
+#ifdef IXG_TRACE
+    if (lane_id() == 0 && blockIdx.x < (1u << 17)) g_trace[blockIdx.x * IXG_TRS + 5] = t5__;
+#endif
     if (lane_id() == 0) {
       const int cnt = s_cnt;
       if (tile > 0) lb_publish<SumOp>(ch, nonce, tile, SumOp::T{ex + cnt}, true);
@@ -703,8 +710,27 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     }
   }
   IXG_TR(3);
+#ifdef IXG_TRACE
+  __shared__ unsigned long long s_arr__[kBW];  // each worker warp's arrival at bar 2
+  {
+    unsigned long long ta__;
+    IXG_TR_NOW(ta__);
+    if (l == 0) s_arr__[w] = ta__;
+  }
+#endif
   bar_sync(2, kBT + 32);  // base resolved; every worker's compaction done
   IXG_TR(4);
+#ifdef IXG_TRACE
+  if (t == 0 && blockIdx.x < (1u << 17)) {
+    unsigned long long mx = 0, mn = ~0ull;
+    for (int q = 0; q < kBW; ++q) {
+      mx = s_arr__[q] > mx ? s_arr__[q] : mx;
+      mn = s_arr__[q] < mn ? s_arr__[q] : mn;
+    }
+    g_trace[blockIdx.x * IXG_TRS + 18] = mx;
+    g_trace[blockIdx.x * IXG_TRS + 19] = mn;
+  }
+#endif
   const long long base = s_excl;
   // kSeg: thread t scans the output piece [q0, q1) of odd length L (L <= 49
   // outputs: its flags span <= 3 bitmap words); the L2 loads of those words

@@ -89,6 +89,11 @@ def main():
     else:
         phase(a, "store", 4, 6)
     cum = {c: int(np.median(a[:, c] - a[:, 0])) for c in range(1, 18) if a[:, c].any() and c not in (7, 13)}
+    if a[:, 18].any():
+        lb, last, first = a[:, 5] - a[:, 0], a[:, 18] - t0 - a[:, 0], a[:, 19] - t0 - a[:, 0]
+        print(f"  bar 2: first worker warp arrives {np.median(first):.0f}, last {np.median(last):.0f}, "
+              f"look-back warp {np.median(lb):.0f} (median); look-back warp last in "
+              f"{100 * np.mean(lb > last):.0f} % of tiles, by median {np.median(np.maximum(lb - last, 0)):.0f}")
     print("  cumulative medians from start (slot: ns):", cum)
     for r in [x for x in (100, 5000, 15000) if x < tiles]:
         print(f"  tile {r}:", {c: int(a[r, c] - a[r, 0]) for c in (1, 2, 3, 4, 5, 6, 14, 15, 16, 17)})
