@@ -170,8 +170,8 @@ class Interp:
             v |= (s.bits & 0xF) << (4 * i)
         return v
 
-    def _raise(self, st: ops.Status, fdef, site_map=None):
-        s = st.read()
+    def _raise(self, st: ops.Status, fdef, site_map=None, s=None):
+        s = st.read() if s is None else s
         if s.ok:
             if s.narrow:
                 raise errors.NarrowingOverflow("a result does not fit its 32-bit storage")
@@ -566,8 +566,8 @@ class Interp:
         p, xs = _pred(a[0]), _dev_i64(a[1], self.dev)
         st = ops.Status(self.dev)
         ys, dk = ops.filter(xs, p, self._variant(f), st)
-        k = int(dk.item())
-        self._raise(st, f)
+        s, (k,) = st.read_with(dk)
+        self._raise(st, f, s=s)
         return self._out(ys, k)
 
     def _p_filter_by(self, f, a):
@@ -576,8 +576,8 @@ class Interp:
             raise errors.OracleError("map arrays disagree on length")  # map2 c o (maxmatching.ixl:6)
         st = ops.Status(self.dev)
         ys, dk = ops.filter_by(cs, xs, self._variant(f), st)
-        k = int(dk.item())
-        self._raise(st, f)
+        s, (k,) = st.read_with(dk)
+        self._raise(st, f, s=s)
         return self._out(ys, k)
 
     def _p_partition2l(self, f, a):
@@ -619,16 +619,16 @@ class Interp:
         p, xs = _pred(a[0]), _dev_i64(a[1], self.dev)
         st = ops.Status(self.dev)
         ys, dnt = ops.partition2(xs, p, self._variant(f), st)
-        nt = int(dnt.item())
-        self._raise(st, f)
+        s, (nt,) = st.read_with(dnt)
+        self._raise(st, f, s=s)
         return (nt, self._out(ys))
 
     def _p_partition3(self, f, a):
         p, q, xs = _pred(a[0]), _pred(a[1]), _dev_i64(a[2], self.dev)
         st = ops.Status(self.dev)
         ys, dm = ops.partition3(xs, p, q, self._variant(f), st)
-        m1, m2 = dm.cpu().tolist()
-        self._raise(st, f)
+        s, (m1, m2) = st.read_with(dm)
+        self._raise(st, f, s=s)
         return (m1, m2, self._out(ys))
 
     def _p_mksgmdescr(self, f, a):
@@ -661,8 +661,8 @@ class Interp:
         variant = self._variant(filt) | (self._variant(mkf) << 8)
         st = ops.Status(self.dev)
         ys, zs, dk = ops.c2(xs, p, shape, variant, st, z_dtype=torch.int64)
-        k = int(dk.item())
-        self._raise(st, f, lambda s: (filt, s) if s < 2 else (mkf, s - 2))
+        s, (k,) = st.read_with(dk)
+        self._raise(st, f, lambda s: (filt, s) if s < 2 else (mkf, s - 2), s=s)
         return (self._out(ys, k), self._out(zs, k))
 
     def _p_get_smallest_pairs(self, f, a):

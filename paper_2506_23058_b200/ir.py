@@ -301,8 +301,18 @@ def canonical(fundef) -> str:
     return f"(def ({sizes}) ({params}) {ex(fundef.body)})"
 
 
+_FP_CACHE: dict = {}  # id(fundef) -> (fundef, fingerprint): programs are immutable values
+
+
 def fingerprint(fundef) -> str:
-    return hashlib.sha256(canonical(fundef).encode()).hexdigest()[:16]
+    hit = _FP_CACHE.get(id(fundef))
+    if hit is not None and hit[0] is fundef:
+        return hit[1]
+    fp = hashlib.sha256(canonical(fundef).encode()).hexdigest()[:16]
+    if len(_FP_CACHE) > 4096:
+        _FP_CACHE.clear()
+    _FP_CACHE[id(fundef)] = (fundef, fp)
+    return fp
 
 
 def find_def(program, name: str):

@@ -134,6 +134,20 @@ class Status:
         h = self.t.cpu().numpy().view("uint64")
         return StatusView(int(h[0]), int(h[1]) & 0xFFFFFFFF, int(h[1]) >> 32)
 
+    def read_with(self, *scalars: torch.Tensor):
+        """The status and some device int64 scalars (counts) in one host
+        round trip: async copies into a pinned buffer, one stream sync."""
+        n = 2 + sum(int(t.numel()) for t in scalars)
+        h = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        h[:2].copy_(self.t, non_blocking=True)
+        o = 2
+        for t in scalars:
+            h[o:o + t.numel()].copy_(t.reshape(-1).to(torch.int64), non_blocking=True)
+            o += t.numel()
+        torch.cuda.current_stream(self.t.device).synchronize()
+        u = h[:2].numpy().view("uint64")
+        return StatusView(int(u[0]), int(u[1]) & 0xFFFFFFFF, int(u[1]) >> 32), h[2:].tolist()
+
 
 # ------------------------------------------------------------------ builtins
 def scan_add(xs: torch.Tensor, ne: int = 0, exclusive: bool = False, out=None) -> torch.Tensor:

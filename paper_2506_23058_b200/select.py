@@ -184,15 +184,38 @@ def frozen() -> dict:
     return _FROZEN
 
 
+_SEL_CACHE: dict = {}  # (id(program), id(fundef), live | checked) -> (program, fundef, selection)
+
+
+def _cached(key, program, fundef, make):
+    hit = _SEL_CACHE.get(key)
+    if hit is not None and hit[0] is program and hit[1] is fundef:
+        return hit[2]
+    v = make()
+    if len(_SEL_CACHE) > 4096:
+        _SEL_CACHE.clear()
+    _SEL_CACHE[key] = (program, fundef, v)
+    return v
+
+
 def checked_selection(fundef) -> FunSelection:
     """Every site CHECKED: the reference interpreter's own behaviour."""
+    return _cached((None, id(fundef), "checked"), None, fundef, lambda: _checked_selection(fundef))
+
+
+def _checked_selection(fundef) -> FunSelection:
     sites = [SiteVerdict(k, pos, ir.expr_str(n)) for k, pos, n in ir.sites(fundef)]
     return FunSelection(fundef.name, ir.fingerprint(fundef), "checked (no verdict)", sites)
 
 
 def selection_for(program, fundef, live: bool = True) -> FunSelection:
     """Verdicts for one function: live verifier when importable, else the
-    frozen corpus table by fingerprint, else all CHECKED."""
+    frozen corpus table by fingerprint, else all CHECKED (memoised per
+    program and function object)."""
+    return _cached((id(program), id(fundef), live), program, fundef, lambda: _selection_for(program, fundef, live))
+
+
+def _selection_for(program, fundef, live: bool) -> FunSelection:
     fp = ir.fingerprint(fundef)
     fz = frozen().get(fp)
     if fz is not None:
