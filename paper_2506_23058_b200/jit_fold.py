@@ -35,7 +35,6 @@ import hashlib
 
 import torch
 
-from . import _lib as L
 from . import ir
 from .jit import _CACHE, _PRELUDE, LAUNCHES, _ctype, _Gen, _Kernel, _ok, _scalar_param, scalar_args
 from .vm import Unsupported
