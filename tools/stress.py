@@ -1,0 +1,100 @@
+"""Randomised parity sweep of the ELIDED kernels against the C restatement
+(test infrastructure: development tool, not part of the product).
+
+Random sizes (ragged tiles, one-tile, multi-wave), predicates (selectivity
+0 .. 1, edge thresholds), element types, for filter / partition2 /
+partition3 / C2, each checked bit for bit against oracle/ixoracle.  Runs
+for --seconds (default 300) and prints a JSON summary; exits 1 on the first
+mismatch.
+
+python tools/stress.py [--seconds S] [--max-log2 L]
+"""
+
+import argparse
+import json
+import os
+import random
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import ixoracle as O  # noqa: E402
+from paper_2506_23058_b200 import _lib as L  # noqa: E402
+from paper_2506_23058_b200 import gen, ops  # noqa: E402
+from paper_2506_23058_b200.pred import Pred  # noqa: E402
+
+
+def rand_pred(rng, lo, hi):
+    kind = rng.choice(["lt", "ge", "gt", "le", "eq", "ne", "hash", "true", "false"])
+    thr = rng.choice([0, -1, 1, lo, hi, rng.randint(lo, hi)])
+    if kind == "hash":
+        return Pred.hash(rng.getrandbits(63))
+    if kind == "true":
+        return Pred(7)
+    if kind == "false":
+        return Pred(8)
+    return {"lt": Pred.lt, "ge": Pred.ge, "gt": Pred.gt, "le": Pred.le, "eq": lambda t: Pred(4, t),
+            "ne": lambda t: Pred(5, t)}[kind](thr)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=300)
+    ap.add_argument("--max-log2", type=int, default=25)
+    a = ap.parse_args()
+    dev = torch.device("cuda")
+    rng = random.Random(1234)
+    t_end = time.time() + a.seconds
+    counts = {}
+    it = 0
+    while time.time() < t_end:
+        it += 1
+        op = rng.choice(["filter", "partition2", "partition3", "c2"])
+        dt = rng.choice([np.int32, np.int64])
+        lg = rng.randint(0, a.max_log2)
+        n = max(0, (1 << lg) + rng.randint(-7, 7) * rng.choice([1, 17, 4099]))
+        span = rng.choice([(-128, 127), (-(1 << 31), (1 << 31) - 1), (0, 3)])
+        xs_h = gen.uniform(it, n, span[0], span[1], dt)
+        xs = torch.from_numpy(xs_h).to(dev)
+        st = ops.Status(dev)
+        p = rand_pred(rng, *span)
+        if op == "filter":
+            ys, dk = ops.filter(xs, p, L.VARIANT_ELIDED, st)
+            k = int(dk.item())
+            want = O.filter_(p, xs_h)
+            ok = k == len(want) and np.array_equal(ys[:k].cpu().numpy().astype(np.int64), want)
+        elif op == "partition2":
+            ys, dnt = ops.partition2(xs, p, L.VARIANT_ELIDED, st)
+            wnt, wys = O.partition2(p, xs_h)
+            ok = int(dnt.item()) == wnt and np.array_equal(ys.cpu().numpy().astype(np.int64), wys)
+        elif op == "partition3":
+            q = rand_pred(rng, *span)
+            ys, dm = ops.partition3(xs, p, q, L.VARIANT_ELIDED, st)
+            w1, w2, wys = O.partition3(p, q, xs_h)
+            ok = dm.cpu().tolist() == [w1, w2] and np.array_equal(ys.cpu().numpy().astype(np.int64), wys)
+        else:
+            xs_h = gen.uniform(it, n, -128, 127, dt)
+            xs = torch.from_numpy(xs_h).to(dev)
+            p = Pred.ge(rng.choice([0, -50, 50, -200, 200]))
+            k = len(O.filter_(p, xs_h))
+            m = max(1, rng.choice([1, 7, k // 64 + 1, k // 3 + 1]))
+            shape = gen.segment_shape(it, m, k)
+            ys, zs, dk = ops.c2(xs, p, torch.from_numpy(shape).to(dev), L.VARIANT_ELIDED, st)
+            kk = int(dk.item())
+            wys, wzs = O.c2(p, xs_h, shape)
+            ok = kk == len(wys) and np.array_equal(ys[:kk].cpu().numpy().astype(np.int64), wys) and \
+                np.array_equal(zs[:kk].cpu().numpy().astype(np.int64), wzs)
+        s = st.read()
+        ok = ok and s.ok
+        counts[op] = counts.get(op, 0) + 1
+        if not ok:
+            print(json.dumps({"mismatch": op, "n": n, "dtype": np.dtype(dt).name, "pred": repr(p), "iter": it}))
+            sys.exit(1)
+    print(json.dumps({"iterations": it, "per_op": counts, "ok": True}))
+
+
+if __name__ == "__main__":
+    main()
