@@ -3,7 +3,9 @@
 
 Random sizes (ragged tiles, one-tile, multi-wave), predicates (selectivity
 0 .. 1, edge thresholds), element types, for filter / partition2 /
-partition3 / C2, each checked bit for bit against oracle/ixoracle.  Runs
+partition3 / C2 / scan (+) / segmented scan / scatter (ELIDED permutation and
+CHECKED with OOB and duplicates) / CSR gather / hist, each checked bit for
+bit against oracle/ixoracle.  Runs
 for --seconds (default 300) and prints a JSON summary; exits 1 on the first
 mismatch.
 
@@ -52,7 +54,7 @@ def main():
     it = 0
     while time.time() < t_end:
         it += 1
-        op = rng.choice(["filter", "partition2", "partition3", "c2"])
+        op = rng.choice(["filter", "partition2", "partition3", "c2", "scan", "segscan", "scatter", "csr", "hist"])
         dt = rng.choice([np.int32, np.int64])
         lg = rng.randint(0, a.max_log2)
         n = max(0, (1 << lg) + rng.randint(-7, 7) * rng.choice([1, 17, 4099]))
@@ -75,6 +77,45 @@ def main():
             ys, dm = ops.partition3(xs, p, q, L.VARIANT_ELIDED, st)
             w1, w2, wys = O.partition3(p, q, xs_h)
             ok = dm.cpu().tolist() == [w1, w2] and np.array_equal(ys.cpu().numpy().astype(np.int64), wys)
+        elif op == "scan":
+            ne = rng.randint(-1000, 1000)
+            v_h = gen.uniform(it, n, -(1 << 20), 1 << 20, dt)
+            got = ops.scan_add(torch.from_numpy(v_h).to(dev), ne)
+            ok = np.array_equal(got.cpu().numpy(), O.scan_add(v_h, ne))
+        elif op == "segscan":
+            v_h = gen.uniform(it, n, -(1 << 20), 1 << 20, np.int64)
+            f_h = (gen.uniform(it + 1, n, 0, rng.choice([1, 5, 100, 10000]), np.int64) == 0).astype(np.uint8)
+            got = ops.segscan_add(torch.from_numpy(f_h).to(dev), torch.from_numpy(v_h).to(dev))
+            ok = np.array_equal(got.cpu().numpy(), O.sgmsum(f_h.astype(np.int64), v_h))
+        elif op == "scatter":
+            # a permutation (ELIDED Sc1) or random indices with OOB (CHECKED: no conflicts -> equal values)
+            vs_h = gen.uniform(it, n, -(1 << 30), 1 << 30, np.int64)
+            if rng.random() < 0.5:
+                is_h = np.random.default_rng(it).permutation(n).astype(np.int64)
+                bits, dst_h = 0, np.zeros(n, dtype=np.int64)
+            else:
+                is_h = gen.uniform(it + 2, n, -3, n + 3, np.int64)
+                vs_h = is_h * 7 + 1  # duplicates carry equal values: never a conflict
+                bits, dst_h = L.V_BOUNDS | L.V_CONFLICT | L.V_INIT, gen.uniform(it + 3, n, -9, 9, np.int64)
+            out = torch.from_numpy(dst_h.copy()).to(dev)
+            ops.scatter(out, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev), bits, st)
+            ok = np.array_equal(out.cpu().numpy(), O.scatter(dst_h, is_h, vs_h))
+        elif op == "csr":
+            ncols = rng.choice([1, 97, 1 << 16])
+            x_h = gen.uniform(it, ncols, -(1 << 15), (1 << 15) - 1, np.int64)
+            v_h = gen.uniform(it + 1, n, -(1 << 15), (1 << 15) - 1, np.int64)
+            i_h = gen.uniform(it + 2, n, 0, ncols - 1, np.int64)
+            got = ops.csr_gather(torch.from_numpy(x_h).to(dev), torch.from_numpy(v_h).to(dev),
+                                 torch.from_numpy(i_h).to(dev), L.VARIANT_ELIDED, st)
+            ok = np.array_equal(got.cpu().numpy(), O.csrg(x_h, v_h, i_h))
+        elif op == "hist":
+            dlen = rng.choice([0, 1, 100, n // 3 + 1])
+            hop = rng.choice([O.HIST_MIN, O.HIST_MAX, O.HIST_ADD])
+            is_h = gen.uniform(it, n, -2, dlen + 2, np.int64)
+            vs_h = gen.uniform(it + 1, n, -(1 << 30), 1 << 30, np.int64)
+            ne = rng.randint(-5, 5)
+            got = ops.hist(hop, ne, dlen, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev))
+            ok = np.array_equal(got.cpu().numpy(), O.hist(hop, ne, dlen, is_h, vs_h))
         else:
             xs_h = gen.uniform(it, n, -128, 127, dt)
             xs = torch.from_numpy(xs_h).to(dev)
