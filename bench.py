@@ -227,9 +227,9 @@ class C2:
             # one pass: xs read once, ys and zs written once, the flag bits
             # of the k outputs read from the mkFlags bitmap
             return (L.K_FILTER_FUSED, 4 * self.N + 8 * self.k + self.k // 8,
-                    "k_filter_b<int32,kSeg> (filter + sgmSum in one pass, 96 KB TMA tiles, two look-back chains)")
+                    "k_filter_b<int32,kSeg> (filter + sgmSum in one pass: 48 KB TMA tiles, runs leave as phase-shifted bulk stores, two look-back chains)")
         # sharded: the filter pass; the sgmSum pass is reported alongside
-        return L.K_FILTER_FUSED, 4 * self.N + 4 * self.k, "k_filter_b<int32> (single-pass filter, 96 KB TMA tiles)"
+        return L.K_FILTER_FUSED, 4 * self.N + 4 * self.k, "k_filter_b<int32> (single-pass filter, 48 KB TMA tiles)"
 
     def kernels_extra(self):
         from paper_2506_23058_b200 import _lib as L
