@@ -1,19 +1,22 @@
 // k_big.cuh -- big-tile streaming kernels: the tile is staged in shared
-// memory with asynchronous 16-byte copies (cp.async, LDGSTS), so a CTA keeps
-// 64-96 KB of HBM reads in flight without spending registers on them.
+// memory by the TMA engine (cp.async.bulk on mbarriers; per-lane cp.async
+// only for the ragged last tile), so a CTA keeps its whole tile of HBM reads
+// in flight without spending registers on them.
 //
-// Why: a %globaltimer trace of the register-tiled kernels
-// showed every CTA spending ~5 us alive for 32 KB of input, most of it behind
-// the look-back (each L2 round trip ~1 us under full HBM load).  Throughput
-// per SM = bytes-in-flight / CTA life, so the lever is bytes per CTA: three
-// 8192-element chunks per tile (96 KB of int32) with ONE look-back per tile,
+// Why: a trace of the register-tiled kernels showed every CTA
+// spending ~5 us alive for 32 KB of input, most of it behind the look-back
+// (each L2 round trip ~1 us under full HBM load).  Throughput per SM =
+// bytes-in-flight / CTA life, so the lever is bytes per CTA: 3 chunks of 4096
+// int32 per tile (48 KB, 4 CTAs per SM) with ONE look-back per tile,
 // resolved by a dedicated warp while the copies land.
 //
-//   k_filter_b   filter / filter_by [+ C2's sgmSum]: "quad" layout (below),
-//                count pass, warp-packed scans of per-piece counts, stable
-//                compaction IN PLACE to tile-local slots (an element's output
-//                slot never lies after its input slot) while the look-back
-//                resolves the base, then 16-byte stores of the run.
+//   k_filter_b   filter / filter_by / partition2/3 [+ C2's sgmSum]: "quad"
+//                layout (below), count pass, warp-packed scans of per-piece
+//                counts, stable compaction IN PLACE to tile-local slots (an
+//                element's output slot never lies after its input slot)
+//                while the look-back resolves the base, then the run leaves
+//                with 16-byte stores (C2: phase-shifted to the base and
+//                written by 1-D bulk stores while the sgmSum passes run).
 //   k_segsum_b   sgmSum over an array (C2's zs = sgmSum flags ys): flags are
 //                bits of the mkFlags bitmap at the element's own position, so
 //                they are fetched together with the data; the segmented
@@ -21,10 +24,10 @@
 //                writes its 16 results with two 256-bit stores.
 //
 // k_segsum_b's shared-memory layout gives a thread 16 consecutive elements:
-// one 16*sizeof(T)-byte block per chunk, its 16-byte pieces XOR-swizzled by
-// the thread index so that the LDS.128 reads of a quarter-warp hit 8
-// distinct bank groups (the copies into it still cost ~7x the ideal
-// wavefronts; k_filter_b's quad layout avoids that).
+// int32 full tiles are TMA-loaded into a linear buffer and read with an XOR
+// rotation of the piece order (lin_read_xor: a quarter-warp's LDS.128 hit 8
+// distinct bank groups); int64 and ragged tiles use per-lane cp.async with
+// the same swizzle applied on the copy side.
 #pragma once
 #include "k_stream.cuh"
 
