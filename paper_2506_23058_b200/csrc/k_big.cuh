@@ -72,6 +72,9 @@ constexpr int big_min_blocks() {
 #define IXG_P2_UNROLL 8  // measured 0.5 % faster than 4 on C2
 #endif
 constexpr int kP1Unroll = IXG_P1_UNROLL, kP2Unroll = IXG_P2_UNROLL;
+#ifndef IXG_SEGSUM_TMA64
+#define IXG_SEGSUM_TMA64 1  // k_segsum_b int64: TMA linear tiles + lin_read_xor64
+#endif
 #ifndef IXG_LB_DEFER
 #define IXG_LB_DEFER 1  // look-back polling deferred until it can succeed: C2 0.463 -> 0.458 ms, filter -0.7 %
 #endif
@@ -207,6 +210,32 @@ IXG_DEV void lin_read_xor(const int32_t* buf, int c, int t, int32_t (&x)[kSItems
     x[4 * k + 1] = (int32_t)v[k].y;
     x[4 * k + 2] = (int32_t)v[k].z;
     x[4 * k + 3] = (int32_t)v[k].w;
+  }
+}
+
+// The int64 twin: thread t's 16 consecutive int64 are 8 pieces; step j reads
+// piece j ^ (t & 7) (a quarter-warp's LDS.128 hit 8 distinct bank groups),
+// three conditional swap stages put piece k back at k.
+IXG_DEV void lin_read_xor64(const long long* buf, int c, int t, long long (&x)[kSItems]) {
+  const int r = t & 7;
+  const long long* b = buf + Big<long long>::PAD + c * kBChunk + kSItems * t;
+  uint4 v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const uint4*>(b + 2 * (j ^ r));
+  auto cswap = [](bool p, uint4& a, uint4& d) {
+    const uint4 a0 = a, d0 = d;
+    a = make_uint4(p ? d0.x : a0.x, p ? d0.y : a0.y, p ? d0.z : a0.z, p ? d0.w : a0.w);
+    d = make_uint4(p ? a0.x : d0.x, p ? a0.y : d0.y, p ? a0.z : d0.z, p ? a0.w : d0.w);
+  };
+#pragma unroll
+  for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (!(j & bit)) cswap(r & bit, v[j], v[j | bit]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    x[2 * k] = (long long)(((unsigned long long)v[k].y << 32) | v[k].x);
+    x[2 * k + 1] = (long long)(((unsigned long long)v[k].w << 32) | v[k].z);
   }
 }
 
@@ -906,7 +935,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   }
   // int32 full tiles: one TMA bulk copy per chunk into a linear buffer
   // (read back with lin_read_xor); otherwise swizzled per-lane cp.async
-  const bool tma = sizeof(T) == 4 && tile_base + B::TILE <= n;
+  const bool tma = (sizeof(T) == 4 || IXG_SEGSUM_TMA64) && tile_base + B::TILE <= n;
   if (tma) {
     if (t == 0) {
 #pragma unroll
@@ -947,7 +976,12 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
         big_read<T>(buf, c, t, x);
       }
     } else {
-      big_read<T>(buf, c, t, x);
+      if (tma) {
+        mbar_wait(&s_mbar[c], 0);
+        lin_read_xor64(reinterpret_cast<const long long*>(buf), c, t, reinterpret_cast<long long(&)[kSItems]>(x));
+      } else {
+        big_read<T>(buf, c, t, x);
+      }
     }
     const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
     const uint32_t vm = valid_mask(g, n);
@@ -992,7 +1026,8 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
       if (tma) lin_read_xor(reinterpret_cast<const int32_t*>(buf), c, t, reinterpret_cast<int32_t(&)[kSItems]>(x));
       else big_read<T>(buf, c, t, x);
     } else {
-      big_read<T>(buf, c, t, x);
+      if (tma) lin_read_xor64(reinterpret_cast<const long long*>(buf), c, t, reinterpret_cast<long long(&)[kSItems]>(x));
+      else big_read<T>(buf, c, t, x);
     }
     const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
     long long run = SegOp::op(carry, chunk_pre[c]).v;
