@@ -213,13 +213,14 @@ template <typename T, typename Z>
 int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32_t* bits, long long flag_base, Z* zs,
                     LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s) {
   auto kern = k_segsum_b<T, Z>;
+  using B = Big<T, kSegsumCH<T, Z>>;
   static bool attr = false;
   if (!attr) {
-    allow_smem(kern, Big<T>::SMEM);
+    allow_smem(kern, B::SMEM);
     attr = true;
   }
   TimedLaunch tl(IXG_K_SEGSUM, s);
-  kern<<<(unsigned)tiles_of(n, Big<T>::TILE), kBT + 32, Big<T>::SMEM, s>>>(vs, n, d_n, bits, flag_base, zs, ch,
+  kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, zs, ch,
                                                                            next_nonce(), carry_v, carry_f, d_total,
                                                                            st);
   LAUNCHED();

@@ -75,6 +75,12 @@ constexpr int kP1Unroll = IXG_P1_UNROLL, kP2Unroll = IXG_P2_UNROLL;
 #ifndef IXG_SEGSUM_TMA64
 #define IXG_SEGSUM_TMA64 1  // k_segsum_b int64: TMA linear tiles + lin_read_xor64
 #endif
+#ifndef IXG_SCAN32_CH
+#define IXG_SCAN32_CH 4  // k_segsum_b<int32, int64> (scan (+) of int32): 64 KB tiles, 0.606 -> 0.590 ms at 2^28
+#endif
+// chunks per tile of k_segsum_b<T, Z> (0 = Big's default)
+template <typename T, typename Z>
+constexpr int kSegsumCH = (sizeof(T) == 4 && sizeof(Z) == 8) ? IXG_SCAN32_CH : 0;
 #ifndef IXG_LB_DEFER
 #define IXG_LB_DEFER 1  // look-back polling deferred until it can succeed: C2 0.463 -> 0.458 ms, filter -0.7 %
 #endif
@@ -82,11 +88,11 @@ constexpr int kP1Unroll = IXG_P1_UNROLL, kP2Unroll = IXG_P2_UNROLL;
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
 #endif
 
-template <typename T>
+template <typename T, int CHO = 0>  // CHO: chunks per tile if not the default
 struct Big {
   static constexpr int P = (int)sizeof(T);           // 16-byte pieces per thread block (16 elements)
   static constexpr int EP = 16 / (int)sizeof(T);     // elements per piece
-  static constexpr int CH = sizeof(T) == 4 ? IXG_CH32 : IXG_CH64;  // chunks per tile
+  static constexpr int CH = CHO ? CHO : (sizeof(T) == 4 ? IXG_CH32 : IXG_CH64);  // chunks per tile
   static constexpr int PAD = 32 / (int)sizeof(T);    // >= the 32-byte store phase
   static constexpr int TILE = CH * kBChunk;
   static constexpr int SMEM = (PAD + TILE) * (int)sizeof(T);
@@ -144,9 +150,9 @@ IXG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memo
 IXG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // issue the copies of thread t's blocks for all chunks of the tile
-template <typename T>
+template <typename T, int CHO = 0>
 IXG_DEV void big_issue(T* buf, const T* __restrict__ xs, long long n, long long tile_base, int t) {
-  using B = Big<T>;
+  using B = Big<T, CHO>;
   if (tile_base + B::TILE <= n) {  // full tile: no per-piece bounds
     const T* src = xs + tile_base + kSItems * t;
     const uint32_t s0 = smem_u32(buf + B::PAD + kSItems * t);
@@ -907,7 +913,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
                                                           Z* __restrict__ zs, LBChan ch, uint32_t nonce,
                                                           long long carry_v, int carry_f, longlong2* d_total,
                                                           ixg_status* st) {
-  using B = Big<T>;
+  using B = Big<T, kSegsumCH<T, Z>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
   __shared__ SegOp::T s_w[B::CH][kBW];
@@ -949,7 +955,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     }
     bar_sync(1, kBT);  // the mbarriers are initialised
   } else {
-    big_issue<T>(buf, vs, n, tile_base, t);
+    big_issue<T, kSegsumCH<T, Z>>(buf, vs, n, tile_base, t);
   }
   // the thread's 16 flag bits per chunk (positions are known up front)
   uint32_t fl[B::CH];
