@@ -349,3 +349,18 @@ def test_jit_loops_floats_and_inlining_compile():
         opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device"]
         (err,) = nvrtc.nvrtcCompileProgram(p_, len(opts), opts)
         assert err == nvrtc.nvrtcResult.NVRTC_SUCCESS, s
+
+
+def test_fuzz_fixtures_load():
+    """tests/golden/fuzz.json (the reference's results on random programs,
+    replayed on the GPU by test_gpu_fuzz.py) is well formed."""
+    fz = json.load(open(os.path.join(ROOT, "tests", "golden", "fuzz.json")))
+    assert len(fz["programs"]) >= 200 and len(fz["cases"]) >= 1000
+    kinds = set()
+    for key, d in fz["programs"].items():
+        prog = ir.from_json(d["program"])
+        assert len(prog.defs) == 1 and len(ir.fingerprint(prog.defs[0])) == 16
+    for c in fz["cases"]:
+        assert c["program"] in fz["programs"] and ("result" in c) != ("error" in c)
+        kinds.add(c["kind"])
+    assert kinds == {"map", "scan", "hist", "loop"}
