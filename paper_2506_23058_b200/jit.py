@@ -77,6 +77,7 @@ class _Spec:
     preds: list = field(default_factory=list)    # Pred
     sites: list = field(default_factory=list)    # IndexE nodes in site order
     out_types: list = field(default_factory=list)  # 'i' | 'f' per output
+    need_budget: bool = False  # a loop: the kernel's gbud counter bounds all its iterations
 
 
 def _size_binds(f, slot_len):
@@ -446,7 +447,13 @@ class _Gen:
         it = self.mut("i")
         self.line(f"{it} = 0;")
         cap = self.scalar(self.loop_cap)
-        guard = (f"if (++{it} > {cap}) {{ fail_oob(st, stmt, i, {BUDGET_SITE}); {self.on_fail} }}")
+        self.spec.need_budget = True
+        # the step budget bounds one loop instance AND, through the shared
+        # counter (256 iterations at a time), all loops of the launch -- a
+        # never-ending loop over many elements fails fast instead of running
+        # budget x elements iterations
+        guard = (f"if (++{it} > {cap} || (({it} & 255) == 0 && atomicAdd(gbud, 256ULL) + 256ULL > (u64){cap})) "
+                 f"{{ fail_oob(st, stmt, i, {BUDGET_SITE}); {self.on_fail} }}")
         if e.kind == "for":
             bound = self.new(self.conv(self.expr(e.bound, scope), "i"))
             c = self.tmp()
@@ -589,6 +596,7 @@ def generate(lam, arrays: list, env: dict, site_bits=lambda node: L.V_BOUNDS, ou
     params += ["long long n", "int stmt", "ixg_status* st"]
     params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
+    params += ["unsigned long long* gbud"]
     stores = []
     for j, (r, o) in enumerate(zip(res, ots)):
         if o in (torch.uint8, torch.bool):
@@ -655,6 +663,20 @@ def scalar_args(spec) -> list:
     return vals
 
 
+_BUDGET_KEEP: list = []  # the counters of launches in flight (freed by the caching allocator later)
+
+
+def budget_arg(spec, dev) -> list:
+    """the kernel's shared loop counter: a zeroed device word when the
+    generated code has a loop, else a null pointer"""
+    if not spec.need_budget:
+        return [ctypes.c_void_p(0)]
+    t = torch.zeros(1, dtype=torch.int64, device=dev)
+    _BUDGET_KEEP.append(t)
+    del _BUDGET_KEEP[:-64]
+    return [ctypes.c_void_p(t.data_ptr())]
+
+
 def map_jit(lam, arrays: list, env: dict, site_bits, n: int, status, out_dtype=None, device=None, funs=None,
             bits_for=None, loop_cap: int = 1 << 31, k_out: int = 1):
     """map lam arrays... on the GPU through a generated, cached kernel;
@@ -681,6 +703,7 @@ def map_jit(lam, arrays: list, env: dict, site_bits, n: int, status, out_dtype=N
     vals += [ctypes.c_void_p(o.data_ptr()) for o in outs]
     vals += [ctypes.c_longlong(n), ctypes.c_int(0), ctypes.c_void_p(status.t.data_ptr())]
     vals += scalar_args(spec)
+    vals += budget_arg(spec, dev)
     argv = (ctypes.c_void_p * len(vals))(*[ctypes.addressof(v) for v in vals])
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = max(1, min((n + 255) // 256, sms * 8))

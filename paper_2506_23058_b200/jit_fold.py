@@ -36,7 +36,7 @@ import hashlib
 import torch
 
 from . import ir
-from .jit import _CACHE, _PRELUDE, LAUNCHES, _ctype, _Gen, _Kernel, _ok, _scalar_param, scalar_args
+from .jit import _CACHE, _PRELUDE, LAUNCHES, _ctype, _Gen, _Kernel, _ok, _scalar_param, budget_arg, scalar_args
 from .vm import Unsupported
 
 _CMPS = ("<", "<=", ">", ">=", "==", "!=")
@@ -344,6 +344,7 @@ def _seq_scan_source(lam, k, in_types, env, site_bits, acc_tys=None):
     params += ["long long n", "int stmt", "ixg_status* st"] + [f"{_CT2[acc_tys[j]]} ne{j}" for j in range(k)]
     params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
+    params += ["unsigned long long* gbud"]
     decl = "\n".join(f"  __shared__ {ein[j]} si{j}[{_SEQ_TILE}];\n  __shared__ {_CT2[acc_tys[j]]} so{j}[{_SEQ_TILE}];"
                      for j in range(k))
     load = "\n".join(f"      si{j}[q] = ({ein[j]})in{j}[base + q];" for j in range(k))
@@ -411,6 +412,7 @@ def _hist_seq_source(lam, v_type, env, site_bits, acc_ty="i"):
     params += [f"{ct}* __restrict__ dst", "long long dlen", "long long m", "int stmt", "ixg_status* st", f"{ct} ne"]
     params += [_scalar_param(j, v) for j, v in enumerate(g.spec.scalars)]
     params += [f"int pk{j}, long long pt{j}, u64 ps{j}" for j in range(len(g.spec.preds))]
+    params += ["unsigned long long* gbud"]
     src = _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__(256) ixg_hist_seq({", ".join(params)}) {{
   __shared__ long long si[{_SEQ_TILE}];
@@ -551,7 +553,7 @@ def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None
         return outs, spec.sites, False
     kern = _kernel(src, ("ixg_scan_seq",))
     vals = [_p(t) for t in ins] + _captures(spec) + [_p(o) for o in outs]
-    vals += [ctypes.c_longlong(n), ctypes.c_int(0), _p(status.t)] + nev + _tail(spec)
+    vals += [ctypes.c_longlong(n), ctypes.c_int(0), _p(status.t)] + nev + _tail(spec) + budget_arg(spec, dev)
     _launch(kern, "ixg_scan_seq", 1, 256, vals, dev)
     return outs, spec.sites, False
 
@@ -586,5 +588,5 @@ def hist(lam, ne, dlen: int, is_: torch.Tensor, vs: torch.Tensor, env: dict, sit
         nev = ctypes.c_double(float(ne)) if acc_ty == "f" else ctypes.c_longlong(int(ne))
         vals = [_p(iss), _p(vss)] + _captures(spec)
         vals += [_p(dst), ctypes.c_longlong(nd), ctypes.c_longlong(m), ctypes.c_int(0), _p(status.t), nev]
-        _launch(kern, "ixg_hist_seq", 1, 256, vals + _tail(spec), dev)
+        _launch(kern, "ixg_hist_seq", 1, 256, vals + _tail(spec) + budget_arg(spec, dev), dev)
     return dst, spec.sites, "seq"

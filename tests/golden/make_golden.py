@@ -296,7 +296,9 @@ def main():
             for origin_kind, a in draws:
                 rec = {"program": key, "fun": f.name, "kind": origin_kind, "args": enc(a)}
                 # a never-ending loop is cut by the default budget (oracle.py:118)
-                rec.update(run(prog, f.name, a, 10**6 if (f.name, origin_kind) == ("countdown", "error") else BUDGET))
+                bud = 10**6 if (f.name, origin_kind) == ("countdown", "error") else BUDGET
+                rec.update(run(prog, f.name, a, bud))
+                rec["budget"] = bud  # the step budget the reference ran with
                 cases.append(rec)
     data = os.path.join(ROOT, "paper_2506_23058_b200", "data")
     os.makedirs(data, exist_ok=True)

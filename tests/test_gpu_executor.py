@@ -47,7 +47,8 @@ def test_eval_program_matches_reference(cuda, idx, mode):
         pytest.skip("loop body: pipeline only")
     prog = program(case["program"])
     args = dec(case["args"])
-    kw = {"variant": "checked" if mode == "checked" else "selected", "generic_only": mode == "generic"}
+    kw = {"variant": "checked" if mode == "checked" else "selected", "generic_only": mode == "generic",
+          "step_budget": case.get("budget", 10**6)}
     if "error" in case:
         if mode == "generic":
             kw["variant"] = "checked"  # generic path with the reference's own checks

@@ -4,6 +4,9 @@ at sizes with many tiles, and the CAS hist against the in-order hist.  The
 small-size parity with the reference interpreter itself is the golden replay
 (test_gpu_executor.py over corpus/scanops.ixl)."""
 
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -121,3 +124,22 @@ def test_hist_cas_and_inorder(cuda, m):
         got, kind = _hist(cuda, op, 0, 4 * dlen, is_[:small], v2)
         assert kind == "seq"
         assert got.tolist() == O.fold_hist(f, 0, 4 * dlen, is_[:small].tolist(), v2.tolist())
+
+
+def test_never_ending_loop_fails_fast(cuda):
+    """A while loop that never ends, mapped over many elements, stops at the
+    step budget for the whole launch (the shared counter), not after
+    budget x elements iterations."""
+    import time
+
+    from paper_2506_23058_b200 import errors
+    from paper_2506_23058_b200.executor import eval_program
+
+    prog = ir.from_json(json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..",
+                                                    "paper_2506_23058_b200", "data", "programs.json")))
+                        ["own:kmeans_rows.ixl"]["program"])
+    xs = [-1] * (1 << 16)  # every element loops forever
+    t0 = time.time()
+    with pytest.raises(errors.StepBudgetExceeded):
+        eval_program(prog, "countdown", [xs], step_budget=10**6, variant="checked")
+    assert time.time() - t0 < 30
