@@ -13,6 +13,7 @@ function of the shapes
     scan (\\a b -> E) c xs           (any operator: associative or not)
     hist (\\a b -> E) c m is vs
     map  (\\x -> loop (acc) = (c) for j < 3 do E) xs
+    map  (\\x y -> F) xs ys                   (f64: Python float arithmetic)
 
 with E drawn from + - *, comparisons, && || !, if / let, and table reads
 tbl[E] that may fall outside the table (CHECKED sites raise OutOfBounds).
@@ -70,8 +71,31 @@ def cond(rng, vars_, depth, tbl):
 ASSOC = ["a + b", "a * b", "if a < b then a else b", "if b <= a then a else b", "b", "a"]
 
 
+def fexpr(rng, vars_, depth):
+    """a float expression (Python floats: IEEE double, no contraction)"""
+    if depth <= 0 or rng.random() < 0.25:
+        if rng.random() < 0.7:
+            return rng.choice(vars_)
+        return rng.choice(["0.5", "1.25", "3.0", "0.1", "2"])
+    k = rng.random()
+    if k < 0.6:
+        op = rng.choice(["+", "-", "*"])
+        return f"({fexpr(rng, vars_, depth - 1)} {op} {fexpr(rng, vars_, depth - 1)})"
+    if k < 0.85:
+        c = rng.choice(["<", "<=", ">", ">="])
+        return f"(if ({fexpr(rng, vars_, depth - 1)} {c} {fexpr(rng, vars_, depth - 1)}) then " \
+               f"{fexpr(rng, vars_, depth - 1)} else {fexpr(rng, vars_, depth - 1)})"
+    v = f"u{depth}"
+    return f"(let {v} = {fexpr(rng, vars_, depth - 1)} in {fexpr(rng, vars_ + [v], depth - 1)})"
+
+
 def program(rng, i):
-    kind = rng.choice(["map", "map", "scan", "hist", "loop"])
+    kind = rng.choice(["map", "map", "scan", "hist", "loop", "fmap"])
+    if kind == "fmap":
+        body = fexpr(rng, ["x", "y"], 3)
+        src = (f"def f{i} [n] (xs: [n]f64) (ys: [n]f64) : [n]f64 =\n"
+               f"  map (\\x y -> {body}) xs ys\n")
+        return kind, src
     if kind == "map":
         body = expr(rng, ["x", "y", "s"], 3)
         src = (f"def f{i} [n] [m] (tbl: [m]i64) (s: i64) (xs: [n]i64) (ys: [n]i64) : [n]i64 =\n"
@@ -98,6 +122,8 @@ def args_for(rng, kind, n):
         return [tbl, rng.randint(-5, 5), xs, [rng.randint(-9, 9) for _ in range(n)]]
     if kind in ("scan", "loop"):
         return [tbl, xs]
+    if kind == "fmap":
+        return [[round(rng.uniform(-9, 9), 3) for _ in range(n)], [round(rng.uniform(-9, 9), 3) for _ in range(n)]]
     k = rng.randint(0, 8)
     return [k, [rng.randint(-2, k + 1) for _ in range(n)], xs]
 
@@ -107,13 +133,21 @@ def main():
     programs, cases = {}, []
     budget = 10**7
     made = 0
-    while made < 240:
+    import signal
+
+    def _slow(*_):
+        raise TimeoutError
+
+    signal.signal(signal.SIGALRM, _slow)
+    while made < 300:
         kind, src = program(rng, made)
+        signal.alarm(5)  # a candidate the reference needs seconds for is dropped
         # keep value magnitudes bounded: the reference's ints are unbounded
         try:
             prog = normalize(parse_program(src, f"fuzz{made}.ixl"))
             check_well_formed(prog)
         except Exception:
+            signal.alarm(0)
             continue
         fname = prog.defs[0].name
         key = f"fuzz:{made}"
@@ -128,6 +162,9 @@ def main():
                     ok = False
                     break
                 rows.append({"program": key, "fun": fname, "kind": kind, "args": a, "result": res})
+            except TimeoutError:
+                ok = False
+                break
             except OracleError as e:
                 d = {"program": key, "fun": fname, "kind": kind, "args": a, "error": type(e).__name__}
                 if hasattr(e, "site"):
@@ -135,7 +172,9 @@ def main():
                 if getattr(e, "pos", None) is not None:
                     d["pos"] = list(e.pos)
                 rows.append(d)
+        signal.alarm(0)
         if not ok:
+            print("dropped (slow or huge):", src.strip()[:160], file=sys.stderr)
             continue
         programs[key] = {"source": src, "program": ir.to_json(prog)}
         cases += rows

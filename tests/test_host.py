@@ -363,7 +363,7 @@ def test_fuzz_fixtures_load():
     for c in fz["cases"]:
         assert c["program"] in fz["programs"] and ("result" in c) != ("error" in c)
         kinds.add(c["kind"])
-    assert kinds == {"map", "scan", "hist", "loop"}
+    assert kinds == {"map", "scan", "hist", "loop", "fmap"}
 
 
 def test_bench_reference_arm_contract():
