@@ -209,10 +209,10 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
 }
 
 // zs = sgmSum over the first *d_n elements of vs (capacity n)
-template <typename T, typename Z>
+template <typename T, typename Z, class M = SegOp>
 int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32_t* bits, long long flag_base, Z* zs,
                     LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s) {
-  auto kern = k_segsum_b<T, Z>;
+  auto kern = k_segsum_b<T, Z, M>;
   using B = Big<T, kSegsumCH<T, Z>>;
   static bool attr = false;
   if (!attr) {
@@ -491,9 +491,11 @@ int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, i
   // carry into the first tile; exclusive / u8 keep the generic k_scan
   if (!exclusive && n > 0 && (dt == IXG_I32 || dt == IXG_I64) && aligned16(xs) && aligned16(out)) {
     if (dt == IXG_I32)
-      return launch_segsum_b<int32_t, long long>((const int32_t*)xs, n, nullptr, nullptr, 0, (long long*)out, c, ne,
+      return launch_segsum_b<int32_t, long long, SumOp>((const int32_t*)xs, n, nullptr, nullptr, 0, (long long*)out, c,
+                                                        ne,
                                                  0, nullptr, nullptr, S(stream));
-    return launch_segsum_b<long long, long long>((const long long*)xs, n, nullptr, nullptr, 0, (long long*)out, c, ne,
+    return launch_segsum_b<long long, long long, SumOp>((const long long*)xs, n, nullptr, nullptr, 0, (long long*)out, c,
+                                                         ne,
                                                  0, nullptr, nullptr, S(stream));
   }
   const EpiScanOut epi{ne, exclusive, (long long*)out};

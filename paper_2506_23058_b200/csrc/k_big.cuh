@@ -906,7 +906,20 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
 // ---------------------------------------------------------------------------
 // zs = sgmSum flags vs over n elements; flag of element i = bit (flag_base + i)
 // of `bits` (mkFlags' bitmap over output positions).  Z: zs storage.
-template <typename T, typename Z>
+// k_segsum_b's monoid: SegOp for sgmSum, SumOp for a flag-free scan (+)
+template <class M>
+IXG_DEV typename M::T seg_mk(long long v, int f);
+template <>
+IXG_DEV SegOp::T seg_mk<SegOp>(long long v, int f) { return SegOp::T{v, f}; }
+template <>
+IXG_DEV SumOp::T seg_mk<SumOp>(long long v, int) { return SumOp::T{v}; }
+template <class M>
+IXG_DEV int seg_f(const typename M::T& a) {
+  if constexpr (std::is_same<M, SegOp>::value) return a.f;
+  else return 0;
+}
+
+template <typename T, typename Z, class M = SegOp>
 __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T* __restrict__ vs, long long n,
                                                           const long long* __restrict__ d_n,
                                                           const uint32_t* __restrict__ bits, long long flag_base,
@@ -916,9 +929,9 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   using B = Big<T, kSegsumCH<T, Z>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
-  __shared__ SegOp::T s_w[B::CH][kBW];
-  __shared__ SegOp::T s_agg;
-  __shared__ SegOp::T s_carry;
+  __shared__ typename M::T s_w[B::CH][kBW];
+  __shared__ typename M::T s_agg;
+  __shared__ typename M::T s_carry;
   __shared__ __align__(8) uint64_t s_mbar[B::CH];
 
   if (d_n) n = *d_n;  // length known only on the device (C2: k = filter's count)
@@ -928,14 +941,14 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   const long long tile_base = tile * B::TILE;
   const int t = threadIdx.x;
   if (warp_id() == kBW) {  // look-back warp
-    SegOp::T ex = SegOp::T{carry_v, carry_f};  // carry into the first tile (earlier shards)
-    if (tile > 0) ex = lb_lookback<SegOp>(ch, nonce, tile);
+    typename M::T ex = seg_mk<M>(carry_v, carry_f);  // carry into the first tile (earlier shards)
+    if (tile > 0) ex = lb_lookback<M>(ch, nonce, tile);
     if (lane_id() == 0) s_carry = ex;
     bar_sync(2, kBT + 32);
     if (lane_id() == 0) {
-      const SegOp::T incl = SegOp::op(ex, s_agg);
-      if (tile > 0) lb_publish<SegOp>(ch, nonce, tile, incl, true);
-      if (tile == ntiles - 1 && d_total) *d_total = make_longlong2(incl.v, incl.f);
+      const typename M::T incl = M::op(ex, s_agg);
+      if (tile > 0) lb_publish<M>(ch, nonce, tile, incl, true);
+      if (tile == ntiles - 1 && d_total) *d_total = make_longlong2(incl.v, seg_f<M>(incl));
     }
     return;
   }
@@ -965,12 +978,12 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     const long long pos = flag_base + g;
     const long long wd = pos >> 5;
     uint32_t f = 0;
-    if (g < n && bits)  // bits == nullptr: no flags -- a plain inclusive scan (ixg_scan_add)
+    if (std::is_same<M, SegOp>::value && g < n && bits)  // SumOp / bits == nullptr: a plain inclusive scan (ixg_scan_add)
       f = (uint32_t)((((uint64_t)__ldg(&bits[wd + 1]) << 32) | (uint64_t)__ldg(&bits[wd])) >> (pos & 31));
     fl[c] = f & valid_mask(g, n);
   }
   if (!tma) cp_async_wait_all();
-  SegOp::T a[B::CH];
+  typename M::T a[B::CH];
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     T x[kSItems];
@@ -995,35 +1008,35 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     long long s = 0;
 #pragma unroll
     for (int j = 0; j < kSItems; ++j) s += ((tail >> j) & 1u) ? (long long)x[j] : 0LL;
-    a[c] = SegOp::T{s, fl[c] != 0};
-    SegOp::T inc = warp_inclusive<SegOp>(a[c]);
+    a[c] = seg_mk<M>(s, fl[c] != 0);
+    typename M::T inc = warp_inclusive<M>(a[c]);
     if (lane_id() == 31) s_w[c][warp_id()] = inc;
-    SegOp::T lex = SegOp::shfl_up(inc, 1);
-    if (lane_id() == 0) lex = SegOp::identity();
+    typename M::T lex = M::shfl_up(inc, 1);
+    if (lane_id() == 0) lex = M::identity();
     a[c] = lex;  // the lane's exclusive prefix within its warp and chunk
   }
   bar_sync(1, kBT);
   // tile aggregate (chunk-major order) and each (chunk, warp) prefix
-  SegOp::T tagg = SegOp::identity();
-  SegOp::T chunk_pre[B::CH];
+  typename M::T tagg = M::identity();
+  typename M::T chunk_pre[B::CH];
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     chunk_pre[c] = tagg;
-    SegOp::T wp = SegOp::identity();
+    typename M::T wp = M::identity();
 #pragma unroll
     for (int w = 0; w < kBW; ++w) {
-      if (w < warp_id()) wp = SegOp::op(wp, s_w[c][w]);
-      tagg = SegOp::op(tagg, s_w[c][w]);
+      if (w < warp_id()) wp = M::op(wp, s_w[c][w]);
+      tagg = M::op(tagg, s_w[c][w]);
     }
-    chunk_pre[c] = SegOp::op(SegOp::op(chunk_pre[c], wp), a[c]);
+    chunk_pre[c] = M::op(M::op(chunk_pre[c], wp), a[c]);
   }
   if (t == 0) {
     s_agg = tagg;
-    if (tile == 0) lb_publish<SegOp>(ch, nonce, tile, SegOp::op(SegOp::T{carry_v, carry_f}, tagg), true);
-    else lb_publish<SegOp>(ch, nonce, tile, tagg, false);
+    if (tile == 0) lb_publish<M>(ch, nonce, tile, M::op(seg_mk<M>(carry_v, carry_f), tagg), true);
+    else lb_publish<M>(ch, nonce, tile, tagg, false);
   }
   bar_sync(2, kBT + 32);
-  const SegOp::T carry = s_carry;
+  const typename M::T carry = s_carry;
   bool narrow = false;
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
@@ -1036,7 +1049,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
       else big_read<T>(buf, c, t, x);
     }
     const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
-    long long run = SegOp::op(carry, chunk_pre[c]).v;
+    long long run = M::op(carry, chunk_pre[c]).v;
     Z z[kSItems];
 #pragma unroll
     for (int j = 0; j < kSItems; ++j) {
