@@ -241,9 +241,11 @@ int ixg_c2(int dt, const void* xs, int64_t n, const ixg_pred* p, const int64_t* 
            void* ws, size_t ws_bytes, void* stream);
 
 /* mkSgmDescr (corpus/mksgmdescr.ixl:4-11; sites 0 = shape[i-1], 1 = scn[m-1],
- * 2 = shape[m-1], 3 = scatter).  res: capacity `cap`, *d_len = max(len, 0);
- * IXG_BADARG recorded in st (code bit) if len > cap. */
-int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t* res, int64_t cap,
+ * 2 = shape[m-1], 3 = scatter).  shape: m elements, xs: nxs elements (the
+ * scatter pairs min(m, nxs) of them, zip truncation, oracle.py:299).
+ * res: capacity `cap`, *d_len = max(len, 0); call once with cap = 0 to get
+ * len, then with cap >= len. */
+int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t nxs, int64_t* res, int64_t cap,
                    int64_t* d_len, uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes,
                    void* stream);
 
@@ -348,6 +350,23 @@ int ixg_timer_start(int kernel_id);
 int ixg_trace_read(unsigned long long* host, size_t count);
 /* synchronises the recorded events; total device time (ms) and launch count */
 int ixg_timer_stop(double* total_ms, int64_t* launches);
+
+/* ---- preconditions of an entry function (contract.py) --------------------
+ * The verifier's proofs ASSUME the parameter annotations (infer.py:231-338);
+ * the reference interpreter never checks them (oracle.py:117-135).  Before
+ * the executor uses ELIDED variants it checks them with these, restating
+ * oracle.py chk_range / chk_mono / chk_inj / chk_bij (:478-520):
+ *   ixg_minmax      out2 = [min, max] of xs ([INT64_MAX, INT64_MIN] if n == 0);
+ *   ixg_mono_check  *out_bad = adjacent pairs violating op (0 <=, 1 <, 2 >=, 3 >);
+ *   ixg_inj_check   over the values v of xs with lo <= v <= hi: out3[0] = how
+ *                   many, out3[1] = repeated values, out3[2] = how many lie
+ *                   outside [img_lo, img_hi]; `bitmap` = device scratch of
+ *                   ixg_inj_bitmap_bytes(lo, hi) bytes (-1: range too wide). */
+int ixg_minmax(int dt, const void* xs, int64_t n, int64_t* out2, void* stream);
+int ixg_mono_check(int dt, const void* xs, int64_t n, int op, int64_t* out_bad, void* stream);
+int64_t ixg_inj_bitmap_bytes(int64_t lo, int64_t hi);
+int ixg_inj_check(const int64_t* xs, int64_t n, int64_t lo, int64_t hi, int64_t img_lo, int64_t img_hi,
+                  uint32_t* bitmap, int64_t bitmap_bytes, int64_t* out3, void* stream);
 
 /* ---- synthetic inputs (bench / tests): counter-based, identical to
  * paper_2506_23058_b200.gen and oracle/ixoracle.c ixo_rand ----------------- */

@@ -258,7 +258,7 @@ static int seg_starts(const int64_t* shape, int64_t m, int64_t* scn, int64_t* in
 
 /* mkSgmDescr -- /root/reference/pkg/corpus/mksgmdescr.ixl:4-11.
  * *len receives max(len, 0); IXO_BADARG if it exceeds cap. */
-int ixo_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m,
+int ixo_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t nxs,
                    int64_t* res, int64_t cap, int64_t* len_out) {
   int64_t *scn = ALLOC(int64_t, m), *ind = ALLOC(int64_t, m);
   int64_t* zeros = NULL;
@@ -273,7 +273,7 @@ int ixo_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m,
   zeros = ALLOC(int64_t, len);
   if (!zeros) { rc = IXO_NOMEM; goto out; }
   for (int64_t i = 0; i < len; ++i) zeros[i] = 0;
-  rc = ixo_scatter(zeros, len, ind, m, xs, m, res);                         /* :10 */
+  rc = ixo_scatter(zeros, len, ind, m, xs, nxs, res);     /* :10, zip(ind, xs) truncates */
 out:
   free(scn); free(ind); free(zeros);
   return rc;
@@ -288,7 +288,7 @@ int ixo_mkii(const int64_t* shape, int64_t m, int64_t* out, int64_t cap, int64_t
   int64_t* fl = ALLOC(int64_t, cap);
   int rc = IXO_NOMEM;
   if (!s1 || !fl) goto out;
-  if ((rc = ixo_mksgmdescr(shape, beg, m, s1, cap, len))) goto out;
+  if ((rc = ixo_mksgmdescr(shape, beg, m, m, s1, cap, len))) goto out;
   for (int64_t i = 0; i < *len; ++i) s1[i] = s1[i] == 0 ? 0 : s1[i] - 1;
   for (int64_t i = 0; i < *len; ++i) fl[i] = s1[i] > 0;
   rc = ixo_sgmsum(fl, s1, *len, out);
@@ -424,7 +424,7 @@ int ixo_partition2l(const int64_t* shp, int64_t m, const int64_t* cs, const int6
     offs[k] = acc;
     ones[k] = 1;                                                                  /* :35 */
   }
-  if ((rc = ixo_mksgmdescr(shp, ones, m, descr, cap, &len))) goto out;          /* :36 */
+  if ((rc = ixo_mksgmdescr(shp, ones, m, m, descr, cap, &len))) goto out;       /* :36 */
   for (int64_t i = 0; i < len; ++i) fl[i] = descr[i] > 0;                         /* :37 */
   if ((rc = ixo_sgmsum(fl, cs, len, tb))) goto out;                               /* :38-39: fs = cs as 0/1 */
   for (int64_t k = 0; k < m; ++k) {                                               /* :40 */

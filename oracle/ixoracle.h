@@ -71,8 +71,8 @@ int ixo_partition3(const ixo_pred* p, const ixo_pred* q, const int64_t* xs, int6
                    int64_t* m1, int64_t* m2, int64_t* ys);
 int ixo_filter(const ixo_pred* p, const int64_t* xs, int64_t n, int64_t* ys, int64_t* count);
 int ixo_filter_by(const int64_t* cs, const int64_t* xs, int64_t n, int64_t* ys, int64_t* count);
-int ixo_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m,
-                   int64_t* res, int64_t cap, int64_t* len);
+int ixo_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t nxs,
+                   int64_t* res, int64_t cap, int64_t* len_out);
 int ixo_mkii(const int64_t* shape, int64_t m, int64_t* out, int64_t cap, int64_t* len);
 int ixo_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags);
 int ixo_c2(const ixo_pred* p, const int64_t* xs, int64_t n, const int64_t* shape, int64_t m,

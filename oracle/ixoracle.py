@@ -168,8 +168,8 @@ def mksgmdescr(shape, xs):
     for _ in range(2):
         res = np.empty(cap, dtype=np.int64)
         ln = ctypes.c_int64(0)
-        rc = lib().ixo_mksgmdescr(_p(shape), _p(xs), ctypes.c_int64(len(shape)), _p(res), ctypes.c_int64(cap),
-                                  ctypes.byref(ln))
+        rc = lib().ixo_mksgmdescr(_p(shape), _p(xs), ctypes.c_int64(len(shape)), ctypes.c_int64(len(xs)), _p(res),
+                                  ctypes.c_int64(cap), ctypes.byref(ln))
         if rc == BADARG and ln.value > cap:
             cap = ln.value
             continue

@@ -85,11 +85,15 @@ SIGNATURES = {
     "ixg_partition2": (_I, [_I, _P, _I64, _PP, _P, _P, _U32, _P, _P, _SZ, _P]),
     "ixg_partition3": (_I, [_I, _P, _I64, _PP, _PP, _P, _P, _U32, _P, _P, _SZ, _P]),
     "ixg_c2": (_I, [_I, _P, _I64, _PP, _P, _I64, _P, _I, _P, _P, _U32, _P, _P, _SZ, _P]),
-    "ixg_mksgmdescr": (_I, [_P, _P, _I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
+    "ixg_mksgmdescr": (_I, [_P, _P, _I64, _I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
     "ixg_csr_gather": (_I, [_I, _P, _I64, _P, _P, _I64, _P, _U32, _P, _P]),
     "ixg_kmeans_ker": (_I, [_P, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _U32, _P, _P]),
     "ixg_eq_gather": (_I, [_P, _I64, _P, _P, _I64, _P, _U32, _I, _P, _P]),
     "ixg_gen_uniform": (_I, [_I, _P, _I64, _I64, _I64, _U64, _I64, _P]),
+    "ixg_minmax": (_I, [_I, _P, _I64, _P, _P]),
+    "ixg_mono_check": (_I, [_I, _P, _I64, _I, _P, _P]),
+    "ixg_inj_bitmap_bytes": (_I64, [_I64, _I64]),
+    "ixg_inj_check": (_I, [_P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "ixg_mkflags": (_I, [_I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
     "ixg_map": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _I64, _I, _P, _P]),
     "ixg_bitmap_words": (_I64, [_I64]),

@@ -15,6 +15,7 @@
 #include "k_stream.cuh"
 #include "k_big.cuh"
 #include "k_vm.cuh"
+#include "k_contract.cuh"
 
 using namespace ixg;
 
@@ -95,9 +96,17 @@ inline bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
     if (e__ != cudaSuccess) return cuda_rc(e__); \
   } while (0)
 
+// The dynamic shared-memory opt-in is a per-DEVICE attribute of a kernel:
+// set it once per (call site, device) -- `done` is that call site's bitmask
+// of devices already configured.
 template <typename K>
-void allow_smem(K kernel, int bytes) {
+void allow_smem(K kernel, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
 // ------------------------------------------------------------------ pieces
@@ -154,11 +163,8 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
     // kernel: striped lanes would all hit the same claim word (a warp's 32
     // sources are ~2 destination runs), serialising the atomics.
     if (mode == 0 && !check && aligned16(is) && aligned16(vs)) {
-      static bool attr = false;
-      if (!attr) {
-        allow_smem(k_scatter_t<E>, ScSmem<E>::BYTES);
-        attr = true;
-      }
+      static std::atomic<unsigned long long> attr{0};
+      allow_smem(k_scatter_t<E>, ScSmem<E>::BYTES, attr);
       k_scatter_t<E><<<(unsigned)tiles_of(m, kScTile), 256, ScSmem<E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m,
                                                                                  check ? 1 : 0, claim, hdr);
     } else if (aligned32(is) && aligned32(vs))
@@ -194,11 +200,8 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
                     long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr}, ixg_status* st = nullptr,
                     const ixg_pred& q = ixg_pred{}, const PeerOut<T>& po = PeerOut<T>{}) {
   auto kern = k_filter_b<T, kByCs, kSeg, Z, NS, kPeer>;
-  static bool attr = false;
-  if (!attr) {
-    allow_smem(kern, Big<T>::SMEM);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  allow_smem(kern, Big<T>::SMEM, attr);
   TimedLaunch tl(NS > 1 ? IXG_K_PLACE : IXG_K_FILTER_FUSED, s);
   const long long seg_tiles = tiles_of(n, Big<T>::TILE);
   kern<<<(unsigned)(NS * seg_tiles), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(), d_count, zs,
@@ -214,11 +217,8 @@ int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32
                     LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s) {
   auto kern = k_segsum_b<T, Z, M>;
   using B = Big<T, kSegsumCH<T, Z>>;
-  static bool attr = false;
-  if (!attr) {
-    allow_smem(kern, B::SMEM);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  allow_smem(kern, B::SMEM, attr);
   TimedLaunch tl(IXG_K_SEGSUM, s);
   kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, zs, ch,
                                                                            next_nonce(), carry_v, carry_f, d_total,
@@ -489,7 +489,8 @@ int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, i
   // inclusive scans of int32 / int64: the big-tile sgmSum kernel without
   // flags (TMA-loaded 48 KB int32 tiles, one look-back per tile), `ne` as the
   // carry into the first tile; exclusive / u8 keep the generic k_scan
-  if (!exclusive && n > 0 && (dt == IXG_I32 || dt == IXG_I64) && aligned16(xs) && aligned16(out)) {
+  // (k_segsum_b stores 32-byte vectors: `out` must be 32-byte aligned)
+  if (!exclusive && n > 0 && (dt == IXG_I32 || dt == IXG_I64) && aligned16(xs) && aligned32(out)) {
     if (dt == IXG_I32)
       return launch_segsum_b<int32_t, long long, SumOp>((const int32_t*)xs, n, nullptr, nullptr, 0, (long long*)out, c,
                                                         ne,
@@ -774,9 +775,11 @@ int ixg_c2(int dt, const void* xs, int64_t n, const ixg_pred* p, const int64_t* 
   return do_c2<int64_t, int64_t>((const int64_t*)xs, n, p, sh, m, (int64_t*)ys, (int64_t*)zs, dk, variant, st, w, s);
 }
 
-int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t* res, int64_t cap, int64_t* d_len,
-                   uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
-  if (m < 0 || cap < 0 || !d_len || (m > 0 && (!shape || !xs)) || (cap > 0 && !res)) return IXG_BADARG;
+int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t nxs, int64_t* res, int64_t cap,
+                   int64_t* d_len, uint32_t variant, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+  if (m < 0 || nxs < 0 || cap < 0 || !d_len || (m > 0 && !shape) || (nxs > 0 && !xs) || (cap > 0 && !res))
+    return IXG_BADARG;
+  const long long pairs = m < nxs ? m : nxs;  // scatter's zip(ind, xs) truncates (oracle.py:299)
   if (ws_bytes < ixg_ws_bytes(IXG_OP_MKSGMDESCR, cap, m)) return IXG_BADARG;
   cudaStream_t s = S(stream);
   WS w(ws);
@@ -791,8 +794,8 @@ int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t* 
   // passes cap >= len (read back from d_len), res[0..len) = 0, checked scatter.
   const uint32_t sb = IXG_SITE_BITS(variant, 3) | IXG_V_INIT;
   if ((rc = launch_fill<long long>((long long*)res, 0, (const long long*)d_len, 0LL, s))) return rc;
-  return launch_scatter<long long>((long long*)res, 0, (const long long*)d_len, cap, ind, (const long long*)xs, m, sb,
-                                   3, 3, st, w, 1, s);
+  return launch_scatter<long long>((long long*)res, 0, (const long long*)d_len, cap, ind, (const long long*)xs, pairs,
+                                   sb, 3, 3, st, w, 1, s);
 }
 
 int ixg_csr_gather(int dt, const void* x, int64_t num_cols, const void* values, const int64_t* indices, int64_t nnz,
@@ -837,6 +840,64 @@ int ixg_eq_gather(const int64_t* H, int64_t hlen, const int64_t* es, const int64
   const int check = (IXG_SITE_BITS(variant, 0) & IXG_V_BOUNDS) ? 1 : 0;
   k_eq_gather<<<grid_for(n), kGThreads, 0, S(stream)>>>((const long long*)H, hlen, (const long long*)es,
                                                          (const long long*)is, n, cs, check, st, stmt);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+// ---- preconditions (contract.py): Range / Mono / Inj / Bij on the device ----
+int ixg_minmax(int dt, const void* xs, int64_t n, int64_t* out2, void* stream) {
+  if (n < 0 || !out2 || (n > 0 && !xs)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  const long long init[2] = {LLONG_MAX, LLONG_MIN};
+  int rc = cuda_rc(cudaMemcpyAsync(out2, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (rc || n == 0) return rc;
+  if (dt == IXG_I32)
+    k_minmax<int32_t><<<grid_for(n / 4 + 1), kGThreads, 0, s>>>((const int32_t*)xs, n, (long long*)out2);
+  else if (dt == IXG_U8)
+    k_minmax<uint8_t><<<grid_for(n / 16 + 1), kGThreads, 0, s>>>((const uint8_t*)xs, n, (long long*)out2);
+  else
+    k_minmax<long long><<<grid_for(n / 2 + 1), kGThreads, 0, s>>>((const long long*)xs, n, (long long*)out2);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int ixg_mono_check(int dt, const void* xs, int64_t n, int op, int64_t* out_bad, void* stream) {
+  if (n < 0 || !out_bad || op < 0 || op > 3 || (n > 0 && !xs)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  int rc = cuda_rc(cudaMemsetAsync(out_bad, 0, 8, s));
+  if (rc || n < 2) return rc;
+  unsigned long long* b = (unsigned long long*)out_bad;
+  if (dt == IXG_I32)
+    k_mono<int32_t><<<grid_for(n), kGThreads, 0, s>>>((const int32_t*)xs, n, op, b);
+  else
+    k_mono<long long><<<grid_for(n), kGThreads, 0, s>>>((const long long*)xs, n, op, b);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
+int64_t ixg_inj_bitmap_bytes(int64_t lo, int64_t hi) {
+  if (hi < lo) return 0;
+  const unsigned long long span = (unsigned long long)hi - (unsigned long long)lo + 1ULL;
+  if (span == 0 || span > (1ULL << 34)) return -1;  // wider than 2^34 values: not checkable here
+  return (int64_t)bitmap_bytes((long long)span);
+}
+
+int ixg_inj_check(const int64_t* xs, int64_t n, int64_t lo, int64_t hi, int64_t img_lo, int64_t img_hi,
+                  uint32_t* bitmap, int64_t bitmap_bytes_, int64_t* out3, void* stream) {
+  if (n < 0 || !out3 || (n > 0 && !xs)) return IXG_BADARG;
+  const int64_t need = ixg_inj_bitmap_bytes(lo, hi);
+  if (need < 0 || (need > 0 && (!bitmap || bitmap_bytes_ < need))) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  int rc = cuda_rc(cudaMemsetAsync(out3, 0, 3 * 8, s));
+  if (rc || n == 0 || need == 0) return rc;
+  if ((rc = cuda_rc(cudaMemsetAsync(bitmap, 0, (size_t)need, s)))) return rc;
+  LAUNCHED();
+  const unsigned long long span = (unsigned long long)hi - (unsigned long long)lo + 1ULL;
+  k_inj_claim<<<grid_for(n), kGThreads, 0, s>>>((const long long*)xs, n, lo, span, img_lo, img_hi, bitmap,
+                                                (unsigned long long*)out3);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -900,7 +961,7 @@ int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint
   if (n < 0 || (n > 0 && (!vs || !zs || !bits))) return IXG_BADARG;
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SEGSCAN, n, 0)) return IXG_BADARG;
   if (n == 0) return IXG_OK;
-  if (!aligned16(vs) || !aligned16(zs)) return IXG_BADARG;
+  if (!aligned16(vs) || !aligned32(zs)) return IXG_BADARG;  // TMA loads / 32-byte vector stores
   WS w(ws);
   LBChan c = w.chan(0, tiles_of(n, kGTile));
   cudaStream_t s = S(stream);

@@ -224,15 +224,18 @@ __device__ unsigned long long g_trace[(1 << 17) * IXG_TRS];
   } while (0)
 #endif
 
+// SM count of the CURRENT device (cached per device ordinal)
 inline int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
   }
-  return sms;
+  return sms[dev];
 }
 
 inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? IXG_OK : IXG_CUDA_ERR + (int)e; }

@@ -32,7 +32,7 @@ from typing import Optional
 import torch
 
 from . import _lib as L
-from . import errors, ir, jit_fold, ops
+from . import contract, errors, ir, jit_fold, ops
 from . import select as sel
 from .pred import Pred
 
@@ -144,23 +144,53 @@ class Interp:
     """``ixverify.oracle.Interp`` with the same constructor and ``call``."""
 
     def __init__(self, program, step_budget: int = 10**6, *, variant: str = "selected", device=None,
-                 as_tensors: bool = False, generic_only: bool = False):
+                 as_tensors: bool = False, generic_only: bool = False, preconditions: str = "check"):
         self.program = program
         self.generic_only = generic_only
         self.funs = {f.name: f for f in program.defs}
         self.budget = step_budget  # kernels terminate by construction; kept for signature parity
         if variant not in ("selected", "checked"):
             raise ValueError("variant must be 'selected' (verifier-chosen) or 'checked' (reference behaviour)")
+        if preconditions not in ("check", "trust"):
+            raise ValueError("preconditions must be 'check' (validated on the device) or 'trust' (caller's contract)")
         self.variant = variant
+        self.preconditions = preconditions
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.as_tensors = as_tensors
+        self._internal = False  # a call made by a program function (its preconditions were proved)
+        # (function, verdict source, variant bits per site) of every selection
+        # a call used, and the precondition checks it made -- tests assert on it
+        self.trace: list = []
         L.load(require_device=True)
 
     # -- selection ---------------------------------------------------------
     def _sel(self, fdef) -> sel.FunSelection:
-        if self.variant == "checked":
-            return sel.checked_selection(fdef)
-        return sel.selection_for(self.program, fdef)
+        fs = sel.checked_selection(fdef) if self.variant == "checked" else sel.selection_for(self.program, fdef)
+        self.trace.append(("select", fdef.name, fs.source, tuple(s.bits for s in fs.sites)))
+        return fs
+
+    def _contract_ok(self, fdef, values: dict) -> bool:
+        """Do fdef's annotations hold for these arguments?  Checked on the
+        device (contract.py) unless the caller vouches for them."""
+        if self.preconditions == "trust" or not contract.has_preconditions(fdef):
+            return True
+        ok, why = contract.check(fdef, values)
+        self.trace.append(("pre", fdef.name, ok, why))
+        return ok
+
+    def _callee_variant(self, fdef, values: dict) -> int:
+        """Variant word of a callee a fused pipeline runs with ITS OWN
+        verdicts (c2 -> mkFlags): they assume the callee's annotations,
+        which nobody proved for this caller -- check them on the values the
+        pipeline passes, else run the callee CHECKED."""
+        if self.variant == "selected" and sel.selection_for(self.program, fdef).elides \
+                and not self._contract_ok(fdef, values):
+            saved, self.variant = self.variant, "checked"
+            try:
+                return self._variant(fdef)
+            finally:
+                self.variant = saved
+        return self._variant(fdef)
 
     def _variant(self, fdef, order=None) -> int:
         """pipeline variant word: site ordinal s -> 4 bits at 4*s."""
@@ -188,6 +218,12 @@ class Interp:
 
     # -- entry -------------------------------------------------------------
     def call(self, name: str, args: list):
+        # every kernel of the call runs on this interpreter's device (ops.py
+        # launches on the current device's current stream)
+        with torch.cuda.device(self.dev):
+            return self._call(name, args)
+
+    def _call(self, name: str, args: list):
         f = self.funs[name]
         if len(args) != len(f.params):
             raise errors.OracleError(f"{name} expects {len(f.params)} arguments")
@@ -197,9 +233,20 @@ class Interp:
                 if cname not in self.funs or ir.fingerprint(self.funs[cname]) != cfp:
                     ent = None
                     break
-        if ent is not None:
-            return getattr(self, "_p_" + ent.pipeline)(f, list(args))
-        return self._generic(f, list(args))
+        args = [self._marshal(p.type, v) for p, v in zip(f.params, args)]  # once; pipelines reuse the tensors
+        forced = False
+        if self.variant == "selected" and not self._internal and sel.selection_for(self.program, f).elides:
+            # an entry point: the verdicts assume its annotations -- check them
+            forced = not self._contract_ok(f, {p.name: v for p, v in zip(f.params, args)})
+        if forced:
+            self.variant = "checked"
+        try:
+            if ent is not None:
+                return getattr(self, "_p_" + ent.pipeline)(f, list(args))
+            return self._generic(f, list(args))
+        finally:
+            if forced:
+                self.variant = "selected"
 
     # -- generic combinator-level execution ----------------------------------
     # Any function whose body is built from the builtins runs one kernel per
@@ -461,7 +508,8 @@ class Interp:
             sub = Interp.__new__(Interp)
             sub.__dict__.update(self.__dict__)
             sub.as_tensors = True  # arrays stay on the device between calls
-            if fs.status != "verified":  # see _callee_sel
+            sub._internal = True  # the verifier proved the callee's preconditions at this call ...
+            if fs.status != "verified":  # ... only in a verified caller (see _callee_sel)
                 sub.variant = "checked"
             vals = [ev(a) for a in e.args]
             return sub.call(name, vals)
@@ -632,9 +680,7 @@ class Interp:
         return (m1, m2, self._out(ys))
 
     def _p_mksgmdescr(self, f, a):
-        shape, xs = _dev_i64(a[0], self.dev), _dev_i64(a[1], self.dev)
-        if shape.numel() != xs.numel():
-            xs = xs[: shape.numel()] if xs.numel() > shape.numel() else xs
+        shape, xs = _dev_i64(a[0], self.dev), _dev_i64(a[1], self.dev)  # the ABI pairs min(m, len xs)
         st = ops.Status(self.dev)
         res = ops.mksgmdescr(shape, xs, self._variant(f), st)
         self._raise(st, f)
@@ -658,7 +704,7 @@ class Interp:
     def _p_c2(self, f, a):
         p, xs, shape = _pred(a[0]), _dev_i64(a[1], self.dev), _dev_i64(a[2], self.dev)
         filt, mkf = self.funs["filter"], self.funs["mkFlags"]
-        variant = self._variant(filt) | (self._variant(mkf) << 8)
+        variant = self._callee_variant(filt, {"p": p, "xs": xs}) | (self._callee_variant(mkf, {"shape": shape}) << 8)
         st = ops.Status(self.dev)
         ys, zs, dk = ops.c2(xs, p, shape, variant, st, z_dtype=torch.int64)
         s, (k,) = st.read_with(dk)
@@ -675,8 +721,9 @@ class Interp:
         H = ops.hist(L.HIST_MIN, n_es, n_verts, es, is_)                      # :17
         cs = ops.eq_gather(H, es, is_, self._variant(f), st)                 # :18, site H[i]
         self._raise(st, f)
-        xs, k1 = ops.filter_by(cs, es, self._variant(fb), st)                # :19
-        ys, k2 = ops.filter_by(cs, is_, self._variant(fb), st)               # :20
+        vfb = self._callee_variant(fb, {"cs": cs, "xs": es})
+        xs, k1 = ops.filter_by(cs, es, vfb, st)                             # :19
+        ys, k2 = ops.filter_by(cs, is_, vfb, st)                            # :20
         k = int(k1.item())
         self._raise(st, fb)
         return (self._out(xs, k), self._out(ys, k))
@@ -840,7 +887,15 @@ def _is_bool_expr(e, funs=None) -> bool:
 
 
 def eval_program(program, fun: str, args: list, step_budget: int = 10**6, *, variant: str = "selected",
-                 device=None, as_tensors: bool = False, generic_only: bool = False):
-    """Drop-in for ``ixverify.oracle.eval_program`` (oracle.py:332-333)."""
+                 device=None, as_tensors: bool = False, generic_only: bool = False, preconditions: str = "check"):
+    """Drop-in for ``ixverify.oracle.eval_program`` (oracle.py:332-333).
+
+    variant="selected" runs each site in the form the reference verifier
+    chose (ELIDED where it proved the check unnecessary), "checked" every
+    site with the interpreter's own dynamic checks.  preconditions="check"
+    (default) validates the entry function's annotations on the device first
+    and falls back to CHECKED when one fails, so the result always equals the
+    reference's; "trust" skips that when the caller guarantees them (the
+    paper's contract)."""
     return Interp(program, step_budget, variant=variant, device=device, as_tensors=as_tensors,
-                  generic_only=generic_only).call(fun, args)
+                  generic_only=generic_only, preconditions=preconditions).call(fun, args)

@@ -229,10 +229,19 @@ def sites(fundef):
 
 
 # ----------------------------------------------------------------- fingerprint
-def canonical(fundef) -> str:
+def canonical(fundef, contract: bool = False) -> str:
     """Position-free, alpha-normalised text of a normalized function: bound
     names (params, lets, lambda params, loop variables) become v0, v1, ...
-    in binding order; free names (builtins, other functions) stay."""
+    in binding order; free names (builtins, other functions) stay.
+
+    contract=False: the body only (what a pipeline must compute -- the
+    registry's key).  contract=True adds everything the verifier ASSUMES or
+    PROVES about the function: the parameter preconditions (``Param.pre``,
+    assumed by infer.py:231-338 ``_bind_param`` / ``_assume_cond``), loop
+    parameter types and preconditions, the result type and the
+    postcondition (``FunDef.post``) -- two functions with the same body but
+    different annotations get different verdicts, so the frozen verdict
+    table is keyed by this form (``closure_fingerprint``)."""
     names: dict = {}
 
     def bind(n):
@@ -291,6 +300,8 @@ def canonical(fundef) -> str:
             inits = " ".join(ex(x) for x in e.inits)
             bound = ex(e.bound) if e.bound is not None else ""
             ps = " ".join(bind(p.name) for p in e.params)
+            if contract:
+                ps += " | " + " ".join(f"{ty(p.type)}:{ex(p.pre) if p.pre is not None else '-'}" for p in e.params)
             cnt = bind(e.counter) if e.counter else ""
             cond = ex(e.cond) if e.cond is not None else ""
             return f"(loop {e.kind} ({ps}) ({inits}) {cnt} {bound} {cond} {ex(e.body)})"
@@ -298,7 +309,14 @@ def canonical(fundef) -> str:
 
     sizes = " ".join(bind(s) for s in fundef.sizes)
     params = " ".join(f"{bind(p.name)}:{ty(p.type)}" for p in fundef.params)
-    return f"(def ({sizes}) ({params}) {ex(fundef.body)})"
+    if not contract:
+        return f"(def ({sizes}) ({params}) {ex(fundef.body)})"
+    # every parameter is bound before any precondition is printed (a
+    # precondition may name a later parameter)
+    pres = " ".join(ex(p.pre) if p.pre is not None else "-" for p in fundef.params)
+    post = ex(fundef.post) if fundef.post is not None else "-"
+    return (f"(def ({sizes}) ({params}) (pre {pres}) (res {ty(fundef.result_type)}) (post {post}) "
+            f"{ex(fundef.body)})")
 
 
 _FP_CACHE: dict = {}  # id(fundef) -> (fundef, fingerprint): programs are immutable values
@@ -313,6 +331,49 @@ def fingerprint(fundef) -> str:
         _FP_CACHE.clear()
     _FP_CACHE[id(fundef)] = (fundef, fp)
     return fp
+
+
+def callees(fundef, names) -> list:
+    """Program functions (from `names`) that `fundef` applies, sorted."""
+    out = set()
+
+    def walk(e):
+        if kind(e) == "App" and kind(e.fun) == "VarE" and e.fun.name in names:
+            out.add(e.fun.name)
+        for c in children(e):
+            walk(c)
+
+    walk(fundef.body)
+    return sorted(out)
+
+
+def closure_fingerprint(program, fundef) -> str:
+    """Key of a function's verifier verdicts: its contract form (body +
+    annotations, ``canonical(contract=True)``) together with the closure
+    fingerprints of every program function it calls, transitively -- the
+    verifier proves a caller's sites from its callees' analysis results
+    (infer.py:1387-1420 applies a callee's gamma and postcondition), so a
+    redefined helper must change the caller's key.  Recursion is cut by
+    naming the cycle."""
+    defs = {f.name: f for f in program.defs}
+    memo: dict = {}
+
+    def fp(f, stack):
+        if f.name in memo:
+            return memo[f.name]
+        if f.name in stack:
+            return f"rec:{f.name}"
+        parts = [canonical(f, contract=True)]
+        for c in callees(f, defs):
+            if c == f.name:
+                parts.append(f"{c}=self")
+            else:
+                parts.append(f"{c}={fp(defs[c], stack | {f.name})}")
+        h = hashlib.sha256("\n".join(parts).encode()).hexdigest()[:16]
+        memo[f.name] = h
+        return h
+
+    return fp(fundef, frozenset())
 
 
 def find_def(program, name: str):

@@ -400,14 +400,14 @@ def mksgmdescr(shape: torch.Tensor, xs: torch.Tensor, variant: int, status: Stat
     d_len = torch.empty(1, dtype=torch.int64, device=xs.device)
     ws, wsb = _ws(L.OP_MKSGMDESCR, 0, m, xs.device)
     lib = _lib()
-    L.check(lib.ixg_mksgmdescr(_ptr(shape), _ptr(xs), m, _ptr(None), 0, _ptr(d_len), variant, status.ptr, ws, wsb,
-                               _stream()), "mksgmdescr")
+    L.check(lib.ixg_mksgmdescr(_ptr(shape), _ptr(xs), m, xs.numel(), _ptr(None), 0, _ptr(d_len), variant, status.ptr,
+                               ws, wsb, _stream()), "mksgmdescr")
     cap = int(d_len.item())
     res = torch.empty(max(cap, 0), dtype=torch.int64, device=xs.device)
     if cap > 0:
         ws, wsb = _ws(L.OP_MKSGMDESCR, cap, m, xs.device)
-        L.check(lib.ixg_mksgmdescr(_ptr(shape), _ptr(xs), m, _ptr(res), cap, _ptr(d_len), variant, status.ptr, ws,
-                                   wsb, _stream()), "mksgmdescr")
+        L.check(lib.ixg_mksgmdescr(_ptr(shape), _ptr(xs), m, xs.numel(), _ptr(res), cap, _ptr(d_len), variant,
+                                   status.ptr, ws, wsb, _stream()), "mksgmdescr")
     return res
 
 
@@ -523,3 +523,35 @@ def gen_uniform(n: int, lo: int, hi: int, seed: int, dtype=torch.int32, offset: 
 
 def launch_count() -> int:
     return int(_lib().ixg_launch_count())
+
+
+# ------------------------------------------------------------------ preconditions
+def minmax(xs: torch.Tensor) -> torch.Tensor:
+    """[min, max] of an integer array as a device int64 pair (ixg_minmax)."""
+    xs = _contig(xs.view(torch.uint8) if xs.dtype == torch.bool else xs)
+    out = torch.empty(2, dtype=torch.int64, device=xs.device)
+    L.check(_lib().ixg_minmax(_dt(xs), _ptr(xs), xs.numel(), _ptr(out), _stream()), "minmax")
+    return out
+
+
+def mono_violations(xs: torch.Tensor, op: int) -> torch.Tensor:
+    """adjacent pairs of xs violating op (0 <=, 1 <, 2 >=, 3 >) (ixg_mono_check)."""
+    xs = _contig(xs)
+    out = torch.empty(1, dtype=torch.int64, device=xs.device)
+    L.check(_lib().ixg_mono_check(_dt(xs), _ptr(xs), xs.numel(), op, _ptr(out), _stream()), "mono_check")
+    return out
+
+
+def inj_check(xs: torch.Tensor, lo: int, hi: int, img_lo: int, img_hi: int) -> Optional[torch.Tensor]:
+    """[in-range count, repeats, in-range values outside the image] over the
+    values of xs in [lo, hi] (ixg_inj_check); None if the range is too wide
+    for a claim bitmap."""
+    xs = _contig(xs.to(torch.int64))
+    nb = int(_lib().ixg_inj_bitmap_bytes(lo, hi))
+    if nb < 0:
+        return None
+    bitmap = torch.empty(max(nb, 16), dtype=torch.uint8, device=xs.device)
+    out = torch.empty(3, dtype=torch.int64, device=xs.device)
+    L.check(_lib().ixg_inj_check(_ptr(xs), xs.numel(), lo, hi, img_lo, img_hi, _ptr(bitmap), bitmap.numel(), _ptr(out),
+                                 _stream()), "inj_check")
+    return out

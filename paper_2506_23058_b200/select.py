@@ -22,7 +22,9 @@ Per site:
 
 The verifier only exists where the reference is installed; the verdicts for
 the bundled corpus are frozen in ``data/selection.json`` (keyed by
-``ir.fingerprint``) so the GPU box can select without it.
+``ir.closure_fingerprint``: body, annotations and callees) so the GPU box
+can select without it.  The live verifier always wins when it is
+importable; a frozen key held with two different verdicts is dropped.
 """
 
 from __future__ import annotations
@@ -68,6 +70,13 @@ class FunSelection:
     fingerprint: str
     status: str
     sites: list = field(default_factory=list)
+    closure: str = ""  # ir.closure_fingerprint: the key the verdicts are valid for
+    source: str = ""   # "live" | "frozen" | "checked" (where these verdicts came from)
+
+    @property
+    def elides(self) -> bool:
+        """does any site run without its check?"""
+        return any(s.bits != (L.V_BOUNDS if s.kind == "bounds" else L.V_CONFLICT | L.V_INIT) for s in self.sites)
 
     def bits(self, ordinal: int) -> int:
         return self.sites[ordinal].bits
@@ -80,6 +89,7 @@ class FunSelection:
 
     def to_json(self):
         d = asdict(self)
+        d.pop("source", None)
         for s in d["sites"]:
             s["pos"] = list(s["pos"])
         return d
@@ -87,7 +97,7 @@ class FunSelection:
     @classmethod
     def from_json(cls, d):
         sites = [SiteVerdict(**{**s, "pos": tuple(s["pos"])}) for s in d["sites"]]
-        return cls(d["name"], d["fingerprint"], d["status"], sites)
+        return cls(d["name"], d["fingerprint"], d["status"], sites, d.get("closure", ""))
 
 
 @dataclass
@@ -162,29 +172,47 @@ def select(program, max_rewrites: int = 1000) -> Selection:
                     except Exception:
                         v.sc1 = False
             sites.append(v)
-        funcs[f.name] = FunSelection(f.name, ir.fingerprint(f), status, sites)
+        funcs[f.name] = FunSelection(f.name, ir.fingerprint(f), status, sites, ir.closure_fingerprint(program, f),
+                                     "live")
     return Selection(funcs)
 
 
 # ----------------------------------------------------------------- frozen
 _FROZEN = None
+AMBIGUOUS: set = set()  # closure keys the frozen table holds with conflicting verdicts
+
+
+def _verdict_key(fs: FunSelection):
+    # the status text carries source positions; compare its class only
+    return (":".join(fs.status.split(":")[:2]), tuple((s.kind, s.recorded, s.proved, s.sc1) for s in fs.sites))
 
 
 def frozen() -> dict:
-    """fingerprint -> FunSelection for the bundled corpus (data/selection.json)."""
+    """closure fingerprint -> FunSelection for the bundled corpus
+    (data/selection.json).  A key that occurs with two different verdicts is
+    dropped (it selects all-CHECKED), never resolved by load order."""
     global _FROZEN
     if _FROZEN is None:
         path = os.path.join(DATA, "selection.json")
-        _FROZEN = {}
+        table: dict = {}
         if os.path.exists(path):
             with open(path) as fh:
                 for d in json.load(fh).values():
                     fs = FunSelection.from_json(d)
-                    _FROZEN[fs.fingerprint] = fs
+                    if not fs.closure:
+                        continue  # a verdict without its contract key is never trusted
+                    prev = table.get(fs.closure)
+                    if prev is not None and _verdict_key(prev) != _verdict_key(fs):
+                        AMBIGUOUS.add(fs.closure)
+                    table.setdefault(fs.closure, fs)
+        for k in AMBIGUOUS:
+            table.pop(k, None)
+        _FROZEN = table
     return _FROZEN
 
 
 _SEL_CACHE: dict = {}  # (id(program), id(fundef), live | checked) -> (program, fundef, selection)
+_LIVE_CACHE: dict = {}  # id(program) -> (program, Selection)
 
 
 def _cached(key, program, fundef, make):
@@ -205,25 +233,45 @@ def checked_selection(fundef) -> FunSelection:
 
 def _checked_selection(fundef) -> FunSelection:
     sites = [SiteVerdict(k, pos, ir.expr_str(n)) for k, pos, n in ir.sites(fundef)]
-    return FunSelection(fundef.name, ir.fingerprint(fundef), "checked (no verdict)", sites)
+    return FunSelection(fundef.name, ir.fingerprint(fundef), "checked (no verdict)", sites, "", "checked")
 
 
 def selection_for(program, fundef, live: bool = True) -> FunSelection:
-    """Verdicts for one function: live verifier when importable, else the
-    frozen corpus table by fingerprint, else all CHECKED (memoised per
-    program and function object)."""
+    """Verdicts for one function, in this order:
+      1. the live reference verifier, whenever it is importable and
+         `program` is the reference's own AST (run once per program);
+      2. the frozen corpus table, matched on the closure fingerprint (body,
+         annotations and every callee, ``ir.closure_fingerprint``) -- an
+         unannotated or re-annotated copy of a corpus function, or one whose
+         helper was redefined, never inherits the corpus verdicts;
+      3. otherwise every site CHECKED.
+    Memoised per program and function object."""
     return _cached((id(program), id(fundef), live), program, fundef, lambda: _selection_for(program, fundef, live))
 
 
+def _live(program) -> Selection:
+    hit = _LIVE_CACHE.get(id(program))
+    if hit is not None and hit[0] is program:
+        return hit[1]
+    s = select(program)
+    if len(_LIVE_CACHE) > 256:
+        _LIVE_CACHE.clear()
+    _LIVE_CACHE[id(program)] = (program, s)
+    return s
+
+
 def _selection_for(program, fundef, live: bool) -> FunSelection:
-    fp = ir.fingerprint(fundef)
-    fz = frozen().get(fp)
-    if fz is not None:
-        # positions may differ from the frozen source: re-key by ordinal
-        cur = ir.sites(fundef)
-        if len(cur) == len(fz.sites):
-            sites = [SiteVerdict(**{**asdict(s), "pos": pos}) for s, (_, pos, _) in zip(fz.sites, cur)]
-            return FunSelection(fundef.name, fp, fz.status, sites)
-    if live and reference_available() and type(program).__module__.startswith("ixverify"):
-        return select(program)[fundef.name]
+    if live and program is not None and type(program).__module__.startswith("ixverify") and reference_available():
+        fs = _live(program).funcs.get(fundef.name)
+        if fs is not None:
+            return fs
+    if program is not None:
+        key = ir.closure_fingerprint(program, fundef)
+        fz = frozen().get(key)
+        if fz is not None:
+            # positions may differ from the frozen source: re-key by ordinal
+            cur = ir.sites(fundef)
+            if len(cur) == len(fz.sites) and all(a.kind == k for a, (k, _, _) in zip(fz.sites, cur)):
+                sites = [SiteVerdict(**{**asdict(s), "pos": pos}) for s, (_, pos, _) in zip(fz.sites, cur)]
+                return FunSelection(fundef.name, fz.fingerprint, fz.status, sites, key, "frozen")
     return checked_selection(fundef)

@@ -39,6 +39,7 @@ sys.path.insert(0, REF)
 import numpy as np  # noqa: E402
 from ixverify.normalize import check_well_formed, normalize  # noqa: E402
 from ixverify.oracle import Interp, OracleError, eval_program, gen_args  # noqa: E402
+from ixverify.oracle import _check_pre_atom, _conjuncts, chk_bij, chk_inj  # noqa: E402
 from ixverify.parser import parse_program  # noqa: E402
 
 from paper_2506_23058_b200 import gen, ir  # noqa: E402
@@ -84,6 +85,46 @@ def run(program, fun, args, budget=BUDGET):
         if getattr(e, "pos", None) is not None:
             d["pos"] = list(e.pos)
         return d
+
+
+PROPERTY_HEADS = {"Range", "Equiv", "Mono", "Inj", "Bij", "FiltPart", "InvFiltPart", "OrthogPreds"}
+
+
+def ref_pre_holds(program, fun, args):
+    """Do the entry function's annotations hold for these arguments, by the
+    reference's own concrete predicates?  Range / Mono through
+    oracle.py:712-734 _check_pre_atom, Inj / Bij over their codomain interval
+    through chk_inj / chk_bij (oracle.py:492-520; the interval is what the
+    verifier assumes, infer.py:306-324).  None = no annotations; False also
+    for properties with no concrete check (Equiv, FiltPart, ...)."""
+    interp = Interp(program, BUDGET)
+    f = interp.funs[fun]
+    if all(p.pre is None for p in f.params) or len(args) != len(f.params):
+        return None
+    env = {p.name: a for p, a in zip(f.params, args)}
+    interp._bind_sizes(f, args, env)
+    for p in f.params:
+        if p.pre is None:
+            continue
+        for atom in _conjuncts(p.pre):
+            head = atom.fun.name if type(atom).__name__ == "App" and type(atom.fun).__name__ == "VarE" else None
+            try:
+                if head in ("Inj", "Bij"):
+                    x = env[atom.args[0].name]
+                    lo, hi = (interp.eval(e, env) for e in atom.args[1].items)
+                    if head == "Inj":
+                        ok = chk_inj(x, lo, hi)
+                    else:
+                        ok = chk_bij(x, (lo, hi), None, [tuple(interp.eval(e, env) for e in atom.args[2].items)])
+                elif head in PROPERTY_HEADS and head not in ("Range", "Mono"):
+                    ok = False
+                else:
+                    ok = _check_pre_atom(atom, p, env, interp)
+            except Exception:
+                ok = False
+            if not ok:
+                return False
+    return True
 
 
 def swap_preds(args, rng):
@@ -219,16 +260,28 @@ def error_cases(fun):
         return [[[0, 0, 0, 0], [0, 2, 0], [1, 2, 3]],      # conflicting duplicate
                 [[0, 0, 0], [1, 1, 7, -1], [5, 5, 9, 9]],  # equal duplicate + OOB
                 [[0, 0, 0], [0, 1, 2], [7, 8]]]            # zip truncation
-    if fun == "csrg_any":
-        return [[[1, 2, 3], [4, 5, 6, 7], [0, 2, 3, 1]], [[1, 2, 3], [4, 5], [-1, 0]]]
+    if fun in ("csrg_any", "csrg"):  # csrg: its Range annotation violated
+        return [[[1, 2, 3], [4, 5, 6, 7], [0, 2, 3, 1]], [[1, 2, 3], [4, 5], [-1, 0]], [[1, 2, 3], [4, 5], [0, 3]]]
+    if fun == "sc_bij":  # Inj / Bij violated: conflict, equal duplicate, out of range, not onto
+        return [[[0, 0, 0], [0, 0, 1], [5, 6, 7]], [[0, 0, 0], [0, 0, 1], [5, 5, 7]],
+                [[9, 9, 9], [0, 5, 1], [1, 2, 3]], [[9, 9, 9], [2, 1, 1], [4, 4, 4]]]
+    if fun == "sc_inj":
+        return [[[0, 0, 0], [1, 1, 2], [4, 5, 6]], [[0, 0, 0], [1, 1, 2], [4, 4, 6]]]
+    if fun == "c2":  # Range shape (0, inf) violated
+        return [[Pred.ge(0), [1, -2, 3, 4, 0], [2, -1, 1, 1]], [Pred.ge(0), [5, 6, 7], [-2, 3, 2]]]
     if fun == "kmeans_ker":
         return [[2, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],         # pointers[row+1] OOB
                 [0, [0, 3], [1.0], [0.5, 1.0, 2.0], [0, 0, 0]],          # values[...] OOB at j=2
-                [0, [0, 2], [1.0, 2.0], [0.5, 1.0], [1, 5]]]             # cluster[column] OOB
+                [0, [0, 2], [1.0, 2.0], [0.5, 1.0], [1, 5]],             # cluster[column] OOB
+                [3, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],          # pointers[row] OOB
+                [-1, [0, 1, 2], [1.5, 2.5], [0.5, 1.0], [0, 1]],         # negative row
+                [0, [0, 2, 1], [1.5], [0.5, 1.0], [0, 0]]]               # Range pointers holds, row 1 empty
     if fun == "mkSgmDescr":
-        return [[[3, -3, 4, 1], [1, 2, 3, 4]]]                           # negative shape -> conflict
+        return [[[3, -3, 4, 1], [1, 2, 3, 4]],                           # negative shape -> conflict
+                [[2, 1, 3], [7, 8]], [[2, 0, 1], [1, 2, 3, 4]]]          # zip truncation: short / long xs
     if fun == "get_smallest_pairs":
-        return [[3, 99, [0, 5, 1], [4, 2, 7]]]                           # H[i] OOB
+        return [[3, 99, [0, 5, 1], [4, 2, 7]],                           # H[i] OOB
+                [3, 99, [0, 1, 2, 1], [4, 4, 7, 7]]]                     # Inj is violated
     if fun == "all_rows":
         return [[[0, 2, 5], [1.5, 2.0], [0.5, 1.0, 2.0, 3.0], [0, 1, 1, 0]],     # vals[lo + j] OOB in row 1
                 [[0, 1, 3], [1.5], [0.5, 1.0, 2.0], [0, 0, 4]]]                  # cl[cols[lo + j]] OOB
@@ -298,6 +351,7 @@ def main():
                 # a never-ending loop is cut by the default budget (oracle.py:118)
                 bud = 10**6 if (f.name, origin_kind) == ("countdown", "error") else BUDGET
                 rec.update(run(prog, f.name, a, bud))
+                rec["pre"] = ref_pre_holds(prog, f.name, a)
                 rec["budget"] = bud  # the step budget the reference ran with
                 cases.append(rec)
     data = os.path.join(ROOT, "paper_2506_23058_b200", "data")

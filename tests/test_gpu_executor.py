@@ -11,6 +11,7 @@ import os
 import pytest
 
 from paper_2506_23058_b200 import errors, ir
+from paper_2506_23058_b200 import select as sel
 
 from test_oracle_golden import CASES, dec
 
@@ -37,36 +38,55 @@ def _same(got, want):
     return got == want
 
 
+def expected_entry_bits(prog, fun, mode, pre):
+    """The variant bits the executor must run the entry function's sites
+    with: the verifier's (frozen, closure-keyed) verdicts in selected mode
+    when the reference's own predicates say the annotations hold
+    (cases.json "pre", make_golden.ref_pre_holds), else every check."""
+    f = ir.find_def(prog, fun)
+    chk = sel.checked_selection(f)
+    if mode == "checked":
+        return tuple(s.bits for s in chk.sites)
+    fs = sel.selection_for(prog, f)
+    if pre is False and fs.elides:
+        return tuple(s.bits for s in chk.sites)
+    return tuple(s.bits for s in fs.sites)
+
+
 @pytest.mark.parametrize("mode", ["selected", "checked", "generic"])
 @pytest.mark.parametrize("idx", range(len(CASES)))
 def test_eval_program_matches_reference(cuda, idx, mode):
-    from paper_2506_23058_b200.executor import eval_program
+    """Every golden case in every mode -- including inputs that violate the
+    annotations the verifier relied on: selected mode checks them on the
+    device and runs CHECKED, so it must raise / answer exactly like the
+    reference -- and the variant bits actually used for the entry function's
+    sites are asserted, not just the values."""
+    from paper_2506_23058_b200.executor import Interp
 
     case = CASES[idx]
     if mode == "generic" and case["fun"] in GENERIC_UNSUPPORTED:
         pytest.skip("loop body: pipeline only")
     prog = program(case["program"])
     args = dec(case["args"])
-    kw = {"variant": "checked" if mode == "checked" else "selected", "generic_only": mode == "generic",
-          "step_budget": case.get("budget", 10**6)}
+    kw = {"variant": "checked" if mode == "checked" else "selected", "generic_only": mode == "generic"}
+    if "error" in case and mode == "generic":
+        kw["variant"] = "checked"  # generic path with the reference's own checks
+    it = Interp(prog, case.get("budget", 10**6), **kw)
     if "error" in case:
-        if mode == "generic":
-            kw["variant"] = "checked"  # generic path with the reference's own checks
-        if mode == "selected" and case["fun"] not in ("sc_any", "csrg_any", "mkSgmDescr"):
-            # the input violates a precondition the verifier relied on: the
-            # ELIDED form is only defined for inputs that satisfy it
-            pytest.skip("unsafe input for sites the verifier proved")
         cls = getattr(errors, case["error"])
         with pytest.raises(cls) as ei:
-            eval_program(prog, case["fun"], args, **kw)
+            it.call(case["fun"], args)
         if "site" in case:
             assert ei.value.site == case["site"]
         if "pos" in case:
             assert list(ei.value.pos) == case["pos"]
-        return
-    got = eval_program(prog, case["fun"], args, **kw)
-    want = dec(case["result"])
-    assert _same(got, want), (got, want)
+    else:
+        got = it.call(case["fun"], args)
+        want = dec(case["result"])
+        assert _same(got, want), (got, want)
+    used = [t[3] for t in it.trace if t[0] == "select" and t[1] == case["fun"]]
+    if used and ir.sites(ir.find_def(prog, case["fun"])):
+        assert used[0] == expected_entry_bits(prog, case["fun"], kw["variant"], case.get("pre")), it.trace
 
 
 def test_opaque_callable_rejected(cuda):

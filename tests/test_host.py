@@ -383,3 +383,114 @@ def test_bench_reference_arm_contract():
     assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in line["config"]
+
+
+# ----------------------------------------------------------------- soundness of the selection
+def _prog(key):
+    return ir.from_json(PROGRAMS[key]["program"])
+
+
+def test_closure_keys_distinguish_annotations():
+    """csrg / csrg_any and sc_bij / sc_inj share a body but not their
+    annotations: their verdicts must not share a key."""
+    def key(k, fn):
+        p = _prog(k)
+        return ir.closure_fingerprint(p, ir.find_def(p, fn))
+
+    c4, c3 = "own:c4_csr_gather.ixl", "own:c3_scatter.ixl"
+    assert ir.fingerprint(ir.find_def(_prog(c4), "csrg")) == ir.fingerprint(ir.find_def(_prog(c4), "csrg_any"))
+    assert key(c4, "csrg") != key(c4, "csrg_any")
+    assert key(c3, "sc_bij") != key(c3, "sc_inj") != key(c3, "sc_any")
+    assert key("ref:kmeans_ker.ixl", "kmeans_ker") != key("own:kmeans_noann.ixl", "kmeans_ker")
+
+
+def test_frozen_table_unambiguous_and_selects_by_contract():
+    fz = sel.frozen()
+    assert not sel.AMBIGUOUS, sel.AMBIGUOUS
+    assert all(fs.closure for fs in fz.values())
+    bits = lambda k, fn: [s.bits for s in sel.selection_for(_prog(k), ir.find_def(_prog(k), fn), live=False).sites]
+    assert bits("own:c4_csr_gather.ixl", "csrg") == [0]
+    assert bits("own:c4_csr_gather.ixl", "csrg_any") == [L.V_BOUNDS]
+    assert bits("own:c3_scatter.ixl", "sc_bij") == [0]
+    assert bits("own:c3_scatter.ixl", "sc_inj") == [L.V_INIT]
+    assert bits("own:c3_scatter.ixl", "sc_any") == [L.V_CONFLICT | L.V_INIT]
+    # kmeans_ker without its Range annotations: every site CHECKED
+    assert bits("ref:kmeans_ker.ixl", "kmeans_ker") == [0] * 5
+    assert bits("own:kmeans_noann.ixl", "kmeans_ker") == [L.V_BOUNDS] * 5
+
+
+def _strip_pre(prog, fn):
+    d = ir.to_json(prog)
+    for f in d["defs"]:
+        if f["name"] == fn:
+            for p in f["params"]:
+                p["pre"] = None
+    return ir.from_json(d)
+
+
+def test_unannotated_copy_never_inherits_verdicts():
+    """The same body with its annotations removed (or a different postcondition)
+    is not in the table: all CHECKED, never the corpus verdict."""
+    for key, fn in (("ref:kmeans_ker.ixl", "kmeans_ker"), ("own:c4_csr_gather.ixl", "csrg"),
+                    ("own:c3_scatter.ixl", "sc_bij"), ("ref:maxmatching.ixl", "get_smallest_pairs")):
+        p = _strip_pre(_prog(key), fn)
+        fs = sel.selection_for(p, ir.find_def(p, fn), live=False)
+        assert not fs.elides, (key, fn, fs.source)
+
+
+def test_redefined_callee_changes_caller_key():
+    """A caller's verdicts come from its callees' analysis (infer.py:1387-1420):
+    redefining a helper must change the caller's key, so the caller does not
+    inherit the corpus verdicts."""
+    prog = _prog("ref:maxmatching.ixl")
+    gsp = ir.find_def(prog, "get_smallest_pairs")
+    assert sel.selection_for(prog, gsp, live=False).source == "frozen"
+    d = ir.to_json(prog)
+    for f in d["defs"]:
+        if f["name"] == "filter_by":  # a different helper under the same name
+            f["body"] = {"$": "VarE", "name": "xs", "pos": [1, 1]}
+    prog2 = ir.from_json(d)
+    assert ir.fingerprint(ir.find_def(prog2, "get_smallest_pairs")) == ir.fingerprint(gsp)
+    assert ir.closure_fingerprint(prog2, ir.find_def(prog2, "get_smallest_pairs")) != ir.closure_fingerprint(prog, gsp)
+    assert sel.selection_for(prog2, ir.find_def(prog2, "get_smallest_pairs"), live=False).source == "checked"
+
+
+@pytest.mark.reference
+def test_live_verifier_wins_over_frozen(reference):
+    """With the reference importable, a reference AST is verified live, even
+    when the frozen table holds the same key."""
+    from ixverify.normalize import normalize
+    from ixverify.parser import parse_program
+
+    src = PROGRAMS["own:kmeans_noann.ixl"]["source"]
+    prog = normalize(parse_program(src, "kmeans_noann.ixl"))
+    fs = sel.selection_for(prog, ir.find_def(prog, "kmeans_ker"))
+    assert fs.source == "live" and [s.bits for s in fs.sites] == [L.V_BOUNDS] * 5
+    src = PROGRAMS["ref:kmeans_ker.ixl"]["source"]
+    prog = normalize(parse_program(src, "kmeans_ker.ixl"))
+    fs = sel.selection_for(prog, ir.find_def(prog, "kmeans_ker"))
+    assert fs.source == "live" and [s.bits for s in fs.sites] == [0] * 5
+
+
+def test_contract_host_side():
+    """The host half of the precondition check: sizes, scalar annotations,
+    intervals with inf (contract.py; oracle.py:712-734)."""
+    from paper_2506_23058_b200 import contract
+
+    prog = _prog("ref:kmeans_ker.ixl")
+    f = ir.find_def(prog, "kmeans_ker")
+    env = contract.bind_sizes(f, {"pointers": [0, 1, 2], "values": [0.5], "indices": [0], "cluster": [1.0, 2.0]})
+    assert env["n"] == 2 and env["nnz"] == 1 and env["num_cols"] == 2
+    row_pre = f.params[0].pre
+    atom = next(contract.conjuncts(row_pre))
+    assert contract._atom(atom, {**env, "row": 1}) is True
+    assert contract._atom(atom, {**env, "row": 2}) is False
+    assert contract._atom(atom, {**env, "row": -1}) is False
+    ok, why = contract.check(f, {"row": 5, "pointers": [0, 1, 2]})
+    assert not ok and "row" in why
+    gsp = ir.find_def(_prog("ref:maxmatching.ixl"), "get_smallest_pairs")
+    inj = list(contract.conjuncts(gsp.params[3].pre))[0]
+    lo, hi = contract._interval(inj.args[1], {})
+    assert lo == float("-inf") and hi == float("inf")
+    assert contract._clamp_int(lo, hi, -5, 9) == (-5, 9)
+    assert contract._clamp_int(0, 3, -5, 9) == (0, 3)
