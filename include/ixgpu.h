@@ -102,6 +102,13 @@ typedef struct ixg_status {
   unsigned int codes;
   unsigned int flags;
 } ixg_status;
+/* An integer result left int64.  The reference's ints are unbounded
+ * (oracle.py:214-240; a scan of [2^62, 2^62, 2^62] gives 3*2^62), the device
+ * computes in int64: every i64 path checks its results exactly (scans: each
+ * output against its predecessor, hist (+): 128-bit bins, lambdas: every
+ * + - *) and records IXG_OVERFLOW with site IXG_OVF_SITE; the host raises
+ * instead of returning a wrapped value. */
+#define IXG_OVF_SITE 254
 #define IXG_F_DUP 1u      /* a scatter destination was claimed twice       */
 #define IXG_F_NARROW 2u   /* a result did not fit its i32 storage          */
 
@@ -120,6 +127,7 @@ typedef struct ixg_status {
 #define IXG_OP_C2 7
 #define IXG_OP_MKSGMDESCR 8
 #define IXG_OP_MKFLAGS 9
+#define IXG_OP_HIST 10     /* m = dlen */
 
 /* ---- library / device --------------------------------------------------- */
 int ixg_version(void);
@@ -135,9 +143,10 @@ unsigned long long ixg_launch_count(void);
 
 /* scan (+) ne xs  (oracle.py:281-293, k = 1, f = (+)): out[i] = ne + sum_{j<=i} xs[j]
  * (ne folded once).  `exclusive` != 0 gives out[i] = ne + sum_{j<i} xs[j].
- * xs: dt in {I32, I64, U8}; out: int64. */
+ * xs: dt in {I32, I64, U8}; out: int64.  st (nullable): IXG_OVERFLOW at the
+ * first element whose sum leaves int64. */
 int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, int64_t* out,
-                 void* ws, size_t ws_bytes, void* stream);
+                 void* ws, size_t ws_bytes, ixg_status* st, void* stream);
 
 /* partition2L's scatter destinations (corpus/partition2l.ixl:41, PAPER.md:
  * 3250-3261) for a jagged array with sum shp == n: bits = row starts (the
@@ -159,7 +168,7 @@ int ixg_reduce_add(int dt, const void* xs, int64_t n, int64_t* out, void* stream
  * component.  flags: dt_f in {U8, I32, I64} (non-zero = true); xs: dt_x. */
 int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64_t n, int f0,
                     int64_t v0, int64_t* out_v, uint8_t* out_f, void* ws, size_t ws_bytes,
-                    void* stream);
+                    ixg_status* st, void* stream);
 
 /* scatter dst is vs (oracle.py:294-305).  `out` must already hold the copy of
  * dst (length ndst) unless the site's IXG_V_INIT bit is clear (Sc1: every
@@ -177,9 +186,12 @@ int ixg_gather(int dt, const void* arr, int64_t len, const int64_t* idx, int64_t
                uint32_t site_bits, int stmt, int site, ixg_status* st, void* stream);
 
 /* hist op ne dlen is vs (oracle.py:306-316): out[0..dlen) = ne, then
- * out[i] = op(out[i], v) for in-range i.  is: int64; vs/out: int64. */
+ * out[i] = op(out[i], v) for in-range i.  is: int64; vs/out: int64.
+ * IXG_HIST_ADD accumulates each bin in 128 bits (the high words live in
+ * ws, ixg_ws_bytes(IXG_OP_HIST, 0, dlen)) and records IXG_OVERFLOW in st
+ * for a bin whose sum leaves int64. */
 int ixg_hist(int op, int64_t ne, int64_t dlen, const int64_t* is, int64_t nis, const int64_t* vs,
-             int64_t nvs, int64_t* out, void* stream);
+             int64_t nvs, int64_t* out, void* ws, size_t ws_bytes, ixg_status* st, void* stream);
 
 /* replicate n v (oracle.py:319-322) / iota n (oracle.py:317-318) */
 int ixg_fill(int dt, void* out, int64_t n, int64_t v, void* stream);

@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("IXGPU_LIB") or os.path.join(_HERE, "libixgpu.so")  # 
 
 # status / return codes (include/ixgpu.h)
 OK, OOB, CONFLICT, LENGTH, BADARG, NOMEM, OVERFLOW, NODEVICE = 0, 1, 2, 3, 4, 5, 6, 7
+OVF_SITE = 254  # status site of an int64 overflow (IXG_OVF_SITE)
 CUDA_ERR = 100
 I32, I64, U8, F64 = 0, 1, 2, 3
 V_BOUNDS, V_CONFLICT, V_INIT = 1, 2, 4
@@ -23,7 +24,8 @@ VARIANT_CHECKED = 0x77777777
 VARIANT_ELIDED = 0
 F_DUP, F_NARROW = 1, 2
 HIST_MIN, HIST_MAX, HIST_ADD = 0, 1, 2
-OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR, OP_MKFLAGS = range(1, 10)
+OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR, OP_MKFLAGS, OP_HIST = \
+    range(1, 11)
 
 
 class ixg_pred(ctypes.Structure):
@@ -64,7 +66,7 @@ SIGNATURES = {
     "ixg_ws_init": (_I, [_P, _SZ, _P]),
     "ixg_status_init": (_I, [_P, _P]),
     "ixg_launch_count": (ctypes.c_ulonglong, []),
-    "ixg_scan_add": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _SZ, _P]),
+    "ixg_scan_add": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _SZ, _P, _P]),
     "ixg_reduce_add": (_I, [_I, _P, _I64, _P, _P]),
     "ixg_jagged_dest": (_I, [_P, _I64, _P, _P, _P, _P]),
     "ixg_partition_counts": (_I, [_I, _P, _I64, _P, _P, _I, _P, _P, _SZ, _P]),
@@ -74,10 +76,10 @@ SIGNATURES = {
     "ixg_ipc_handle": (_I, [_P, _P]),
     "ixg_ipc_open": (_I, [_P, _P]),
     "ixg_ipc_close": (_I, [_P]),
-    "ixg_segscan_add": (_I, [_I, _P, _I, _P, _I64, _I, _I64, _P, _P, _P, _SZ, _P]),
+    "ixg_segscan_add": (_I, [_I, _P, _I, _P, _I64, _I, _I64, _P, _P, _P, _SZ, _P, _P]),
     "ixg_scatter": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _U32, _I, _I, _P, _P, _SZ, _P]),
     "ixg_gather": (_I, [_I, _P, _I64, _P, _I64, _P, _U32, _I, _I, _P, _P]),
-    "ixg_hist": (_I, [_I, _I64, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "ixg_hist": (_I, [_I, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _SZ, _P, _P]),
     "ixg_fill": (_I, [_I, _P, _I64, _I64, _P]),
     "ixg_iota": (_I, [_P, _I64, _P]),
     "ixg_filter": (_I, [_I, _P, _I64, _PP, _P, _P, _U32, _P, _P, _SZ, _P]),

@@ -120,11 +120,12 @@ inline uint32_t next_nonce() {
   return v;
 }
 
+// n = element count, or the capacity when d_n (device count) is given
 template <class M, class Src, class Epi>
-int launch_scan(long long n, Src src, Epi epi, LBChan ch, cudaStream_t s) {
+int launch_scan(long long n, Src src, Epi epi, LBChan ch, cudaStream_t s, const long long* d_n = nullptr) {
   if (n <= 0) return IXG_OK;
   TimedLaunch tl(IXG_K_SCAN, s);
-  k_scan<M, Src, Epi><<<(unsigned)tiles_of(n, kGTile), kGThreads, 0, s>>>(n, src, epi, ch, next_nonce());
+  k_scan<M, Src, Epi><<<(unsigned)tiles_of(n, kGTile), kGThreads, 0, s>>>(n, d_n, src, epi, ch, next_nonce());
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -249,8 +250,7 @@ int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T*
   long long* inds = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<T>(ys, 0, d_count, n, inds, xs, n, sb, 1, 1, st, ws, 1, s);
   if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
-  int rc = launch_scan<SumOp>(n, SrcPred{sizeof(T) == 4 ? IXG_I32 : IXG_I64, xs, cs, pp},
-                              EpiFilterInds{n, inds, d_count}, c0, s);
+  int rc = launch_scan<SumOp>(n, SrcPredT<T>{xs, cs, pp}, EpiFilterInds{inds, d_count}, c0, s);
   if (rc) return rc;
   if (sb & IXG_V_INIT) {
     if ((rc = launch_fill<T>(ys, 0, d_count, T(0), s))) return rc;
@@ -292,12 +292,11 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
   k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
   LAUNCHED();
   CHECK_LAUNCH();
-  const int dt = sizeof(T) == 4 ? IXG_I32 : IXG_I64;
   int rc;
   if constexpr (kClasses == 2) {
-    rc = launch_scan<SumOp>(n, SrcPred{dt, xs, nullptr, pp}, EpiPart2Inds{d_tot, inds}, c0, s);
+    rc = launch_scan<SumOp>(n, SrcPredT<T>{xs, nullptr, pp}, EpiPart2Inds{d_tot, inds}, c0, s);
   } else {
-    rc = launch_scan<Sum2Op>(n, SrcClass3{dt, xs, pp, qq}, EpiPart3Inds{d_tot, inds}, c0, s);
+    rc = launch_scan<Sum2Op>(n, SrcClass3T<T>{xs, pp, qq}, EpiPart3Inds{d_tot, inds}, c0, s);
   }
   if (rc) return rc;
   if (sb & IXG_V_INIT) {
@@ -359,10 +358,9 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
   if ((rc = launch_fill<long long>(flags, 0, d_k, 0LL, s))) return rc;
   if ((rc = launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s))) return rc;
-  // sgmSum over k elements: k is on the device, so scan all n positions of
-  // the capacity; positions >= k are never read back (ys beyond k unused).
-  return launch_scan<SegOp>(n, SrcSeg{IXG_I64, sizeof(T) == 4 ? IXG_I32 : IXG_I64, flags, ys},
-                            EpiSegOut{sizeof(Z) == 4 ? IXG_I32 : IXG_I64, zs, nullptr, st}, cz, s);
+  // sgmSum over the k = *d_k outputs (a capacity-n grid; tiles past k retire)
+  return launch_scan<SegOp>(n, SrcSegT<long long, T>{flags, ys},
+                            EpiSegOut{sizeof(Z) == 4 ? IXG_I32 : IXG_I64, zs, nullptr, st}, cz, s, d_k);
 }
 
 }  // namespace
@@ -470,6 +468,7 @@ size_t ixg_ws_bytes(int op, int64_t n, int64_t m) {
       ws.take((size_t)(m > 0 ? m : 1) * 8);
       ws.take(bitmap_bytes(n));  // n = k
       break;
+    case IXG_OP_HIST: ws.take((size_t)(m > 0 ? m : 1) * 8); break;  // m = dlen: the bins' high words
     case IXG_OP_MKSGMDESCR:
       ws.chan(0, tiles_of(m, kGTile));
       ws.take((size_t)(m > 0 ? m : 1) * 8);
@@ -481,7 +480,7 @@ size_t ixg_ws_bytes(int op, int64_t n, int64_t m) {
 }
 
 int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, int64_t* out, void* ws,
-                 size_t ws_bytes, void* stream) {
+                 size_t ws_bytes, ixg_status* st, void* stream) {
   if (n < 0 || (n > 0 && (!xs || !out))) return IXG_BADARG;
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, n, 0)) return IXG_BADARG;
   WS w(ws);
@@ -493,13 +492,11 @@ int ixg_scan_add(int dt, const void* xs, int64_t n, int64_t ne, int exclusive, i
   if (!exclusive && n > 0 && (dt == IXG_I32 || dt == IXG_I64) && aligned16(xs) && aligned32(out)) {
     if (dt == IXG_I32)
       return launch_segsum_b<int32_t, long long, SumOp>((const int32_t*)xs, n, nullptr, nullptr, 0, (long long*)out, c,
-                                                        ne,
-                                                 0, nullptr, nullptr, S(stream));
+                                                        ne, 0, nullptr, st, S(stream));
     return launch_segsum_b<long long, long long, SumOp>((const long long*)xs, n, nullptr, nullptr, 0, (long long*)out, c,
-                                                         ne,
-                                                 0, nullptr, nullptr, S(stream));
+                                                         ne, 0, nullptr, st, S(stream));
   }
-  const EpiScanOut epi{ne, exclusive, (long long*)out};
+  const EpiScanOut epi{ne, exclusive, (long long*)out, st};
   if (dt == IXG_I32) return launch_scan<SumOp>(n, SrcArrT<int32_t>{(const int32_t*)xs}, epi, c, S(stream));
   if (dt == IXG_U8) return launch_scan<SumOp>(n, SrcArrT<uint8_t>{(const uint8_t*)xs}, epi, c, S(stream));
   return launch_scan<SumOp>(n, SrcArrT<long long>{(const long long*)xs}, epi, c, S(stream));
@@ -533,7 +530,7 @@ int ixg_jagged_dest(const uint32_t* bits, int64_t n, const uint8_t* cs, const in
 }
 
 int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64_t n, int f0, int64_t v0,
-                    int64_t* out_v, uint8_t* out_f, void* ws, size_t ws_bytes, void* stream) {
+                    int64_t* out_v, uint8_t* out_f, void* ws, size_t ws_bytes, ixg_status* st, void* stream) {
   if (n < 0 || (n > 0 && (!flags || !xs || !out_v))) return IXG_BADARG;
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SEGSCAN, n, 0)) return IXG_BADARG;
   WS w(ws);
@@ -541,8 +538,17 @@ int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64
   (void)f0;
   (void)v0;
   if (f0 != 0 || v0 != 0) return IXG_BADARG;  // only the (false, 0) neutral of sgmSum is supported
-  return launch_scan<SegOp>(n, SrcSeg{dt_f, dt_x, flags, xs}, EpiSegOut{IXG_I64, out_v, out_f, nullptr}, c,
-                            S(stream));
+  const EpiSegOut epi{IXG_I64, out_v, out_f, st};
+  cudaStream_t s = S(stream);
+  auto run = [&](auto fl) -> int {
+    using EF = typename std::remove_const<typename std::remove_pointer<decltype(fl)>::type>::type;
+    if (dt_x == IXG_I32) return launch_scan<SegOp>(n, SrcSegT<EF, int32_t>{fl, (const int32_t*)xs}, epi, c, s);
+    if (dt_x == IXG_U8) return launch_scan<SegOp>(n, SrcSegT<EF, uint8_t>{fl, (const uint8_t*)xs}, epi, c, s);
+    return launch_scan<SegOp>(n, SrcSegT<EF, long long>{fl, (const long long*)xs}, epi, c, s);
+  };
+  if (dt_f == IXG_U8) return run((const uint8_t*)flags);
+  if (dt_f == IXG_I32) return run((const int32_t*)flags);
+  return run((const long long*)flags);
 }
 
 int ixg_scatter(int dt, void* out, int64_t ndst, const int64_t* is, int64_t nis, const void* vs, int64_t nvs,
@@ -579,18 +585,28 @@ int ixg_gather(int dt, const void* arr, int64_t len, const int64_t* idx, int64_t
 }
 
 int ixg_hist(int op, int64_t ne, int64_t dlen, const int64_t* is, int64_t nis, const int64_t* vs, int64_t nvs,
-             int64_t* out, void* stream) {
+             int64_t* out, void* ws, size_t ws_bytes, ixg_status* st, void* stream) {
   const long long m = nis < nvs ? nis : nvs;
   if (dlen < 0) dlen = 0;  // [ne] * negative == []
   if (op < 0 || op > 2 || m < 0 || (dlen > 0 && !out)) return IXG_BADARG;
+  const bool add = op == IXG_HIST_ADD;
+  if (add && dlen > 0 && (!ws || ws_bytes < ixg_ws_bytes(IXG_OP_HIST, 0, dlen))) return IXG_BADARG;
   cudaStream_t s = S(stream);
+  WS w(ws);
+  long long* hi = add ? (long long*)w.take((size_t)(dlen > 0 ? dlen : 1) * 8) : nullptr;
   int rc;
   if (dlen > 0 && (rc = launch_fill<long long>((long long*)out, dlen, nullptr, (long long)ne, s))) return rc;
+  if (add && dlen > 0 && (rc = launch_fill<long long>(hi, dlen, nullptr, ne < 0 ? -1LL : 0LL, s))) return rc;
   if (m == 0 || dlen == 0) return IXG_OK;
   k_hist<<<grid_for(m), kGThreads, 0, s>>>(op, dlen, (const long long*)is, (const long long*)vs, m,
-                                            (long long*)out);
+                                            (long long*)out, hi);
   LAUNCHED();
   CHECK_LAUNCH();
+  if (add) {
+    k_hist_check<<<grid_for(dlen), kGThreads, 0, s>>>((const long long*)out, hi, dlen, st);
+    LAUNCHED();
+    CHECK_LAUNCH();
+  }
   return IXG_OK;
 }
 

@@ -152,6 +152,36 @@ IXG_DEV void status_fail(ixg_status* st, int code, int stmt, long long elem, int
   atomicOr(&st->codes, 1u << code);
 }
 
+// ------------------------------------------------------ checked int64 arithmetic
+// The reference's ints are unbounded (oracle.py:214-240): each op returns the
+// wrapped result and whether the exact one left int64.
+IXG_DEV bool add_ovf(long long a, long long b, long long* r) {
+  const long long s = (long long)((unsigned long long)a + (unsigned long long)b);
+  *r = s;
+  return ((a ^ s) & (b ^ s)) < 0;
+}
+IXG_DEV bool sub_ovf(long long a, long long b, long long* r) {
+  const long long s = (long long)((unsigned long long)a - (unsigned long long)b);
+  *r = s;
+  return ((a ^ b) & (a ^ s)) < 0;
+}
+IXG_DEV bool mul_ovf(long long a, long long b, long long* r) {
+  const long long lo = (long long)((unsigned long long)a * (unsigned long long)b);
+  *r = lo;
+  return __mul64hi(a, b) != (lo >> 63);
+}
+// Did the sequential step prev + x = cur (all wrapped) overflow?  Exact for
+// a scan: at the first position whose true prefix leaves int64 every earlier
+// wrapped prefix equals the true one (modular arithmetic is exact until
+// then), so checking cur against cur - x at every position finds it.
+IXG_DEV bool step_ovf(long long cur, long long x) {
+  const long long prev = (long long)((unsigned long long)cur - (unsigned long long)x);
+  return ((prev ^ cur) & (x ^ cur)) < 0;
+}
+IXG_DEV void status_overflow(ixg_status* st, int stmt, long long elem) {
+  status_fail(st, IXG_OVERFLOW, stmt, elem, IXG_OVF_SITE);
+}
+
 // --------------------------------------------------------- vector helpers
 template <typename T>
 struct Vec;

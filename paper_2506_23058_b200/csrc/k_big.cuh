@@ -875,11 +875,22 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       }
       if ((int32_t)ov < 0 && st) atomicOr(&st->flags, IXG_F_NARROW);
     } else {
+      // 64-bit run from the first flag on: the exact check of each
+      // sequential step (the reference's ints are unbounded)
       long long r = init.v;
+      bool ov = false;
+      int jo = len;
       for (; j < len; ++j, fb >>= 1) {
-        r = ((fb & 1ull) ? 0LL : r) + (long long)zbuf[j];
+        const long long x = (long long)zbuf[j];
+        const long long rr = (fb & 1ull) ? 0LL : r;
+        r = (long long)((unsigned long long)rr + (unsigned long long)x);
+        if (!ov && ((rr ^ r) & (x ^ r)) < 0) {
+          ov = true;
+          jo = j;
+        }
         zbuf[j] = (Z)r;
       }
+      if (ov) status_overflow(st, 0, base + q0 + jo);
     }
     IXG_TR(9);
     bar_sync(3, kBT + 32);  // carry of the preceding tiles
@@ -888,7 +899,25 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
       const long long cv = s_carry.v;
       if (sizeof(Z) == 4 && st && (cv + lo < (long long)INT32_MIN || cv + hi > (long long)INT32_MAX))
         atomicOr(&st->flags, IXG_F_NARROW);
-      for (int q = 0; q < jm; ++q) zbuf[q] = (Z)((unsigned long long)zbuf[q] + (unsigned long long)cv);
+      if constexpr (sizeof(Z) == 8) {
+        // the values before the piece's first flag get the carry now: check
+        // each sequential step (x_j = local_j - local_{j-1}, all wrapped)
+        long long prevl = init.v;
+        for (int q = 0; q < jm; ++q) {
+          const long long loc = (long long)zbuf[q];
+          const long long x = (long long)((unsigned long long)loc - (unsigned long long)prevl);
+          const long long fin = (long long)((unsigned long long)loc + (unsigned long long)cv);
+          prevl = loc;
+          zbuf[q] = (Z)fin;
+          if (step_ovf(fin, x)) {
+            status_overflow(st, 0, base + q0 + q);
+            for (++q; q < jm; ++q) zbuf[q] = (Z)((unsigned long long)zbuf[q] + (unsigned long long)cv);
+            break;
+          }
+        }
+      } else {
+        for (int q = 0; q < jm; ++q) zbuf[q] = (Z)((unsigned long long)zbuf[q] + (unsigned long long)cv);
+      }
     }
     if (bulk) {
       fence_async_smem();
@@ -1038,6 +1067,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   bar_sync(2, kBT + 32);
   const typename M::T carry = s_carry;
   bool narrow = false;
+  long long ovf_at = LLONG_MAX;  // first element whose int64 sum overflowed (Z = int64)
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     T x[kSItems];
@@ -1053,8 +1083,12 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     Z z[kSItems];
 #pragma unroll
     for (int j = 0; j < kSItems; ++j) {
-      run = (((fl[c] >> j) & 1u) ? 0LL : run) + (long long)x[j];
+      const long long prev = ((fl[c] >> j) & 1u) ? 0LL : run;
+      run = (long long)((unsigned long long)prev + (unsigned long long)(long long)x[j]);
       if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
+      // exact: the sequential step prev + x in the reference's unbounded ints
+      if (sizeof(Z) == 8 && (((prev ^ run) & ((long long)x[j] ^ run)) < 0) && g + j < n && ovf_at == LLONG_MAX)
+        ovf_at = g + j;
       z[j] = (Z)run;
     }
     if (g + kSItems <= n) {
@@ -1080,6 +1114,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     }
   }
   if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+  if (sizeof(Z) == 8 && ovf_at != LLONG_MAX) status_overflow(st, 0, ovf_at);
 }
 
 // ---------------------------------------------------------------------------

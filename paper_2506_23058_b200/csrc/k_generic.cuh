@@ -6,6 +6,7 @@
 #pragma once
 #include <type_traits>
 
+#include "k_stream.cuh"
 #include "lookback.cuh"
 
 namespace ixg {
@@ -14,118 +15,235 @@ constexpr int kGThreads = 256;
 constexpr int kGItems = 16;
 constexpr int kGTile = kGThreads * kGItems;
 
-// ---------------------------------------------------------------- sources
+// ---------------------------------------------------------------- loads
+// 16 consecutive elements of E[] from i0 as int64: 256-bit (u8: 128-bit)
+// vector loads when the 16 are in range and the address is aligned, else
+// bounded scalar loads (out-of-range elements read as 0)
 template <typename E>
-IXG_DEV long long load_as_i64(const void* p, long long i) {
-  return (long long)reinterpret_cast<const E*>(p)[i];
-}
-IXG_DEV long long load_dt(int dt, const void* p, long long i) {
-  switch (dt) {
-    case IXG_I32: return load_as_i64<int32_t>(p, i);
-    case IXG_U8: return load_as_i64<uint8_t>(p, i);
-    default: return load_as_i64<int64_t>(p, i);
-  }
-}
-IXG_DEV void store_dt(int dt, void* p, long long i, long long v) {
-  if (dt == IXG_I32) reinterpret_cast<int32_t*>(p)[i] = (int32_t)v;
-  else if (dt == IXG_U8) reinterpret_cast<uint8_t*>(p)[i] = (uint8_t)v;
-  else reinterpret_cast<int64_t*>(p)[i] = v;
-}
-
-struct SrcArr {  // scan (+) over an integer array (any element width)
-  int dt;
-  const void* xs;
-  IXG_DEV SumOp::T operator()(long long i) const { return SumOp::T{load_dt(dt, xs, i)}; }
-};
-template <typename E>
-struct SrcArrT {  // scan (+) over E[], 16 elements per thread through 256-bit loads
-  const E* xs;
-  IXG_DEV SumOp::T operator()(long long i) const { return SumOp::T{(long long)xs[i]}; }
-  IXG_DEV void load16(long long i0, long long n, SumOp::T (&v)[kGItems]) const {
-    if (sizeof(E) >= 2 && i0 + kGItems <= n && (((uintptr_t)(xs + i0)) & 31) == 0) {
-      constexpr int PER = 32 / (int)sizeof(E);
+IXG_DEV void load16_i64(const E* __restrict__ xs, long long i0, long long n, long long (&v)[kGItems]) {
+  const E* p = xs + i0;
+  if (i0 + kGItems <= n) {
+    if constexpr (sizeof(E) == 1) {
+      if ((((uintptr_t)p) & 15) == 0) {
+        const int4 r = ld_stream_v4(p);
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&r);
 #pragma unroll
-      for (int k = 0; k < kGItems / PER; ++k) {
-        uint32_t r[8];
-        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                       "=r"(r[7])
-                     : "l"(xs + i0 + k * PER));
-        const E* e = reinterpret_cast<const E*>(r);
-#pragma unroll
-        for (int q = 0; q < PER; ++q) v[k * PER + q] = SumOp::T{(long long)e[q]};
+        for (int q = 0; q < kGItems; ++q) v[q] = (long long)b[q];
+        return;
       }
     } else {
+      if ((((uintptr_t)p) & 31) == 0) {
+        constexpr int PER = 32 / (int)sizeof(E);
 #pragma unroll
-      for (int j = 0; j < kGItems; ++j) v[j] = SumOp::T{(i0 + j < n) ? (long long)xs[i0 + j] : 0};
+        for (int k = 0; k < kGItems / PER; ++k) {
+          uint32_t r[8];
+          ld256(p + k * PER, r);
+          const E* e = reinterpret_cast<const E*>(r);
+#pragma unroll
+          for (int q = 0; q < PER; ++q) v[k * PER + q] = (long long)e[q];
+        }
+        return;
+      }
     }
   }
+#pragma unroll
+  for (int q = 0; q < kGItems; ++q) v[q] = (i0 + q < n) ? (long long)p[q] : 0LL;
+}
+
+// 16 consecutive int64 (or int32) outputs from i0: four (two) 256-bit
+// stores when all 16 are in range and 32-byte aligned
+IXG_DEV void store16_i64(long long* __restrict__ out, long long i0, long long n, const long long (&o)[kGItems]) {
+  long long* p = out + i0;
+  if (i0 + kGItems <= n && (((uintptr_t)p) & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < kGItems / 4; ++k) {
+      uint32_t r[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        r[2 * q] = (uint32_t)(unsigned long long)o[4 * k + q];
+        r[2 * q + 1] = (uint32_t)((unsigned long long)o[4 * k + q] >> 32);
+      }
+      st256(p + 4 * k, r);
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kGItems; ++q)
+    if (i0 + q < n) p[q] = o[q];
+}
+IXG_DEV void store16_i32(int32_t* __restrict__ out, long long i0, long long n, const long long (&o)[kGItems]) {
+  int32_t* p = out + i0;
+  if (i0 + kGItems <= n && (((uintptr_t)p) & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < kGItems / 8; ++k) {
+      uint32_t r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r[q] = (uint32_t)o[8 * k + q];
+      st256(p + 8 * k, r);
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kGItems; ++q)
+    if (i0 + q < n) p[q] = (int32_t)o[q];
+}
+
+// ---------------------------------------------------------------- sources
+// A source gives thread t its 16 consecutive scan elements (load16); every
+// source is typed at compile time (no per-element width switch) and loads
+// with 256-bit vectors.
+template <typename E>
+struct SrcArrT {  // scan (+) over E[]
+  const E* xs;
+  IXG_DEV void load16(long long i0, long long n, SumOp::T (&v)[kGItems]) const {
+    long long x[kGItems];
+    load16_i64<E>(xs, i0, n, x);
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) v[q] = SumOp::T{x[q]};
+  }
 };
-struct SrcPred {  // map (\x -> if p x then 1 else 0) xs, fused into the scan
-  int dt;
-  const void* xs;
+template <typename E>
+struct SrcPredT {  // map (\x -> if p x then 1 else 0) xs, fused into the scan
+  const E* xs;
   const uint8_t* cs;  // filter_by: the bool array instead of p
   ixg_pred p;
-  IXG_DEV SumOp::T operator()(long long i) const {
-    if (cs) return SumOp::T{cs[i] != 0};
-    return SumOp::T{pred_eval(p, load_dt(dt, xs, i)) ? 1 : 0};
+  IXG_DEV void load16(long long i0, long long n, SumOp::T (&v)[kGItems]) const {
+    uint32_t m;
+    if (cs) {
+      long long c[kGItems];
+      load16_i64<uint8_t>(cs, i0, n, c);
+      m = 0;
+#pragma unroll
+      for (int q = 0; q < kGItems; ++q) m |= (uint32_t)(c[q] != 0) << q;
+    } else {
+      using TE = typename std::conditional<sizeof(E) == 4, int32_t, long long>::type;
+      long long x[kGItems];
+      load16_i64<E>(xs, i0, n, x);
+      TE xe[kGItems];
+#pragma unroll
+      for (int q = 0; q < kGItems; ++q) xe[q] = (TE)x[q];
+      m = Selector<TE>(p).mask(xe);
+    }
+    m &= valid_mask(i0, n);
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) v[q] = SumOp::T{(long long)((m >> q) & 1u)};
   }
 };
-struct SrcClass3 {  // partition3: (flags1, flags2)
-  int dt;
-  const void* xs;
+template <typename E>
+struct SrcClass3T {  // partition3: (flags1, flags2)
+  const E* xs;
   ixg_pred p, q;
-  IXG_DEV Sum2Op::T operator()(long long i) const {
-    const long long x = load_dt(dt, xs, i);
-    const bool c1 = pred_eval(p, x);
-    const bool c2 = !c1 && pred_eval(q, x);
-    return Sum2Op::T{c1 ? 1 : 0, c2 ? 1 : 0};
+  IXG_DEV void load16(long long i0, long long n, Sum2Op::T (&v)[kGItems]) const {
+    using TE = typename std::conditional<sizeof(E) == 4, int32_t, long long>::type;
+    long long x[kGItems];
+    load16_i64<E>(xs, i0, n, x);
+    TE xe[kGItems];
+#pragma unroll
+    for (int k = 0; k < kGItems; ++k) xe[k] = (TE)x[k];
+    const uint32_t vm = valid_mask(i0, n);
+    const uint32_t m1 = Selector<TE>(p).mask(xe) & vm;
+    const uint32_t m2 = Selector<TE>(q).mask(xe) & ~m1 & vm;
+#pragma unroll
+    for (int k = 0; k < kGItems; ++k) v[k] = Sum2Op::T{(long long)((m1 >> k) & 1u), (long long)((m2 >> k) & 1u)};
   }
 };
-struct SrcSeg {  // (flags, xs) of the segmented scan
-  int dt_f, dt_x;
-  const void* flags;
-  const void* xs;
-  IXG_DEV SegOp::T operator()(long long i) const {
-    return SegOp::T{load_dt(dt_x, xs, i), load_dt(dt_f, flags, i) != 0};
+template <typename EF, typename EX>
+struct SrcSegT {  // (flags, xs) of the segmented scan
+  const EF* flags;
+  const EX* xs;
+  IXG_DEV void load16(long long i0, long long n, SegOp::T (&v)[kGItems]) const {
+    long long f[kGItems], x[kGItems];
+    load16_i64<EF>(flags, i0, n, f);
+    load16_i64<EX>(xs, i0, n, x);
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) v[q] = SegOp::T{x[q], f[q] != 0};
   }
 };
 
 // ---------------------------------------------------------------- epilogues
+// An epilogue receives a thread's 16 inclusive prefixes at once (int64
+// outputs leave as 256-bit stores).  The elements themselves are recovered
+// from consecutive prefixes (xstep: wrapped differences, exact in modular
+// arithmetic; SegOp's flags come as a bit mask), which keeps one array of
+// 16 values live instead of two.
+IXG_DEV SumOp::T xstep(const SumOp::T& prev, const SumOp::T& cur, uint32_t) {
+  return SumOp::T{(long long)((unsigned long long)cur.v - (unsigned long long)prev.v)};
+}
+IXG_DEV Sum2Op::T xstep(const Sum2Op::T& prev, const Sum2Op::T& cur, uint32_t) {
+  return Sum2Op::T{cur.a - prev.a, cur.b - prev.b};
+}
+IXG_DEV SegOp::T xstep(const SegOp::T& prev, const SegOp::T& cur, uint32_t f) {
+  return SegOp::T{f ? cur.v : (long long)((unsigned long long)cur.v - (unsigned long long)prev.v), (int)f};
+}
+template <class T>
+struct Run16 {  // incl[q] and the element x(q) = xstep(incl[q-1], incl[q])
+  const T (&incl)[kGItems];
+  const T& prev0;
+  uint32_t fm;
+  IXG_DEV T x(int q) const { return xstep(q ? incl[q - 1] : prev0, incl[q], (fm >> q) & 1u); }
+};
+
 struct EpiScanOut {  // out[i] = ne + inclusive (or exclusive) sum
   long long ne;
   int exclusive;
   long long* out;
-  IXG_DEV void operator()(long long i, SumOp::T incl, SumOp::T x) const {
-    out[i] = ne + (exclusive ? incl.v - x.v : incl.v);
+  ixg_status* st;  // nullable: IXG_OVERFLOW at the first sum leaving int64
+  IXG_DEV void operator()(long long i0, long long n, const Run16<SumOp::T>& r) const {
+    long long o[kGItems];
+    long long ovf = -1;
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) {
+      const long long x = r.x(q).v;
+      const long long cur = (long long)((unsigned long long)ne + (unsigned long long)r.incl[q].v);
+      if (ovf < 0 && i0 + q < n && step_ovf(cur, x)) ovf = i0 + q;  // the reference's left fold, exactly
+      o[q] = exclusive ? (long long)((unsigned long long)cur - (unsigned long long)x) : cur;
+    }
+    if (ovf >= 0) status_overflow(st, 0, ovf);
+    store16_i64(out, i0, n, o);
   }
 };
 struct EpiFilterInds {  // filter.ixl:10-12: inds[i] = if c then offs[i]-1 else -1; count = offs[n-1]
-  long long n;
   long long* inds;
   long long* d_count;
-  IXG_DEV void operator()(long long i, SumOp::T incl, SumOp::T x) const {
-    inds[i] = x.v ? incl.v - 1 : -1;
-    if (i == n - 1) *d_count = incl.v;
+  IXG_DEV void operator()(long long i0, long long n, const Run16<SumOp::T>& r) const {
+    long long o[kGItems];
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) o[q] = r.x(q).v ? r.incl[q].v - 1 : -1;
+    store16_i64(inds, i0, n, o);
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q)  // static indices: incl stays in registers
+      if (i0 + q == n - 1) *d_count = r.incl[q].v;
   }
 };
 struct EpiPart2Inds {  // partition2.ixl:11-16 with num_true from the count pass
   const long long* d_nt;
   long long* inds;
-  IXG_DEV void operator()(long long i, SumOp::T incl, SumOp::T x) const {
-    const long long t = incl.v;             // indicesT[i]
-    const long long f = (i + 1 - t) + *d_nt;  // indicesF[i] = tmp[i] + num_true
-    inds[i] = x.v ? t - 1 : f - 1;
+  IXG_DEV void operator()(long long i0, long long n, const Run16<SumOp::T>& r) const {
+    const long long nt = *d_nt;
+    long long o[kGItems];
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) {
+      const long long t = r.incl[q].v;               // indicesT[i]
+      const long long f = (i0 + q + 1 - t) + nt;     // indicesF[i] = tmp[i] + num_true
+      o[q] = r.x(q).v ? t - 1 : f - 1;
+    }
+    store16_i64(inds, i0, n, o);
   }
 };
 struct EpiPart3Inds {  // partition3.ixl:14-24 with (m1, m2) from the count pass
   const long long* d_m;
   long long* inds;
-  IXG_DEV void operator()(long long i, Sum2Op::T incl, Sum2Op::T x) const {
+  IXG_DEV void operator()(long long i0, long long n, const Run16<Sum2Op::T>& r) const {
     const long long m1 = d_m[0], m2 = d_m[1];
-    const long long inds1 = incl.a - 1, inds2 = m1 + incl.b - 1;
-    const long long inds3 = m1 + m2 + i - (incl.a + incl.b);
-    inds[i] = x.a ? inds1 : (x.b ? inds2 : inds3);
+    long long o[kGItems];
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) {
+      const Sum2Op::T x = r.x(q);
+      const long long inds1 = r.incl[q].a - 1, inds2 = m1 + r.incl[q].b - 1;
+      const long long inds3 = m1 + m2 + (i0 + q) - (r.incl[q].a + r.incl[q].b);
+      o[q] = x.a ? inds1 : (x.b ? inds2 : inds3);
+    }
+    store16_i64(inds, i0, n, o);
   }
 };
 struct EpiSegOut {  // sgmSum value (and flag) components
@@ -133,14 +251,30 @@ struct EpiSegOut {  // sgmSum value (and flag) components
   void* out_v;
   uint8_t* out_f;
   ixg_status* st;
-  IXG_DEV void operator()(long long i, SegOp::T incl, SegOp::T) const {
-    if (dt_out == IXG_I32) {
-      if (incl.v != (long long)(int)incl.v && st) atomicOr(&st->flags, IXG_F_NARROW);
-      reinterpret_cast<int32_t*>(out_v)[i] = (int32_t)incl.v;
-    } else {
-      reinterpret_cast<int64_t*>(out_v)[i] = incl.v;
+  IXG_DEV void operator()(long long i0, long long n, const Run16<SegOp::T>& r) const {
+    long long o[kGItems];
+    long long ovf = -1;
+    bool narrow = false;
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) {
+      const SegOp::T x = r.x(q);
+      o[q] = r.incl[q].v;
+      // within a segment: the step prev + x of the reference's left fold
+      if (ovf < 0 && i0 + q < n && !x.f && step_ovf(o[q], x.v)) ovf = i0 + q;
+      narrow |= i0 + q < n && o[q] != (long long)(int)o[q];
     }
-    if (out_f) out_f[i] = (uint8_t)incl.f;
+    if (ovf >= 0) status_overflow(st, 0, ovf);
+    if (dt_out == IXG_I32) {
+      if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+      store16_i32(reinterpret_cast<int32_t*>(out_v), i0, n, o);
+    } else {
+      store16_i64(reinterpret_cast<long long*>(out_v), i0, n, o);
+    }
+    if (out_f) {
+#pragma unroll
+      for (int q = 0; q < kGItems; ++q)
+        if (i0 + q < n) out_f[i0 + q] = (uint8_t)r.incl[q].f;
+    }
   }
 };
 struct EpiSegStarts {  // mkSgmDescr / mkFlags: ind[i] = if shape[i] <= 0 then -1 else scn[i]
@@ -150,70 +284,100 @@ struct EpiSegStarts {  // mkSgmDescr / mkFlags: ind[i] = if shape[i] <= 0 then -
   uint32_t* bits;        // nullable: set bit scn[i] (flag array as a bitmap)
   long long nbits;
   long long* d_total;    // nullable: scn[m-1] + shape[m-1]
-  IXG_DEV void operator()(long long i, SumOp::T incl, SumOp::T x) const {
-    const long long s = x.v, start = incl.v - s;
-    if (ind) ind[i] = s <= 0 ? -1 : start;
-    if (bits && s > 0 && start >= 0 && start < nbits) atomicOr(&bits[start >> 5], 1u << (start & 31));
-    if (d_total && i == m - 1) *d_total = incl.v;
+  IXG_DEV void operator()(long long i0, long long n, const Run16<SumOp::T>& r) const {
+    long long o[kGItems];
+#pragma unroll
+    for (int q = 0; q < kGItems; ++q) {
+      const long long s = r.x(q).v, start = r.incl[q].v - s;
+      o[q] = s <= 0 ? -1 : start;
+      if (bits && i0 + q < n && s > 0 && start >= 0 && start < nbits)
+        atomicOr(&bits[start >> 5], 1u << (start & 31));
+    }
+    if (ind) store16_i64(ind, i0, n, o);
+    if (d_total) {
+#pragma unroll
+      for (int q = 0; q < kGItems; ++q)
+        if (i0 + q == m - 1) *d_total = r.incl[q].v;
+    }
   }
 };
 
-// Single-pass blocked scan with a source functor and an epilogue functor.
-// tile = blockIdx.x (see lookback.cuh / k_stream.cuh for the protocol); a
-// source may provide load16() with 256-bit loads of its 16 elements.
-template <class Src, class T>
-IXG_DEV auto src_load16(const Src& src, long long i0, long long n, T (&v)[kGItems], int)
-    -> decltype(src.load16(i0, n, v), void()) {
-  src.load16(i0, n, v);
+template <class T>
+IXG_DEV uint32_t flag_mask(const T (&)[kGItems]) {
+  return 0u;
 }
-template <class Src, class T>
-IXG_DEV void src_load16(const Src& src, long long i0, long long n, T (&v)[kGItems], long) {
+IXG_DEV uint32_t flag_mask(const SegOp::T (&v)[kGItems]) {
+  uint32_t m = 0;
 #pragma unroll
-  for (int j = 0; j < kGItems; ++j) v[j] = (i0 + j < n) ? src(i0 + j) : T{};
+  for (int q = 0; q < kGItems; ++q) m |= (uint32_t)(v[q].f != 0) << q;
+  return m;
 }
 
+// Single-pass blocked scan: 16 consecutive elements per thread (vector
+// loads), tiles of 4096 with decoupled look-back (lookback.cuh).  Tiles are
+// numbered in the order CTAs START (an atomicAdd ticket on the channel
+// header), so a tile only ever waits on tiles whose CTAs are already
+// resident -- forward progress without relying on in-order block dispatch;
+// the last CTA to retire resets the ticket for the next launch.  `d_n`
+// (nullable): the element count known only on the device (a count pass
+// before it) -- the grid covers the capacity, surplus tiles retire at once.
 template <class M, class Src, class Epi>
-__global__ void __launch_bounds__(kGThreads) k_scan(long long n, Src src, Epi epi, LBChan ch, uint32_t nonce) {
+__global__ void __launch_bounds__(kGThreads, 3) k_scan(long long n, const long long* __restrict__ d_n, Src src, Epi epi,
+                                                    LBChan ch, uint32_t nonce) {
   using T = typename M::T;
   __shared__ T s_w[kGThreads / 32];
   __shared__ T s_carry;
-  const long long tile = blockIdx.x;
-  const long long i0 = tile * kGTile + (long long)threadIdx.x * kGItems;
-  T v[kGItems];
-  src_load16(src, i0, n, v, 0);
-  T a = M::identity();
-#pragma unroll
-  for (int j = 0; j < kGItems; ++j) {
-    if (i0 + j >= n) v[j] = M::identity();
-    a = M::op(a, v[j]);
-  }
-  T inc = warp_inclusive<M>(a);
-  T lex = M::shfl_up(inc, 1);
-  if (lane_id() == 0) lex = M::identity();
-  if (lane_id() == 31) s_w[warp_id()] = inc;
+  __shared__ long long s_tile;
+  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ch.hdr->ticket, 1u);
+  if (d_n) n = *d_n;
   __syncthreads();
-  T wpre = M::identity(), tagg = M::identity();
+  const long long tile = s_tile;
+  if (tile * kGTile < n) {
+    const long long i0 = tile * kGTile + (long long)threadIdx.x * kGItems;
+    T v[kGItems];
+    src.load16(i0, n, v);
+    T a = M::identity();
 #pragma unroll
-  for (int w = 0; w < kGThreads / 32; ++w) {
-    if (w < warp_id()) wpre = M::op(wpre, s_w[w]);
-    tagg = M::op(tagg, s_w[w]);
-  }
-  if (threadIdx.x == 0) lb_publish<M>(ch, nonce, tile, tagg, tile == 0);
-  if (warp_id() == 0) {
-    T c = M::identity();
-    if (tile > 0) c = lb_lookback<M>(ch, nonce, tile);
-    if (lane_id() == 0) {
-      s_carry = c;
-      if (tile > 0) lb_publish<M>(ch, nonce, tile, M::op(c, tagg), true);
+    for (int j = 0; j < kGItems; ++j) {
+      if (i0 + j >= n) v[j] = M::identity();
+      a = M::op(a, v[j]);
     }
-  }
-  __syncthreads();
-  T run = M::op(M::op(s_carry, wpre), lex);
+    T inc = warp_inclusive<M>(a);
+    T lex = M::shfl_up(inc, 1);
+    if (lane_id() == 0) lex = M::identity();
+    if (lane_id() == 31) s_w[warp_id()] = inc;
+    __syncthreads();
+    T wpre = M::identity(), tagg = M::identity();
 #pragma unroll
-  for (int j = 0; j < kGItems; ++j) {
-    if (i0 + j < n) {
+    for (int w = 0; w < kGThreads / 32; ++w) {
+      if (w < warp_id()) wpre = M::op(wpre, s_w[w]);
+      tagg = M::op(tagg, s_w[w]);
+    }
+    if (threadIdx.x == 0) lb_publish<M>(ch, nonce, tile, tagg, tile == 0);
+    if (warp_id() == 0) {
+      T c = M::identity();
+      if (tile > 0) c = lb_lookback<M>(ch, nonce, tile);
+      if (lane_id() == 0) {
+        s_carry = c;
+        if (tile > 0) lb_publish<M>(ch, nonce, tile, M::op(c, tagg), true);
+      }
+    }
+    __syncthreads();
+    const T prev0 = M::op(M::op(s_carry, wpre), lex);
+    const uint32_t fm = flag_mask(v);
+    T run = prev0;
+#pragma unroll
+    for (int j = 0; j < kGItems; ++j) {  // v becomes the inclusive prefixes in place
       run = M::op(run, v[j]);
-      epi(i0 + j, run, v[j]);
+      v[j] = run;
+    }
+    epi(i0, n, Run16<T>{v, prev0, fm});
+  }
+  if (threadIdx.x == 0) {  // retire: the last CTA out resets the ticket
+    __threadfence();
+    if (atomicAdd(&ch.hdr->done, 1u) == gridDim.x - 1) {
+      atomicExch(&ch.hdr->ticket, 0u);
+      atomicExch(&ch.hdr->done, 0u);
     }
   }
 }
@@ -328,7 +492,12 @@ __global__ void __launch_bounds__(kGThreads) k_csr_gather(const E* __restrict__ 
         o[e] = E(0);
         continue;
       }
-      const long long prod = (long long)v[e] * (long long)__ldg(&x[c[e]]);
+      long long prod;
+      if constexpr (sizeof(E) == 8) {  // int64 x int64: checked (int32 x int32 always fits)
+        if (mul_ovf((long long)v[e], (long long)__ldg(&x[c[e]]), &prod)) status_overflow(st, 0, k * V + e);
+      } else {
+        prod = (long long)v[e] * (long long)__ldg(&x[c[e]]);
+      }
       if (sizeof(E) == 4 && prod != (long long)(int)prod) narrow = true;
       o[e] = (E)prod;
     }
@@ -342,7 +511,12 @@ __global__ void __launch_bounds__(kGThreads) k_csr_gather(const E* __restrict__ 
         out[i] = E(0);
         continue;
       }
-      const long long prod = (long long)values[i] * (long long)x[c];
+      long long prod;
+      if constexpr (sizeof(E) == 8) {
+        if (mul_ovf((long long)values[i], (long long)x[c], &prod)) status_overflow(st, 0, i);
+      } else {
+        prod = (long long)values[i] * (long long)x[c];
+      }
       if (sizeof(E) == 4 && prod != (long long)(int)prod) narrow = true;
       out[i] = (E)prod;
     }
@@ -425,9 +599,14 @@ __global__ void __launch_bounds__(kGThreads) k_jagged_dest(const uint32_t* __res
 }
 
 // ---------------------------------------------------------------- hist
+// (+): every bin is a 128-bit integer (hi:lo) -- lo = out[d], updated with
+// one 64-bit atomicAdd whose returned old value gives the carry; the high
+// word (hi[d], in the workspace) moves only when the carry and the sign
+// extension of v do not cancel.  The bin's exact sum fits int64 iff hi is
+// the sign extension of lo (k_hist_check).
 __global__ void __launch_bounds__(kGThreads) k_hist(int op, long long dlen, const long long* __restrict__ is,
                                                      const long long* __restrict__ vs, long long m,
-                                                     long long* __restrict__ out) {
+                                                     long long* __restrict__ out, long long* __restrict__ hi) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
     const long long d = is[i];
@@ -435,8 +614,20 @@ __global__ void __launch_bounds__(kGThreads) k_hist(int op, long long dlen, cons
     const long long v = vs[i];
     if (op == IXG_HIST_MIN) atomicMin(&out[d], v);
     else if (op == IXG_HIST_MAX) atomicMax(&out[d], v);
-    else atomicAdd(reinterpret_cast<unsigned long long*>(&out[d]), (unsigned long long)v);
+    else {
+      const unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long*>(&out[d]), (unsigned long long)v);
+      const long long c = (v < 0 ? -1LL : 0LL) + ((old + (unsigned long long)v < old) ? 1LL : 0LL);
+      if (c) atomicAdd(reinterpret_cast<unsigned long long*>(&hi[d]), (unsigned long long)c);
+    }
   }
+}
+
+__global__ void __launch_bounds__(kGThreads) k_hist_check(const long long* __restrict__ out,
+                                                           const long long* __restrict__ hi, long long dlen,
+                                                           ixg_status* st) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x; d < dlen; d += stride)
+    if (hi[d] != (out[d] >> 63)) status_overflow(st, 0, d);
 }
 
 // ---------------------------------------------------------------- fill / iota

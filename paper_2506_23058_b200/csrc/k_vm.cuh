@@ -46,9 +46,22 @@ __global__ void __launch_bounds__(256) k_map_vm(const __grid_constant__ VmProgra
       switch (I.op) {
         case IXG_VM_IN: r[I.dst] = vm_load(P.in[I.a], i); break;
         case IXG_VM_CONST: r[I.dst] = I.imm; break;
-        case IXG_VM_ADD: r[I.dst] = r[I.a] + r[I.b]; break;
-        case IXG_VM_SUB: r[I.dst] = r[I.a] - r[I.b]; break;
-        case IXG_VM_MUL: r[I.dst] = r[I.a] * r[I.b]; break;
+        case IXG_VM_ADD:
+        case IXG_VM_SUB:
+        case IXG_VM_MUL: {  // int64, checked: the reference's ints are unbounded (oracle.py:214-240)
+          long long v;
+          const bool o = I.op == IXG_VM_ADD ? add_ovf(r[I.a], r[I.b], &v)
+                         : I.op == IXG_VM_SUB ? sub_ovf(r[I.a], r[I.b], &v)
+                                              : mul_ovf(r[I.a], r[I.b], &v);
+          if (o) {
+            status_overflow(st, stmt, i);
+            failed = true;
+            pc = P.ninsn;
+            break;
+          }
+          r[I.dst] = v;
+          break;
+        }
         case IXG_VM_EQ: r[I.dst] = r[I.a] == r[I.b]; break;
         case IXG_VM_NE: r[I.dst] = r[I.a] != r[I.b]; break;
         case IXG_VM_LT: r[I.dst] = r[I.a] < r[I.b]; break;

@@ -61,3 +61,15 @@ else:
 class NarrowingOverflow(OracleError):
     """A result did not fit the i32 storage the caller asked for (the
     reference's ints are unbounded; raise rather than return a wrapped value)."""
+
+
+class IntegerOverflow(OracleError):
+    """An integer value left int64.  The reference's ints are unbounded
+    (oracle.py:214-240: a scan of [2^62, 2^62, 2^62] returns 3 * 2^62); the
+    device computes in int64 and checks every result exactly, so instead of
+    returning a wrapped value the executor raises this at the first element
+    (in the reference's order) whose value does not fit."""
+
+    def __init__(self, what: str = "", elem=None):
+        super().__init__(f"integer overflow: a value left int64{': ' + what if what else ''}")
+        self.elem = elem

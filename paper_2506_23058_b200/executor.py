@@ -29,6 +29,7 @@ import os
 from dataclasses import dataclass
 from typing import Optional
 
+import numpy as np
 import torch
 
 from . import _lib as L
@@ -106,14 +107,25 @@ def jit_map(lam, arrs, env, bits, n, st, device=None):
 
 
 # ----------------------------------------------------------------- marshal
+def _h2d(arr: np.ndarray, dev) -> torch.Tensor:
+    """host array -> device tensor (one copy; the numpy buffer is the source)."""
+    return torch.from_numpy(arr).to(dev)
+
+
 def _dev_i64(a, dev) -> torch.Tensor:
+    """A language [n]i64 argument as a device int64 tensor.  Python lists go
+    through one C-level pass (np.fromiter) and one host->device copy."""
     if isinstance(a, torch.Tensor):
         return a.to(device=dev, dtype=torch.int64).contiguous()
+    if isinstance(a, np.ndarray):
+        return _h2d(np.ascontiguousarray(a, dtype=np.int64), dev)
     try:
-        return torch.tensor(list(a), dtype=torch.int64, device=dev) if len(a) else torch.empty(0, dtype=torch.int64,
-                                                                                               device=dev)
-    except (OverflowError, RuntimeError) as e:
-        raise errors.OracleError(f"value outside the int64 range the GPU path supports: {e}") from None
+        arr = np.fromiter(a, dtype=np.int64, count=len(a))
+    except OverflowError:
+        raise errors.IntegerOverflow("an argument value does not fit int64") from None
+    except (TypeError, ValueError) as e:
+        raise errors.OracleError(f"not an integer array: {e}") from None
+    return _h2d(arr, dev)
 
 
 def _dev_u8(a, dev) -> torch.Tensor:
@@ -121,13 +133,17 @@ def _dev_u8(a, dev) -> torch.Tensor:
         if a.dtype == torch.bool and a.device == dev and a.is_contiguous():
             return a.view(torch.uint8)
         return (a != 0).to(device=dev, dtype=torch.uint8).contiguous()
-    return torch.tensor([1 if bool(x) else 0 for x in a], dtype=torch.uint8, device=dev)
+    if isinstance(a, np.ndarray):
+        return _h2d(np.ascontiguousarray(a != 0, dtype=np.uint8), dev)
+    return _h2d(np.fromiter((1 if x else 0 for x in a), dtype=np.uint8, count=len(a)), dev)
 
 
 def _dev_f64(a, dev) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=dev, dtype=torch.float64).contiguous()
-    return torch.tensor([float(x) for x in a], dtype=torch.float64, device=dev)
+    if isinstance(a, np.ndarray):
+        return _h2d(np.ascontiguousarray(a, dtype=np.float64), dev)
+    return _h2d(np.fromiter(a, dtype=np.float64, count=len(a)), dev)
 
 
 def _pred(p) -> Pred:
@@ -206,6 +222,8 @@ class Interp:
             if s.narrow:
                 raise errors.NarrowingOverflow("a result does not fit its 32-bit storage")
             return
+        if s.site == L.OVF_SITE and s.codes & (1 << L.OVERFLOW):
+            raise errors.IntegerOverflow(fdef.name, s.elem)
         sites = ir.sites(fdef)
         idx = s.site if site_map is None else site_map(s.site)
         owner, ordinal = (fdef, idx) if not isinstance(idx, tuple) else idx
@@ -316,9 +334,7 @@ class Interp:
         if isinstance(v, torch.Tensor):
             if self.as_tensors:
                 return v
-            if v.dtype == torch.bool:
-                return [bool(x) for x in v.cpu().tolist()]
-            return v.cpu().tolist()
+            return v.cpu().numpy().tolist()  # bool arrays come back as bools
         return v
 
     def _bits(self, fs, node) -> int:
@@ -454,12 +470,17 @@ class Interp:
             arrs = [ev(a) for a in e.args[1 + kk:]]
             ints = not any(a.is_floating_point() for a in arrs) and not any(isinstance(v, float) for v in nes)
             if kk == 1 and _is_add(op) and ints:
-                return ops.scan_add(arrs[0], int(nes[0]))
+                st = ops.Status(self.dev)
+                out = ops.scan_add(arrs[0], _int64(nes[0]), status=st)
+                self._raise_site(st, [])
+                return out
             if kk == 2 and ints and _is_segsum(op) and not nes[0] and nes[1] == 0:
                 n = arrs[0].numel()
                 if arrs[1].numel() < n:
                     raise errors.OracleError("scan: value array shorter than flags")
-                v, fl = ops.segscan_add(_u8(arrs[0]), arrs[1][:n], want_flags=True)
+                st = ops.Status(self.dev)
+                v, fl = ops.segscan_add(_u8(arrs[0]), arrs[1][:n], want_flags=True, status=st)
+                self._raise_site(st, [])
                 return (_as_bool(fl), v)
             return self._scan_generic(e, op, nes, arrs, env, fs)
         if name == "scatter":
@@ -483,7 +504,10 @@ class Interp:
                     vs.is_floating_point() or isinstance(ne, float)):
                 code = {"add": L.HIST_ADD, "min": L.HIST_MIN, "max": L.HIST_MAX}.get(jit_fold.classify_hist(op))
             if code is not None:
-                return ops.hist(code, int(ne), int(dlen), is_, vs.to(torch.int64))
+                st = ops.Status(self.dev)
+                out = ops.hist(code, _int64(ne), int(dlen), is_, vs.to(torch.int64), status=st)
+                self._raise_site(st, [])
+                return out
             if ir.kind(op) != "Lambda":
                 raise NotImplementedError(f"hist operator {op}")
             st = ops.Status(self.dev)
@@ -547,6 +571,8 @@ class Interp:
         if not s.ok:
             if s.site == jit.BUDGET_SITE:
                 raise errors.StepBudgetExceeded(f"loop ran past the step budget ({self.budget})")
+            if s.site == L.OVF_SITE:
+                raise errors.IntegerOverflow("", s.elem)
             node = sites[s.site]
             raise errors.OutOfBounds(ir.expr_str(node), node.pos)
 
@@ -600,14 +626,16 @@ class Interp:
             t = t[:n]
         if self.as_tensors:
             return t
-        return t.cpu().tolist()
+        return t.cpu().numpy().tolist()
 
     # -- pipelines ----------------------------------------------------------
     def _p_sum(self, f, a):
         xs = _dev_i64(a[0], self.dev)
         if xs.numel() == 0:
             return 0
-        s = ops.scan_add(xs, 0)
+        st = ops.Status(self.dev)
+        s = ops.scan_add(xs, 0, status=st)
+        self._raise(st, f)
         return int(s[-1].item())
 
     def _p_filter(self, f, a):
@@ -699,7 +727,10 @@ class Interp:
         n = flags.numel()
         if xs.numel() < n:
             raise errors.OracleError("sgmSum: values shorter than flags")  # the reference raises IndexError
-        return self._out(ops.segscan_add(flags, xs[:n]))
+        st = ops.Status(self.dev)
+        zs = ops.segscan_add(flags, xs[:n], status=st)
+        self._raise(st, f)
+        return self._out(zs)
 
     def _p_c2(self, f, a):
         p, xs, shape = _pred(a[0]), _dev_i64(a[1], self.dev), _dev_i64(a[2], self.dev)
@@ -755,6 +786,14 @@ class Interp:
         self._raise(st, f)
         v = float(out.item())
         return v
+
+
+def _int64(v) -> int:
+    """A host scalar that enters a kernel as int64 (a neutral element)."""
+    v = int(v)
+    if not -(1 << 63) <= v < (1 << 63):
+        raise errors.IntegerOverflow(f"scalar {v}")
+    return v
 
 
 def _is_add(op) -> bool:

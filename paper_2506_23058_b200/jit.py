@@ -66,7 +66,26 @@ __device__ __forceinline__ void fail_oob(ixg_status* st, int stmt, long long ele
   atomicMin(&st->first, key);
   atomicOr(&st->codes, 1u << 1);
 }
+// int64 arithmetic of the language, checked: the reference's ints are
+// unbounded (oracle.py:214-240), a value leaving int64 is IXG_OVERFLOW at
+// site IXG_OVF_SITE (254) instead of a wrapped result
+__device__ __forceinline__ void fail_ovf(ixg_status* st, int stmt, long long elem) {
+  const u64 key = ((u64)(stmt & 0xff) << 56) | (((u64)elem & 0xffffffffffffULL) << 8) | 254ULL;
+  atomicMin(&st->first, key);
+  atomicOr(&st->codes, 1u << 6);
+}
+__device__ __forceinline__ int ck_add(long long a, long long b, long long* r) {
+  const long long s = (long long)((u64)a + (u64)b); *r = s; return ((a ^ s) & (b ^ s)) < 0;
+}
+__device__ __forceinline__ int ck_sub(long long a, long long b, long long* r) {
+  const long long s = (long long)((u64)a - (u64)b); *r = s; return ((a ^ b) & (a ^ s)) < 0;
+}
+__device__ __forceinline__ int ck_mul(long long a, long long b, long long* r) {
+  const long long lo = (long long)((u64)a * (u64)b); *r = lo; return __mul64hi(a, b) != (lo >> 63);
+}
 """
+_CK = {"+": "ck_add", "-": "ck_sub", "*": "ck_mul"}
+OVF_SITE = 254  # status site of an int64 overflow (include/ixgpu.h IXG_OVF_SITE)
 
 
 @dataclass
@@ -120,6 +139,10 @@ class _Gen:
         self.inlining = 0
         # what a failed CHECKED index site does after recording the failure
         self.on_fail = "goto next;"
+        # int64 + - *: "fail" = checked, an overflow fails the element like an
+        # index site (needs st / stmt / i in scope); "flag" = checked, ORs into
+        # an `ovf_` variable of the enclosing code; "wrap" = modular
+        self.ovf = "fail"
 
     def line(self, s: str):
         self.body.append("  " * self.depth + s)
@@ -289,8 +312,15 @@ class _Gen:
             if e.op in _ARITH:
                 if fl:
                     return self.new(f"{_FARITH[e.op]}({self.as_f(a)}, {self.as_f(b)})", "f")
-                # two's-complement wrap like the VM's long long arithmetic
-                return self.new(f"(long long)((u64)({a}) {_ARITH[e.op]} (u64)({b}))")
+                if self.ovf == "wrap":
+                    return self.new(f"(long long)((u64)({a}) {_ARITH[e.op]} (u64)({b}))")
+                r = self.mut("i")
+                ck = f"{_CK[e.op]}({a}, {b}, &{r})"
+                if self.ovf == "flag":
+                    self.line(f"ovf_ |= {ck};")
+                else:
+                    self.line(f"if ({ck}) {{ fail_ovf(st, stmt, i); {self.on_fail} }}")
+                return r
             if e.op in _CMP:
                 if fl:
                     return self.new(f"(long long)(({self.as_f(a)}) {_CMP[e.op]} ({self.as_f(b)}))")

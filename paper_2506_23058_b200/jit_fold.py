@@ -167,16 +167,27 @@ def _params_scope(lam, k):
 
 def _op_function(lam, k):
     """The operator as `V op(const V&, const V&)` (no captures: the
-    associative forms only name their parameters and constants)."""
-    g = _Gen({}, lambda node: 0)
-    g.depth = 1
-    res = g.tuple_expr(lam.body, _params_scope(lam, k), k)
-    _ints_only(g, res)
-    lines = ["__device__ __forceinline__ V op(const V& A_, const V& B_) {",
-             "  const long long* A = A_.c; const long long* B = B_.c; (void)A; (void)B;"]
-    lines += g.body
-    lines += ["  V R;"] + [f"  R.c[{j}] = {r};" for j, r in enumerate(res)] + ["  return R;", "}"]
-    return "\n".join(lines)
+    associative forms only name their parameters and constants), modular,
+    for the tree combines; and `V op_ck(const V&, const V&, int& ovf_)`, the
+    same with checked int64 arithmetic, for the down pass's per-element
+    left-fold steps: there the accumulator is the exact wrapped prefix, so a
+    step that leaves int64 is exactly a result the reference would hold as a
+    big int (oracle.py:288-292) -- a combine of two partial aggregates may
+    overflow harmlessly and is never checked."""
+    out = []
+    for name, mode in (("op", "wrap"), ("op_ck", "flag")):
+        g = _Gen({}, lambda node: 0)
+        g.ovf = mode
+        g.depth = 1
+        res = g.tuple_expr(lam.body, _params_scope(lam, k), k)
+        _ints_only(g, res)
+        extra = ", int& ovf_" if mode == "flag" else ""
+        lines = [f"__device__ __forceinline__ V {name}(const V& A_, const V& B_{extra}) {{",
+                 "  const long long* A = A_.c; const long long* B = B_.c; (void)A; (void)B;"]
+        lines += g.body
+        lines += ["  V R;"] + [f"  R.c[{j}] = {r};" for j, r in enumerate(res)] + ["  return R;", "}"]
+        out.append("\n".join(lines))
+    return "\n".join(out)
 
 
 _VHELP = r"""
@@ -274,7 +285,7 @@ extern "C" __global__ void __launch_bounds__(1024) ixg_scan_top(const long long*
 }}
 
 extern "C" __global__ void __launch_bounds__(256) ixg_scan_down({ins}, {outs}, long long n,
-    const long long* __restrict__ carry) {{
+    const long long* __restrict__ carry, ixg_status* st) {{
 {tile_fold}
   if (threadIdx.x == 0)
     for (int q = 1; q < nw; ++q) wv[q] = op(wv[q - 1], wv[q]);
@@ -283,9 +294,11 @@ extern "C" __global__ void __launch_bounds__(256) ixg_scan_down({ins}, {outs}, l
     V run; for (int j = 0; j < K; ++j) run.c[j] = carry[blockIdx.x * (long long)K + j];
     if (w > 0) run = op(run, wv[w - 1]);
     if (lane > 0) run = op(run, ex);
+    int ovf_ = 0, seen = 0;
     for (int q = 0; q < mine; ++q) {{
       {item("f0 + q")}
-      run = op(run, b_);
+      run = op_ck(run, b_, ovf_);  // the left fold's step on the exact prefix
+      if (ovf_ && !seen) {{ fail_ovf(st, 0, base + f0 + q); seen = 1; }}
       for (int j = 0; j < K; ++j) sm[j][PADI(f0 + q)] = run.c[j];
     }}
   }}
@@ -450,14 +463,19 @@ extern "C" __global__ void __launch_bounds__(256) ixg_hist_seq({", ".join(params
 
 
 def _hist_cas_source(lam, v_type):
+    """Commutative + associative hist operator as a CAS loop per element.
+    Its int64 arithmetic is checked per update: an update that leaves int64
+    in THIS order is reported, and the caller re-runs the exact in-order
+    fold (the reference's order decides, oracle.py:313-315)."""
     a, b = lam.params
     g = _Gen({}, lambda node: 0)
+    g.ovf = "flag"
     g.depth = 3
     res = g.expr(lam.body, {a: "cur", b: "v"})
     _ints_only(g, [res])
     return _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__(256) ixg_hist_cas(const long long* __restrict__ is,
-    const {v_type}* __restrict__ vs, long long* __restrict__ dst, long long dlen, long long m) {{
+    const {v_type}* __restrict__ vs, long long* __restrict__ dst, long long dlen, long long m, ixg_status* st) {{
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {{
     const long long bin = is[i];
@@ -465,12 +483,15 @@ extern "C" __global__ void __launch_bounds__(256) ixg_hist_cas(const long long* 
     const long long v = (long long)vs[i];
     unsigned long long* p = (unsigned long long*)(dst + bin);
     unsigned long long old = *(volatile unsigned long long*)p, seen;
+    int ovf_;
     do {{
       seen = old;
+      ovf_ = 0;
       const long long cur = (long long)seen;
 {chr(10).join(g.body)}
       old = atomicCAS(p, seen, (unsigned long long)({res}));
     }} while (old != seen);
+    if (ovf_) fail_ovf(st, 0, i);
   }}
 }}
 """
@@ -546,7 +567,7 @@ def scan(lam, nes: list, arrays: list, env: dict, site_bits, status, device=None
         _launch(kern, "ixg_scan_red", tiles, 256, [_p(t) for t in ins] + [ctypes.c_longlong(n), _p(agg)], dev)
         _launch(kern, "ixg_scan_top", 1, 1024, [_p(agg), ctypes.c_longlong(tiles)] + nev + [_p(carry)], dev)
         _launch(kern, "ixg_scan_down", tiles, 256,
-                [_p(t) for t in ins] + [_p(o) for o in outs] + [ctypes.c_longlong(n), _p(carry)], dev)
+                [_p(t) for t in ins] + [_p(o) for o in outs] + [ctypes.c_longlong(n), _p(carry), _p(status.t)], dev)
         return outs, [], True
     src, spec = _seq_scan_source(lam, k, in_types, env, site_bits, acc_tys)
     if n == 0:
@@ -578,8 +599,11 @@ def hist(lam, ne, dlen: int, is_: torch.Tensor, vs: torch.Tensor, env: dict, sit
             kern = _kernel(src, ("ixg_hist_cas",))
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             grid = max(1, min((m + 255) // 256, sms * 8))
+            st = ops.Status(dev)
             _launch(kern, "ixg_hist_cas", grid, 256,
-                    [_p(iss), _p(vss), _p(dst), ctypes.c_longlong(nd), ctypes.c_longlong(m)], dev)
+                    [_p(iss), _p(vss), _p(dst), ctypes.c_longlong(nd), ctypes.c_longlong(m), _p(st.t)], dev)
+            if not st.read().ok:  # an update left int64 in the atomic order: decide in the reference's order
+                return hist(lam, ne, dlen, is_, vs, env, site_bits, status, force_seq=True)
         return dst, [], "cas"
     dst = torch.empty(nd, dtype=torch.float64 if acc_ty == "f" else torch.int64, device=dev)
     src, spec = _hist_seq_source(lam, v_type, env, site_bits, acc_ty)

@@ -150,13 +150,17 @@ class Status:
 
 
 # ------------------------------------------------------------------ builtins
-def scan_add(xs: torch.Tensor, ne: int = 0, exclusive: bool = False, out=None) -> torch.Tensor:
-    """scan (+) ne xs (oracle.py:281-293): int64 inclusive (or exclusive) sums."""
+def scan_add(xs: torch.Tensor, ne: int = 0, exclusive: bool = False, out=None, status=None) -> torch.Tensor:
+    """scan (+) ne xs (oracle.py:281-293): int64 inclusive (or exclusive)
+    sums; with a Status, the first sum that leaves int64 is recorded
+    (IXG_OVERFLOW at site L.OVF_SITE)."""
     xs = _contig(xs)
     n = xs.numel()
     out = torch.empty(n, dtype=torch.int64, device=xs.device) if out is None else out
     ws, wsb = _ws(L.OP_SCAN, n, 0, xs.device)
-    L.check(_lib().ixg_scan_add(_dt(xs), _ptr(xs), n, ne, int(exclusive), _ptr(out), ws, wsb, _stream()), "scan_add")
+    st = status.ptr if status is not None else _ptr(None)
+    L.check(_lib().ixg_scan_add(_dt(xs), _ptr(xs), n, ne, int(exclusive), _ptr(out), ws, wsb, st, _stream()),
+            "scan_add")
     return out
 
 
@@ -177,16 +181,18 @@ def jagged_dest(bits: torch.Tensor, cs: torch.Tensor, tb: torch.Tensor, out=None
     return out
 
 
-def segscan_add(flags: torch.Tensor, xs: torch.Tensor, want_flags: bool = False):
-    """sgmSum's 2-ary scan; returns values (and flags)."""
+def segscan_add(flags: torch.Tensor, xs: torch.Tensor, want_flags: bool = False, status=None):
+    """sgmSum's 2-ary scan; returns values (and flags).
+    With a Status, a segment sum leaving int64 is recorded (L.OVF_SITE)."""
     flags, xs = _contig(flags), _contig(xs)
     n = flags.numel()
     out_v = torch.empty(n, dtype=torch.int64, device=xs.device)
     out_f = torch.empty(n, dtype=torch.uint8, device=xs.device) if want_flags else None
     ws, wsb = _ws(L.OP_SEGSCAN, n, 0, xs.device)
+    st = status.ptr if status is not None else _ptr(None)
     L.check(
         _lib().ixg_segscan_add(_dt(flags), _ptr(flags), _dt(xs), _ptr(xs), n, 0, 0, _ptr(out_v), _ptr(out_f), ws, wsb,
-                               _stream()),
+                               st, _stream()),
         "segscan_add",
     )
     return (out_v, out_f) if want_flags else out_v
@@ -221,12 +227,16 @@ def gather(arr: torch.Tensor, idx: torch.Tensor, site_bits: int, status: Status,
     return out
 
 
-def hist(op: int, ne: int, dlen: int, is_: torch.Tensor, vs: torch.Tensor) -> torch.Tensor:
-    """hist op ne dlen is vs (oracle.py:306-316)."""
+def hist(op: int, ne: int, dlen: int, is_: torch.Tensor, vs: torch.Tensor, status=None) -> torch.Tensor:
+    """hist op ne dlen is vs (oracle.py:306-316).  (+) bins are summed in
+    128 bits; with a Status, a bin whose sum leaves int64 is recorded."""
     is_, vs = _contig(is_), _contig(vs)
     out = torch.empty(max(dlen, 0), dtype=torch.int64, device=is_.device)
+    ws, wsb = _ws(L.OP_HIST, 0, max(dlen, 0), is_.device) if op == L.HIST_ADD else (_ptr(None), ctypes.c_size_t(0))
+    st = status.ptr if status is not None else _ptr(None)
     L.check(
-        _lib().ixg_hist(op, ne, dlen, _ptr(is_), is_.numel(), _ptr(vs), vs.numel(), _ptr(out), _stream()), "hist"
+        _lib().ixg_hist(op, ne, dlen, _ptr(is_), is_.numel(), _ptr(vs), vs.numel(), _ptr(out), ws, wsb, st, _stream()),
+        "hist"
     )
     return out
 

@@ -6,6 +6,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+_GOLDEN = os.path.join(ROOT, "tests", "golden")  # bigtrack.fits
+if _GOLDEN not in sys.path:
+    sys.path.append(_GOLDEN)
 
 REFERENCE_SRC = "/root/reference/pkg/src"
 

@@ -30,11 +30,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 from ixverify.normalize import check_well_formed, normalize  # noqa: E402
 from ixverify.oracle import OracleError, eval_program  # noqa: E402
 from ixverify.parser import parse_program  # noqa: E402
 
+import bigtrack  # noqa: E402
 from paper_2506_23058_b200 import ir  # noqa: E402
 
 
@@ -155,23 +157,25 @@ def main():
         ok = True
         for n in (0, 1, 5, 33, 300):
             a = args_for(rng, kind, n)
-            try:
-                res = eval_program(prog, fname, a, budget)
-                flat = res if isinstance(res, list) else [res]
-                if any(isinstance(v, int) and not isinstance(v, bool) and abs(v) >= 1 << 62 for v in flat):
+            # values are NOT bounded: a result or intermediate that leaves int64
+            # is kept and marked "big" (bigtrack.py) -- the GPU must then raise
+            # IntegerOverflow (or still match), never return a wrapped value
+            with bigtrack.tracking() as big:
+                try:
+                    res = eval_program(prog, fname, a, budget)
+                    d = {"program": key, "fun": fname, "kind": kind, "args": a, "result": res}
+                except TimeoutError:
                     ok = False
                     break
-                rows.append({"program": key, "fun": fname, "kind": kind, "args": a, "result": res})
-            except TimeoutError:
-                ok = False
-                break
-            except OracleError as e:
-                d = {"program": key, "fun": fname, "kind": kind, "args": a, "error": type(e).__name__}
-                if hasattr(e, "site"):
-                    d["site"] = e.site
-                if getattr(e, "pos", None) is not None:
-                    d["pos"] = list(e.pos)
-                rows.append(d)
+                except OracleError as e:
+                    d = {"program": key, "fun": fname, "kind": kind, "args": a, "error": type(e).__name__}
+                    if hasattr(e, "site"):
+                        d["site"] = e.site
+                    if getattr(e, "pos", None) is not None:
+                        d["pos"] = list(e.pos)
+            if big[0]:
+                d["big"] = True
+            rows.append(d)
         signal.alarm(0)
         if not ok:
             print("dropped (slow or huge):", src.strip()[:160], file=sys.stderr)

@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 REF = "/root/reference/pkg/src"
 sys.path.insert(0, ROOT)
 sys.path.insert(0, REF)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import numpy as np  # noqa: E402
 from ixverify.normalize import check_well_formed, normalize  # noqa: E402
@@ -42,6 +43,7 @@ from ixverify.oracle import Interp, OracleError, eval_program, gen_args  # noqa:
 from ixverify.oracle import _check_pre_atom, _conjuncts, chk_bij, chk_inj  # noqa: E402
 from ixverify.parser import parse_program  # noqa: E402
 
+import bigtrack  # noqa: E402
 from paper_2506_23058_b200 import gen, ir  # noqa: E402
 from paper_2506_23058_b200 import select as sel  # noqa: E402
 from paper_2506_23058_b200.pred import GT, HASH, LT, Pred  # noqa: E402
@@ -76,15 +78,19 @@ def enc(v):
 
 
 def run(program, fun, args, budget=BUDGET):
-    try:
-        return {"result": enc(eval_program(program, fun, args, budget))}
-    except OracleError as e:
-        d = {"error": type(e).__name__}
-        if hasattr(e, "site"):
-            d["site"] = e.site
-        if getattr(e, "pos", None) is not None:
-            d["pos"] = list(e.pos)
-        return d
+    """the reference's answer; "big" when its evaluation left int64 (bigtrack.py)"""
+    with bigtrack.tracking() as big:
+        try:
+            d = {"result": enc(eval_program(program, fun, args, budget))}
+        except OracleError as e:
+            d = {"error": type(e).__name__}
+            if hasattr(e, "site"):
+                d["site"] = e.site
+            if getattr(e, "pos", None) is not None:
+                d["pos"] = list(e.pos)
+    if big[0] or not bigtrack.fits([a for a in args if not isinstance(a, Pred)]):
+        d["big"] = True
+    return d
 
 
 PROPERTY_HEADS = {"Range", "Equiv", "Mono", "Inj", "Bij", "FiltPart", "InvFiltPart", "OrthogPreds"}
@@ -254,6 +260,32 @@ def kmeans_cases(rng_seed):
     return out
 
 
+BIG = 1 << 62
+
+
+def overflow_cases(fun):
+    """Values whose results leave int64 in the reference (its ints are
+    unbounded: scan of [2^62, 2^62, 2^62] = [.., 3*2^62]),
+    and ones that come close without leaving it."""
+    if fun == "sum":
+        return [[[BIG, BIG, BIG]], [[BIG, BIG - 1, -BIG]], [[-BIG, -BIG, -1]], [[(1 << 63) - 1, 1]],
+                [[-BIG, -BIG]]]
+    if fun == "sgmSum":
+        return [[[True, False, False, True, False], [BIG, BIG, 5, BIG, BIG - 1]],
+                [[True, False, True, False], [BIG, BIG, BIG, -BIG]]]
+    if fun in ("csrg", "csrg_any"):
+        return [[[1 << 40, 3], [1 << 30, 1 << 20], [0, 1]], [[1 << 31, 3], [1 << 31, -(1 << 31)], [0, 0]]]
+    if fun == "c2":
+        return [[Pred.ge(0), [BIG, BIG, -1, 3], [2, 1]], [Pred.ge(0), [BIG, BIG, -1, 3], [1, 1, 1]]]
+    if fun in ("scan_mul",):
+        return [[[1 << 40, 1 << 30, 1]], [[1 << 31, -(1 << 31), 2]], [[3] * 50]]
+    if fun in ("hist_mul",):
+        return [[2, [0, 0, 0, 1], [1 << 40, 1 << 30, 0, 5]], [2, [0, 0, 1], [1 << 40, 1 << 30, 5]]]
+    if fun == "scan_pair":
+        return [[[BIG, BIG], [1, 2]]]
+    return []
+
+
 def error_cases(fun):
     """Inputs that violate the annotations, so the CHECKED paths fire."""
     if fun == "sc_any":
@@ -345,6 +377,7 @@ def main():
                 draws += [("kmeans", a) for a in kmeans_cases(sum(map(ord, key)))]
             draws += [("big", a) for a in big_cases(f.name)]
             draws += [("error", a) for a in error_cases(f.name)]
+            draws += [("overflow", a) for a in overflow_cases(f.name)]
             draws += [("demo", a) for a in DEMOS.get((key, f.name), [])]
             for origin_kind, a in draws:
                 rec = {"program": key, "fun": f.name, "kind": origin_kind, "args": enc(a)}

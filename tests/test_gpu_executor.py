@@ -15,6 +15,8 @@ from paper_2506_23058_b200 import select as sel
 
 from test_oracle_golden import CASES, dec
 
+import bigtrack
+
 pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -72,6 +74,19 @@ def test_eval_program_matches_reference(cuda, idx, mode):
     if "error" in case and mode == "generic":
         kw["variant"] = "checked"  # generic path with the reference's own checks
     it = Interp(prog, case.get("budget", 10**6), **kw)
+    if case.get("big"):
+        # the reference held an integer outside int64 (tests/golden/bigtrack.py):
+        # IntegerOverflow -- mandatory when a result does not fit -- or its answer
+        try:
+            got = it.call(case["fun"], args)
+        except errors.IntegerOverflow:
+            return
+        except errors.OracleError as ex:
+            assert "error" in case and type(ex).__name__ == case["error"], ex
+            return
+        want = dec(case["result"])
+        assert "result" in case and bigtrack.fits(want) and _same(got, want), (got, case)
+        return
     if "error" in case:
         cls = getattr(errors, case["error"])
         with pytest.raises(cls) as ei:

@@ -424,3 +424,79 @@ def test_c2_extremes(cuda, pred, seg):
         assert np.array_equal(_np(zs)[:kk].astype(np.int64), want_zs)
         s = st.read()
         assert s.ok and not s.narrow
+
+
+# ----------------------------------------------------------------- int64 overflow (the reference's ints are unbounded)
+@pytest.mark.parametrize("n", [3, 5000, 1 << 20])
+def test_scan_overflow_exact(cuda, n):
+    """scan (+) over int64: IXG_OVERFLOW exactly at the first prefix leaving
+    int64 (both scan kernels), never for sums that stay inside -- including
+    prefixes that touch INT64_MAX/MIN and come back."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    big = 1 << 62
+    xs = np.zeros(n, np.int64)
+    xs[0], xs[1] = big, big - 1            # 2^63 - 1: fits
+    if n > 2:
+        xs[2] = -big
+    st = ops.Status(cuda)
+    got = ops.scan_add(_t(xs, cuda), 0, status=st)
+    assert st.read().ok and np.array_equal(_np(got), np.cumsum(xs))
+    for at in sorted({2, n // 2, n - 1}):
+        ys = xs.copy()
+        ys[2] = 0
+        ys[at] += 1                        # the prefix at `at` becomes 2^63
+        for exclusive in (False, True):
+            st = ops.Status(cuda)
+            ops.scan_add(_t(ys, cuda), 0, exclusive=exclusive, status=st)
+            s = st.read()
+            assert not s.ok and s.site == L.OVF_SITE and s.elem == at, (at, s)
+    # via the ne seed (int32 input path too)
+    st = ops.Status(cuda)
+    ops.scan_add(torch.ones(n, dtype=torch.int32, device=cuda), (1 << 63) - 2, status=st)
+    s = st.read()
+    assert not s.ok and s.elem == 1
+
+
+def test_segscan_overflow_resets_at_flags(cuda):
+    from paper_2506_23058_b200 import ops
+
+    big = 1 << 62
+    xs = np.array([big, big - 1, big, big, 5, -big, -big, -1], np.int64)
+    fl = np.array([1, 0, 1, 0, 1, 0, 0, 0], np.uint8)
+    st = ops.Status(cuda)
+    ops.segscan_add(_t(fl, cuda), _t(xs, cuda), status=st)
+    s = st.read()
+    assert not s.ok and s.elem == 3  # big + big in the second segment
+    xs[3] = big - 1
+    st = ops.Status(cuda)
+    ops.segscan_add(_t(fl, cuda), _t(xs, cuda), status=st)
+    s = st.read()
+    assert not s.ok and s.elem == 7  # 5 - 2^62 - 2^62 - 1 < -2^63
+    xs[7] = 0
+    st = ops.Status(cuda)
+    got = ops.segscan_add(_t(fl, cuda), _t(xs, cuda), status=st)
+    assert st.read().ok and _np(got).tolist() == O.sgmsum(fl.astype(np.int64), xs).tolist()
+
+
+def test_hist_add_128bit_bins(cuda):
+    """hist (+): bins hold exact 128-bit sums; only a FINAL value outside
+    int64 is an overflow (atomic order does not matter)."""
+    from paper_2506_23058_b200 import ops
+
+    big = 1 << 62
+    is_ = np.array([0, 0, 0, 1, 1, 1, 2], np.int64)
+    vs = np.array([big, big, -big, big, big, big, -5], np.int64)
+    st = ops.Status(cuda)
+    got = ops.hist(L.HIST_ADD, 0, 3, _t(is_, cuda), _t(vs, cuda), status=st)
+    s = st.read()
+    assert not s.ok and s.elem == 1  # bin 1 = 3 * 2^62
+    assert _np(got)[0] == big and _np(got)[2] == -5
+    n = 1 << 20
+    is2 = (np.arange(n, dtype=np.int64) // 2) % 100
+    vs2 = np.where(np.arange(n) % 2 == 0, big, -big).astype(np.int64)  # the atomic order's partial sums swing
+    st = ops.Status(cuda)
+    got = ops.hist(L.HIST_ADD, 7, 100, _t(is2, cuda), _t(vs2, cuda), status=st)
+    assert st.read().ok and np.array_equal(_np(got), O.hist(L.HIST_ADD, 7, 100, is2, vs2))
