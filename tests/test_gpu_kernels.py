@@ -471,11 +471,12 @@ def test_segscan_overflow_resets_at_flags(cuda):
     s = st.read()
     assert not s.ok and s.elem == 3  # big + big in the second segment
     xs[3] = big - 1
+    xs[4] = -5
     st = ops.Status(cuda)
     ops.segscan_add(_t(fl, cuda), _t(xs, cuda), status=st)
     s = st.read()
-    assert not s.ok and s.elem == 7  # 5 - 2^62 - 2^62 - 1 < -2^63
-    xs[7] = 0
+    assert not s.ok and s.elem == 6  # -5 - 2^62 - 2^62 < -2^63
+    xs[4], xs[7] = 5, 0  # 5 - 2^63: fits
     st = ops.Status(cuda)
     got = ops.segscan_add(_t(fl, cuda), _t(xs, cuda), status=st)
     assert st.read().ok and _np(got).tolist() == O.sgmsum(fl.astype(np.int64), xs).tolist()
