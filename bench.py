@@ -150,12 +150,21 @@ class C2:
 
     name = "c2"
 
+    scaling = "weak"  # N per GPU
+
+    def describe(self, quick, ws):
+        self.N = (1 << 22) if quick else (1 << 28)
+        self.m = (1 << 14) if quick else (1 << 20)
+        self.workload = (f"c2 = filter (x >= 0) + mkFlags + sgmSum: N=2^{self.N.bit_length() - 1} int32 uniform "
+                         f"[-128,127] per GPU, m=2^{self.m.bit_length() - 1} segments per GPU (i64 shape, sum = k, "
+                         ">=1% empty), zs int32" + (f"; {ws} contiguous shards, device all-gathers of counts and "
+                                                     "segmented aggregates" if ws > 1 else ""))
+
     def __init__(self, quick, rank, ws):
         from paper_2506_23058_b200 import gen
         from paper_2506_23058_b200.pred import Pred
 
-        self.N = (1 << 22) if quick else (1 << 28)
-        self.m = (1 << 14) if quick else (1 << 20)
+        self.describe(quick, ws)
         self.p = Pred.ge(0)
         self.rank, self.ws = rank, ws
         # each rank owns one contiguous shard of the global xs
@@ -172,10 +181,6 @@ class C2:
         else:
             self.k_total = self.k
             self.shape_h = gen.segment_shape(1 + rank, self.m, self.k)
-        self.workload = (f"c2 = filter (x >= 0) + mkFlags + sgmSum: N=2^{self.N.bit_length() - 1} int32 uniform "
-                         f"[-128,127] per GPU, m=2^{self.m.bit_length() - 1} segments per GPU (i64 shape, sum = k, "
-                         ">=1% empty), zs int32" + (f"; {ws} contiguous shards, all-gathers of counts and "
-                                                     "segmented aggregates" if ws > 1 else ""))
 
     def setup_device(self):
         import torch
@@ -199,9 +204,7 @@ class C2:
         from paper_2506_23058_b200 import ops
 
         if self.ws > 1:
-            from paper_2506_23058_b200 import dist as D
-
-            D.c2_sharded(self.local)
+            self.local.step_device()  # counts, offsets and carries stay on the device
             return
         ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
 
@@ -246,10 +249,8 @@ class C2:
         self.xs.copy_(xs_p, non_blocking=True)
         self.shape.copy_(shape_p, non_blocking=True)
         if self.ws > 1:
-            from paper_2506_23058_b200 import dist as D
-
-            D.c2_sharded(self.local)
-            k = self.local.k
+            self.local.step_device()
+            k = int(self.dk.item())
         else:
             ops.c2(self.xs, self.p, self.shape, variant, self.st, ys=self.ys, zs=self.zs, d_k=self.dk)
             k = int(self.dk.item())
@@ -318,20 +319,26 @@ class C1:
 
     name = "c1"
 
+    def describe(self, quick, ws, big=False):
+        self.name = "c5" if big else "c1"
+        self.big = big
+        # C5: 2^32 in total over the GPUs (strong scaling); C1: 2^20 per GPU
+        self.scaling = "strong" if big else "weak"
+        self.N = ((1 << 24) if quick else (1 << 32) // ws) if big else (1 << 20)
+        self.workload = (f"partition2 (x < 0), N=2^{self.N.bit_length() - 1} int32 uniform over int32"
+                         + (f" per GPU (2^{(self.N * ws).bit_length() - 1} total)" if big else "")
+                         + (f"; {ws} contiguous shards: device all-gather of per-shard true counts -> each shard's "
+                            "two output runs of the global result, moved to the shards owning their positions"
+                            if ws > 1 else ""))
+
     def __init__(self, quick, rank, ws, big=False):
         from paper_2506_23058_b200 import gen
         from paper_2506_23058_b200.pred import Pred
 
-        self.name = "c5" if big else "c1"
-        self.N = ((1 << 24) if quick else (1 << 32) // ws) if big else (1 << 20)
+        self.describe(quick, ws, big)
         self.p = Pred.lt(0)
         self.xs_h = None if big else gen.uniform(0, self.N, -(1 << 31), (1 << 31) - 1, np.int32, offset=rank * self.N)
-        self.big, self.rank, self.ws = big, rank, ws
-        self.workload = (f"partition2 (x < 0), N=2^{self.N.bit_length() - 1} int32 uniform over int32"
-                         + (" per GPU (2^32 total)" if big else "")
-                         + (f"; {ws} contiguous shards: all-gather of per-shard true counts -> each shard's two "
-                            "output runs of the global result, moved to the shards owning their positions"
-                            if ws > 1 else ""))
+        self.rank, self.ws = rank, ws
 
     def setup_device(self):
         import torch
@@ -379,7 +386,7 @@ class C1:
             from paper_2506_23058_b200 import dist as D
 
             if self.peer is not None:
-                self.nt_global = self.peer.step()
+                self.d_off = self.peer.step()  # [T_<rank, NT] on the device; no host round trip
             else:
                 self.nt_global, self.runs, self.mine = D.partition2_sharded(self.local, exchange=True)
             return
@@ -485,13 +492,23 @@ class C3:
     sc_any (dst init + OOB test + idempotence check)."""
 
     name = "c3"
-    cpu_threads = 1
-    cpu_desc = "oracle/ixoracle.c ixo_scatter (sequential restatement of oracle.py:294-305, 2^24 prefix)"
+    cpu_desc = ("oracle/ixoracle_par.c ixo_par_scatter_i32 (OpenMP restatement of oracle.py:294-305 with its "
+                "idempotence check: claim bitmap + value re-check)")
 
-    def __init__(self, quick, rank, ws):
+    scaling = "weak"  # an independent scatter per GPU (replicas, SURVEY §8e)
+
+    def describe(self, quick, ws, perm="streams"):
         self.N = (1 << 22) if quick else (1 << 29)
-        self.workload = (f"scatter dst is vs: n = m = 2^{self.N.bit_length() - 1}, is = partition2 indices of random "
-                         "xs (i64 permutation, two monotone streams), vs int32, dst int32 zeros")
+        self.perm = perm
+        if perm == "random":
+            pat = "a uniformly random permutation (torch.randperm, Philox)"
+        else:
+            pat = "partition2 indices of random xs (i64 permutation, two monotone streams)"
+        self.workload = (f"scatter dst is vs: n = m = 2^{self.N.bit_length() - 1}, is = {pat}, vs int32, "
+                         "dst int32 zeros" + (f"; {ws} independent replicas" if ws > 1 else ""))
+
+    def __init__(self, quick, rank, ws, perm="streams"):
+        self.describe(quick, ws, perm)
         self.rank, self.ws = rank, ws
 
     def setup_device(self):
@@ -500,13 +517,18 @@ class C3:
         from paper_2506_23058_b200 import ops
 
         dev = torch.device("cuda")
-        xs = ops.gen_uniform(self.N, -(1 << 31), (1 << 31) - 1, 11, torch.int32, offset=self.rank * self.N)
-        c = xs < 0
-        t = torch.cumsum(c, 0, dtype=torch.int64)
-        nt = t[-1]
-        i1 = torch.arange(1, self.N + 1, device=dev, dtype=torch.int64)
-        self.is_ = torch.where(c, t - 1, nt + (i1 - t) - 1)
-        del xs, c, t, i1
+        if self.perm == "random":
+            g = torch.Generator(device=dev)
+            g.manual_seed(11 + self.rank)
+            self.is_ = torch.randperm(self.N, generator=g, device=dev, dtype=torch.int64)
+        else:
+            xs = ops.gen_uniform(self.N, -(1 << 31), (1 << 31) - 1, 11, torch.int32, offset=self.rank * self.N)
+            c = xs < 0
+            t = torch.cumsum(c, 0, dtype=torch.int64)
+            nt = t[-1]
+            i1 = torch.arange(1, self.N + 1, device=dev, dtype=torch.int64)
+            self.is_ = torch.where(c, t - 1, nt + (i1 - t) - 1)
+            del xs, c, t, i1
         self.vs = ops.gen_uniform(self.N, -(1 << 31), (1 << 31) - 1, 12, torch.int32, offset=self.rank * self.N)
         self.dst = torch.zeros(self.N, dtype=torch.int32, device=dev)
         self.out = torch.empty_like(self.dst)
@@ -586,23 +608,17 @@ class C3:
         out_p.copy_(self.out, non_blocking=True)
         return 12 * self.N, 4 * self.N
 
-    def cpu_run(self, is_, vs, threads=0):
+    def cpu_run(self, dst, is_, vs, out, threads=0):
         from oracle import ixoracle as O
 
-        return O.scatter(np.zeros(len(is_), np.int64), is_, vs)
+        return O.par_scatter_i32(dst, is_, vs, threads, out=out)
 
     def cpu_sample(self, budget_s):
-        import torch
-
-        from paper_2506_23058_b200 import ops
-
-        n = min(self.N, 1 << 24)  # the sequential port on a 2^24 instance of the same construction
-        xs = ops.gen_uniform(n, -(1 << 31), (1 << 31) - 1, 11, torch.int32)
-        c = xs < 0
-        t = torch.cumsum(c, 0, dtype=torch.int64)
-        i1 = torch.arange(1, n + 1, device=xs.device, dtype=torch.int64)
-        is_ = torch.where(c, t - 1, t[-1] + (i1 - t) - 1)
-        return is_.cpu().numpy(), self.vs[:n].cpu().numpy().astype(np.int64), n
+        """the full per-GPU workload (same is / vs / dst as the device arm)"""
+        if not hasattr(self, "is_"):
+            self.setup_device()
+        out = np.empty(self.N, np.int32)
+        return np.zeros(self.N, np.int32), self.is_.cpu().numpy(), self.vs.cpu().numpy(), out, self.N
 
 
 class C4:
@@ -611,15 +627,19 @@ class C4:
     64; ELIDED = csrg (Range proved), CHECKED = csrg_any (bounds checks)."""
 
     name = "c4"
-    cpu_threads = 1
-    cpu_desc = "oracle/ixoracle.c ixo_csrg (sequential restatement, 2^24-nnz prefix)"
+    cpu_desc = "oracle/ixoracle_par.c ixo_par_csrg_i32 (OpenMP restatement with the bounds check of oracle.py:177-184)"
 
-    def __init__(self, quick, rank, ws):
+    scaling = "weak"  # an nnz shard per GPU, x replicated
+
+    def describe(self, quick, ws):
         self.N = (1 << 22) if quick else (1 << 28)
         self.ncols = 1 << 20
+        self.workload = (f"CSR gather v * x[c]: nnz = 2^{self.N.bit_length() - 1} per GPU, num_cols = 2^20, values/x "
+                         "int32 in [-2^15, 2^15), indices i64 sorted within rows of 64")
+
+    def __init__(self, quick, rank, ws):
+        self.describe(quick, ws)
         self.rank, self.ws = rank, ws
-        self.workload = (f"CSR gather v * x[c]: nnz = 2^{self.N.bit_length() - 1}, num_cols = 2^20, values/x int32 in "
-                         "[-2^15, 2^15), indices i64 sorted within rows of 64")
 
     def setup_device(self):
         import torch
@@ -749,15 +769,17 @@ class C4:
         o_p.copy_(self.out, non_blocking=True)
         return 12 * self.N, 4 * self.N
 
-    def cpu_run(self, x, vals, idx, threads=0):
+    def cpu_run(self, x, vals, idx, out, threads=0):
         from oracle import ixoracle as O
 
-        return O.csrg(x, vals, idx)
+        return O.par_csrg_i32(x, vals, idx, threads, out=out)
 
     def cpu_sample(self, budget_s):
-        n = min(self.N, 1 << 24)
-        return (self.x.cpu().numpy().astype(np.int64), self.vals[:n].cpu().numpy().astype(np.int64),
-                self.idx[:n].cpu().numpy(), n)
+        """the full per-GPU workload (same x / values / indices as the device arm)"""
+        if not hasattr(self, "vals"):
+            self.setup_device()
+        return (self.x.cpu().numpy(), self.vals.cpu().numpy(), self.idx.cpu().numpy(), np.empty(self.N, np.int32),
+                self.N)
 
 
 # ----------------------------------------------------------------- timing
@@ -949,20 +971,13 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": wl.scaling,
         "vs_baseline": None,
         "dtype": "int32",
         "data": "synthetic",
-        "config": {
-            "workload": wl.workload,
-            "variant": "verifier-selected (ELIDED: Sc1 scatters fused, mkFlags Ss2)",
-            "parallelism": f"shards{ws}" if ws > 1 else "single",
-            "l2": ("256 MB L2 flush write between steps, outside the per-step events (8 MB working set)"
-                   if wl.name == "c1"
-                   else "inputs larger than the 126 MB L2, no flush"),
-            "parity_vs_cpu_port": bool(parity) if want is not None else "checked in tests",
-            "parity_checked_variant": bool(parity_chk) if want is not None else "checked in tests",
-        },
+        "config": config_of(wl, ws),
+        "parity": {"vs_cpu_port": bool(parity) if want is not None else "checked in tests",
+                   "checked_variant": bool(parity_chk) if want is not None else "checked in tests"},
         "hbm_gbs_step": round(wl.algo_bytes_step() / (ms * 1e-3) / 1e9, 1),
         "checked": {
             "ms_per_step": round(ms_chk, 4),
@@ -1013,6 +1028,17 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def config_of(wl, ws) -> dict:
+    """The `config` object of BOTH arms (identical keys and values)."""
+    return {
+        "workload": wl.workload,
+        "variant": "verifier-selected (ELIDED: Sc1 scatters fused, mkFlags Ss2)",
+        "parallelism": f"shards{ws}" if ws > 1 else "single",
+        "l2": ("256 MB L2 flush write between steps, outside the per-step events (8 MB working set)"
+               if wl.name == "c1" else "inputs larger than the 126 MB L2, no flush"),
+    }
+
+
 def _ncu_traffic(name, units=None):
     """dram bytes per launch of the dominant kernel from the committed ncu
     --set full capture (profiles/ncu_<name>_full.json; scaled by the units of
@@ -1031,7 +1057,7 @@ def cpu_baseline(wl, args):
     """The oracle port (OpenMP, all host threads) on the same workload."""
     from oracle import ixoracle as O
 
-    threads = getattr(wl, "cpu_threads", None) or O.threads()
+    threads = O.threads()
     inputs = wl.cpu_sample(20.0)
     n = inputs[-1]
     res = wl.cpu_run(*inputs[:-1], threads)
@@ -1053,8 +1079,8 @@ def cpu_baseline(wl, args):
                    f"{getattr(wl, 'cpu_desc', 'oracle/ixoracle_par.c (OpenMP)')}, median"),
         "ms_per_run": round(best * 1e3, 2),
     }
-    if n == wl.units():
-        out["_result"] = (res[0], res[1]) if wl.name == "c2" else (res[0], res[1])
+    if n == wl.units() and wl.name in ("c1", "c2", "c5"):
+        out["_result"] = (res[0], res[1])  # (ys, zs) / (num_true, ys): the parity reference of the device arm
     return out
 
 
@@ -1063,12 +1089,13 @@ def run_reference(args):
     reference is Python and cannot travel to the GPU box, so this is its
     restatement oracle/ (C, OpenMP, every host thread) on the same config."""
     rank = int(os.environ.get("RANK", "0"))
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     from oracle import ixoracle as O
 
     wl = make_workload(args, 0, 1)
+    wl_cfg = make_workload(args, 0, ws, describe_only=True)
     threads = O.threads()
     inputs = wl.cpu_sample(20.0)
     n = inputs[-1]
@@ -1089,30 +1116,46 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": wl_cfg.scaling,
         "vs_baseline": None,
         "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": wl.workload, "per_step": f"one full pass over n={n}"},
+        "config": config_of(wl_cfg, ws),
         "cpu_baseline": {"value": round(value, 4), "unit": "Gelem/s", "cores": threads, "kind": "port",
-                         "sample": f"n={n} per step, oracle/ixoracle_par.c (OpenMP)"},
+                         "sample": f"one full pass over n={n} per step (the single-GPU workload): "
+                                   f"{getattr(wl, 'cpu_desc', 'oracle/ixoracle_par.c (OpenMP)')}"},
         "e2e": {"value": round(value, 4), "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def make_workload(args, rank, ws):
+def make_workload(args, rank, ws, describe_only=False):
+    """describe_only: the workload's name / description / scaling for `ws`
+    ranks without touching a device or a process group (the reference arm)."""
     if args.config == "c2":
-        return C2(args.quick, rank, ws)
-    if args.config == "c1":
-        return C1(args.quick, rank, ws)
-    if args.config == "c5":
-        return C1(args.quick, rank, ws, big=True)
-    if args.config == "c3":
-        return C3(args.quick, rank, ws)
-    if args.config == "c4":
-        return C4(args.quick, rank, ws)
-    raise SystemExit(f"unknown config {args.config}")
+        wl = C2.__new__(C2) if describe_only else C2(args.quick, rank, ws)
+    elif args.config in ("c1", "c5"):
+        wl = C1.__new__(C1) if describe_only else C1(args.quick, rank, ws, big=args.config == "c5")
+    elif args.config == "c3":
+        wl = C3.__new__(C3) if describe_only else C3(args.quick, rank, ws, perm=args.perm)
+    elif args.config == "c4":
+        wl = C4.__new__(C4) if describe_only else C4(args.quick, rank, ws)
+    else:
+        raise SystemExit(f"unknown config {args.config}")
+    if describe_only:
+        wl.describe(args.quick, ws, **({"big": args.config == "c5"} if args.config in ("c1", "c5") else {}),
+                    **({"perm": args.perm} if args.config == "c3" else {}))
+    return wl
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
@@ -1124,12 +1167,22 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4", "c5"])
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--perm", default="streams", choices=["streams", "random"],
+                    help="c3: the index array (two monotone streams, SURVEY §8d C3, or a random permutation)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun (NCCL, 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+        os.execv(sys.executable, cmd + sys.argv[1:])
+    if ws_env is not None and int(ws_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
+    run_ours(args)
 
 
 if __name__ == "__main__":

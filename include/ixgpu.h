@@ -213,16 +213,20 @@ int ixg_filter_by(int dt, const uint8_t* cs, const void* xs, int64_t n, void* ys
  * (d_tot[0] = trues; classes 3 adds d_tot[1] = class 1), the all-gather input.
  * ixg_partition2_peer: the single-pass partition of this rank's shard whose
  * runs are stored straight to their global positions of the output sharded
- * over `ranks` GPUs (`shard` elements each, shard % (16 / elem size) == 0):
- * dst[r] = rank r's shard, mapped with ixg_ipc_open for r != this rank (peer
- * stores over NVLink); true_base / false_base = this rank's first global
- * position of each class (T_<r and NT + F_<r), local_true = its true count.
+ * over `ranks` GPUs (`shard` elements each = this rank's n, shard % (16 / elem
+ * size) == 0): dst[r] = rank r's shard, mapped with ixg_ipc_open for r != this
+ * rank (peer stores over NVLink); d_counts = DEVICE int64[ranks], every rank's
+ * true count (all-gathered on the device, e.g. ncclAllGather of d_tot): the
+ * kernel derives this rank's class bases itself (trues at T_<rank, falses at
+ * NT + F_<rank), so a sharded step needs no host round trip.
  * Replaces partition2.ixl's scatter (:17) for the sharded case. */
 int ixg_partition_counts(int dt, const void* xs, int64_t n, const ixg_pred* p, const ixg_pred* q, int classes,
                          int64_t* d_tot, void* ws, size_t ws_bytes, void* stream);
 int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, void* const* dst, int ranks,
-                        int64_t shard, int64_t true_base, int64_t false_base, int64_t local_true, void* ws,
-                        size_t ws_bytes, void* stream);
+                        int64_t shard, const int64_t* d_counts, int rank, void* ws, size_t ws_bytes, void* stream);
+/* out2 = [sum of d_counts[r * stride] over r < rank, over all r]: a rank's
+ * exclusive offset and the global total from an all-gathered device array. */
+int ixg_rank_offsets(const int64_t* d_counts, int ranks, int rank, int stride, int64_t* out2, void* stream);
 /* device buffers shared between the ranks' processes (CUDA IPC):
  * handle = 64 opaque bytes, exchanged by the host (torch.distributed). */
 int ixg_dev_alloc(size_t bytes, void** out);
@@ -291,21 +295,27 @@ int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint
  * A rank filters its contiguous shard (ixg_filter), learns its global output
  * offset K from an all-gather of counts, then:
  *   ixg_flag_bitmap  the mkFlags array of ALL shards' outputs as a bitmap
- *                    (bit scn[i] for non-empty segments below nbits);
+ *                    (bit scn[i] for non-empty segments below nbits, or below
+ *                    *d_nbits <= nbits when the total is on the device);
  *   ixg_segsum       zs = sgmSum over its n (or *d_n) outputs, flags = bits
- *                    [flag_base + j], seeded with the carry (carry_v, carry_f);
- *                    *d_total (2 x int64) = its segmented aggregate (v, f);
+ *                    [flag_base + j] (or *d_flag_base + j), seeded with the
+ *                    carry (carry_v, carry_f); *d_total (2 x int64) = its
+ *                    segmented aggregate (v, f);
  *   ixg_seg_carry    after the all-gather of aggregates: adds the carry of
- *                    the earlier ranks to its outputs before its first flag.
+ *                    the earlier ranks to its outputs before its first flag
+ *                    (carry_v, or -- device-resident -- folded from d_aggs
+ *                    = every rank's (v, f) and this rank's index).
+ * Every count / offset / carry can stay on the device (d_* arguments). 
  * ixg_bitmap_words(nbits) = uint32 words to allocate for `bits`. */
 int64_t ixg_bitmap_words(int64_t nbits);
-int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, void* ws, size_t ws_bytes,
-                    void* stream);
+int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, const int64_t* d_nbits, void* ws,
+                    size_t ws_bytes, void* stream);
 int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,
-               int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total, ixg_status* st, void* ws,
-               size_t ws_bytes, void* stream);
-int ixg_seg_carry(const uint32_t* bits, int64_t flag_base, int dt_z, void* zs, int64_t n, const int64_t* d_n,
-                  int64_t carry_v, void* scratch8, ixg_status* st, void* stream);
+               const int64_t* d_flag_base, int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total,
+               ixg_status* st, void* ws, size_t ws_bytes, void* stream);
+int ixg_seg_carry(const uint32_t* bits, int64_t flag_base, const int64_t* d_flag_base, int dt_z, void* zs, int64_t n,
+                  const int64_t* d_n, int64_t carry_v, const int64_t* d_aggs, int rank, void* scratch8, ixg_status* st,
+                  void* stream);
 
 /* ---- map with a compiled lambda (oracle.py:274-280) ----------------------
  * The host compiles the lambda body (paper_2506_23058_b200/vm.py) into a

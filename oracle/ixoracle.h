@@ -101,6 +101,12 @@ int ixo_par_c2_i32(const ixo_pred* p, const int32_t* xs, int64_t n, const int64_
                    int64_t m, int32_t* ys, int32_t* zs, int64_t* k, int threads);
 int ixo_par_partition2_i32(const ixo_pred* p, const int32_t* xs, int64_t n,
                            int64_t* num_true, int32_t* ys, int threads);
+/* scatter (oracle.py:294-305, with its idempotence check) and the CSR
+ * gather (with its bounds check) at the BASELINE widths, OpenMP */
+int ixo_par_scatter_i32(const int32_t* dst, int64_t ndst, const int64_t* is, const int32_t* vs, int64_t m,
+                        int32_t* out, int threads);
+int ixo_par_csrg_i32(const int32_t* x, int64_t ncols, const int32_t* vals, const int64_t* idx, int64_t nnz,
+                     int32_t* out, int64_t* first_bad, int threads);
 
 #ifdef __cplusplus
 }

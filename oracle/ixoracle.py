@@ -269,6 +269,32 @@ def par_partition2_i32(p, xs, nthreads=0):
     return nt.value, ys[: len(xs)]
 
 
+def par_scatter_i32(dst, is_, vs, nthreads=0, out=None):
+    """scatter with the reference's checks (ixo_par_scatter_i32, OpenMP)."""
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    is_ = _i64(is_)
+    vs = np.ascontiguousarray(vs, dtype=np.int32)
+    out = np.empty(max(len(dst), 1), dtype=np.int32) if out is None else out
+    m = min(len(is_), len(vs))
+    _ok(lib().ixo_par_scatter_i32(_p(dst), ctypes.c_int64(len(dst)), _p(is_), _p(vs), ctypes.c_int64(m), _p(out),
+                                  int(nthreads)))
+    return out[: len(dst)]
+
+
+def par_csrg_i32(x, vals, idx, nthreads=0, out=None):
+    """map2 (\\v c -> v * x[c]) with its bounds check (ixo_par_csrg_i32, OpenMP)."""
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.int32)
+    idx = _i64(idx)
+    out = np.empty(max(len(vals), 1), dtype=np.int32) if out is None else out
+    bad = ctypes.c_int64(0)
+    rc = lib().ixo_par_csrg_i32(_p(x), ctypes.c_int64(len(x)), _p(vals), _p(idx), ctypes.c_int64(len(vals)), _p(out),
+                                ctypes.byref(bad), int(nthreads))
+    if rc:
+        raise OracleFail(rc, 0, bad.value)
+    return out[: len(vals)]
+
+
 def partition2l(shp, cs, xs):
     """corpus/partition2l.ixl (ixo_partition2l)."""
     shp, cs, xs = _i64(shp), _i64(cs), _i64(xs)

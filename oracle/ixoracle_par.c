@@ -136,3 +136,67 @@ int ixo_par_c2_i32(const ixo_pred* p, const int32_t* xs, int64_t n, const int64_
   free(cnt); free(tail); free(hasf); free(carry); free(scn); free(bits);
   return ovf ? IXO_OVERFLOW : IXO_OK;
 }
+
+/* scatter dst is vs (oracle.py:294-305) on int32 values with int64 indices,
+ * with the reference's dynamic checks: out = copy of dst, out-of-range
+ * indices skipped, and NonIdempotentScatter (IXO_CONFLICT) iff one in-range
+ * index receives two DIFFERENT values (equal-valued duplicates are legal,
+ * oracle.py:301).  Parallel form: every in-range destination is claimed in a
+ * bitmap with an atomic OR; only if some destination was claimed twice does a
+ * second pass compare each pair's value with the value that landed. */
+int ixo_par_scatter_i32(const int32_t* dst, int64_t ndst, const int64_t* is, const int32_t* vs, int64_t m,
+                        int32_t* out, int threads) {
+  if (threads <= 0) threads = omp_get_max_threads();
+  omp_set_dynamic(0);
+  uint64_t* claim = (uint64_t*)calloc((size_t)(ndst / 64 + 1), sizeof(uint64_t));
+  if (!claim) return IXO_NOMEM;
+  int dup = 0, conflict = 0;
+#pragma omp parallel num_threads(threads) reduction(| : dup, conflict)
+  {
+    int t = omp_get_thread_num(), T = omp_get_num_threads();
+    int64_t lo, hi;
+    chunk(ndst, t, T, &lo, &hi);
+    if (out != dst) memcpy(out + lo, dst + lo, (size_t)(hi - lo) * sizeof(int32_t));
+#pragma omp barrier
+    chunk(m, t, T, &lo, &hi);
+    for (int64_t k = lo; k < hi; ++k) {
+      const int64_t i = is[k];
+      if (0 <= i && i < ndst) {
+        const uint64_t bit = 1ULL << (i & 63);
+        if (__atomic_fetch_or(&claim[i >> 6], bit, __ATOMIC_RELAXED) & bit) dup = 1;
+        out[i] = vs[k];
+      }
+    }
+  }
+  if (dup) {
+#pragma omp parallel for num_threads(threads) reduction(| : conflict)
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t i = is[k];
+      if (0 <= i && i < ndst && out[i] != vs[k]) conflict = 1;
+    }
+  }
+  free(claim);
+  return conflict ? IXO_CONFLICT : IXO_OK;
+}
+
+/* CSR flat gather map2 (\v c -> v * x[c]) values indices (corpus
+ * c4_csr_gather.ixl) on int32 values, with the reference's bounds check on
+ * x[c] (oracle.py:177-184): IXO_OOB and *first_bad = the first failing index
+ * in sequential order. */
+int ixo_par_csrg_i32(const int32_t* x, int64_t ncols, const int32_t* vals, const int64_t* idx, int64_t nnz,
+                     int32_t* out, int64_t* first_bad, int threads) {
+  if (threads <= 0) threads = omp_get_max_threads();
+  omp_set_dynamic(0);
+  int64_t bad = nnz;
+#pragma omp parallel for num_threads(threads) schedule(static) reduction(min : bad)
+  for (int64_t i = 0; i < nnz; ++i) {
+    const int64_t c = idx[i];
+    if ((uint64_t)c >= (uint64_t)ncols) {
+      if (i < bad) bad = i;
+      continue;
+    }
+    out[i] = (int32_t)((int64_t)vals[i] * (int64_t)x[c]);
+  }
+  if (first_bad) *first_bad = bad;
+  return bad < nnz ? IXO_OOB : IXO_OK;
+}

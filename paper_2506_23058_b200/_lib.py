@@ -70,7 +70,8 @@ SIGNATURES = {
     "ixg_reduce_add": (_I, [_I, _P, _I64, _P, _P]),
     "ixg_jagged_dest": (_I, [_P, _I64, _P, _P, _P, _P]),
     "ixg_partition_counts": (_I, [_I, _P, _I64, _P, _P, _I, _P, _P, _SZ, _P]),
-    "ixg_partition2_peer": (_I, [_I, _P, _I64, _P, _P, _I, _I64, _I64, _I64, _I64, _P, _SZ, _P]),
+    "ixg_partition2_peer": (_I, [_I, _P, _I64, _P, _P, _I, _I64, _P, _I, _P, _SZ, _P]),
+    "ixg_rank_offsets": (_I, [_P, _I, _I, _I, _P, _P]),
     "ixg_dev_alloc": (_I, [_SZ, _P]),
     "ixg_dev_free": (_I, [_P]),
     "ixg_ipc_handle": (_I, [_P, _P]),
@@ -99,9 +100,9 @@ SIGNATURES = {
     "ixg_mkflags": (_I, [_I64, _P, _I64, _P, _U32, _P, _P, _SZ, _P]),
     "ixg_map": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _I64, _I, _P, _P]),
     "ixg_bitmap_words": (_I64, [_I64]),
-    "ixg_flag_bitmap": (_I, [_P, _I64, _P, _I64, _P, _SZ, _P]),
-    "ixg_segsum": (_I, [_I, _P, _I64, _P, _P, _I64, _I, _P, _I64, _I, _P, _P, _P, _SZ, _P]),
-    "ixg_seg_carry": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _P, _P, _P]),
+    "ixg_flag_bitmap": (_I, [_P, _I64, _P, _I64, _P, _P, _SZ, _P]),
+    "ixg_segsum": (_I, [_I, _P, _I64, _P, _P, _I64, _P, _I, _P, _I64, _I, _P, _P, _P, _SZ, _P]),
+    "ixg_seg_carry": (_I, [_P, _I64, _P, _I, _P, _I64, _P, _I64, _P, _I, _P, _P, _P]),
     "ixg_timer_start": (_I, [_I]),
     "ixg_trace_read": (_I, [_P, _SZ]),
     "ixg_timer_stop": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),

@@ -215,15 +215,15 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
 // zs = sgmSum over the first *d_n elements of vs (capacity n)
 template <typename T, typename Z, class M = SegOp>
 int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32_t* bits, long long flag_base, Z* zs,
-                    LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s) {
+                    LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s,
+                    const long long* d_flag_base = nullptr) {
   auto kern = k_segsum_b<T, Z, M>;
   using B = Big<T, kSegsumCH<T, Z>>;
   static std::atomic<unsigned long long> attr{0};
   allow_smem(kern, B::SMEM, attr);
   TimedLaunch tl(IXG_K_SEGSUM, s);
-  kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, zs, ch,
-                                                                           next_nonce(), carry_v, carry_f, d_total,
-                                                                           st);
+  kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, d_flag_base, zs, ch,
+                                                                  next_nonce(), carry_v, carry_f, d_total, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -328,7 +328,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     if (!aligned16(xs) || !aligned16(ys) || !aligned16(zs)) return IXG_BADARG;
     cudaMemsetAsync(bits, 0, bitmap_bytes(n), s);
     LAUNCHED();
-    int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr}, cs, s);
+    int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr, nullptr}, cs, s);
     if (rc) return rc;
     if constexpr (sizeof(Z) == sizeof(T)) {
       if (!seg_split_mode()) {
@@ -353,7 +353,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
   long long* flags = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s);
   if (n <= 0) return IXG_OK;
-  if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr}, cs, s)))
+  if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr, nullptr}, cs, s)))
     return rc;
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
   if ((rc = launch_fill<long long>(flags, 0, d_k, 0LL, s))) return rc;
@@ -686,9 +686,10 @@ int ixg_partition_counts(int dt, const void* xs, int64_t n, const ixg_pred* p, c
 }
 
 int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, void* const* dst, int ranks,
-                        int64_t shard, int64_t true_base, int64_t false_base, int64_t local_true, void* ws,
-                        size_t ws_bytes, void* stream) {
-  if (n < 0 || !p || !dst || ranks < 1 || ranks > 8 || shard <= 0 || (n > 0 && !xs)) return IXG_BADARG;
+                        int64_t shard, const int64_t* d_counts, int rank, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !p || !dst || !d_counts || ranks < 1 || ranks > 8 || rank < 0 || rank >= ranks || shard <= 0 ||
+      n != shard || (n > 0 && !xs))
+    return IXG_BADARG;
   const int ep = dt == IXG_I32 ? 4 : 2;
   if (shard % ep) return IXG_BADARG;  // a 16-byte chunk never straddles two shards
   if (ws_bytes < ixg_ws_bytes(IXG_OP_PARTITION2, n, 0)) return IXG_BADARG;
@@ -705,11 +706,10 @@ int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, vo
     PeerOut<int32_t> po{};
     for (int r = 0; r < ranks; ++r) po.dst[r] = (int32_t*)dst[r];
     po.shard = shard;
-    po.seg_base[0] = true_base;
-    po.seg_base[1] = false_base;
-    po.seg_local[0] = 0;
-    po.seg_local[1] = local_true;
     po.ranks = ranks;
+    po.d_counts = (const long long*)d_counts;
+    po.rank = rank;
+    po.in_shard = n;
     return launch_filter_b<int32_t, false, false, int32_t, 2, true>((const int32_t*)xs, nullptr, n, pp, nullptr, c0,
                                                                     scratch, s, nullptr, nullptr, 0,
                                                                     LBChan{nullptr, nullptr}, nullptr, ixg_pred{},
@@ -718,11 +718,10 @@ int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, vo
   PeerOut<long long> po{};
   for (int r = 0; r < ranks; ++r) po.dst[r] = (long long*)dst[r];
   po.shard = shard;
-  po.seg_base[0] = true_base;
-  po.seg_base[1] = false_base;
-  po.seg_local[0] = 0;
-  po.seg_local[1] = local_true;
   po.ranks = ranks;
+  po.d_counts = (const long long*)d_counts;
+  po.rank = rank;
+  po.in_shard = n;
   return launch_filter_b<long long, false, false, long long, 2, true>((const long long*)xs, nullptr, n, pp, nullptr,
                                                                       c0, scratch, s, nullptr, nullptr, 0,
                                                                       LBChan{nullptr, nullptr}, nullptr, ixg_pred{},
@@ -804,7 +803,7 @@ int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t n
   if (m == 0) return cuda_rc(cudaMemsetAsync(d_len, 0, 8, s));
   // scn / ind / len (mksgmdescr.ixl:6-9); len = scn[m-1] + shape[m-1] = sum shape
   int rc = launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
-                              EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, (long long*)d_len}, c, s);
+                              EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr, (long long*)d_len}, c, s);
   if (rc || cap == 0) return rc;
   // the scatter is never proved for mkSgmDescr: the host
   // passes cap >= len (read back from d_len), res[0..len) = 0, checked scatter.
@@ -949,31 +948,47 @@ int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint
   if (k > 0 && (rc = launch_fill<long long>((long long*)flags, k, nullptr, 0LL, s))) return rc;
   if (m == 0) return IXG_OK;
   if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
-                               EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr}, c, s)))
+                               EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr, nullptr}, c, s)))
     return rc;
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
   return launch_scatter<long long>((long long*)flags, k, nullptr, k, ind, ones, m,
                                    IXG_SITE_BITS(variant, 1) | IXG_V_INIT, 1, 1, st, w, 1, s);
 }
 
+int ixg_rank_offsets(const int64_t* d_counts, int ranks, int rank, int stride, int64_t* out2, void* stream) {
+  if (!d_counts || !out2 || ranks < 1 || rank < 0 || rank >= ranks || stride < 1) return IXG_BADARG;
+  k_rank_offsets<<<1, 32, 0, S(stream)>>>((const long long*)d_counts, ranks, rank, stride, (long long*)out2);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
+}
+
 int64_t ixg_bitmap_words(int64_t nbits) { return (int64_t)(bitmap_bytes(nbits) / 4); }
 
-int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, void* ws, size_t ws_bytes,
-                    void* stream) {
+int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, const int64_t* d_nbits, void* ws,
+                    size_t ws_bytes, void* stream) {
   if (m < 0 || nbits < 0 || (m > 0 && !shape) || !bits) return IXG_BADARG;
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, m, 0)) return IXG_BADARG;
   cudaStream_t s = S(stream);
   WS w(ws);
   LBChan c = w.chan(0, tiles_of(m, kGTile));
-  cudaMemsetAsync(bits, 0, bitmap_bytes(nbits), s);
-  LAUNCHED();
+  if (d_nbits) {  // nbits on the device (<= the capacity nbits): clear just those words
+    k_bitmap_clear<<<grid_for((nbits + 31) / 32 + 514), kGThreads, 0, s>>>(bits, (const long long*)d_nbits);
+    LAUNCHED();
+    CHECK_LAUNCH();
+  } else {
+    cudaMemsetAsync(bits, 0, bitmap_bytes(nbits), s);
+    LAUNCHED();
+  }
   return launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
-                            EpiSegStarts{m, (const long long*)shape, nullptr, bits, nbits, nullptr}, c, s);
+                            EpiSegStarts{m, (const long long*)shape, nullptr, bits, nbits,
+                                         (const long long*)d_nbits, nullptr},
+                            c, s);
 }
 
 int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,
-               int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total, ixg_status* st, void* ws,
-               size_t ws_bytes, void* stream) {
+               const int64_t* d_flag_base, int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total,
+               ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
   if (n < 0 || (n > 0 && (!vs || !zs || !bits))) return IXG_BADARG;
   if (ws_bytes < ixg_ws_bytes(IXG_OP_SEGSCAN, n, 0)) return IXG_BADARG;
   if (n == 0) return IXG_OK;
@@ -982,34 +997,39 @@ int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint
   LBChan c = w.chan(0, tiles_of(n, kGTile));
   cudaStream_t s = S(stream);
   const long long* dn = (const long long*)d_n;
+  const long long* dfb = (const long long*)d_flag_base;
   longlong2* tot = (longlong2*)d_total;
   if (dt == IXG_I32 && dt_z == IXG_I32)
     return launch_segsum_b<int32_t, int32_t>((const int32_t*)vs, n, dn, bits, flag_base, (int32_t*)zs, c, carry_v,
-                                             carry_f, tot, st, s);
+                                             carry_f, tot, st, s, dfb);
   if (dt == IXG_I32)
     return launch_segsum_b<int32_t, long long>((const int32_t*)vs, n, dn, bits, flag_base, (long long*)zs, c,
-                                               carry_v, carry_f, tot, st, s);
+                                               carry_v, carry_f, tot, st, s, dfb);
   if (dt_z == IXG_I32) return IXG_BADARG;
   return launch_segsum_b<long long, long long>((const long long*)vs, n, dn, bits, flag_base, (long long*)zs, c,
-                                               carry_v, carry_f, tot, st, s);
+                                               carry_v, carry_f, tot, st, s, dfb);
 }
 
-int ixg_seg_carry(const uint32_t* bits, int64_t flag_base, int dt_z, void* zs, int64_t n, const int64_t* d_n,
-                  int64_t carry_v, void* scratch8, ixg_status* st, void* stream) {
-  if (n < 0 || !bits || !scratch8 || (n > 0 && !zs)) return IXG_BADARG;
-  if (n == 0 || carry_v == 0) return IXG_OK;
+int ixg_seg_carry(const uint32_t* bits, int64_t flag_base, const int64_t* d_flag_base, int dt_z, void* zs, int64_t n,
+                  const int64_t* d_n, int64_t carry_v, const int64_t* d_aggs, int rank, void* scratch8, ixg_status* st,
+                  void* stream) {
+  if (n < 0 || !bits || !scratch8 || (n > 0 && !zs) || (d_aggs && rank < 0)) return IXG_BADARG;
+  if (n == 0 || (!d_aggs && carry_v == 0)) return IXG_OK;
   cudaStream_t s = S(stream);
   unsigned long long* first = (unsigned long long*)scratch8;
   cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), s);
   LAUNCHED();
-  k_first_flag<<<grid_for(n / 32 + 1), 256, 0, s>>>(bits, flag_base, n, (const long long*)d_n, first);
+  k_first_flag<<<grid_for(n / 32 + 1), 256, 0, s>>>(bits, flag_base, (const long long*)d_flag_base, n,
+                                                     (const long long*)d_n, first);
   LAUNCHED();
   CHECK_LAUNCH();
+  const long long* ag = (const long long*)d_aggs;
   if (dt_z == IXG_I32)
-    k_add_prefix<int32_t><<<grid_for(n), 256, 0, s>>>((int32_t*)zs, first, n, (const long long*)d_n, carry_v, st);
+    k_add_prefix<int32_t><<<grid_for(n), 256, 0, s>>>((int32_t*)zs, first, n, (const long long*)d_n, carry_v, ag,
+                                                       rank, st);
   else
-    k_add_prefix<long long><<<grid_for(n), 256, 0, s>>>((long long*)zs, first, n, (const long long*)d_n, carry_v,
-                                                        st);
+    k_add_prefix<long long><<<grid_for(n), 256, 0, s>>>((long long*)zs, first, n, (const long long*)d_n, carry_v, ag,
+                                                         rank, st);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;

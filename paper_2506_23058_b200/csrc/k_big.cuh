@@ -362,7 +362,28 @@ struct PeerOut {
   long long seg_base[3];
   long long seg_local[3];
   int ranks;
+  // device-resident bases (no host round trip): every rank's true count,
+  // all-gathered on the device; this rank's index; the input shard size
+  const long long* d_counts;
+  int rank;
+  long long in_shard;
 };
+
+// global start of local chain position `base` of class segment `seg`:
+// trues of rank r follow the trues of ranks < r, its falses follow every
+// true and the falses of ranks < r
+template <typename T>
+IXG_DEV long long peer_gbase(const PeerOut<T>& po, int seg, long long base) {
+  if (!po.d_counts) return po.seg_base[seg] + (base - po.seg_local[seg]);
+  long long tb = 0, nt = 0;
+  for (int r = 0; r < po.ranks; ++r) {
+    const long long c = po.d_counts[r];
+    nt += c;
+    tb += r < po.rank ? c : 0;
+  }
+  if (seg == 0) return tb + base;
+  return nt + ((long long)po.rank * po.in_shard - tb) + (base - po.d_counts[po.rank]);
+}
 
 // store_run to the global positions [gbase, gbase + cnt) of a sharded
 // output: every 16-byte chunk lies in one shard (shard % EP == 0) and goes
@@ -787,7 +808,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   const bool bulk = kBulk && ((((uintptr_t)ys) | (kSeg ? (uintptr_t)zs : (uintptr_t)0)) & 15) == 0;  // 16-byte aligned outputs
   T* run = buf;
   if constexpr (kPeer) {
-    store_run_peer<T, kBT>(po, po.seg_base[seg] + (base - po.seg_local[seg]), cnt, buf);
+    store_run_peer<T, kBT>(po, peer_gbase(po, seg, base), cnt, buf);
   } else if (bulk) {
     const int sh0 = (int)(base & (B::EP - 1));
     if (sh0) {
@@ -952,6 +973,7 @@ template <typename T, typename Z, class M = SegOp>
 __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T* __restrict__ vs, long long n,
                                                           const long long* __restrict__ d_n,
                                                           const uint32_t* __restrict__ bits, long long flag_base,
+                                                          const long long* __restrict__ d_flag_base,
                                                           Z* __restrict__ zs, LBChan ch, uint32_t nonce,
                                                           long long carry_v, int carry_f, longlong2* d_total,
                                                           ixg_status* st) {
@@ -964,6 +986,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   __shared__ __align__(8) uint64_t s_mbar[B::CH];
 
   if (d_n) n = *d_n;  // length known only on the device (C2: k = filter's count)
+  if (d_flag_base) flag_base = *d_flag_base;  // sharded C2: this rank's first global output position
   const long long ntiles = (n + B::TILE - 1) / B::TILE;
   const long long tile = blockIdx.x;
   if (tile >= ntiles) return;  // capacity grid: tiles past the data do nothing
@@ -1121,9 +1144,10 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
 // Shard carry (multi-GPU C2): the first flag at or after `flag_base` within
 // [flag_base, flag_base + n), then zs[0 .. first) += carry.
 __global__ void __launch_bounds__(256) k_first_flag(const uint32_t* __restrict__ bits, long long flag_base,
-                                                    long long n, const long long* __restrict__ d_n,
-                                                    unsigned long long* first) {
+                                                    const long long* __restrict__ d_flag_base, long long n,
+                                                    const long long* __restrict__ d_n, unsigned long long* first) {
   if (d_n) n = *d_n;
+  if (d_flag_base) flag_base = *d_flag_base;
   const long long nw = (n + 31) / 32 + 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nw; k += stride) {
@@ -1137,11 +1161,22 @@ __global__ void __launch_bounds__(256) k_first_flag(const uint32_t* __restrict__
   }
 }
 
+// carry into `rank` from every rank's segmented aggregate (v, f) (an
+// all-gathered device array [ranks][2]): the segmented combine of those of
+// ranks < rank
+IXG_DEV long long seg_carry_from(const long long* __restrict__ aggs, int rank) {
+  long long v = 0;
+  for (int r = 0; r < rank; ++r) v = aggs[2 * r + 1] ? aggs[2 * r] : (long long)((unsigned long long)v + (unsigned long long)aggs[2 * r]);
+  return v;
+}
+
 template <typename Z>
 __global__ void __launch_bounds__(256) k_add_prefix(Z* __restrict__ zs, const unsigned long long* __restrict__ first,
                                                     long long n, const long long* __restrict__ d_n, long long c,
-                                                    ixg_status* st) {
+                                                    const long long* __restrict__ d_aggs, int rank, ixg_status* st) {
   if (d_n) n = *d_n;
+  if (d_aggs) c = seg_carry_from(d_aggs, rank);
+  if (c == 0) return;
   long long stop = (long long)*first;
   if (stop > n) stop = n;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1152,6 +1187,22 @@ __global__ void __launch_bounds__(256) k_add_prefix(Z* __restrict__ zs, const un
     zs[q] = (Z)v;
   }
   if (narrow && st) atomicOr(&st->flags, IXG_F_NARROW);
+}
+
+// out2 = [sum of counts[r * stride] over r < rank, over all r] (a rank's
+// exclusive offset and the global total from an all-gathered device array)
+__global__ void k_rank_offsets(const long long* __restrict__ counts, int ranks, int rank, int stride,
+                               long long* __restrict__ out2) {
+  if (threadIdx.x == 0) {
+    long long before = 0, total = 0;
+    for (int r = 0; r < ranks; ++r) {
+      const long long c = counts[(long long)r * stride];
+      total += c;
+      before += r < rank ? c : 0;
+    }
+    out2[0] = before;
+    out2[1] = total;
+  }
 }
 
 // partition3's single pass leaves the prefix at the end of segment 1 (m1 + m2)

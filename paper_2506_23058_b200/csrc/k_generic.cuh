@@ -283,14 +283,16 @@ struct EpiSegStarts {  // mkSgmDescr / mkFlags: ind[i] = if shape[i] <= 0 then -
   long long* ind;        // nullable
   uint32_t* bits;        // nullable: set bit scn[i] (flag array as a bitmap)
   long long nbits;
+  const long long* d_nbits;  // nullable: nbits on the device
   long long* d_total;    // nullable: scn[m-1] + shape[m-1]
   IXG_DEV void operator()(long long i0, long long n, const Run16<SumOp::T>& r) const {
+    const long long nb = d_nbits ? *d_nbits : nbits;
     long long o[kGItems];
 #pragma unroll
     for (int q = 0; q < kGItems; ++q) {
       const long long s = r.x(q).v, start = r.incl[q].v - s;
       o[q] = s <= 0 ? -1 : start;
-      if (bits && i0 + q < n && s > 0 && start >= 0 && start < nbits)
+      if (bits && i0 + q < n && s > 0 && start >= 0 && start < nb)
         atomicOr(&bits[start >> 5], 1u << (start & 31));
     }
     if (ind) store16_i64(ind, i0, n, o);
@@ -628,6 +630,14 @@ __global__ void __launch_bounds__(kGThreads) k_hist_check(const long long* __res
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x; d < dlen; d += stride)
     if (hi[d] != (out[d] >> 63)) status_overflow(st, 0, d);
+}
+
+// the words of a flag bitmap over *d_nbits positions (+ the readers' slack)
+__global__ void __launch_bounds__(kGThreads) k_bitmap_clear(uint32_t* __restrict__ bits,
+                                                             const long long* __restrict__ d_nbits) {
+  const long long words = (*d_nbits + 31) / 32 + 2 + 512;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) bits[w] = 0u;
 }
 
 // ---------------------------------------------------------------- fill / iota

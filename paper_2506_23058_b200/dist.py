@@ -96,6 +96,40 @@ def all_gather_ints(values: Sequence[int], group=None) -> List[List[int]]:
     return [o.cpu().tolist() for o in out]
 
 
+def all_gather_dev(t, out, group=None):
+    """Device-resident all-gather of a few int64 per rank: rank r's `t` lands
+    in out[r * len(t) : (r + 1) * len(t)].  Written as a SUM all-reduce of a
+    zero-padded buffer, which NCCL runs stream-ordered (no host round trip)
+    and gloo also supports on CUDA tensors (the 1-GPU functional tests)."""
+    import torch.distributed as dist
+
+    rank, k = dist.get_rank(group), t.numel()
+    if out.is_cuda and dist.get_backend(group) != "nccl":  # gloo: through the host (functional runs only)
+        host = out.new_zeros(out.shape, device="cpu")
+        host[rank * k:(rank + 1) * k].copy_(t.reshape(-1))
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(host)
+        return out
+    out.zero_()
+    out[rank * k:(rank + 1) * k].copy_(t.reshape(-1))
+    dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def device_barrier(flag, group=None):
+    """Stream-ordered barrier: when this completes on the stream, every
+    rank's earlier work on its own stream has completed (each rank's
+    contribution is issued after that work)."""
+    import torch
+    import torch.distributed as dist
+
+    if flag.is_cuda and dist.get_backend(group) != "nccl":  # gloo: host barrier (functional runs only)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+        return
+    dist.all_reduce(flag, op=dist.ReduceOp.SUM, group=group)
+
+
 # ----------------------------------------------------------------- drivers
 def c2_sharded(local, group=None):
     """Sharded C2.  `local` provides: filter() -> k; flag_bitmap(K_total);
@@ -339,25 +373,27 @@ class GpuPart2PeerLocal:
                 self.opened.append(ptr)
                 self.ptrs.append(ptr)
         self.d_tot = torch.empty(1, dtype=torch.int64, device=xs.device)
+        self.d_counts = torch.empty(self.world, dtype=torch.int64, device=xs.device)
+        self.d_off = torch.empty(2, dtype=torch.int64, device=xs.device)
+        self.flag = torch.zeros(1, dtype=torch.int64, device=xs.device)
 
     @property
     def out(self):
         """this rank's contiguous slice of the global result"""
         return self.buf.tensor
 
-    def step(self) -> int:
-        import torch
-        import torch.distributed as dist
-
-        t = int(self.ops.partition_counts(self.xs, self.pred, d_tot=self.d_tot).item())
-        ts = [r[0] for r in all_gather_ints([t], self.group)]
-        nt = sum(ts)
-        tb = exclusive_offsets(ts)[self.rank]
-        fb = exclusive_offsets([n - x for n, x in zip(self.sizes, ts)])[self.rank]
-        self.ops.partition2_peer(self.xs, self.pred, self.ptrs, self.shard, tb, nt + fb, t)
-        torch.cuda.synchronize()  # this rank's peer stores are done ...
-        dist.barrier(group=self.group)  # ... and so are everyone else's into our shard
-        return nt
+    def step(self):
+        """One sharded partition2, entirely stream-ordered: count pass ->
+        device all-gather of the counts -> the peer-storing partition kernel
+        (bases derived on the device) -> device barrier (every rank's peer
+        stores into this rank's shard have landed).  Returns the device pair
+        [T_<rank, NT] (read it only when needed)."""
+        self.ops.partition_counts(self.xs, self.pred, d_tot=self.d_tot)
+        all_gather_dev(self.d_tot, self.d_counts, self.group)
+        self.ops.partition2_peer(self.xs, self.pred, self.ptrs, self.shard, self.d_counts, self.rank)
+        self.ops.rank_offsets(self.d_counts, self.world, self.rank, out=self.d_off)
+        device_barrier(self.flag, self.group)
+        return self.d_off
 
     def close(self):
         for ptr in self.opened:
@@ -387,6 +423,37 @@ class GpuC2Local:
         self.st = ops.Status(self.dev)
         self.k = 0
         self.bits = None
+        self.d_ks = self.d_off = self.d_aggs = None
+
+    def step_device(self, group=None):
+        """The whole sharded C2 step with every count, offset and carry kept
+        on the device (no host round trip): filter -> all-gather of the
+        counts -> [K_r, K_total] -> mkFlags bitmap over the K_total global
+        outputs -> sgmSum of this rank's outputs from flag K_r -> all-gather
+        of the segmented aggregates -> the carry of the ranks before, added
+        before the first flag.  Outputs: ys / zs [0, *dk), global offset
+        d_off[0]."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib as L
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        n = self.xs.numel()
+        if self.d_ks is None:
+            self.d_ks = torch.empty(world, dtype=torch.int64, device=self.dev)
+            self.d_off = torch.empty(2, dtype=torch.int64, device=self.dev)
+            self.d_aggs = torch.empty(2 * world, dtype=torch.int64, device=self.dev)
+            self.cap = n * world  # every global output position (K_total <= cap)
+        self.ops.filter(self.xs, self.pred, L.VARIANT_ELIDED, self.st, ys=self.ys, d_count=self.dk)
+        all_gather_dev(self.dk, self.d_ks, group)
+        self.ops.rank_offsets(self.d_ks, world, rank, out=self.d_off)
+        self.bits = self.ops.flag_bitmap(self.shape, self.cap, d_nbits=self.d_off[1:], bits=self.bits)
+        self.ops.segsum(self.ys, n, self.bits, 0, self.zs, 0, False, self.tot, self.st, d_n=self.dk,
+                        d_flag_base=self.d_off)
+        all_gather_dev(self.tot, self.d_aggs, group)
+        self.ops.seg_carry(self.bits, 0, self.zs, n, 0, self.scratch, self.st, d_n=self.dk, d_flag_base=self.d_off,
+                           d_aggs=self.d_aggs, rank=rank)
 
     def filter(self) -> int:
         from . import _lib as L

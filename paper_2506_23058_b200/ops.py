@@ -316,17 +316,25 @@ def partition_counts(xs: torch.Tensor, p: Pred, q: Optional[Pred] = None, d_tot=
     return d_tot
 
 
-def partition2_peer(xs: torch.Tensor, p: Pred, dst_ptrs, shard: int, true_base: int, false_base: int,
-                    local_true: int) -> None:
+def partition2_peer(xs: torch.Tensor, p: Pred, dst_ptrs, shard: int, d_counts: torch.Tensor, rank: int) -> None:
     """this rank's partition2 runs stored straight into the sharded global
-    output (dst_ptrs[r] = rank r's shard, peer-mapped; see ixg_partition2_peer)."""
+    output (dst_ptrs[r] = rank r's shard, peer-mapped; d_counts = every
+    rank's true count on the device; see ixg_partition2_peer)."""
     xs = _contig(xs)
     n = xs.numel()
     ws, wsb = _ws(L.OP_PARTITION2, n, 0, xs.device)
     cp = _c_pred(p)
     arr = (ctypes.c_void_p * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
-    L.check(_lib().ixg_partition2_peer(_dt(xs), _ptr(xs), n, ctypes.byref(cp), arr, len(dst_ptrs), shard, true_base,
-                                       false_base, local_true, ws, wsb, _stream()), "partition2_peer")
+    L.check(_lib().ixg_partition2_peer(_dt(xs), _ptr(xs), n, ctypes.byref(cp), arr, len(dst_ptrs), shard,
+                                       _ptr(d_counts), rank, ws, wsb, _stream()), "partition2_peer")
+
+
+def rank_offsets(d_counts: torch.Tensor, ranks: int, rank: int, stride: int = 1, out=None) -> torch.Tensor:
+    """[this rank's exclusive offset, the total] of an all-gathered device
+    count array (ixg_rank_offsets)."""
+    out = torch.empty(2, dtype=torch.int64, device=d_counts.device) if out is None else out
+    L.check(_lib().ixg_rank_offsets(_ptr(d_counts), ranks, rank, stride, _ptr(out), _stream()), "rank_offsets")
+    return out
 
 
 class DeviceBuffer:
@@ -432,34 +440,40 @@ def mkflags(k: int, shape: torch.Tensor, variant: int, status: Status) -> torch.
     return out
 
 
-def flag_bitmap(shape: torch.Tensor, nbits: int) -> torch.Tensor:
-    """mkFlags over nbits output positions as a bitmap (int32 words)."""
+def flag_bitmap(shape: torch.Tensor, nbits: int, d_nbits=None, bits=None) -> torch.Tensor:
+    """mkFlags over nbits output positions as a bitmap (int32 words); with
+    d_nbits, over the device count (nbits is then the capacity)."""
     shape = _contig(shape.to(torch.int64))
     words = int(_lib().ixg_bitmap_words(nbits))
-    bits = torch.empty(words, dtype=torch.int32, device=shape.device)
+    if bits is None or bits.numel() < words:
+        bits = torch.empty(words, dtype=torch.int32, device=shape.device)
     ws, wsb = _ws(L.OP_SCAN, shape.numel(), 0, shape.device)
-    L.check(_lib().ixg_flag_bitmap(_ptr(shape), shape.numel(), _ptr(bits), nbits, ws, wsb, _stream()), "flag_bitmap")
+    L.check(_lib().ixg_flag_bitmap(_ptr(shape), shape.numel(), _ptr(bits), nbits, _ptr(d_nbits), ws, wsb, _stream()),
+            "flag_bitmap")
     return bits
 
 
 def segsum(vs: torch.Tensor, n: int, bits: torch.Tensor, flag_base: int, zs: torch.Tensor, carry_v: int,
-           carry_f: bool, d_total: torch.Tensor, status: Status):
-    """zs[0..n) = sgmSum over vs with flags bits[flag_base + j] (ixg_segsum)."""
+           carry_f: bool, d_total: torch.Tensor, status: Status, d_n=None, d_flag_base=None):
+    """zs[0..n) = sgmSum over vs with flags bits[flag_base + j] (ixg_segsum);
+    d_n / d_flag_base: the same read from the device (n is then a capacity)."""
     ws, wsb = _ws(L.OP_SEGSCAN, vs.numel(), 0, vs.device)
     L.check(
-        _lib().ixg_segsum(_dt(vs), _ptr(vs), n, _ptr(None), _ptr(bits), flag_base, _dt(zs), _ptr(zs), carry_v,
-                          int(carry_f), _ptr(d_total), status.ptr, ws, wsb, _stream()),
+        _lib().ixg_segsum(_dt(vs), _ptr(vs), n, _ptr(d_n), _ptr(bits), flag_base, _ptr(d_flag_base), _dt(zs), _ptr(zs),
+                          carry_v, int(carry_f), _ptr(d_total), status.ptr, ws, wsb, _stream()),
         "segsum",
     )
     return zs
 
 
 def seg_carry(bits: torch.Tensor, flag_base: int, zs: torch.Tensor, n: int, carry_v: int, scratch: torch.Tensor,
-              status: Status):
-    """zs[q] += carry_v for q before the first flag of [flag_base, flag_base + n)."""
+              status: Status, d_n=None, d_flag_base=None, d_aggs=None, rank: int = 0):
+    """zs[q] += carry for q before the first flag of [flag_base, flag_base + n);
+    carry = carry_v, or folded on the device from d_aggs (every rank's
+    segmented aggregate) for `rank`."""
     L.check(
-        _lib().ixg_seg_carry(_ptr(bits), flag_base, _dt(zs), _ptr(zs), n, _ptr(None), carry_v, _ptr(scratch),
-                             status.ptr, _stream()),
+        _lib().ixg_seg_carry(_ptr(bits), flag_base, _ptr(d_flag_base), _dt(zs), _ptr(zs), n, _ptr(d_n), carry_v,
+                             _ptr(d_aggs), rank, _ptr(scratch), status.ptr, _stream()),
         "seg_carry",
     )
     return zs

@@ -143,10 +143,10 @@ def test_partition2_peer_kernel(cuda, G, per, dtype):
     shards = [torch.from_numpy(xs[r * per:(r + 1) * per].copy()).to(cuda) for r in range(G)]
     ts = [int(ops.partition_counts(x, p).item()) for x in shards]
     assert sum(ts) == want_nt
-    tb = D.exclusive_offsets(ts)
-    fb = D.exclusive_offsets([per - t for t in ts])
+    d_counts = torch.tensor(ts, dtype=torch.int64, device=cuda)  # what the device all-gather delivers
     for r in range(G):
-        ops.partition2_peer(shards[r], p, ptrs, per, tb[r], want_nt + fb[r], ts[r])
+        ops.partition2_peer(shards[r], p, ptrs, per, d_counts, r)
+        assert ops.rank_offsets(d_counts, G, r).tolist() == [sum(ts[:r]), want_nt]
     got = torch.cat(bufs).cpu().numpy().astype(np.int64)
     assert np.array_equal(got, want)
 
@@ -164,7 +164,7 @@ def _ipc_worker(rank, world, port, per, q):
         n = world * per
         xs = gen.uniform(99, n, -(1 << 31), (1 << 31) - 1, np.int32)
         loc = D.GpuPart2PeerLocal(torch.from_numpy(xs[rank * per:(rank + 1) * per].copy()).cuda(), Pred.lt(0))
-        nt = loc.step()
+        nt = int(loc.step()[1].item())
         want_nt, want = O.partition2(Pred.lt(0), xs)
         ok = nt == want_nt and np.array_equal(loc.out.cpu().numpy().astype(np.int64), want[rank * per:(rank + 1) * per])
         dist.barrier()
@@ -192,6 +192,62 @@ def test_partition2_peer_ipc_two_processes(cuda):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, 200_000, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(300)
+        assert pr.exitcode == 0
+    assert q.get() is True
+
+
+def _c2_worker(rank, world, port, per, m, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = world * per
+        xs = gen.uniform(7, n, -128, 127, np.int32)
+        k_total = int((xs >= 0).sum())
+        shape = gen.segment_shape(8, m, k_total)
+        loc = D.GpuC2Local(torch.from_numpy(xs[rank * per:(rank + 1) * per].copy()).cuda(), Pred.ge(0),
+                           torch.from_numpy(shape).cuda())
+        for _ in range(2):  # twice: the bitmap / workspaces are reused
+            loc.step_device()
+        k, off = int(loc.dk.item()), int(loc.d_off[0].item())
+        want_ys, want_zs = O.c2(Pred.ge(0), xs, shape)
+        ok = (np.array_equal(loc.ys[:k].cpu().numpy().astype(np.int64), want_ys[off:off + k])
+              and np.array_equal(loc.zs[:k].cpu().numpy().astype(np.int64), want_zs[off:off + k])
+              and int(loc.d_off[1].item()) == k_total and loc.st.read().ok)
+        oks = [None] * world
+        dist.all_gather_object(oks, bool(ok))
+        if rank == 0:
+            q.put(all(oks))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c2_step_device_processes(cuda, world):
+    """GpuC2Local.step_device -- the sharded C2 with every count, offset and
+    carry on the device -- in `world` processes sharing one GPU (gloo for the
+    tiny exchanges; NCCL on a multi-GPU box): each rank's slice equals the
+    single-process C2 at its global offset."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_c2_worker, args=(r, world, port, 150_001, 3000, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
