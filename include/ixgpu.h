@@ -128,6 +128,12 @@ typedef struct ixg_status {
 #define IXG_OP_MKSGMDESCR 8
 #define IXG_OP_MKFLAGS 9
 #define IXG_OP_HIST 10     /* m = dlen */
+#define IXG_OP_SCATTER_BINNED 11  /* n = pairs, m = ndst */
+
+/* scatter layouts (ixg_scatter) */
+#define IXG_SCATTER_DIRECT 0  /* pairs stored in their own order            */
+#define IXG_SCATTER_BINNED 1  /* pairs first partitioned by destination
+                                 window (32 MB windows, ndst <= 2^32)      */
 
 /* ---- library / device --------------------------------------------------- */
 int ixg_version(void);
@@ -175,10 +181,17 @@ int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64
  * destination is written).  m = min(nis, nvs) pairs (zip truncation).
  * Out-of-range indices are skipped in every variant (oracle.py:300).  With
  * IXG_V_CONFLICT the idempotence check runs: conflicting values at one
- * in-range index -> IXG_CONFLICT in `st` (stmt, site).  is: int64; vs/out: dt. */
+ * in-range index -> IXG_CONFLICT in `st` (stmt, site).  is: int64; vs/out: dt.
+ * layout: IXG_SCATTER_DIRECT or IXG_SCATTER_BINNED (ws sized with
+ * IXG_OP_SCATTER_BINNED); CHECKED claims are privatised per tile in shared
+ * memory windows, merged with one atomic per bitmap word. */
 int ixg_scatter(int dt, void* out, int64_t ndst, const int64_t* is, int64_t nis, const void* vs,
-                int64_t nvs, uint32_t site_bits, int stmt, int site, ixg_status* st, void* ws,
+                int64_t nvs, uint32_t site_bits, int stmt, int site, int layout, ixg_status* st, void* ws,
                 size_t ws_bytes, void* stream);
+/* Which layout suits an index array: *d_flag = 1 when sampled runs of `is`
+ * jump between 4096-destination windows at most elements (no locality:
+ * IXG_SCATTER_BINNED pays off), 0 otherwise.  The host reads the flag. */
+int ixg_scatter_probe(const int64_t* is, int64_t m, int* d_flag, void* stream);
 
 /* gather: out[i] = arr[idx[i]] (IndexE, oracle.py:177-184).  With
  * IXG_V_BOUNDS, out-of-range -> IXG_OOB at (stmt, elem i, site).  arr/out: dt. */
@@ -366,6 +379,7 @@ int ixg_map(const ixg_vm_insn* prog, int ninsn, const ixg_array* ins, int nins, 
 #define IXG_K_SCATTER 5      /* k_scatter                                  */
 #define IXG_K_CSR_GATHER 6   /* k_csr_gather                               */
 #define IXG_K_SEGSUM 7       /* k_segsum_b (C2 sgmSum pass)                */
+#define IXG_K_BIN 8          /* k_bin_partition (binned scatter, pass 1)   */
 int ixg_timer_start(int kernel_id);
 /* development builds (-DIXG_TRACE) only: per-CTA %globaltimer trace of the
  * compaction kernels; IXG_BADARG otherwise */

@@ -24,8 +24,9 @@ VARIANT_CHECKED = 0x77777777
 VARIANT_ELIDED = 0
 F_DUP, F_NARROW = 1, 2
 HIST_MIN, HIST_MAX, HIST_ADD = 0, 1, 2
-OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR, OP_MKFLAGS, OP_HIST = \
-    range(1, 11)
+(OP_SCAN, OP_SEGSCAN, OP_SCATTER, OP_FILTER, OP_PARTITION2, OP_PARTITION3, OP_C2, OP_MKSGMDESCR, OP_MKFLAGS, OP_HIST,
+ OP_SCATTER_BINNED) = range(1, 12)
+SCATTER_DIRECT, SCATTER_BINNED = 0, 1
 
 
 class ixg_pred(ctypes.Structure):
@@ -78,7 +79,8 @@ SIGNATURES = {
     "ixg_ipc_open": (_I, [_P, _P]),
     "ixg_ipc_close": (_I, [_P]),
     "ixg_segscan_add": (_I, [_I, _P, _I, _P, _I64, _I, _I64, _P, _P, _P, _SZ, _P, _P]),
-    "ixg_scatter": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _U32, _I, _I, _P, _P, _SZ, _P]),
+    "ixg_scatter": (_I, [_I, _P, _I64, _P, _I64, _P, _I64, _U32, _I, _I, _I, _P, _P, _SZ, _P]),
+    "ixg_scatter_probe": (_I, [_P, _I64, _P, _P]),
     "ixg_gather": (_I, [_I, _P, _I64, _P, _I64, _P, _U32, _I, _I, _P, _P]),
     "ixg_hist": (_I, [_I, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _SZ, _P, _P]),
     "ixg_fill": (_I, [_I, _P, _I64, _I64, _P]),
@@ -107,7 +109,7 @@ SIGNATURES = {
     "ixg_trace_read": (_I, [_P, _SZ]),
     "ixg_timer_stop": (_I, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
 }
-K_FILTER_FUSED, K_PLACE, K_CLASS_COUNT, K_SCAN, K_SCATTER, K_CSR_GATHER, K_SEGSUM = 1, 2, 3, 4, 5, 6, 7
+K_FILTER_FUSED, K_PLACE, K_CLASS_COUNT, K_SCAN, K_SCATTER, K_CSR_GATHER, K_SEGSUM, K_BIN = 1, 2, 3, 4, 5, 6, 7, 8
 
 _lib = None
 _lock = threading.Lock()

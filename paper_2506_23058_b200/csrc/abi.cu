@@ -16,6 +16,7 @@
 #include "k_big.cuh"
 #include "k_vm.cuh"
 #include "k_contract.cuh"
+#include "k_scatter.cuh"
 
 using namespace ixg;
 
@@ -139,19 +140,94 @@ int launch_fill(E* out, long long n, const long long* d_n, E v, cudaStream_t s) 
   return IXG_OK;
 }
 
-// checked/elided scatter of m pairs into out[0..ndst) (ndst from d_ndst when given)
+// binned-scatter geometry for ndst destinations of E: window shift (32 MB
+// windows) and window count; nb == 0 when binning does not apply
+template <typename E>
+inline void bin_geometry(long long ndst, int* shift, int* nb) {
+  int sh = sizeof(E) == 4 ? 23 : 22;
+  if (const char* e = getenv("IXG_BIN_SHIFT")) sh = atoi(e);  // tests: many windows at small sizes
+  *shift = sh;
+  *nb = 0;
+  if (ndst <= 0 || ndst > (1LL << 32)) return;  // u32 binned indices
+  while (((ndst - 1) >> sh) + 1 > kBinMax) ++sh;
+  *shift = sh;
+  *nb = (int)(((ndst - 1) >> sh) + 1);
+}
+
+// checked/elided scatter of m pairs into out[0..ndst) (ndst from d_ndst when
+// given).  layout: IXG_SCATTER_DIRECT, or IXG_SCATTER_BINNED (pairs first
+// partitioned by destination window; ndst <= 2^32 and a host-known ndst).
 template <typename E>
 int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long ndst_cap, const long long* is,
                    const E* vs, long long m, uint32_t bits, int stmt, int site, ixg_status* st, WS& ws,
-                   int hdr_idx, cudaStream_t s) {
+                   int hdr_idx, cudaStream_t s, int layout = IXG_SCATTER_DIRECT) {
   const bool check = (bits & IXG_V_CONFLICT) != 0;
+  int shift = 0, nb = 0;
+  if (layout == IXG_SCATTER_BINNED && !d_ndst) bin_geometry<E>(ndst, &shift, &nb);
+  const bool binned = nb > 1;
   uint32_t* claim = nullptr;
   if (check) claim = (uint32_t*)ws.take(bitmap_bytes(ndst_cap));
+  unsigned long long *counts = nullptr, *cursor = nullptr, *end = nullptr;
+  long long* d_m = nullptr;
+  uint32_t* bis = nullptr;
+  E* bvs = nullptr;
+  if (layout == IXG_SCATTER_BINNED) {  // sized whether or not this call bins (ixg_ws_bytes)
+    counts = (unsigned long long*)ws.take(3 * kBinMax * 8 + 64);
+    cursor = counts + kBinMax;
+    end = cursor + kBinMax;
+    d_m = (long long*)(end + kBinMax);
+    bis = (uint32_t*)ws.take((size_t)(m > 0 ? m : 1) * 4);
+    bvs = (E*)ws.take((size_t)(m > 0 ? m : 1) * sizeof(E));
+  }
   if (ws.dry || m <= 0) return IXG_OK;
   LBHeader* hdr = ws.hdr(hdr_idx);
   if (check) {
     cudaMemsetAsync(claim, 0, bitmap_bytes(ndst_cap), s);
     LAUNCHED();
+  }
+  const unsigned tiles = (unsigned)tiles_of(m, kScTile);
+  if (binned) {
+    // the window sizes of a bijection onto [0, ndst) when Sc1 holds (no init,
+    // no checks: every destination written once), else pass 0 counts them
+    const bool sc1 = (bits & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;
+    if (!sc1) {
+      cudaMemsetAsync(counts, 0, kBinMax * 8, s);
+      LAUNCHED();
+      k_bin_count<<<grid_for(m), 256, 0, s>>>(is, m, ndst, shift, counts);
+      LAUNCHED();
+      CHECK_LAUNCH();
+    }
+    k_bin_layout<<<1, 32, 0, s>>>(sc1 ? nullptr : counts, nb, ndst, shift, cursor, end, d_m);
+    LAUNCHED();
+    CHECK_LAUNCH();
+    {
+      static std::atomic<unsigned long long> attr{0};
+      allow_smem(k_bin_partition<E>, BinSmem<E>::BYTES, attr);
+      TimedLaunch tl(IXG_K_BIN, s);
+      k_bin_partition<E><<<tiles, 256, BinSmem<E>::BYTES, s>>>(is, vs, m, ndst, shift, nb, cursor, end, bis, bvs);
+      LAUNCHED();
+      CHECK_LAUNCH();
+    }
+    TimedLaunch tl(IXG_K_SCATTER, s);
+    if (check) {
+      static std::atomic<unsigned long long> attr{0};
+      allow_smem(k_scatter_pc<uint32_t, E>, PcSmem<uint32_t, E>::BYTES, attr);
+      k_scatter_pc<uint32_t, E><<<tiles, 256, PcSmem<uint32_t, E>::BYTES, s>>>(out, ndst, nullptr, bis, bvs, m, d_m,
+                                                                               claim, hdr);
+    } else {
+      static std::atomic<unsigned long long> attr{0};
+      allow_smem(k_scatter_ti<uint32_t, E>, PcSmem<uint32_t, E>::BYTES, attr);
+      k_scatter_ti<uint32_t, E><<<tiles, 256, PcSmem<uint32_t, E>::BYTES, s>>>(out, ndst, nullptr, bis, bvs, m, d_m);
+    }
+    LAUNCHED();
+    CHECK_LAUNCH();
+    if (check) {
+      k_scatter_verify_i<uint32_t, E><<<grid_for(m), kGThreads, 0, s>>>(out, ndst, nullptr, bis, bvs, m, d_m, hdr, st,
+                                                                       stmt, site);
+      LAUNCHED();
+      CHECK_LAUNCH();
+    }
+    return IXG_OK;
   }
   {
     TimedLaunch tl(IXG_K_SCATTER, s);
@@ -160,14 +236,20 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
       const char* e = getenv("IXG_SCATTER");
       mode = e ? atoi(e) : 0;
     }
-    // ELIDED: TMA-staged striped scatter.  CHECKED keeps the blocked
-    // kernel: striped lanes would all hit the same claim word (a warp's 32
-    // sources are ~2 destination runs), serialising the atomics.
-    if (mode == 0 && !check && aligned16(is) && aligned16(vs)) {
-      static std::atomic<unsigned long long> attr{0};
-      allow_smem(k_scatter_t<E>, ScSmem<E>::BYTES, attr);
-      k_scatter_t<E><<<(unsigned)tiles_of(m, kScTile), 256, ScSmem<E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m,
-                                                                                 check ? 1 : 0, claim, hdr);
+    // TMA-staged tiles walked striped (each warp store covers 32 consecutive
+    // sources); CHECKED claims through the shared-memory windows
+    // (k_scatter_pc); IXG_SCATTER=1: the register-blocked kernels for A/B
+    if (mode == 0 && aligned16(is) && aligned16(vs)) {
+      if (check) {
+        static std::atomic<unsigned long long> attr{0};
+        allow_smem(k_scatter_pc<long long, E>, PcSmem<long long, E>::BYTES, attr);
+        k_scatter_pc<long long, E><<<tiles, 256, PcSmem<long long, E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m,
+                                                                                  nullptr, claim, hdr);
+      } else {
+        static std::atomic<unsigned long long> attr{0};
+        allow_smem(k_scatter_t<E>, ScSmem<E>::BYTES, attr);
+        k_scatter_t<E><<<tiles, 256, ScSmem<E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m, 0, claim, hdr);
+      }
     } else if (aligned32(is) && aligned32(vs))
       k_scatter_v<E><<<grid_for(m / 8 + 1, 256), 256, 0, s>>>(out, ndst, d_ndst, is, vs, m, check ? 1 : 0, claim,
                                                                hdr);
@@ -438,6 +520,10 @@ size_t ixg_ws_bytes(int op, int64_t n, int64_t m) {
     case IXG_OP_SCAN: ws.chan(0, tiles_of(n, kGTile)); break;
     case IXG_OP_SEGSCAN: ws.chan(0, tiles_of(n, kGTile)); break;
     case IXG_OP_SCATTER: ws.take(bitmap_bytes(m)); break;  // n = pairs, m = ndst
+    case IXG_OP_SCATTER_BINNED:  // the claim bitmap + the binned (u32, i64) pairs
+      launch_scatter<long long>(nullptr, m, nullptr, m, nullptr, nullptr, n, IXG_V_CONFLICT, 0, 0, nullptr, ws, 1,
+                                0, IXG_SCATTER_BINNED);
+      break;
     case IXG_OP_FILTER:
       do_filter<int64_t>(nullptr, nullptr, n, &p, nullptr, nullptr, IXG_VARIANT_CHECKED, nullptr, ws, 0);
       {
@@ -552,16 +638,30 @@ int ixg_segscan_add(int dt_f, const void* flags, int dt_x, const void* xs, int64
 }
 
 int ixg_scatter(int dt, void* out, int64_t ndst, const int64_t* is, int64_t nis, const void* vs, int64_t nvs,
-                uint32_t site_bits, int stmt, int site, ixg_status* st, void* ws, size_t ws_bytes, void* stream) {
+                uint32_t site_bits, int stmt, int site, int layout, ixg_status* st, void* ws, size_t ws_bytes,
+                void* stream) {
   const long long m = nis < nvs ? nis : nvs;  // zip truncation, oracle.py:299
   if (ndst < 0 || m < 0 || (m > 0 && (!is || !vs)) || (ndst > 0 && !out)) return IXG_BADARG;
-  if ((site_bits & IXG_V_CONFLICT) && ws_bytes < ixg_ws_bytes(IXG_OP_SCATTER, m, ndst)) return IXG_BADARG;
+  if (layout != IXG_SCATTER_DIRECT && layout != IXG_SCATTER_BINNED) return IXG_BADARG;
+  const long long need = layout == IXG_SCATTER_BINNED ? ixg_ws_bytes(IXG_OP_SCATTER_BINNED, m, ndst)
+                                                      : ixg_ws_bytes(IXG_OP_SCATTER, m, ndst);
+  if (((site_bits & IXG_V_CONFLICT) || layout == IXG_SCATTER_BINNED) && (long long)ws_bytes < need) return IXG_BADARG;
   WS w(ws);
   if (dt == IXG_I32)
     return launch_scatter<int32_t>((int32_t*)out, ndst, nullptr, ndst, (const long long*)is, (const int32_t*)vs, m,
-                                   site_bits, stmt, site, st, w, 1, S(stream));
+                                   site_bits, stmt, site, st, w, 1, S(stream), layout);
   return launch_scatter<long long>((long long*)out, ndst, nullptr, ndst, (const long long*)is,
-                                   (const long long*)vs, m, site_bits, stmt, site, st, w, 1, S(stream));
+                                   (const long long*)vs, m, site_bits, stmt, site, st, w, 1, S(stream), layout);
+}
+
+int ixg_scatter_probe(const int64_t* is, int64_t m, int* d_flag, void* stream) {
+  if (m < 0 || !d_flag || (m > 0 && !is)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  if (m < 512) return cuda_rc(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+  k_scatter_probe<<<1, 256, 0, s>>>((const long long*)is, m, d_flag);
+  LAUNCHED();
+  CHECK_LAUNCH();
+  return IXG_OK;
 }
 
 int ixg_gather(int dt, const void* arr, int64_t len, const int64_t* idx, int64_t n, void* out,

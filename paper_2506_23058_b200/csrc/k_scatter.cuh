@@ -1,0 +1,323 @@
+// k_scatter.cuh -- the generic scatter (oracle.py:294-305) beyond the fused
+// pipelines: the CHECKED form's duplicate detection as a shared-memory-
+// privatised claim histogram, and destination-window binning for index
+// arrays without locality.
+//
+// CHECKED scatter (k_scatter_pc).  The reference keeps a `written` dict
+// (oracle.py:298-302); the device form claims every in-range destination in
+// a bitmap (one bit per destination) and only if some destination was
+// claimed twice re-reads the pairs to compare values (equal-valued
+// duplicates are legal).  Instead of one global atomicOr per element, each
+// 4096-pair tile claims into up to kWinSlots shared-memory windows of 4096
+// destinations (a window is 128 words; shared atomics), then merges each
+// touched window into the global bitmap with ONE coalesced atomicOr per
+// non-zero word -- a collision inside the tile shows in the shared OR, one
+// across tiles in the global OR's old value.  An index array with locality
+// (C3's partition indices: two monotone streams, so a tile touches <= 4
+// windows) does ~16x fewer global atomics; pairs whose window finds no free
+// slot fall back to the global atomic.
+//
+// Binned scatter (k_bin_*).  A random permutation scatters one 4-byte store
+// per 32-byte sector over a 2 GB destination: every store misses, and the
+// sector is read back before it is written (partial-sector writes).  The
+// binned form first partitions the (index, value) pairs by destination
+// window (B <= 256 windows of 8M int32 destinations = 32 MB, L2-resident):
+// each tile counts its pairs per window in shared memory, reserves room in
+// each window's global run with one atomicAdd per (tile, window), stages the
+// pairs window by window in shared memory and writes each window's run
+// contiguously (indices narrowed to u32).  The second pass is the ordinary
+// (ELIDED or CHECKED) scatter over the binned pairs: at any moment the
+// resident tiles write into one or two 32 MB windows, which the L2 absorbs
+// until their lines are complete.  Pairs outside [0, ndst) are dropped by the
+// first pass (the reference ignores them, oracle.py:300).
+#pragma once
+#include "k_big.cuh"
+
+namespace ixg {
+
+constexpr int kWinBits = 12;                      // claim window: 4096 destinations
+constexpr int kWinWords = (1 << kWinBits) / 32;  // 128 bitmap words
+constexpr int kWinSlots = 8;                      // windows per tile in shared memory
+constexpr int kBinMax = 256;                      // destination windows of the binned scatter
+
+template <typename I, typename E>
+struct PcSmem {  // TMA-staged tile of (I index, E value) pairs
+  static constexpr int BYTES = kScTile * ((int)sizeof(I) + (int)sizeof(E));
+};
+
+// CHECKED scatter, privatised claims (see above); I = index type (int64 for
+// the language's arrays, u32 for binned pairs), the tile TMA-staged when full
+template <typename I, typename E>
+__global__ void __launch_bounds__(256) k_scatter_pc(E* __restrict__ out, long long ndst,
+                                                    const long long* __restrict__ d_ndst,
+                                                    const I* __restrict__ is, const E* __restrict__ vs, long long m,
+                                                    const long long* __restrict__ d_m, uint32_t* __restrict__ claim,
+                                                    LBHeader* hdr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  I* s_is = reinterpret_cast<I*>(smem_raw);
+  E* s_vs = reinterpret_cast<E*>(smem_raw + kScTile * sizeof(I));
+  __shared__ uint32_t s_bits[kWinSlots * kWinWords];
+  __shared__ unsigned long long s_win[kWinSlots];
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (d_ndst) ndst = *d_ndst;
+  if (d_m) m = *d_m;
+  const long long base = (long long)blockIdx.x * kScTile;
+  if (base >= m) return;
+  const int t = threadIdx.x;
+  const bool full = base + kScTile <= m;
+  for (int q = t; q < kWinSlots * kWinWords; q += 256) s_bits[q] = 0u;
+  if (t < kWinSlots) s_win[t] = ~0ull;
+  if (full && t == 0) {
+    mbar_init(&s_mbar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&s_mbar, (uint32_t)PcSmem<I, E>::BYTES);
+    bulk_g2s(s_is, is + base, kScTile * (uint32_t)sizeof(I), &s_mbar);
+    bulk_g2s(s_vs, vs + base, kScTile * (uint32_t)sizeof(E), &s_mbar);
+  }
+  __syncthreads();
+  if (full) mbar_wait(&s_mbar, 0);
+  volatile unsigned long long* vw = s_win;
+  bool dup = false;
+  const int cnt = full ? kScTile : (int)(m - base);
+  for (int k = t; k < cnt; k += 256) {  // striped: a warp's stores cover 32 consecutive sources
+    const long long d = full ? (long long)s_is[k] : (long long)is[base + k];
+    if ((unsigned long long)d >= (unsigned long long)ndst) continue;  // oracle.py:300
+    const E v = full ? s_vs[k] : vs[base + k];
+    const unsigned long long w = (unsigned long long)d >> kWinBits;
+    int slot = -1;
+#pragma unroll 1
+    for (int j = 0; j < kWinSlots; ++j) {
+      unsigned long long cur = vw[j];
+      if (cur == ~0ull) {  // a free slot: claim it for w (or learn who did)
+        cur = atomicCAS(&s_win[j], ~0ull, w);
+        if (cur == ~0ull) cur = w;
+      }
+      if (cur == w) {
+        slot = j;
+        break;
+      }
+    }
+    const uint32_t bit = 1u << (d & 31);
+    if (slot >= 0) {
+      if (atomicOr(&s_bits[slot * kWinWords + (int)((d >> 5) & (kWinWords - 1))], bit) & bit) dup = true;
+    } else if (atomicOr(&claim[d >> 5], bit) & bit) {
+      dup = true;
+    }
+    out[d] = v;
+  }
+  __syncthreads();
+  // merge the touched windows: one coalesced atomicOr per non-zero word
+  for (int q = t; q < kWinSlots * kWinWords; q += 256) {
+    const unsigned long long w = s_win[q / kWinWords];
+    const uint32_t word = s_bits[q];
+    if (w != ~0ull && word && (atomicOr(&claim[w * kWinWords + (q % kWinWords)], word) & word)) dup = true;
+  }
+  if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
+}
+
+// ELIDED scatter of TMA-staged tiles (k_scatter_t) for any index type, with
+// the pair count optionally on the device (binned pairs)
+template <typename I, typename E>
+__global__ void __launch_bounds__(256) k_scatter_ti(E* __restrict__ out, long long ndst,
+                                                    const long long* __restrict__ d_ndst,
+                                                    const I* __restrict__ is, const E* __restrict__ vs, long long m,
+                                                    const long long* __restrict__ d_m) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  I* s_is = reinterpret_cast<I*>(smem_raw);
+  E* s_vs = reinterpret_cast<E*>(smem_raw + kScTile * sizeof(I));
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (d_ndst) ndst = *d_ndst;
+  if (d_m) m = *d_m;
+  const long long base = (long long)blockIdx.x * kScTile;
+  if (base >= m) return;
+  const int t = threadIdx.x;
+  if (base + kScTile <= m) {
+    if (t == 0) {
+      mbar_init(&s_mbar, 1);
+      mbar_fence_init();
+      mbar_expect_tx(&s_mbar, (uint32_t)PcSmem<I, E>::BYTES);
+      bulk_g2s(s_is, is + base, kScTile * (uint32_t)sizeof(I), &s_mbar);
+      bulk_g2s(s_vs, vs + base, kScTile * (uint32_t)sizeof(E), &s_mbar);
+    }
+    __syncthreads();
+    mbar_wait(&s_mbar, 0);
+#pragma unroll 4
+    for (int k = t; k < kScTile; k += 256) {
+      const long long d = (long long)s_is[k];
+      if ((unsigned long long)d < (unsigned long long)ndst) out[d] = s_vs[k];
+    }
+  } else {
+    for (long long i = base + t; i < m; i += 256) {
+      const long long d = (long long)is[i];
+      if ((unsigned long long)d < (unsigned long long)ndst) out[d] = vs[i];
+    }
+  }
+}
+
+// the value check after a duplicate claim (k_scatter_verify for any index type)
+template <typename I, typename E>
+__global__ void __launch_bounds__(kGThreads) k_scatter_verify_i(const E* __restrict__ out, long long ndst,
+                                                                 const long long* __restrict__ d_ndst,
+                                                                 const I* __restrict__ is, const E* __restrict__ vs,
+                                                                 long long m, const long long* __restrict__ d_m,
+                                                                 LBHeader* hdr, ixg_status* st, int stmt, int site) {
+  __shared__ bool s_last;
+  if (((volatile LBHeader*)hdr)->dup == 0u) return;  // no destination claimed twice
+  if (d_ndst) ndst = *d_ndst;
+  if (d_m) m = *d_m;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const long long d = (long long)is[i];
+    if ((unsigned long long)d < (unsigned long long)ndst && out[d] != vs[i]) bad = true;
+  }
+  if (bad) status_fail(st, IXG_CONFLICT, stmt, 0, site);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&hdr->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    hdr->done = 0;
+    hdr->dup = 0;
+  }
+}
+
+// ------------------------------------------------------------------ binning
+// Locality probe: 64 sample runs of 256 consecutive indices; a run of
+// indices with locality changes 4096-destination window a handful of times,
+// a random one at almost every element.  *flag = 1 (bin) when the samples
+// average more than 32 window changes per 256 indices.
+__global__ void __launch_bounds__(256) k_scatter_probe(const long long* __restrict__ is, long long m,
+                                                       int* __restrict__ flag) {
+  __shared__ int s_changes;
+  if (threadIdx.x == 0) s_changes = 0;
+  __syncthreads();
+  int changes = 0;
+  for (int sIdx = 0; sIdx < 64; ++sIdx) {
+    const long long start = (m - 257) * sIdx / 63;
+    const long long i = start + threadIdx.x + 1;
+    if (start >= 0 && i < m) changes += ((is[i] >> kWinBits) != (is[i - 1] >> kWinBits)) ? 1 : 0;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) changes += __shfl_xor_sync(0xffffffffu, changes, d);
+  if (lane_id() == 0) atomicAdd(&s_changes, changes);
+  __syncthreads();
+  if (threadIdx.x == 0) *flag = s_changes > 64 * 32 ? 1 : 0;
+}
+
+// pass 0 (CHECKED / unknown counts): pairs per destination window
+__global__ void __launch_bounds__(256) k_bin_count(const long long* __restrict__ is, long long m, long long ndst,
+                                                   int shift, unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int s_cnt[kBinMax];
+  for (int b = threadIdx.x; b < kBinMax; b += 256) s_cnt[b] = 0u;
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const long long d = __ldcs(&is[i]);
+    if ((unsigned long long)d < (unsigned long long)ndst) atomicAdd(&s_cnt[d >> shift], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBinMax; b += 256)
+    if (s_cnt[b]) atomicAdd(&counts[b], (unsigned long long)s_cnt[b]);
+}
+
+// run starts (cursor[b]), ends (end[b]) and the in-range total (*d_m) of the
+// B windows: from counts (exclusive scan) or, without counts, the window
+// sizes of a bijection onto [0, ndst) (the Sc1 contract: window b receives
+// exactly its own destinations)
+__global__ void k_bin_layout(const unsigned long long* __restrict__ counts, int nb, long long ndst, int shift,
+                             unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ end,
+                             long long* __restrict__ d_m) {
+  if (threadIdx.x != 0) return;
+  unsigned long long acc = 0;
+  for (int b = 0; b < nb; ++b) {
+    cursor[b] = acc;
+    const unsigned long long w0 = (unsigned long long)b << shift;
+    const unsigned long long sz = counts ? counts[b]
+                                         : ((unsigned long long)ndst - w0 < (1ull << shift) ? (unsigned long long)ndst - w0
+                                                                                            : (1ull << shift));
+    acc += sz;
+    end[b] = acc;
+  }
+  *d_m = (long long)acc;
+}
+
+// pass 1: partition the pairs by destination window (see the file comment);
+// one CTA per 4096-pair tile, indices narrowed to u32 (ndst <= 2^32)
+template <typename E>
+struct BinSmem {  // staged pairs of one tile, window by window
+  static constexpr int BYTES = kScTile * (4 + (int)sizeof(E) + 1);
+};
+template <typename E>
+__global__ void __launch_bounds__(256) k_bin_partition(const long long* __restrict__ is, const E* __restrict__ vs,
+                                                       long long m, long long ndst, int shift, int nb,
+                                                       unsigned long long* __restrict__ cursor,
+                                                       const unsigned long long* __restrict__ end,
+                                                       uint32_t* __restrict__ bis, E* __restrict__ bvs) {
+  constexpr int PER = kScTile / 256;  // 16 pairs per thread
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  E* s_vs = reinterpret_cast<E*>(smem_raw);
+  uint32_t* s_is = reinterpret_cast<uint32_t*>(smem_raw + kScTile * sizeof(E));
+  uint8_t* s_b = smem_raw + kScTile * (sizeof(E) + 4);
+  __shared__ unsigned int s_cnt[kBinMax];
+  __shared__ unsigned int s_off[kBinMax];
+  __shared__ unsigned long long s_base[kBinMax];
+  __shared__ unsigned int s_wsum[8];
+  const long long base = (long long)blockIdx.x * kScTile;
+  const int t = threadIdx.x;
+  for (int b = t; b < kBinMax; b += 256) s_cnt[b] = 0u;
+  __syncthreads();
+  long long d[PER];
+  E v[PER];
+  int slot[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {  // striped: coalesced loads
+    const long long i = base + q * 256 + t;
+    d[q] = i < m ? __ldcs(&is[i]) : -1;
+    v[q] = i < m ? __ldcs(&vs[i]) : E(0);
+    slot[q] = -1;
+    if ((unsigned long long)d[q] < (unsigned long long)ndst) slot[q] = (int)atomicAdd(&s_cnt[d[q] >> shift], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the window counts (nb <= 256: one per thread)
+  const unsigned int c = t < nb ? s_cnt[t] : 0u;
+  unsigned int inc = c;
+#pragma unroll
+  for (int k = 1; k < 32; k <<= 1) {
+    const unsigned int o = __shfl_up_sync(0xffffffffu, inc, k);
+    if (lane_id() >= k) inc += o;
+  }
+  if (lane_id() == 31) s_wsum[warp_id()] = inc;
+  __syncthreads();
+  unsigned int wpre = 0;
+  for (int w = 0; w < warp_id(); ++w) wpre += s_wsum[w];
+  if (t < nb) {
+    s_off[t] = wpre + inc - c;
+    s_base[t] = c ? atomicAdd(&cursor[t], (unsigned long long)c) : 0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (slot[q] >= 0) {
+      const int b = (int)(d[q] >> shift);
+      const unsigned int p = s_off[b] + (unsigned int)slot[q];
+      s_is[p] = (uint32_t)d[q];
+      s_vs[p] = v[q];
+      s_b[p] = (uint8_t)b;
+    }
+  }
+  __syncthreads();
+  const unsigned int total = s_wsum[0] + s_wsum[1] + s_wsum[2] + s_wsum[3] + s_wsum[4] + s_wsum[5] + s_wsum[6] + s_wsum[7];
+  for (unsigned int p = t; p < total; p += 256) {  // each window's run is contiguous in s_* and in the output
+    const int b = s_b[p];
+    const unsigned long long g = s_base[b] + (p - s_off[b]);
+    if (g < end[b]) {  // a run never outgrows its window (always true under the layout's contract)
+      bis[g] = s_is[p];
+      bvs[g] = s_vs[p];
+    }
+  }
+}
+
+}  // namespace ixg

@@ -58,7 +58,10 @@ def _contig(t: torch.Tensor) -> torch.Tensor:
 
 # ------------------------------------------------------------------ workspace
 class Workspace:
-    """Per-(device, op) scratch, zeroed whenever its layout (op, n, m) changes.
+    """Per-(device, op, stream) scratch, zeroed whenever its layout (op, n, m)
+    changes.  One workspace per stream: two streams running the same op never
+    share look-back slots or tile tickets (one stream /
+    workspace per concurrent caller).
 
     The kernels leave their look-back state ready for the next launch
     (epoch-tagged flags), so steady-state calls do no memset."""
@@ -68,7 +71,8 @@ class Workspace:
 
     def get(self, op: int, n: int, m: int, device) -> torch.Tensor:
         need = int(_lib().ixg_ws_bytes(op, n, m))
-        key = (device.index if isinstance(device, torch.device) else device, op)
+        dev = device.index if isinstance(device, torch.device) else device
+        key = (dev, op, torch.cuda.current_stream(device).cuda_stream)
         ent = self._bufs.get(key)
         if ent is None or ent[1].numel() < need:
             buf = torch.zeros(max(need, 4096), dtype=torch.uint8, device=device)
@@ -198,16 +202,33 @@ def segscan_add(flags: torch.Tensor, xs: torch.Tensor, want_flags: bool = False,
     return (out_v, out_f) if want_flags else out_v
 
 
+BIN_MIN_PAIRS = 1 << 22  # below this the destination is L2-sized anyway: direct
+
+
+def scatter_layout(is_: torch.Tensor, ndst: int) -> int:
+    """IXG_SCATTER_BINNED when `is_` has no locality (ixg_scatter_probe on
+    the device; one 4-byte read back), else IXG_SCATTER_DIRECT."""
+    if is_.numel() < BIN_MIN_PAIRS or not (1 << 23) < ndst <= (1 << 32):
+        return L.SCATTER_DIRECT
+    flag = torch.empty(1, dtype=torch.int32, device=is_.device)
+    L.check(_lib().ixg_scatter_probe(_ptr(is_), is_.numel(), _ptr(flag), _stream()), "scatter_probe")
+    return L.SCATTER_BINNED if int(flag.item()) else L.SCATTER_DIRECT
+
+
 def scatter(out: torch.Tensor, is_: torch.Tensor, vs: torch.Tensor, site_bits: int, status: Status,
-            stmt: int = 0, site: int = 0) -> torch.Tensor:
+            stmt: int = 0, site: int = 0, layout="auto") -> torch.Tensor:
     """scatter into `out` in place (oracle.py:294-305); `out` already holds dst
-    unless the site's V_INIT bit is clear."""
+    unless the site's V_INIT bit is clear.  layout: "auto" (probe the index
+    array's locality), L.SCATTER_DIRECT or L.SCATTER_BINNED."""
     is_, vs = _contig(is_), _contig(vs)
     m = min(is_.numel(), vs.numel())
-    ws, wsb = _ws(L.OP_SCATTER, m, out.numel(), out.device)
+    if layout == "auto":
+        layout = scatter_layout(is_[:m], out.numel())
+    op = L.OP_SCATTER_BINNED if layout == L.SCATTER_BINNED else L.OP_SCATTER
+    ws, wsb = _ws(op, m, out.numel(), out.device)
     L.check(
         _lib().ixg_scatter(_dt(out), _ptr(out), out.numel(), _ptr(is_), is_.numel(), _ptr(vs), vs.numel(),
-                           site_bits, stmt, site, status.ptr, ws, wsb, _stream()),
+                           site_bits, stmt, site, layout, status.ptr, ws, wsb, _stream()),
         "scatter",
     )
     return out

@@ -501,3 +501,106 @@ def test_hist_add_128bit_bins(cuda):
     st = ops.Status(cuda)
     got = ops.hist(L.HIST_ADD, 7, 100, _t(is2, cuda), _t(vs2, cuda), status=st)
     assert st.read().ok and np.array_equal(_np(got), O.hist(L.HIST_ADD, 7, 100, is2, vs2))
+
+
+# ----------------------------------------------------------------- generic scatter: privatised claims, binning
+def _scatter_case(n, dtype, kind, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "streams":  # partition2 indices: two monotone streams (C3)
+        c = rng.random(n) < 0.5
+        t = np.cumsum(c)
+        is_ = np.where(c, t - 1, t[-1] + (np.arange(1, n + 1) - t) - 1).astype(np.int64)
+    else:
+        is_ = rng.permutation(n).astype(np.int64)
+    vs = rng.integers(-1000, 1000, n).astype(dtype)
+    return is_, vs
+
+
+@pytest.mark.parametrize("layout", ["direct", "binned"])
+@pytest.mark.parametrize("kind", ["streams", "random"])
+@pytest.mark.parametrize("n", [1000, 65_537, 1 << 20])
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_scatter_layouts(cuda, monkeypatch, layout, kind, n, dtype):
+    """ELIDED (Sc1), injective-only and CHECKED scatters in both layouts
+    (IXG_BIN_SHIFT=12: 4096-destination windows, so small sizes bin into many
+    windows) against the C restatement of oracle.py:294-305: permutations,
+    out-of-range indices (ignored), equal-valued duplicates (legal) and a
+    conflicting duplicate (NonIdempotentScatter)."""
+    from paper_2506_23058_b200 import ops
+
+    monkeypatch.setenv("IXG_BIN_SHIFT", "12")
+    lay = L.SCATTER_BINNED if layout == "binned" else L.SCATTER_DIRECT
+    is_, vs = _scatter_case(n, dtype, kind, n)
+    want = O.scatter(np.zeros(n, np.int64), is_, vs)
+    for bits in (0, L.V_INIT, L.V_CONFLICT | L.V_INIT):
+        st = ops.Status(cuda)
+        out = _t(np.zeros(n, dtype), cuda)
+        ops.scatter(out, _t(is_, cuda), _t(vs, cuda), bits, st, layout=lay)
+        assert st.read().ok and np.array_equal(_np(out).astype(np.int64), want), bits
+    # CHECKED with out-of-range indices, equal duplicates, into a larger dst
+    is2 = is_.copy()
+    is2[::7] = -1
+    is2[3::11] = n + 5
+    is2[1::13] = is2[0]  # many duplicates of one destination ...
+    vs2 = vs.copy()
+    vs2[1::13] = vs2[0]  # ... all with its value: legal
+    dst = np.full(n + 3, 9, dtype)
+    want2 = O.scatter(dst.astype(np.int64), is2, vs2)
+    st = ops.Status(cuda)
+    out = _t(dst, cuda)
+    ops.scatter(out, _t(is2, cuda), _t(vs2, cuda), L.V_CONFLICT | L.V_INIT, st, layout=lay)
+    assert st.read().ok and np.array_equal(_np(out).astype(np.int64), want2)
+    vs2[1 + 13 * (len(vs2[1::13]) // 2)] += 1  # one conflicting value
+    st = ops.Status(cuda)
+    out = _t(dst, cuda)
+    ops.scatter(out, _t(is2, cuda), _t(vs2, cuda), L.V_CONFLICT | L.V_INIT, st, layout=lay)
+    s = st.read()
+    assert not s.ok and s.codes & (1 << L.CONFLICT)
+
+
+def test_scatter_probe_and_auto(cuda):
+    """the locality probe: C3's two monotone streams stay direct, a random
+    permutation bins (and the auto layout still scatters exactly)."""
+    from paper_2506_23058_b200 import ops
+
+    n = 1 << 23
+    for kind, want in (("streams", L.SCATTER_DIRECT), ("random", L.SCATTER_BINNED)):
+        is_, vs = _scatter_case(n, np.int32, kind, 3)
+        assert ops.scatter_layout(_t(is_, cuda), (1 << 23) + 1) == want
+    is_, vs = _scatter_case(n, np.int32, "random", 4)
+    out = _t(np.zeros(n, np.int32), cuda)
+    st = ops.Status(cuda)
+    ops.scatter(out, _t(is_, cuda), _t(vs, cuda), 0, st)
+    w = np.zeros(n, np.int32)
+    w[is_] = vs
+    assert st.read().ok and np.array_equal(_np(out), w)
+
+
+def test_two_streams_concurrently(cuda):
+    """the same ops on two streams at once (per-stream workspaces: look-back
+    slots and tile tickets are never shared) -- both results exact."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    n = 1 << 22
+    xa = gen.uniform(1, n, -128, 127, np.int32)
+    xb = gen.uniform(2, n, -128, 127, np.int32)
+    p = Pred.ge(0)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    res = {}
+    ta, tb = _t(xa, cuda), _t(xb, cuda)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(sa):
+            sta = ops.Status(cuda)
+            ya, dka = ops.filter(ta, p, L.VARIANT_CHECKED, sta)
+            ca = ops.scan_add(ta, 5)
+        with torch.cuda.stream(sb):
+            stb = ops.Status(cuda)
+            yb, dkb = ops.filter(tb, p, L.VARIANT_CHECKED, stb)
+            cb = ops.scan_add(tb, 5)
+        torch.cuda.synchronize()
+        res = (ya[: int(dka.item())], yb[: int(dkb.item())], ca, cb)
+        assert np.array_equal(_np(res[0]), O.filter_(p, xa)) and np.array_equal(_np(res[1]), O.filter_(p, xb))
+        assert np.array_equal(_np(res[2]), O.scan_add(xa, 5)) and np.array_equal(_np(res[3]), O.scan_add(xb, 5))
