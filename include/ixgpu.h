@@ -133,7 +133,7 @@ typedef struct ixg_status {
 /* scatter layouts (ixg_scatter) */
 #define IXG_SCATTER_DIRECT 0  /* pairs stored in their own order            */
 #define IXG_SCATTER_BINNED 1  /* pairs first partitioned by destination
-                                 window (32 MB windows, ndst <= 2^32)      */
+                                 window (16 MB windows, ndst <= 2^32)      */
 
 /* ---- library / device --------------------------------------------------- */
 int ixg_version(void);

@@ -144,7 +144,7 @@ int launch_fill(E* out, long long n, const long long* d_n, E v, cudaStream_t s) 
 // windows) and window count; nb == 0 when binning does not apply
 template <typename E>
 inline void bin_geometry(long long ndst, int* shift, int* nb) {
-  int sh = sizeof(E) == 4 ? 23 : 22;
+  int sh = sizeof(E) == 4 ? 22 : 21;  // 16 MB destination windows
   if (const char* e = getenv("IXG_BIN_SHIFT")) sh = atoi(e);  // tests: many windows at small sizes
   *shift = sh;
   *nb = 0;
@@ -190,6 +190,10 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
     // the window sizes of a bijection onto [0, ndst) when Sc1 holds (no init,
     // no checks: every destination written once), else pass 0 counts them
     const bool sc1 = (bits & (IXG_V_CONFLICT | IXG_V_INIT)) == 0;
+    if (check) {  // the popcount accumulator of k_claim_count
+      cudaMemsetAsync(counts + 3 * kBinMax + 4, 0, 8, s);
+      LAUNCHED();
+    }
     if (!sc1) {
       cudaMemsetAsync(counts, 0, kBinMax * 8, s);
       LAUNCHED();
@@ -211,9 +215,9 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
     TimedLaunch tl(IXG_K_SCATTER, s);
     if (check) {
       static std::atomic<unsigned long long> attr{0};
-      allow_smem(k_scatter_pc<uint32_t, E>, PcSmem<uint32_t, E>::BYTES, attr);
-      k_scatter_pc<uint32_t, E><<<tiles, 256, PcSmem<uint32_t, E>::BYTES, s>>>(out, ndst, nullptr, bis, bvs, m, d_m,
-                                                                               claim, hdr);
+      allow_smem(k_scatter_pc<uint32_t, E, false>, PcSmem<uint32_t, E>::BYTES, attr);
+      k_scatter_pc<uint32_t, E, false><<<tiles, 256, PcSmem<uint32_t, E>::BYTES, s>>>(out, ndst, nullptr, bis, bvs, m,
+                                                                                      d_m, claim, hdr);
     } else {
       static std::atomic<unsigned long long> attr{0};
       allow_smem(k_scatter_ti<uint32_t, E>, PcSmem<uint32_t, E>::BYTES, attr);
@@ -222,6 +226,10 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
     LAUNCHED();
     CHECK_LAUNCH();
     if (check) {
+      const long long nwords = (ndst + 31) / 32;
+      k_claim_count<<<grid_for(nwords / 4 + 1), kGThreads, 0, s>>>(claim, nwords, d_m, counts + 3 * kBinMax + 4, hdr);
+      LAUNCHED();
+      CHECK_LAUNCH();
       k_scatter_verify_i<uint32_t, E><<<grid_for(m), kGThreads, 0, s>>>(out, ndst, nullptr, bis, bvs, m, d_m, hdr, st,
                                                                        stmt, site);
       LAUNCHED();

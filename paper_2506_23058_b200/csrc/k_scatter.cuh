@@ -15,19 +15,21 @@
 // across tiles in the global OR's old value.  An index array with locality
 // (C3's partition indices: two monotone streams, so a tile touches <= 4
 // windows) does ~16x fewer global atomics; pairs whose window finds no free
-// slot fall back to the global atomic.
+// slot fall back to the global atomic.  The shared windows are stored
+// transposed (destination b -> bit b >> 7 of word b & 127) so that a warp's
+// consecutive destinations claim in 32 different banks.
 //
 // Binned scatter (k_bin_*).  A random permutation scatters one 4-byte store
 // per 32-byte sector over a 2 GB destination: every store misses, and the
 // sector is read back before it is written (partial-sector writes).  The
 // binned form first partitions the (index, value) pairs by destination
-// window (B <= 256 windows of 8M int32 destinations = 32 MB, L2-resident):
+// window (B <= 256 windows of 4M int32 destinations = 16 MB, L2-resident):
 // each tile counts its pairs per window in shared memory, reserves room in
 // each window's global run with one atomicAdd per (tile, window), stages the
 // pairs window by window in shared memory and writes each window's run
 // contiguously (indices narrowed to u32).  The second pass is the ordinary
 // (ELIDED or CHECKED) scatter over the binned pairs: at any moment the
-// resident tiles write into one or two 32 MB windows, which the L2 absorbs
+// resident tiles write into one or two 16 MB windows, which the L2 absorbs
 // until their lines are complete.  Pairs outside [0, ndst) are dropped by the
 // first pass (the reference ignores them, oracle.py:300).
 #pragma once
@@ -45,9 +47,40 @@ struct PcSmem {  // TMA-staged tile of (I index, E value) pairs
   static constexpr int BYTES = kScTile * ((int)sizeof(I) + (int)sizeof(E));
 };
 
-// CHECKED scatter, privatised claims (see above); I = index type (int64 for
-// the language's arrays, u32 for binned pairs), the tile TMA-staged when full
-template <typename I, typename E>
+// shared-window atomics in the shared state space (a generic-address atomic
+// re-derives the CTA's shared window -- S2R SR_CgaCtaId -- every time)
+IXG_DEV uint32_t atom_or_shared(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cta.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+IXG_DEV unsigned long long atom_cas_shared(unsigned long long* p, unsigned long long cmp, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.shared::cta.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(smem_u32(p)), "l"(cmp), "l"(v) : "memory");
+  return old;
+}
+
+// L2 policy for streamed-once inputs: evict first, so a binned scatter's
+// destination window stays resident while its pairs stream through
+IXG_DEV uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+IXG_DEV void bulk_g2s_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+// CHECKED scatter, claims privatised in shared-memory windows (kPriv) or
+// straight into the global bitmap (binned pairs: no locality to exploit);
+// I = index type (int64 for the language's arrays, u32 for binned pairs),
+// the tile TMA-staged when full.  A warp looks each distinct window up once
+// (match_any): C3's 32 consecutive sources fall into ~2 windows.
+template <typename I, typename E, bool kPriv = true>
 __global__ void __launch_bounds__(256) k_scatter_pc(E* __restrict__ out, long long ndst,
                                                     const long long* __restrict__ d_ndst,
                                                     const I* __restrict__ is, const E* __restrict__ vs, long long m,
@@ -79,38 +112,81 @@ __global__ void __launch_bounds__(256) k_scatter_pc(E* __restrict__ out, long lo
   volatile unsigned long long* vw = s_win;
   bool dup = false;
   const int cnt = full ? kScTile : (int)(m - base);
-  for (int k = t; k < cnt; k += 256) {  // striped: a warp's stores cover 32 consecutive sources
-    const long long d = full ? (long long)s_is[k] : (long long)is[base + k];
-    if ((unsigned long long)d >= (unsigned long long)ndst) continue;  // oracle.py:300
-    const E v = full ? s_vs[k] : vs[base + k];
-    const unsigned long long w = (unsigned long long)d >> kWinBits;
-    int slot = -1;
+  // the thread's last two windows and their slots (C3: a thread's sources,
+  // 256 apart, go to one of two streams, each advancing ~128 destinations)
+  // the thread's last two windows and their slots (C3: a thread's sources,
+  // 256 apart, go to one of two streams, each advancing ~128 destinations)
+  unsigned long long cw0 = ~0ull, cw1 = ~0ull;
+  int cs0 = -1, cs1 = -1;
+  auto one = [&](long long d, E v) {
+    if ((unsigned long long)d >= (unsigned long long)ndst) return;  // oracle.py:300
+    if constexpr (kPriv) {
+      const unsigned long long w = (unsigned long long)d >> kWinBits;
+      int slot;
+      if (w == cw0) {
+        slot = cs0;
+      } else if (w == cw1) {
+        slot = cs1;
+      } else {
+        slot = -1;
 #pragma unroll 1
-    for (int j = 0; j < kWinSlots; ++j) {
-      unsigned long long cur = vw[j];
-      if (cur == ~0ull) {  // a free slot: claim it for w (or learn who did)
-        cur = atomicCAS(&s_win[j], ~0ull, w);
-        if (cur == ~0ull) cur = w;
+        for (int j = 0; j < kWinSlots; ++j) {
+          unsigned long long cur = vw[j];
+          if (cur == ~0ull) {  // a free slot: claim it for w (or learn who did)
+            cur = atom_cas_shared(&s_win[j], ~0ull, w);
+            if (cur == ~0ull) cur = w;
+          }
+          if (cur == w) {
+            slot = j;
+            break;
+          }
+        }
+        cw1 = cw0;
+        cs1 = cs0;
+        cw0 = w;
+        cs0 = slot;
       }
-      if (cur == w) {
-        slot = j;
-        break;
+      if (slot >= 0) {
+        // transposed window layout: destination b of the window is bit b >> 7
+        // of word b & 127, so the consecutive destinations of a warp's lanes
+        // hit 32 different words (banks) instead of one
+        const uint32_t bit = 1u << (d & 31);
+        if (atom_or_shared(&s_bits[slot * kWinWords + (int)((d >> 5) & (kWinWords - 1))], bit) & bit) dup = true;
+      } else {
+        const uint32_t bit = 1u << (d & 31);
+        if (atomicOr(&claim[d >> 5], bit) & bit) dup = true;
       }
-    }
-    const uint32_t bit = 1u << (d & 31);
-    if (slot >= 0) {
-      if (atomicOr(&s_bits[slot * kWinWords + (int)((d >> 5) & (kWinWords - 1))], bit) & bit) dup = true;
-    } else if (atomicOr(&claim[d >> 5], bit) & bit) {
-      dup = true;
+    } else {
+      // no locality to privatise: a fire-and-forget reduction (RED, no
+      // return trip); duplicates show up as fewer distinct bits than pairs
+      // (k_claim_count)
+      atomicOr(&claim[d >> 5], 1u << (d & 31));
     }
     out[d] = v;
+  };
+  // striped: a warp's stores cover 32 consecutive sources.  Separate loops
+  // for the staged and the ragged tile: a select between a shared and a
+  // global pointer would make every access a generic one
+  if (full) {
+    for (int k = t; k < kScTile; k += 256) one((long long)s_is[k], s_vs[k]);
+  } else {
+    for (int k = t; k < cnt; k += 256) one((long long)is[base + k], vs[base + k]);
+  }
+  if constexpr (!kPriv) {
+    if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
+    return;
   }
   __syncthreads();
-  // merge the touched windows: one coalesced atomicOr per non-zero word
-  for (int q = t; q < kWinSlots * kWinWords; q += 256) {
-    const unsigned long long w = s_win[q / kWinWords];
-    const uint32_t word = s_bits[q];
-    if (w != ~0ull && word && (atomicOr(&claim[w * kWinWords + (q % kWinWords)], word) & word)) dup = true;
+  // merge the touched windows: global word q of a window holds destinations
+  // 32q .. 32q+31, i.e. bit q >> 2 of the shared words (32q + j) & 127 --
+  // transposed back with 32 broadcast reads, then ONE coalesced atomicOr
+  // per non-zero word
+  for (int gq = t; gq < kWinSlots * kWinWords; gq += 256) {
+    const int slot = gq / kWinWords, q = gq % kWinWords;
+    const unsigned long long w = s_win[slot];
+    if (w == ~0ull) continue;
+    const uint32_t word = s_bits[gq];
+    if (word && (atomicOr(&claim[w * kWinWords + q], word) & word)) dup = true;
   }
   if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
 }
@@ -136,8 +212,9 @@ __global__ void __launch_bounds__(256) k_scatter_ti(E* __restrict__ out, long lo
       mbar_init(&s_mbar, 1);
       mbar_fence_init();
       mbar_expect_tx(&s_mbar, (uint32_t)PcSmem<I, E>::BYTES);
-      bulk_g2s(s_is, is + base, kScTile * (uint32_t)sizeof(I), &s_mbar);
-      bulk_g2s(s_vs, vs + base, kScTile * (uint32_t)sizeof(E), &s_mbar);
+      const uint64_t pol = l2_evict_first_policy();
+      bulk_g2s_ef(s_is, is + base, kScTile * (uint32_t)sizeof(I), &s_mbar, pol);
+      bulk_g2s_ef(s_vs, vs + base, kScTile * (uint32_t)sizeof(E), &s_mbar, pol);
     }
     __syncthreads();
     mbar_wait(&s_mbar, 0);
@@ -184,27 +261,58 @@ __global__ void __launch_bounds__(kGThreads) k_scatter_verify_i(const E* __restr
   }
 }
 
+// Duplicate detection by counting (the claims of k_scatter_pc<.., false>):
+// the in-range pairs (*d_m, all of them in range after binning) claimed
+// fewer distinct destinations than there are pairs iff some destination was
+// claimed twice.  Grid-wide popcount of the bitmap; the last CTA decides.
+__global__ void __launch_bounds__(kGThreads) k_claim_count(const uint32_t* __restrict__ claim, long long nwords,
+                                                            const long long* __restrict__ d_m,
+                                                            unsigned long long* __restrict__ acc, LBHeader* hdr) {
+  __shared__ bool s_last;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += stride) c += __popc(claim[q]);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  if (lane_id() == 0 && c) atomicAdd(acc, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&hdr->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long distinct = atomicAdd(acc, 0ull);
+    if (distinct != (unsigned long long)*d_m) atomicExch(&hdr->dup, 1u);
+    *acc = 0;
+    hdr->done = 0;
+  }
+}
+
 // ------------------------------------------------------------------ binning
-// Locality probe: 64 sample runs of 256 consecutive indices; a run of
-// indices with locality changes 4096-destination window a handful of times,
-// a random one at almost every element.  *flag = 1 (bin) when the samples
-// average more than 32 window changes per 256 indices.
+// Locality probe: 64 sample runs of 256 consecutive indices; each warp
+// counts the distinct 4096-destination windows among its 32 (match_any
+// leaders).  Indices with locality -- C3's two interleaved monotone streams
+// -- touch 2-4 windows per warp, a random permutation ~32.  *flag = 1 (bin)
+// when the samples average more than 8 distinct windows per warp.
 __global__ void __launch_bounds__(256) k_scatter_probe(const long long* __restrict__ is, long long m,
                                                        int* __restrict__ flag) {
-  __shared__ int s_changes;
-  if (threadIdx.x == 0) s_changes = 0;
+  __shared__ int s_distinct;
+  if (threadIdx.x == 0) s_distinct = 0;
   __syncthreads();
-  int changes = 0;
+  int distinct = 0;
   for (int sIdx = 0; sIdx < 64; ++sIdx) {
-    const long long start = (m - 257) * sIdx / 63;
-    const long long i = start + threadIdx.x + 1;
-    if (start >= 0 && i < m) changes += ((is[i] >> kWinBits) != (is[i - 1] >> kWinBits)) ? 1 : 0;
+    const long long start = (m - 256) * sIdx / 63;
+    const long long w = is[start + threadIdx.x] >> kWinBits;
+    const unsigned peers = __match_any_sync(0xffffffffu, w);
+    distinct += (__ffs(peers) - 1 == lane_id()) ? 1 : 0;  // one leader per distinct window
   }
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) changes += __shfl_xor_sync(0xffffffffu, changes, d);
-  if (lane_id() == 0) atomicAdd(&s_changes, changes);
+  for (int d = 16; d > 0; d >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, d);
+  if (lane_id() == 0) atomicAdd(&s_distinct, distinct);
   __syncthreads();
-  if (threadIdx.x == 0) *flag = s_changes > 64 * 32 ? 1 : 0;
+  if (threadIdx.x == 0) *flag = s_distinct > 64 * 8 * 8 ? 1 : 0;  // 64 samples x 8 warps x 8 windows
 }
 
 // pass 0 (CHECKED / unknown counts): pairs per destination window

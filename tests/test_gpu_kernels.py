@@ -541,9 +541,9 @@ def test_scatter_layouts(cuda, monkeypatch, layout, kind, n, dtype):
     is2 = is_.copy()
     is2[::7] = -1
     is2[3::11] = n + 5
-    is2[1::13] = is2[0]  # many duplicates of one destination ...
+    is2[1::13] = is_[2]  # many duplicates of one destination ...
     vs2 = vs.copy()
-    vs2[1::13] = vs2[0]  # ... all with its value: legal
+    vs2[1::13] = vs[2]  # ... all with its value (position 2 keeps it too): legal
     dst = np.full(n + 3, 9, dtype)
     want2 = O.scatter(dst.astype(np.int64), is2, vs2)
     st = ops.Status(cuda)
