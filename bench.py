@@ -241,6 +241,19 @@ class C2:
             return []
         return [(L.K_SEGSUM, 8 * self.k, "k_segsum_b<int32,int32> (sgmSum over ys, flags from the mkFlags bitmap)")]
 
+    def checked_families(self):
+        """CHECKED C2: the scans (filter offsets -> inds i64, mkFlags starts,
+        sgmSum over the i64 flag array) and the checked scatters (ys, flags);
+        bytes = what each launch must read and write."""
+        from paper_2506_23058_b200 import _lib as L
+
+        n, m, k = self.N, self.m, self.k
+        return [(L.K_SCAN, 12 * n + 16 * m + 16 * k, "k_scan x3 (pred -> inds, shape starts, sgmSum)"),
+                (L.K_SCATTER, 12 * n + 4 * k + 24 * m, "k_scatter_pc x2 (ys, flags; privatised claims)")]
+
+    def checked_launches(self, kid):
+        return 3 if kid == 4 else 2
+
     def e2e_step(self, bufs):
         """pinned host -> device, pipeline, k -> host, ys/zs -> host."""
         from paper_2506_23058_b200 import ops
@@ -353,7 +366,15 @@ class C1:
         self.ys = torch.empty(self.N, dtype=torch.int32, device=dev)
         self.dnt = torch.empty(1, dtype=torch.int64, device=dev)
         self.st = ops.Status(dev)
-        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if not self.big else None
+        self.sets = None
+        if not self.big:
+            # C1's 8 MB working set would stay in the 126 MB L2: the steps
+            # rotate over 32 copies of (xs, ys) -- 256 MB, twice the L2 -- so
+            # every step starts cold, with no flush kernel between the steps
+            # (whose shared-memory reconfiguration would sit inside the next
+            # step's start event)
+            self.sets = [(self.xs.clone(), torch.empty_like(self.ys), torch.empty_like(self.dnt)) for _ in range(32)]
+            self.turn = 0
         if self.ws > 1:
             from paper_2506_23058_b200 import dist as D
 
@@ -373,12 +394,6 @@ class C1:
                               if self.exchange == "fused" else f"; exchange: one NCCL all-to-all per class "
                               f"({self.exchange})")
 
-    def pre_step(self):
-        """between timed steps, outside the timed region: a 256 MB write
-        evicts the 126 MB L2 (the 2^20 working set would stay resident)"""
-        if self.flush is not None:
-            self.flush.zero_()
-
     def step(self, variant):
         from paper_2506_23058_b200 import ops
 
@@ -390,6 +405,9 @@ class C1:
             else:
                 self.nt_global, self.runs, self.mine = D.partition2_sharded(self.local, exchange=True)
             return
+        if self.sets is not None:
+            self.xs, self.ys, self.dnt = self.sets[self.turn]
+            self.turn = (self.turn + 1) % len(self.sets)
         ops.partition2(self.xs, self.p, variant, self.st, ys=self.ys, d_nt=self.dnt)
 
     def check(self, want):
@@ -411,6 +429,15 @@ class C1:
         # algorithmic bytes: xs read once, ys written once (the kernel reads xs
         # once per class segment; `traffic` shows the measured DRAM bytes)
         return L.K_PLACE, 8 * self.N, "k_filter_b<int32,NS=2> (stable partition: 2 class segments on one look-back chain)"
+
+    def checked_families(self):
+        """CHECKED partition2: the index scan (pred -> inds i64) and the
+        checked scatter (claims privatised per tile)."""
+        from paper_2506_23058_b200 import _lib as L
+
+        n = self.N
+        return [(L.K_SCAN, 12 * n, "k_scan (pred -> indices i64)"),
+                (L.K_SCATTER, 16 * n, "k_scatter_pc (indices + xs -> ys; privatised claims)")]
 
     def e2e_bufs(self, variant):
         import torch
@@ -470,6 +497,46 @@ class C1:
         ys_p.copy_(self.ys, non_blocking=True)
         int(self.dnt.item())
         return 4 * self.N, 4 * self.N + 8
+
+    def dropin(self):
+        """C1 as BASELINE configs[0] states it: the program run through the
+        drop-in eval_program (oracle.py:332-333 signature) with a Python list
+        argument, verifier-selected variants, a Python list result -- and
+        where the time of such a call goes."""
+        import json as _json
+
+        import torch
+
+        from paper_2506_23058_b200 import executor, ir
+
+        with open(os.path.join(ROOT, "paper_2506_23058_b200", "data", "programs.json")) as f:
+            prog = ir.from_json(_json.load(f)["ref:partition2.ixl"]["program"])
+        xs_list = self.xs_h.astype(np.int64).tolist()
+        dev = torch.device("cuda")
+
+        def med(fn, reps=7):
+            ts = []
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r = fn()
+                torch.cuda.synchronize()
+                ts.append(time.perf_counter() - t0)
+            return statistics.median(ts) * 1e3, r
+
+        t_call, (nt, ys) = med(lambda: executor.eval_program(prog, "partition2", [self.p, xs_list]))
+        ok = nt == int((self.xs_h < 0).sum()) and len(ys) == len(xs_list)
+        t_marshal, xd = med(lambda: executor._dev_i64(xs_list, dev))
+        t_dev, _ = med(lambda: executor.eval_program(prog, "partition2", [self.p, xd], as_tensors=True))
+        yd = executor.eval_program(prog, "partition2", [self.p, xd], as_tensors=True)[1]
+        t_ret, _ = med(lambda: yd.cpu().numpy().tolist())
+        return {"value": round(self.N / (t_call * 1e-3) / 1e9, 4), "unit": "Gelem/s",
+                "ms_per_call": round(t_call, 3), "result_ok": bool(ok),
+                "call": "paper_2506_23058_b200.eval_program(partition2.ixl, 'partition2', [Pred(x < 0), list of 2^20 "
+                        "ints]) -> (int, list): selection, marshalling, kernels, status read, list result",
+                "shares_ms": {"marshal_list_to_device": round(t_marshal, 3),
+                              "device_call_incl_dispatch_and_status_read": round(t_dev, 3),
+                              "result_to_list": round(t_ret, 3)}}
 
     def cpu_run(self, xs, threads=0):
         from oracle import ixoracle as O
@@ -543,6 +610,15 @@ class C3:
         else:
             self.out.copy_(self.dst)  # dst init (the reference copies dst, oracle.py:295)
             ops.scatter(self.out, self.is_, self.vs, L.V_CONFLICT | L.V_INIT, self.st)
+
+    def checked_families(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        fams = [(L.K_SCATTER, 16 * self.N, "k_scatter_pc (claims privatised in shared-memory windows)"
+                 if self.perm != "random" else "k_scatter_pc<u32> over the binned pairs (8 + 4 + 4 B)")]
+        if self.perm == "random":
+            fams.append((L.K_BIN, 20 * self.N, "k_bin_partition (12 B in, 8 B binned pairs out)"))
+        return fams
 
     def check(self, want):
         import torch
@@ -676,6 +752,11 @@ class C4:
         from paper_2506_23058_b200 import _lib as L
 
         return L.K_CSR_GATHER, 16 * self.N + 4 * self.ncols, "k_csr_gather<int32>"
+
+    def checked_families(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        return [(L.K_CSR_GATHER, 16 * self.N + 4 * self.ncols, "k_csr_gather (every x[c] bounds-checked)")]
 
     def l2_ceiling(self, kms):
         """C4's binding roof is L2's random-sector rate, not HBM: measured
@@ -920,7 +1001,12 @@ def run_ours(args):
         wl.step(selected)
     torch.cuda.synchronize()
     kid, kbytes, kname = wl.kernel()
-    ms, launches, kms = time_steps(wl, selected, args.steps, args.warmup, ws, kid)
+    # the step on its own (nothing but the pipeline's launches in the stream),
+    # then the dominant kernel's duration from a second pass with event
+    # pairs around each of its launches (events between kernels would also
+    # serialise programmatic dependent launch)
+    ms, launches, _ = time_steps(wl, selected, args.steps, args.warmup, ws)
+    _, _, kms = time_steps(wl, selected, args.steps, args.warmup, ws, kid)
     clocks = sampler.stop()
     others = []
     for okid, obytes, oname in (wl.kernels_extra() if hasattr(wl, "kernels_extra") else []):
@@ -930,9 +1016,22 @@ def run_ours(args):
                            "achieved": round(obytes / (oms * 1e-3) / 1e9, 1),
                            "frac": round(obytes / (oms * 1e-3) / 1e9 / hbm, 4)})
     ms_chk = parity_chk = None
+    chk_fams = []
     if ws == 1:  # the CHECKED pipeline is single-GPU (the sharded path is the verified one)
         ms_chk, _, _ = time_steps(wl, L.VARIANT_CHECKED, max(3, args.steps // 4), 2, ws)
         parity_chk = wl.check(want)
+        # the CHECKED step's kernel families: device time per step (events on
+        # the launching stream around every launch of the family) against the
+        # bytes those launches must move
+        for fkid, fbytes, fname in (wl.checked_families() if hasattr(wl, "checked_families") else []):
+            steps_f = max(3, args.steps // 4)
+            _, _, fms_launch = time_steps(wl, L.VARIANT_CHECKED, steps_f, 2, ws, fkid)
+            nl = wl.checked_launches(fkid) if hasattr(wl, "checked_launches") else 1
+            if fms_launch:
+                fms = fms_launch * nl
+                chk_fams.append({"kernels": fname, "ms_per_step": round(fms, 4), "bytes_per_step": int(fbytes),
+                                 "achieved": round(fbytes / (fms * 1e-3) / 1e9, 1),
+                                 "frac": round(fbytes / (fms * 1e-3) / 1e9 / hbm, 4)})
 
     # e2e: pinned host buffers, copies inside the timed region
     e2e_steps = max(3, min(args.steps, 10))
@@ -983,6 +1082,10 @@ def run_ours(args):
             "ms_per_step": round(ms_chk, 4),
             "value": round(units_total / (ms_chk * 1e-3) / 1e9, 3),
             "elided_speedup": round(ms_chk / ms, 3),
+            # the program's algorithmic bytes over the CHECKED step (what the
+            # reference's behaviour costs on this GPU), and per kernel family
+            "roofline": {"step_frac": round(wl.algo_bytes_step() / (ms_chk * 1e-3) / 1e9 / hbm, 4),
+                         "families": chk_fams},
         } if ms_chk else None,
         "roofline": {
             "bound": "hbm",
@@ -1014,6 +1117,12 @@ def run_ours(args):
         "clocks": clocks,
         "gpu_launches": int(launches),
     }
+    dr = getattr(wl, "dropin", None)
+    if dr is not None and ws == 1 and not wl.big:
+        try:
+            line["dropin"] = dr()
+        except Exception as e:  # informational
+            line["dropin"] = {"unavailable": f"{type(e).__name__}: {e}"}
     l2c = getattr(wl, "l2_ceiling", None)
     if l2c is not None and kms:
         try:
@@ -1034,7 +1143,7 @@ def config_of(wl, ws) -> dict:
         "workload": wl.workload,
         "variant": "verifier-selected (ELIDED: Sc1 scatters fused, mkFlags Ss2)",
         "parallelism": f"shards{ws}" if ws > 1 else "single",
-        "l2": ("256 MB L2 flush write between steps, outside the per-step events (8 MB working set)"
+        "l2": ("steps rotate over 32 copies of the 8 MB working set (256 MB > the 126 MB L2): cold inputs, no flush"
                if wl.name == "c1" else "inputs larger than the 126 MB L2, no flush"),
     }
 

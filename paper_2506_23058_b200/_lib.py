@@ -134,11 +134,20 @@ def load(require_device: bool = False):
                 fn.restype = res
                 fn.argtypes = args
             _lib = lib
-    if require_device:
+    if require_device and not _device_ok:
         rc = _lib.ixg_device_check()
         if rc != OK:
             raise NativeUnavailable("libixgpu.so needs an sm_100 (B200) CUDA device; none is current")
+        _set_device_ok()
     return _lib
+
+
+_device_ok = False  # an sm_100 device was found once (every op call used to re-query it)
+
+
+def _set_device_ok():
+    global _device_ok
+    _device_ok = True
 
 
 def check(rc: int, what: str) -> None:

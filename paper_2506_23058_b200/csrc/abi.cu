@@ -275,6 +275,16 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
 }
 
 // --------------------------------------------------------------- filter
+// IXG_PDL=0: launch the big-tile kernels without programmatic dependent launch (A/B)
+inline bool pdl_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_PDL");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
 // IXG_SEG_SPLIT=1: C2 as two passes (filter, then sgmSum over ys) for A/B
 inline bool seg_split_mode() {
   static int mode = -1;
@@ -295,9 +305,22 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
   allow_smem(kern, Big<T>::SMEM, attr);
   TimedLaunch tl(NS > 1 ? IXG_K_PLACE : IXG_K_FILTER_FUSED, s);
   const long long seg_tiles = tiles_of(n, Big<T>::TILE);
-  kern<<<(unsigned)(NS * seg_tiles), kBT + 32, Big<T>::SMEM, s>>>(xs, cs, n, p, ys, ch, next_nonce(), d_count, zs,
-                                                                  segbits, out_base, ch2, st, q, seg_tiles, po);
+  // programmatic dependent launch: the CTAs become resident while the
+  // previous kernel of the stream drains (k_filter_b waits for it itself)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(NS * seg_tiles));
+  cfg.blockDim = dim3(kBT + 32);
+  cfg.dynamicSmemBytes = Big<T>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, xs, cs, n, p, ys, ch, next_nonce(), d_count, zs, segbits, out_base,
+                                     ch2, st, q, seg_tiles, po);
   LAUNCHED();
+  if (e != cudaSuccess) return cuda_rc(e);
   CHECK_LAUNCH();
   return IXG_OK;
 }

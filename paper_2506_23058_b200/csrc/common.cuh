@@ -62,6 +62,15 @@ IXG_DEV void bar_sync(int id, int nthreads) {
 IXG_DEV void bar_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in
+// the stream still runs; pdl_wait() blocks the calling thread until the
+// predecessor grid has completed and its writes are visible (a no-op for a
+// kernel launched without a programmatic dependency).  pdl_trigger() lets
+// this grid's dependents launch once every CTA of this grid has issued it.
+IXG_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+IXG_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 IXG_DEV int lane_id() { return threadIdx.x & 31; }
 IXG_DEV int warp_id() { return threadIdx.x >> 5; }
 

@@ -611,6 +611,14 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   const int seg = NS > 1 ? (int)(tile / seg_tiles) : 0;
   const long long tile_base = (NS > 1 ? tile - seg * seg_tiles : tile) * B::TILE;
   const int t = threadIdx.x;
+  // PDL (launch_filter_b): the next kernel of the stream may be scheduled
+  // now; this one waits for its predecessor before touching anything the
+  // predecessor writes -- the look-back slots (shared by consecutive
+  // launches on one workspace) and outputs at once, except C2 (kSeg), whose
+  // predecessor is the mkFlags scan: only the bitmap depends on it, so the
+  // tile's load, count and compaction overlap the scan's tail
+  pdl_trigger();
+  if constexpr (!kSeg) pdl_wait();
   if (warp_id() == kBW) {  // look-back warp
     if (kSeg && lane_id() == 0) {
       mbar_init(&s_mbar_bits, 1);
@@ -629,6 +637,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
         // (bitmap_bytes() pads the bitmap past its last word)
         const long long wb = ((out_base + ex) >> 5) & ~3LL;
         s_wbase = wb;
+        pdl_wait();  // the mkFlags scan (the predecessor) has written the bitmap
         mbar_expect_tx(&s_mbar_bits, kBitsW * 4u);
         bulk_g2s(s_bits, segbits + wb, kBitsW * 4u, &s_mbar_bits);
       }

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(kGThreads, 3) k_scan(long long n, const long l
   __shared__ T s_w[kGThreads / 32];
   __shared__ T s_carry;
   __shared__ long long s_tile;
+  pdl_trigger();  // a PDL dependent (C2's fused kernel) may start its own loads now
   if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ch.hdr->ticket, 1u);
   if (d_n) n = *d_n;
   __syncthreads();

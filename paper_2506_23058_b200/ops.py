@@ -26,11 +26,18 @@ def _lib():
 
 
 def _ptr(t: Optional[torch.Tensor]):
-    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else ctypes.c_void_p(0)
+    """a tensor's device address for a void* argument (plain int: ctypes
+    converts it without a wrapper object)"""
+    return t.data_ptr() if t is not None and t.numel() > 0 else None
+
+
+_raw_stream = torch._C._cuda_getCurrentRawStream
 
 
 def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    """the current CUDA stream as a void* (the cheap raw query: a launch-bound
+    call such as C1's 2^20 partition2 spends its time here otherwise)"""
+    return _raw_stream(torch.cuda.current_device())
 
 
 def _dt(t: torch.Tensor) -> int:
@@ -40,13 +47,22 @@ def _dt(t: torch.Tensor) -> int:
         raise TypeError(f"unsupported dtype {t.dtype}") from None
 
 
+_PRED_CACHE: dict = {}
+
+
 def _c_pred(p: Pred) -> L.ixg_pred:
     if not isinstance(p, Pred):
         raise TypeError(
             "predicate arguments must be paper_2506_23058_b200.Pred descriptors "
             f"(got {type(p).__name__}); opaque Python callables cannot run on the device"
         )
-    return L.ixg_pred(p.kind, 0, p.thr, p.seed & ((1 << 64) - 1))
+    key = (p.kind, p.thr, p.seed)
+    c = _PRED_CACHE.get(key)
+    if c is None:
+        if len(_PRED_CACHE) > 1024:
+            _PRED_CACHE.clear()
+        c = _PRED_CACHE[key] = L.ixg_pred(p.kind, 0, p.thr, p.seed & ((1 << 64) - 1))
+    return c
 
 
 def _contig(t: torch.Tensor) -> torch.Tensor:
@@ -68,11 +84,18 @@ class Workspace:
 
     def __init__(self):
         self._bufs: dict = {}
+        self._need: dict = {}
 
     def get(self, op: int, n: int, m: int, device) -> torch.Tensor:
-        need = int(_lib().ixg_ws_bytes(op, n, m))
+        need = self._need.get((op, n, m))
+        if need is None:
+            if len(self._need) > 4096:
+                self._need.clear()
+            need = self._need[(op, n, m)] = int(_lib().ixg_ws_bytes(op, n, m))
         dev = device.index if isinstance(device, torch.device) else device
-        key = (dev, op, torch.cuda.current_stream(device).cuda_stream)
+        if dev is None:
+            dev = torch.cuda.current_device()
+        key = (dev, op, _raw_stream(dev))
         ent = self._bufs.get(key)
         if ent is None or ent[1].numel() < need:
             buf = torch.zeros(max(need, 4096), dtype=torch.uint8, device=device)
@@ -89,7 +112,7 @@ WS = Workspace()
 
 def _ws(op: int, n: int, m: int, device):
     buf = WS.get(op, n, m, device)
-    return ctypes.c_void_p(buf.data_ptr()), ctypes.c_size_t(buf.numel())
+    return buf.data_ptr(), buf.numel()
 
 
 # ------------------------------------------------------------------ status
@@ -253,7 +276,7 @@ def hist(op: int, ne: int, dlen: int, is_: torch.Tensor, vs: torch.Tensor, statu
     128 bits; with a Status, a bin whose sum leaves int64 is recorded."""
     is_, vs = _contig(is_), _contig(vs)
     out = torch.empty(max(dlen, 0), dtype=torch.int64, device=is_.device)
-    ws, wsb = _ws(L.OP_HIST, 0, max(dlen, 0), is_.device) if op == L.HIST_ADD else (_ptr(None), ctypes.c_size_t(0))
+    ws, wsb = _ws(L.OP_HIST, 0, max(dlen, 0), is_.device) if op == L.HIST_ADD else (None, 0)
     st = status.ptr if status is not None else _ptr(None)
     L.check(
         _lib().ixg_hist(op, ne, dlen, _ptr(is_), is_.numel(), _ptr(vs), vs.numel(), _ptr(out), ws, wsb, st, _stream()),

@@ -604,3 +604,39 @@ def test_two_streams_concurrently(cuda):
         res = (ya[: int(dka.item())], yb[: int(dkb.item())], ca, cb)
         assert np.array_equal(_np(res[0]), O.filter_(p, xa)) and np.array_equal(_np(res[1]), O.filter_(p, xb))
         assert np.array_equal(_np(res[2]), O.scan_add(xa, 5)) and np.array_equal(_np(res[3]), O.scan_add(xb, 5))
+
+
+def test_back_to_back_launches(cuda):
+    """Consecutive big-tile kernels on one stream overlap their launch with
+    programmatic dependent launch (each waits for its predecessor in-kernel;
+    C2's fused kernel only before it reads the bitmap): 48 pipelines queued
+    without a host sync, on one shared workspace per op, every result exact."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    n, m = 300_001, 700
+    runs = []
+    for i in range(16):
+        xs = gen.uniform(100 + i, n, -128, 127, np.int32)
+        k = int((xs >= 0).sum())
+        shape = gen.segment_shape(200 + i, m, k)
+        runs.append((xs, shape, _t(xs, cuda), _t(shape, cuda)))
+    torch.cuda.synchronize()
+    outs = []
+    st = ops.Status(cuda)
+    for xs, shape, xd, sd in runs:
+        p2 = ops.partition2(xd, Pred.lt(0), L.VARIANT_ELIDED, st)
+        f = ops.filter(xd, Pred.ge(3), L.VARIANT_ELIDED, st)
+        c = ops.c2(xd, Pred.ge(0), sd, L.VARIANT_ELIDED, st)
+        outs.append((p2, f, c))
+    torch.cuda.synchronize()
+    assert st.read().ok
+    for (xs, shape, _, _), ((ys, dnt), (fy, fk), (cy, cz, ck)) in zip(runs, outs):
+        nt, want = O.partition2(Pred.lt(0), xs)
+        assert int(dnt.item()) == nt and np.array_equal(_np(ys).astype(np.int64), want)
+        kf = int(fk.item())
+        assert np.array_equal(_np(fy[:kf]).astype(np.int64), O.filter_(Pred.ge(3), xs))
+        wy, wz = O.c2(Pred.ge(0), xs, shape)
+        kc = int(ck.item())
+        assert np.array_equal(_np(cy[:kc]).astype(np.int64), wy) and np.array_equal(_np(cz[:kc]).astype(np.int64), wz)
