@@ -323,8 +323,18 @@ IXG_DEV uint32_t flag_mask(const SegOp::T (&v)[kGItems]) {
 // the last CTA to retire resets the ticket for the next launch.  `d_n`
 // (nullable): the element count known only on the device (a count pass
 // before it) -- the grid covers the capacity, surplus tiles retire at once.
+// resident CTAs per SM the registers must allow: 4 for the one-word monoid
+// (64 registers), 3 for the two-word ones
+#ifndef IXG_SCAN_MINB
+#define IXG_SCAN_MINB 4
+#endif
+template <class M>
+constexpr int scan_min_blocks() {
+  return std::is_same<M, SumOp>::value ? IXG_SCAN_MINB : 3;
+}
+
 template <class M, class Src, class Epi>
-__global__ void __launch_bounds__(kGThreads, 3) k_scan(long long n, const long long* __restrict__ d_n, Src src, Epi epi,
+__global__ void __launch_bounds__(kGThreads, scan_min_blocks<M>()) k_scan(long long n, const long long* __restrict__ d_n, Src src, Epi epi,
                                                     LBChan ch, uint32_t nonce) {
   using T = typename M::T;
   __shared__ T s_w[kGThreads / 32];
