@@ -248,11 +248,15 @@ class C2:
         from paper_2506_23058_b200 import _lib as L
 
         n, m, k = self.N, self.m, self.k
-        return [(L.K_SCAN, 12 * n + 16 * m + 16 * k, "k_scan x3 (pred -> inds, shape starts, sgmSum)"),
+        return [(L.K_SEGSUM, 12 * n + 16 * k, "k_segsum_b x2 (pred -> offs -> inds i64; sgmSum over the i64 "
+                                              "flag array + ys -> zs), big-tile scans"),
+                (L.K_SCAN, 16 * m, "k_scan (mkFlags segment starts)"),
                 (L.K_SCATTER, 12 * n + 4 * k + 24 * m, "k_scatter_pc x2 (ys, flags; privatised claims)")]
 
     def checked_launches(self, kid):
-        return 3 if kid == 4 else 2
+        from paper_2506_23058_b200 import _lib as L
+
+        return {L.K_SEGSUM: 2, L.K_SCATTER: 2}.get(kid, 1)
 
     def e2e_step(self, bufs):
         """pinned host -> device, pipeline, k -> host, ys/zs -> host."""
@@ -436,7 +440,8 @@ class C1:
         from paper_2506_23058_b200 import _lib as L
 
         n = self.N
-        return [(L.K_SCAN, 12 * n, "k_scan (pred -> indices i64)"),
+        return [(L.K_CLASS_COUNT, 4 * n, "k_class_count (num_true)"),
+                (L.K_SEGSUM, 12 * n, "k_segsum_b<ScanPart2Inds> (pred -> indices i64, big-tile scan)"),
                 (L.K_SCATTER, 16 * n, "k_scatter_pc (indices + xs -> ys; privatised claims)")]
 
     def e2e_bufs(self, variant):

@@ -285,6 +285,17 @@ inline bool pdl_enabled() {
   return mode == 1;
 }
 
+// IXG_BIG_SCAN=0: the CHECKED index scans on the generic k_scan instead of
+// the big-tile kernel (A/B)
+inline bool big_scan_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_BIG_SCAN");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
 // IXG_SEG_SPLIT=1: C2 as two passes (filter, then sgmSum over ys) for A/B
 inline bool seg_split_mode() {
   static int mode = -1;
@@ -326,17 +337,17 @@ int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred&
 }
 
 // zs = sgmSum over the first *d_n elements of vs (capacity n)
-template <typename T, typename Z, class M = SegOp>
+template <typename T, typename Z, class M = SegOp, class F = ScanId>
 int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32_t* bits, long long flag_base, Z* zs,
                     LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s,
-                    const long long* d_flag_base = nullptr) {
-  auto kern = k_segsum_b<T, Z, M>;
+                    const long long* d_flag_base = nullptr, F fn = F{}) {
+  auto kern = k_segsum_b<T, Z, M, F>;
   using B = Big<T, kSegsumCH<T, Z>>;
   static std::atomic<unsigned long long> attr{0};
   allow_smem(kern, B::SMEM, attr);
   TimedLaunch tl(IXG_K_SEGSUM, s);
   kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, d_flag_base, zs, ch,
-                                                                  next_nonce(), carry_v, carry_f, d_total, st);
+                                                                  next_nonce(), carry_v, carry_f, d_total, st, fn);
   LAUNCHED();
   CHECK_LAUNCH();
   return IXG_OK;
@@ -363,7 +374,18 @@ int do_filter(const T* xs, const uint8_t* cs, long long n, const ixg_pred* p, T*
   long long* inds = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<T>(ys, 0, d_count, n, inds, xs, n, sb, 1, 1, st, ws, 1, s);
   if (n <= 0) return cuda_rc(cudaMemsetAsync(d_count, 0, sizeof(long long), s));
-  int rc = launch_scan<SumOp>(n, SrcPredT<T>{xs, cs, pp}, EpiFilterInds{inds, d_count}, c0, s);
+  int rc;
+  if (!cs && big_scan_enabled() && aligned16(xs) && aligned32(inds)) {
+    // the big-tile scan (TMA tiles, dedicated look-back warp) with the
+    // predicate in front and the index formula behind
+    ScanFilterInds<T> fn{};
+    fn.pb.p = pp;
+    fn.d_count = d_count;
+    rc = launch_segsum_b<T, long long, SumOp>(xs, n, nullptr, nullptr, 0, inds, c0, 0, 0, nullptr, nullptr, s, nullptr,
+                                              fn);
+  } else {
+    rc = launch_scan<SumOp>(n, SrcPredT<T>{xs, cs, pp}, EpiFilterInds{inds, d_count}, c0, s);
+  }
   if (rc) return rc;
   if (sb & IXG_V_INIT) {
     if ((rc = launch_fill<T>(ys, 0, d_count, T(0), s))) return rc;
@@ -402,12 +424,23 @@ int do_partition(const T* xs, long long n, const ixg_pred* p, const ixg_pred* q,
   long long* inds = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<T>(ys, n, nullptr, n, inds, xs, n, sb, scatter_site, scatter_site, st, ws, 1, s);
   if (n <= 0) return cuda_rc(cudaMemsetAsync(d_tot, 0, sizeof(long long) * (kClasses - 1), s));
-  k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
+  {
+    TimedLaunch tl(IXG_K_CLASS_COUNT, s);
+    k_class_count<T, kClasses><<<cgrid, kSThreads, 0, s>>>(xs, n, pp, qq, partials, ws.hdr(5), d_tot);
+  }
   LAUNCHED();
   CHECK_LAUNCH();
   int rc;
   if constexpr (kClasses == 2) {
-    rc = launch_scan<SumOp>(n, SrcPredT<T>{xs, nullptr, pp}, EpiPart2Inds{d_tot, inds}, c0, s);
+    if (big_scan_enabled() && aligned16(xs) && aligned32(inds)) {
+      ScanPart2Inds<T> fn{};
+      fn.pb.p = pp;
+      fn.d_nt = d_tot;
+      rc = launch_segsum_b<T, long long, SumOp>(xs, n, nullptr, nullptr, 0, inds, c0, 0, 0, nullptr, nullptr, s,
+                                                nullptr, fn);
+    } else {
+      rc = launch_scan<SumOp>(n, SrcPredT<T>{xs, nullptr, pp}, EpiPart2Inds{d_tot, inds}, c0, s);
+    }
   } else {
     rc = launch_scan<Sum2Op>(n, SrcClass3T<T>{xs, pp, qq}, EpiPart3Inds{d_tot, inds}, c0, s);
   }
@@ -472,6 +505,11 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
   if ((rc = launch_fill<long long>(flags, 0, d_k, 0LL, s))) return rc;
   if ((rc = launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s))) return rc;
   // sgmSum over the k = *d_k outputs (a capacity-n grid; tiles past k retire)
+  if (big_scan_enabled() && aligned16(ys) && aligned32(zs) && aligned32(flags)) {
+    SegFlagArr fn{};
+    fn.fa = flags;
+    return launch_segsum_b<T, Z, SegOp>(ys, n, d_k, nullptr, 0, zs, cz, 0, 0, nullptr, st, s, nullptr, fn);
+  }
   return launch_scan<SegOp>(n, SrcSegT<long long, T>{flags, ys},
                             EpiSegOut{sizeof(Z) == 4 ? IXG_I32 : IXG_I64, zs, nullptr, st}, cz, s, d_k);
 }

@@ -978,15 +978,95 @@ IXG_DEV int seg_f(const typename M::T& a) {
   else return 0;
 }
 
-template <typename T, typename Z, class M = SegOp>
+// What the scan adds up and what it stores (k_segsum_b's F): ScanId is the
+// plain scan / sgmSum (element = value, output = the running sum, int64
+// overflow checked); the CHECKED pipelines' index scans fuse the predicate
+// map in front and the index formula behind (filter.ixl:9-12,
+// partition2.ixl:9-16), writing the materialised int64 index array at the
+// big-tile kernel's bandwidth.
+struct ScanId {
+  static constexpr bool kOvf = true;
+  static constexpr bool kFlagArr = false;
+  IXG_DEV uint32_t flags16(long long, long long) const { return 0u; }
+  IXG_DEV void init() {}
+  template <typename T>
+  IXG_DEV long long elem(T x) const { return (long long)x; }
+  IXG_DEV long long out(long long run, long long, long long) const { return run; }
+  IXG_DEV void last(long long) const {}
+};
+template <typename T>
+struct PredBit {  // `p x` as 0 / 1 (pred_eval, with the comparison kinds as one interval test)
+  ixg_pred p;
+  PredRange<T> r;
+  IXG_DEV void init() { r = pred_range<T>(p); }
+  IXG_DEV long long bit(T x) const {
+    if (p.kind <= IXG_PRED_NE) return (long long)(((r.test(x) ? 1u : 0u) & (r.keep & 1u)) ^ (r.flip & 1u));
+    return pred_eval(p, (long long)x) ? 1 : 0;
+  }
+};
+// sgmSum over values with the flags of a materialised int64 flag array (the
+// CHECKED C2: mkFlags' scatter result): 16 flags of a
+// thread per chunk through four 256-bit loads
+struct SegFlagArr : ScanId {
+  static constexpr bool kFlagArr = true;
+  const long long* fa;
+  IXG_DEV uint32_t flags16(long long g, long long n) const {
+    uint32_t f = 0;
+    if (g + kSItems <= n && (((uintptr_t)(fa + g)) & 31) == 0) {
+#pragma unroll
+      for (int k = 0; k < kSItems / 4; ++k) {
+        uint32_t r[8];
+        ld256(fa + g + 4 * k, r);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f |= (uint32_t)((r[2 * q] | r[2 * q + 1]) != 0u) << (4 * k + q);
+      }
+    } else {
+      for (int q = 0; q < kSItems; ++q)
+        if (g + q < n) f |= (uint32_t)(fa[g + q] != 0) << q;
+    }
+    return f;
+  }
+};
+
+template <typename T>
+struct ScanFilterInds {  // inds[i] = if p xs[i] then offs[i] - 1 else -1; *d_count = offs[n-1]
+  static constexpr bool kOvf = false;
+  static constexpr bool kFlagArr = false;
+  IXG_DEV uint32_t flags16(long long, long long) const { return 0u; }
+  PredBit<T> pb;
+  long long* d_count;
+  IXG_DEV void init() { pb.init(); }
+  IXG_DEV long long elem(T x) const { return pb.bit(x); }
+  IXG_DEV long long out(long long run, long long xv, long long) const { return xv ? run - 1 : -1; }
+  IXG_DEV void last(long long run) const { *d_count = run; }
+};
+template <typename T>
+struct ScanPart2Inds {  // indices[i] = if p x then indicesT[i] - 1 else i + 1 - indicesT[i] + num_true - 1
+  static constexpr bool kOvf = false;
+  static constexpr bool kFlagArr = false;
+  IXG_DEV uint32_t flags16(long long, long long) const { return 0u; }
+  PredBit<T> pb;
+  const long long* d_nt;
+  long long nt;
+  IXG_DEV void init() {
+    pb.init();
+    nt = *d_nt;
+  }
+  IXG_DEV long long elem(T x) const { return pb.bit(x); }
+  IXG_DEV long long out(long long run, long long xv, long long g) const { return xv ? run - 1 : (g + 1 - run) + nt - 1; }
+  IXG_DEV void last(long long) const {}
+};
+
+template <typename T, typename Z, class M = SegOp, class F = ScanId>
 __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T* __restrict__ vs, long long n,
                                                           const long long* __restrict__ d_n,
                                                           const uint32_t* __restrict__ bits, long long flag_base,
                                                           const long long* __restrict__ d_flag_base,
                                                           Z* __restrict__ zs, LBChan ch, uint32_t nonce,
                                                           long long carry_v, int carry_f, longlong2* d_total,
-                                                          ixg_status* st) {
+                                                          ixg_status* st, F fn = F{}) {
   using B = Big<T, kSegsumCH<T, Z>>;
+  fn.init();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
   __shared__ typename M::T s_w[B::CH][kBW];
@@ -1039,8 +1119,11 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     const long long pos = flag_base + g;
     const long long wd = pos >> 5;
     uint32_t f = 0;
-    if (std::is_same<M, SegOp>::value && g < n && bits)  // SumOp / bits == nullptr: a plain inclusive scan (ixg_scan_add)
+    if constexpr (F::kFlagArr) {  // flags from a materialised int64 array (CHECKED sgmSum)
+      if (g < n) f = fn.flags16(g, n);
+    } else if (std::is_same<M, SegOp>::value && g < n && bits) {  // SumOp / no bits: a plain scan (ixg_scan_add)
       f = (uint32_t)((((uint64_t)__ldg(&bits[wd + 1]) << 32) | (uint64_t)__ldg(&bits[wd])) >> (pos & 31));
+    }
     fl[c] = f & valid_mask(g, n);
   }
   if (!tma) cp_async_wait_all();
@@ -1068,7 +1151,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     const uint32_t tail = fl[c] ? (vm & ~((1u << (31 - __clz(fl[c]))) - 1u)) : vm;
     long long s = 0;
 #pragma unroll
-    for (int j = 0; j < kSItems; ++j) s += ((tail >> j) & 1u) ? (long long)x[j] : 0LL;
+    for (int j = 0; j < kSItems; ++j) s += ((tail >> j) & 1u) ? fn.elem(x[j]) : 0LL;
     a[c] = seg_mk<M>(s, fl[c] != 0);
     typename M::T inc = warp_inclusive<M>(a[c]);
     if (lane_id() == 31) s_w[c][warp_id()] = inc;
@@ -1116,12 +1199,14 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
 #pragma unroll
     for (int j = 0; j < kSItems; ++j) {
       const long long prev = ((fl[c] >> j) & 1u) ? 0LL : run;
-      run = (long long)((unsigned long long)prev + (unsigned long long)(long long)x[j]);
+      const long long xv = fn.elem(x[j]);
+      run = (long long)((unsigned long long)prev + (unsigned long long)xv);
       if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
       // exact: the sequential step prev + x in the reference's unbounded ints
-      if (sizeof(Z) == 8 && (((prev ^ run) & ((long long)x[j] ^ run)) < 0) && g + j < n && ovf_at == LLONG_MAX)
+      if (F::kOvf && sizeof(Z) == 8 && (((prev ^ run) & (xv ^ run)) < 0) && g + j < n && ovf_at == LLONG_MAX)
         ovf_at = g + j;
-      z[j] = (Z)run;
+      if (g + j == n - 1) fn.last(run);
+      z[j] = (Z)fn.out(run, xv, g + j);
     }
     if (g + kSItems <= n) {
       constexpr int ZV = 32 / (int)sizeof(Z);  // elements per 256-bit store
