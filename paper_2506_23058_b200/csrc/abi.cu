@@ -121,13 +121,37 @@ inline uint32_t next_nonce() {
   return v;
 }
 
-// n = element count, or the capacity when d_n (device count) is given
+// IXG_PDL=0: launch the big-tile kernels without programmatic dependent launch (A/B)
+inline bool pdl_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_PDL");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
+// n = element count, or the capacity when d_n (device count) is given;
+// pdl: launched as a programmatic dependent of the previous kernel (k_scan
+// waits for it in-kernel before touching anything)
 template <class M, class Src, class Epi>
-int launch_scan(long long n, Src src, Epi epi, LBChan ch, cudaStream_t s, const long long* d_n = nullptr) {
+int launch_scan(long long n, Src src, Epi epi, LBChan ch, cudaStream_t s, const long long* d_n = nullptr,
+                bool pdl = false) {
   if (n <= 0) return IXG_OK;
   TimedLaunch tl(IXG_K_SCAN, s);
-  k_scan<M, Src, Epi><<<(unsigned)tiles_of(n, kGTile), kGThreads, 0, s>>>(n, d_n, src, epi, ch, next_nonce());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)tiles_of(n, kGTile));
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_scan<M, Src, Epi>, n, d_n, src, epi, ch, next_nonce());
   LAUNCHED();
+  if (e != cudaSuccess) return cuda_rc(e);
   CHECK_LAUNCH();
   return IXG_OK;
 }
@@ -275,16 +299,6 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
 }
 
 // --------------------------------------------------------------- filter
-// IXG_PDL=0: launch the big-tile kernels without programmatic dependent launch (A/B)
-inline bool pdl_enabled() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("IXG_PDL");
-    mode = (e && e[0] == '0') ? 0 : 1;
-  }
-  return mode == 1;
-}
-
 // IXG_BIG_SCAN=0: the CHECKED index scans on the generic k_scan instead of
 // the big-tile kernel (A/B)
 inline bool big_scan_enabled() {
@@ -472,9 +486,14 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     if (ws.dry) return IXG_OK;
     if (n <= 0) return cuda_rc(cudaMemsetAsync(d_k, 0, sizeof(long long), s));
     if (!aligned16(xs) || !aligned16(ys) || !aligned16(zs)) return IXG_BADARG;
+    // the fused kernel is the mkFlags scan's programmatic dependent: its CTAs
+    // load, count and compact while the scan runs and wait only before they
+    // read the bitmap (a kernel clearing the bitmap instead of the memset, to
+    // chain all three launches, measured no faster)
     cudaMemsetAsync(bits, 0, bitmap_bytes(n), s);
     LAUNCHED();
-    int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr, nullptr}, cs, s);
+    int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr, nullptr},
+                                cs, s);
     if (rc) return rc;
     if constexpr (sizeof(Z) == sizeof(T)) {
       if (!seg_split_mode()) {

@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(kGThreads, scan_min_blocks<M>()) k_scan(long l
   __shared__ T s_carry;
   __shared__ long long s_tile;
   pdl_trigger();  // a PDL dependent (C2's fused kernel) may start its own loads now
+  pdl_wait();     // launched as a PDL dependent (C2's mkFlags scan): the predecessor is done
   if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&ch.hdr->ticket, 1u);
   if (d_n) n = *d_n;
   __syncthreads();
