@@ -41,6 +41,10 @@ constexpr int kWinBits = 12;                      // claim window: 4096 destinat
 constexpr int kWinWords = (1 << kWinBits) / 32;  // 128 bitmap words
 constexpr int kWinSlots = 8;                      // windows per tile in shared memory
 constexpr int kBinMax = 256;                      // destination windows of the binned scatter
+#ifndef IXG_BLOCKED_CLAIMS
+#define IXG_BLOCKED_CLAIMS 1
+#endif
+constexpr bool kBlockedClaims = IXG_BLOCKED_CLAIMS;  // k_scatter_pc: register-combined claims (A/B)
 
 template <typename I, typename E>
 struct PcSmem {  // TMA-staged tile of (I index, E value) pairs
@@ -147,9 +151,6 @@ __global__ void __launch_bounds__(256) k_scatter_pc(E* __restrict__ out, long lo
         cs0 = slot;
       }
       if (slot >= 0) {
-        // transposed window layout: destination b of the window is bit b >> 7
-        // of word b & 127, so the consecutive destinations of a warp's lanes
-        // hit 32 different words (banks) instead of one
         const uint32_t bit = 1u << (d & 31);
         if (atom_or_shared(&s_bits[slot * kWinWords + (int)((d >> 5) & (kWinWords - 1))], bit) & bit) dup = true;
       } else {
@@ -167,7 +168,62 @@ __global__ void __launch_bounds__(256) k_scatter_pc(E* __restrict__ out, long lo
   // striped: a warp's stores cover 32 consecutive sources.  Separate loops
   // for the staged and the ragged tile: a select between a shared and a
   // global pointer would make every access a generic one
-  if (full) {
+  if (full && kPriv && kBlockedClaims) {
+    // claims thread-blocked (16 consecutive sources, read in a per-thread
+    // rotated order so a warp's shared loads spread over the banks): the
+    // bits a thread claims in one shared word are combined in a register
+    // first, one shared atomic per run of same-word destinations
+    int key = -1;
+    uint32_t acc = 0;
+#pragma unroll 1
+    for (int jj = 0; jj < kScTile / 256; ++jj) {
+      const long long d = (long long)s_is[t * (kScTile / 256) + ((jj + t) & (kScTile / 256 - 1))];
+      if ((unsigned long long)d >= (unsigned long long)ndst) continue;
+      const unsigned long long w = (unsigned long long)d >> kWinBits;
+      int slot;
+      if (w == cw0) {
+        slot = cs0;
+      } else if (w == cw1) {
+        slot = cs1;
+      } else {
+        slot = -1;
+#pragma unroll 1
+        for (int j = 0; j < kWinSlots; ++j) {
+          unsigned long long cur = vw[j];
+          if (cur == ~0ull) {
+            cur = atom_cas_shared(&s_win[j], ~0ull, w);
+            if (cur == ~0ull) cur = w;
+          }
+          if (cur == w) {
+            slot = j;
+            break;
+          }
+        }
+        cw1 = cw0;
+        cs1 = cs0;
+        cw0 = w;
+        cs0 = slot;
+      }
+      const uint32_t bit = 1u << (d & 31);
+      if (slot < 0) {
+        if (atomicOr(&claim[d >> 5], bit) & bit) dup = true;
+        continue;
+      }
+      const int kk = slot * kWinWords + (int)((d >> 5) & (kWinWords - 1));
+      if (kk != key) {
+        if (key >= 0 && (atom_or_shared(&s_bits[key], acc) & acc)) dup = true;
+        key = kk;
+        acc = 0u;
+      }
+      if (acc & bit) dup = true;
+      acc |= bit;
+    }
+    if (key >= 0 && (atom_or_shared(&s_bits[key], acc) & acc)) dup = true;
+    for (int k = t; k < kScTile; k += 256) {  // the stores, striped
+      const long long d = (long long)s_is[k];
+      if ((unsigned long long)d < (unsigned long long)ndst) out[d] = s_vs[k];
+    }
+  } else if (full) {
     for (int k = t; k < kScTile; k += 256) one((long long)s_is[k], s_vs[k]);
   } else {
     for (int k = t; k < cnt; k += 256) one((long long)is[base + k], vs[base + k]);
