@@ -66,6 +66,38 @@ def test_c3_scatter_full_size(cuda):
     assert torch.equal(out[is_], vs)
     assert int(torch.bincount(is_, minlength=n).max().item()) == 1
     assert st.read().ok
+    # CHECKED at full size: dst init + OOB test + the privatised claims, no
+    # conflict on a permutation; then one duplicate index with another value
+    out2 = torch.full((n,), 7, dtype=torch.int32, device=cuda)
+    st = ops.Status(cuda)
+    ops.scatter(out2, is_, vs, L.V_CONFLICT | L.V_INIT, st)
+    assert st.read().ok and torch.equal(out2, out)
+    is_[n // 3] = is_[2 * n // 3]
+    vs[n // 3] = vs[2 * n // 3] + 1
+    st = ops.Status(cuda)
+    ops.scatter(out2, is_, vs, L.V_CONFLICT | L.V_INIT, st)
+    s = st.read()
+    assert not s.ok and s.codes & (1 << L.CONFLICT)
+
+
+@pytest.mark.parametrize("checked", [False, True])
+def test_c3_random_permutation_full_size(cuda, checked):
+    """C3's secondary at 2^29: a random permutation, binned by destination
+    window (the probe must choose it), ELIDED and CHECKED."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    n = 1 << 29
+    g = torch.Generator(device=cuda)
+    g.manual_seed(5)
+    is_ = torch.randperm(n, generator=g, device=cuda, dtype=torch.int64)
+    assert ops.scatter_layout(is_, n) == L.SCATTER_BINNED
+    vs = ops.gen_uniform(n, -(1 << 31), (1 << 31) - 1, 13, torch.int32)
+    out = torch.full((n,), 7, dtype=torch.int32, device=cuda)
+    st = ops.Status(cuda)
+    ops.scatter(out, is_, vs, (L.V_CONFLICT | L.V_INIT) if checked else 0, st)
+    assert st.read().ok and torch.equal(out[is_], vs)
 
 
 def test_c4_csr_full_size(cuda):
