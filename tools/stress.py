@@ -1,4 +1,4 @@
-"""Randomised parity sweep of the ELIDED kernels against the C restatement
+"""Randomised parity sweep of the ELIDED and CHECKED kernels against the C restatement
 (test infrastructure: development tool, not part of the product).
 
 Random sizes (ragged tiles, one-tile, multi-wave), predicates (selectivity
@@ -21,6 +21,8 @@ import time
 
 import numpy as np
 import torch
+
+os.environ.setdefault("IXG_BIN_SHIFT", "12")  # binned scatters with many windows at these sizes
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import ixoracle as O  # noqa: E402
@@ -54,7 +56,8 @@ def main():
     it = 0
     while time.time() < t_end:
         it += 1
-        op = rng.choice(["filter", "partition2", "partition3", "c2", "scan", "segscan", "scatter", "csr", "hist"])
+        op = rng.choice(["filter", "partition2", "partition3", "c2", "scan", "segscan", "scatter", "csr", "hist",
+                         "filter_chk", "partition2_chk", "partition3_chk", "c2_chk", "scatter_binned"])
         dt = rng.choice([np.int32, np.int64])
         lg = rng.randint(0, a.max_log2)
         n = max(0, (1 << lg) + rng.randint(-7, 7) * rng.choice([1, 17, 4099]))
@@ -63,18 +66,21 @@ def main():
         xs = torch.from_numpy(xs_h).to(dev)
         st = ops.Status(dev)
         p = rand_pred(rng, *span)
+        chk = op.endswith("_chk")
+        variant = L.VARIANT_CHECKED if chk else L.VARIANT_ELIDED
+        op = op.replace("_chk", "")
         if op == "filter":
-            ys, dk = ops.filter(xs, p, L.VARIANT_ELIDED, st)
+            ys, dk = ops.filter(xs, p, variant, st)
             k = int(dk.item())
             want = O.filter_(p, xs_h)
             ok = k == len(want) and np.array_equal(ys[:k].cpu().numpy().astype(np.int64), want)
         elif op == "partition2":
-            ys, dnt = ops.partition2(xs, p, L.VARIANT_ELIDED, st)
+            ys, dnt = ops.partition2(xs, p, variant, st)
             wnt, wys = O.partition2(p, xs_h)
             ok = int(dnt.item()) == wnt and np.array_equal(ys.cpu().numpy().astype(np.int64), wys)
         elif op == "partition3":
             q = rand_pred(rng, *span)
-            ys, dm = ops.partition3(xs, p, q, L.VARIANT_ELIDED, st)
+            ys, dm = ops.partition3(xs, p, q, variant, st)
             w1, w2, wys = O.partition3(p, q, xs_h)
             ok = dm.cpu().tolist() == [w1, w2] and np.array_equal(ys.cpu().numpy().astype(np.int64), wys)
         elif op == "scan":
@@ -100,6 +106,24 @@ def main():
             out = torch.from_numpy(dst_h.copy()).to(dev)
             ops.scatter(out, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev), bits, st)
             ok = np.array_equal(out.cpu().numpy(), O.scatter(dst_h, is_h, vs_h))
+        elif op == "scatter_binned":
+            # destination-window binning (4096-destination windows here, IXG_BIN_SHIFT) in every form
+            vs_h = gen.uniform(it, n, -(1 << 30), 1 << 30, np.int64)
+            mode = rng.randrange(3)
+            if mode == 0:  # Sc1: a permutation
+                is_h = np.random.default_rng(it).permutation(n).astype(np.int64)
+                bits, dst_h = 0, np.zeros(n, dtype=np.int64)
+            elif mode == 1:  # injective only: a permutation of a larger range, some OOB
+                is_h = np.random.default_rng(it).permutation(n + 50).astype(np.int64)[:n] - 3
+                bits, dst_h = L.V_INIT, gen.uniform(it + 3, n, -9, 9, np.int64)
+            else:  # CHECKED: duplicates with equal values, OOB
+                is_h = gen.uniform(it + 2, n, -3, n + 3, np.int64)
+                vs_h = is_h * 5 - 2
+                bits, dst_h = L.V_BOUNDS | L.V_CONFLICT | L.V_INIT, gen.uniform(it + 3, n, -9, 9, np.int64)
+            out = torch.from_numpy(dst_h.copy()).to(dev)
+            ops.scatter(out, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev), bits, st,
+                        layout=L.SCATTER_BINNED)
+            ok = np.array_equal(out.cpu().numpy(), O.scatter(dst_h, is_h, vs_h))
         elif op == "csr":
             ncols = rng.choice([1, 97, 1 << 16])
             x_h = gen.uniform(it, ncols, -(1 << 15), (1 << 15) - 1, np.int64)
@@ -123,7 +147,7 @@ def main():
             k = len(O.filter_(p, xs_h))
             m = max(1, rng.choice([1, 7, k // 64 + 1, k // 3 + 1]))
             shape = gen.segment_shape(it, m, k)
-            ys, zs, dk = ops.c2(xs, p, torch.from_numpy(shape).to(dev), L.VARIANT_ELIDED, st)
+            ys, zs, dk = ops.c2(xs, p, torch.from_numpy(shape).to(dev), variant, st)
             kk = int(dk.item())
             wys, wzs = O.c2(p, xs_h, shape)
             # int32 zs: NARROW is flagged iff some exact sum leaves int32 (then zs wraps, as documented)
@@ -135,6 +159,7 @@ def main():
             counts["c2_narrow"] = counts.get("c2_narrow", 0) + int(narrow)
         s = st.read()
         ok = ok and s.ok  # NARROW is a flag, not a failure code
+        op = op + ("_chk" if chk else "")
         counts[op] = counts.get(op, 0) + 1
         if not ok:
             print(json.dumps({"mismatch": op, "n": n, "dtype": np.dtype(dt).name, "pred": repr(p), "iter": it}))
