@@ -397,7 +397,9 @@ int ixg_timer_stop(double* total_ms, int64_t* launches);
  *   ixg_inj_check   over the values v of xs with lo <= v <= hi: out3[0] = how
  *                   many, out3[1] = repeated values, out3[2] = how many lie
  *                   outside [img_lo, img_hi]; `bitmap` = device scratch of
- *                   ixg_inj_bitmap_bytes(lo, hi) bytes (-1: range too wide). */
+ *                   ixg_inj_bitmap_bytes(lo, hi) bytes (-1: more than 2^31
+ *                   values -- the caller then treats the annotation as
+ *                   unchecked and runs CHECKED). */
 int ixg_minmax(int dt, const void* xs, int64_t n, int64_t* out2, void* stream);
 int ixg_mono_check(int dt, const void* xs, int64_t n, int op, int64_t* out_bad, void* stream);
 int64_t ixg_inj_bitmap_bytes(int64_t lo, int64_t hi);

@@ -1084,7 +1084,7 @@ int ixg_mono_check(int dt, const void* xs, int64_t n, int op, int64_t* out_bad, 
 int64_t ixg_inj_bitmap_bytes(int64_t lo, int64_t hi) {
   if (hi < lo) return 0;
   const unsigned long long span = (unsigned long long)hi - (unsigned long long)lo + 1ULL;
-  if (span == 0 || span > (1ULL << 34)) return -1;  // wider than 2^34 values: not checkable here
+  if (span == 0 || span > (1ULL << 31)) return -1;  // wider than 2^31 values (256 MB of bitmap): not checked here
   return (int64_t)bitmap_bytes((long long)span);
 }
 

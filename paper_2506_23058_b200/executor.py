@@ -24,6 +24,7 @@ There is no CPU path: a function that no GPU pipeline implements raises
 
 from __future__ import annotations
 
+import collections
 import json
 import os
 from dataclasses import dataclass
@@ -175,8 +176,9 @@ class Interp:
         self.as_tensors = as_tensors
         self._internal = False  # a call made by a program function (its preconditions were proved)
         # (function, verdict source, variant bits per site) of every selection
-        # a call used, and the precondition checks it made -- tests assert on it
-        self.trace: list = []
+        # a call used, and the precondition checks it made -- tests assert on
+        # it (bounded: an interpreter can serve many calls)
+        self.trace = collections.deque(maxlen=4096)
         L.load(require_device=True)
 
     # -- selection ---------------------------------------------------------
