@@ -572,6 +572,7 @@ class C3:
     def describe(self, quick, ws, perm="streams"):
         self.N = (1 << 22) if quick else (1 << 29)
         self.perm = perm
+        self.name = "c3r" if perm == "random" else "c3"
         if perm == "random":
             pat = "a uniformly random permutation (torch.randperm, Philox)"
         else:
@@ -642,8 +643,19 @@ class C3:
     def kernel(self):
         from paper_2506_23058_b200 import _lib as L
 
+        if self.perm == "random":  # binned: the second pass over the (u32 index, value) pairs dominates
+            return (L.K_SCATTER, 12 * self.N,
+                    "k_scatter_ti<u32,int32> over the window-binned pairs (8 MB destination windows; u32 index + "
+                    "i32 value read, i32 dst written); k_bin_partition before it")
         return (L.K_SCATTER, 16 * self.N,
                 "k_scatter_t<int32> (TMA-staged 4096-element tiles, striped stores; is i64 + vs i32 read, dst i32 written)")
+
+    def kernels_extra(self):
+        from paper_2506_23058_b200 import _lib as L
+
+        if self.perm != "random":
+            return []
+        return [(L.K_BIN, 20 * self.N, "k_bin_partition (is i64 + vs i32 read, u32 + i32 binned pairs written)")]
 
     def e2e_bufs(self, variant):
         import torch

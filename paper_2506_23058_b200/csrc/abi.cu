@@ -168,7 +168,8 @@ int launch_fill(E* out, long long n, const long long* d_n, E v, cudaStream_t s) 
 // windows) and window count; nb == 0 when binning does not apply
 template <typename E>
 inline void bin_geometry(long long ndst, int* shift, int* nb) {
-  int sh = sizeof(E) == 4 ? 22 : 21;  // 16 MB destination windows
+  int sh = sizeof(E) == 4 ? 21 : 20;  // 8 MB destination windows (2^29 int32: 64.. 256 windows; measured
+                                      // 6.45 ms against 6.74 / 6.93 for 16 / 32 MB windows)
   if (const char* e = getenv("IXG_BIN_SHIFT")) sh = atoi(e);  // tests: many windows at small sizes
   *shift = sh;
   *nb = 0;

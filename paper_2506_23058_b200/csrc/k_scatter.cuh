@@ -23,13 +23,13 @@
 // per 32-byte sector over a 2 GB destination: every store misses, and the
 // sector is read back before it is written (partial-sector writes).  The
 // binned form first partitions the (index, value) pairs by destination
-// window (B <= 256 windows of 4M int32 destinations = 16 MB, L2-resident):
+// window (B <= 256 windows of 2M int32 destinations = 8 MB, L2-resident):
 // each tile counts its pairs per window in shared memory, reserves room in
 // each window's global run with one atomicAdd per (tile, window), stages the
 // pairs window by window in shared memory and writes each window's run
 // contiguously (indices narrowed to u32).  The second pass is the ordinary
 // (ELIDED or CHECKED) scatter over the binned pairs: at any moment the
-// resident tiles write into one or two 16 MB windows, which the L2 absorbs
+// resident tiles write into one or two 8 MB windows, which the L2 absorbs
 // until their lines are complete.  Pairs outside [0, ndst) are dropped by the
 // first pass (the reference ignores them, oracle.py:300).
 #pragma once
@@ -70,6 +70,21 @@ IXG_DEV uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+IXG_DEV uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <typename E>
+IXG_DEV void st_keep(E* p, E v, uint64_t pol) {
+  if constexpr (sizeof(E) == 4)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"((uint32_t)v), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p),
+                 "l"((unsigned long long)v), "l"(pol)
+                 : "memory");
 }
 IXG_DEV void bulk_g2s_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
@@ -274,10 +289,11 @@ __global__ void __launch_bounds__(256) k_scatter_ti(E* __restrict__ out, long lo
     }
     __syncthreads();
     mbar_wait(&s_mbar, 0);
+    const uint64_t keep = l2_evict_last_policy();  // the window's partial lines stay until complete
 #pragma unroll 4
     for (int k = t; k < kScTile; k += 256) {
       const long long d = (long long)s_is[k];
-      if ((unsigned long long)d < (unsigned long long)ndst) out[d] = s_vs[k];
+      if ((unsigned long long)d < (unsigned long long)ndst) st_keep(out + d, s_vs[k], keep);
     }
   } else {
     for (long long i = base + t; i < m; i += 256) {
