@@ -300,6 +300,18 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
 }
 
 // --------------------------------------------------------------- filter
+// the sharded partition2 reads xs once and places both classes (default
+// tiles); IXG_PEER_DUAL=k (1..3) the same on k-chunk tiles, =0 the
+// two-segment form over xs (A/B)
+inline int peer_dual_chunks() {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("IXG_PEER_DUAL");
+    mode = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : -1;
+  }
+  return mode;
+}
+
 // IXG_BIG_SCAN=0: the CHECKED index scans on the generic k_scan instead of
 // the big-tile kernel (A/B)
 inline bool big_scan_enabled() {
@@ -321,22 +333,24 @@ inline bool seg_split_mode() {
   return mode == 1;
 }
 
-template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false>
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false, int CHO = 0>
 int launch_filter_b(const T* xs, const uint8_t* cs, long long n, const ixg_pred& p, T* ys, LBChan ch,
                     long long* d_count, cudaStream_t s, Z* zs = nullptr, const uint32_t* segbits = nullptr,
                     long long out_base = 0, LBChan ch2 = LBChan{nullptr, nullptr}, ixg_status* st = nullptr,
                     const ixg_pred& q = ixg_pred{}, const PeerOut<T>& po = PeerOut<T>{}) {
-  auto kern = k_filter_b<T, kByCs, kSeg, Z, NS, kPeer>;
+  auto kern = k_filter_b<T, kByCs, kSeg, Z, NS, kPeer, CHO>;
+  using B = Big<T, CHO>;
+  constexpr int smem = B::SMEM;
   static std::atomic<unsigned long long> attr{0};
-  allow_smem(kern, Big<T>::SMEM, attr);
+  allow_smem(kern, smem, attr);
   TimedLaunch tl(NS > 1 ? IXG_K_PLACE : IXG_K_FILTER_FUSED, s);
-  const long long seg_tiles = tiles_of(n, Big<T>::TILE);
+  const long long seg_tiles = tiles_of(n, B::TILE);
   // programmatic dependent launch: the CTAs become resident while the
   // previous kernel of the stream drains (k_filter_b waits for it itself)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(NS * seg_tiles));
   cfg.blockDim = dim3(kBT + 32);
-  cfg.dynamicSmemBytes = Big<T>::SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute la[1];
   la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -899,6 +913,25 @@ int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, vo
     po.d_counts = (const long long*)d_counts;
     po.rank = rank;
     po.in_shard = n;
+    switch (peer_dual_chunks()) {  // one read of xs, both classes placed (12 -> 8 B per element)
+#define IXG_DUAL32(K)                                                                                           \
+  case K:                                                                                                       \
+    return launch_filter_b<int32_t, false, false, int32_t, 1, true, K>((const int32_t*)xs, nullptr, n, pp, nullptr, \
+                                                                       c0, scratch, s, nullptr, nullptr, 0,      \
+                                                                       LBChan{nullptr, nullptr}, nullptr,        \
+                                                                       ixg_pred{}, po);
+      case -1:
+        return launch_filter_b<int32_t, false, false, int32_t, 1, true>((const int32_t*)xs, nullptr, n, pp, nullptr,
+                                                                        c0, scratch, s, nullptr, nullptr, 0,
+                                                                        LBChan{nullptr, nullptr}, nullptr, ixg_pred{},
+                                                                        po);
+      IXG_DUAL32(1)
+      IXG_DUAL32(2)
+      IXG_DUAL32(3)
+#undef IXG_DUAL32
+      default:
+        break;
+    }
     return launch_filter_b<int32_t, false, false, int32_t, 2, true>((const int32_t*)xs, nullptr, n, pp, nullptr, c0,
                                                                     scratch, s, nullptr, nullptr, 0,
                                                                     LBChan{nullptr, nullptr}, nullptr, ixg_pred{},
@@ -911,6 +944,23 @@ int ixg_partition2_peer(int dt, const void* xs, int64_t n, const ixg_pred* p, vo
   po.d_counts = (const long long*)d_counts;
   po.rank = rank;
   po.in_shard = n;
+  switch (peer_dual_chunks()) {
+#define IXG_DUAL64(K)                                                                                          \
+  case K:                                                                                                      \
+    return launch_filter_b<long long, false, false, long long, 1, true, K>((const long long*)xs, nullptr, n, pp, \
+                                                                           nullptr, c0, scratch, s, nullptr,      \
+                                                                           nullptr, 0, LBChan{nullptr, nullptr},  \
+                                                                           nullptr, ixg_pred{}, po);
+    case -1:
+      return launch_filter_b<long long, false, false, long long, 1, true>((const long long*)xs, nullptr, n, pp,
+                                                                          nullptr, c0, scratch, s, nullptr, nullptr, 0,
+                                                                          LBChan{nullptr, nullptr}, nullptr,
+                                                                          ixg_pred{}, po);
+    IXG_DUAL64(1)
+#undef IXG_DUAL64
+    default:
+      break;
+  }
   return launch_filter_b<long long, false, false, long long, 2, true>((const long long*)xs, nullptr, n, pp, nullptr,
                                                                       c0, scratch, s, nullptr, nullptr, 0,
                                                                       LBChan{nullptr, nullptr}, nullptr, ixg_pred{},

@@ -276,9 +276,8 @@ struct Quad {
   }
 };
 
-template <typename T>
+template <typename T, typename B = Big<T>>
 IXG_DEV void quad_issue(T* buf, const T* __restrict__ xs, long long n, long long tile_base, int w, int l, bool full) {
-  using B = Big<T>;
   using Q = Quad<T>;
   const int o0 = Q::off(w, 0, l);
   if (full) {
@@ -304,9 +303,8 @@ IXG_DEV void quad_issue(T* buf, const T* __restrict__ xs, long long n, long long
   cp_async_commit();
 }
 
-template <typename T>
+template <typename T, typename B = Big<T>>
 IXG_DEV void quad_read(const T* buf, int c, int w, int l, T (&x)[kSItems]) {
-  using B = Big<T>;
   using Q = Quad<T>;
 #pragma unroll
   for (int k = 0; k < Q::P; ++k) {
@@ -419,6 +417,77 @@ IXG_DEV void store_run_peer(const PeerOut<E>& po, long long gbase, int cnt, cons
 #pragma unroll
       for (int e = 0; e < EP; ++e)
         if (l + e >= 0 && l + e < cnt) dst[e] = buf[l + e];
+    }
+  }
+}
+
+// kDual store of ONE class of a tile: its elements, in class order, are the
+// CH per-chunk sub-runs of the in-place partitioned tile buffer (class rank
+// r in chunk c, pre[c] <= r < pre[c + 1], sits at slot r + D[c] of `buf`,
+// a 16-byte aligned base), and they go to the global positions
+// [g0, g0 + len) of the sharded output.  One loop over the 16-byte output
+// pieces: a piece inside one sub-run is funnel-shifted from the two aligned
+// 16-byte words it straddles, the few pieces at run or chunk edges go
+// element by element.  r0 = g0 / shard when len <= shard (the run then
+// crosses at most one shard edge: each piece picks one of two precomputed
+// bases), else -1 (a division per piece -- shards smaller than a tile).
+template <typename E, int CH, int NT>
+IXG_DEV void store_class_peer(const PeerOut<E>& po, const E* buf, long long g0, int len, const int (&pre)[CH + 1],
+                              const int (&D)[CH], long long r0) {
+  constexpr int EP = 16 / (int)sizeof(E);
+  if (len <= 0) return;
+  const long long c0 = g0 / EP;
+  const int s = (int)(g0 - c0 * EP);
+  const int nch = (int)((g0 + len - 1) / EP - c0) + 1;
+  E* p0 = nullptr;
+  E* p1 = nullptr;
+  long long edge = 0;
+  if (r0 >= 0) {  // dst(g) = (g < edge ? p0 : p1) + g
+    edge = (r0 + 1) * po.shard;
+    p0 = po.dst[r0] - r0 * po.shard;
+    p1 = r0 + 1 < po.ranks ? po.dst[r0 + 1] - edge : p0;
+  }
+  auto chunk_of = [&](int r) {
+    int c = 0;
+#pragma unroll
+    for (int q = 1; q < CH; ++q) c += r >= pre[q] ? 1 : 0;
+    return c;
+  };
+  auto slot_of = [&](int r) {
+    int d = D[0];
+#pragma unroll
+    for (int q = 1; q < CH; ++q) d = r >= pre[q] ? D[q] : d;
+    return r + d;
+  };
+  for (int j = threadIdx.x; j < nch; j += NT) {
+    const int l = j * EP - s;  // class rank of the piece's first element
+    const long long g = (c0 + j) * EP;
+    E* dst;
+    if (r0 >= 0) {
+      dst = (g < edge ? p0 : p1) + g;
+    } else {
+      const long long r = g / po.shard;
+      dst = po.dst[r] + (g - r * po.shard);
+    }
+    if (l >= 0 && l + EP <= len && chunk_of(l) == chunk_of(l + EP - 1)) {
+      const int a = slot_of(l);
+      const int a0 = a & ~(EP - 1);
+      const int sw = (a - a0) * (int)sizeof(E) / 4;
+      const uint4 x = *reinterpret_cast<const uint4*>(buf + a0);
+      uint4 v = x;
+      if (sw) {
+        const uint4 y = *reinterpret_cast<const uint4*>(buf + a0 + EP);
+        if (sw == 1) v = make_uint4(x.y, x.z, x.w, y.x);
+        else if (sw == 2) v = make_uint4(x.z, x.w, y.x, y.y);
+        else v = make_uint4(x.w, y.x, y.y, y.z);
+      }
+      asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(v.x), "r"(v.y),
+                   "r"(v.z), "r"(v.w)
+                   : "memory");
+    } else {
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (l + e >= 0 && l + e < len) dst[e] = buf[slot_of(l + e)];
     }
   }
 }
@@ -581,7 +650,7 @@ IXG_DEV int fieldc(unsigned long long v, int c) {
 // prefix is the class's output position and the whole stable partition is
 // a single pass writing each element once (d_count[s] = the prefix at the
 // end of segment s, for s < NS - 1).
-template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false>
+template <typename T, bool kByCs, bool kSeg = false, typename Z = T, int NS = 1, bool kPeer = false, int CHO = 0>
 __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(const T* __restrict__ xs, const uint8_t* __restrict__ cs,
                                                           long long n, ixg_pred p, T* __restrict__ ys, LBChan ch,
                                                           uint32_t nonce, long long* d_count,
@@ -591,7 +660,8 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
                                                           ixg_status* st = nullptr, ixg_pred q = ixg_pred{},
                                                           long long seg_tiles = 0, PeerOut<T> po = PeerOut<T>{}) {
   static_assert(!kSeg || sizeof(Z) == sizeof(T), "zs is computed in place of ys");
-  using B = Big<T>;
+  constexpr bool kDual = kPeer && NS == 1;  // one pass placing both classes (the count is known)
+  using B = Big<T, CHO>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
   __shared__ SegOp::T s_seg[kBW];
@@ -692,7 +762,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     }
     bar_sync(1, kBT);  // the mbarriers are initialised
   } else {
-    quad_issue<T>(buf, xs, n, tile_base, w, l, false);
+    quad_issue<T, B>(buf, xs, n, tile_base, w, l, false);
   }
   // selection masks of the lane's pieces (bit k*EP + e), filter_by reads cs meanwhile
   uint32_t m[B::CH];
@@ -707,7 +777,7 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
     for (int c = 0; c < B::CH; ++c) {
       if (full) mbar_wait(&s_mbar[c], 0);
       T x[kSItems];
-      quad_read<T>(buf, c, w, l, x);
+      quad_read<T, B>(buf, c, w, l, x);
       m[c] = sel.mask(x);
       if constexpr (NS == 2) {
         if (seg == 1) m[c] ^= 0xffffu;
@@ -759,21 +829,47 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   // the look-back warp resolves the tile's global base: output slot r of an
   // element never exceeds its input slot PAD + i, and chunk c's outputs end
   // before chunk c+1's inputs begin
+  // kDual (the sharded partition2, true counts of every rank known
+  // beforehand): each chunk is partitioned IN PLACE within its own slots --
+  // trues first, then falses, both stable -- after every worker has read it,
+  // so the tile's xs is read once and both classes leave from shared memory
+  // as 2 x CH runs (8 B per element instead of the two-segment form's 12)
+  int bcc = 0;  // trues of the tile's earlier chunks
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     if (kByCs && full) mbar_wait(&s_mbar[c], 0);
     T x[kSItems];
-    quad_read<T>(buf, c, w, l, x);
+    quad_read<T, B>(buf, c, w, l, x);
     bar_sync(1, kBT);
     const uint32_t mc = m[c];
     int pre = before[c];  // + totals of the warp's earlier pieces
+    if constexpr (kDual) {
+      uint32_t vc = 0xffffu;
+      if (!full) vc = quad_valid<Q::EP>(n, tile_base + c * kBChunk + Q::off(w, 0, l));
+      T* const cb = buf + B::PAD + c * kBChunk;
+      const int tc = fieldc<B::CH>(tot, c);
 #pragma unroll
-    for (int k = 0; k < Q::P; ++k) {
-      T* dst = buf + pre + Q::field(ex[c], k);
-      pre += Q::field(wt[c], k);
+      for (int k = 0; k < Q::P; ++k) {
+        int r = pre - bcc + Q::field(ex[c], k);  // chunk-local trues before the piece
+        pre += Q::field(wt[c], k);
+        const int i0 = Q::off(w, k, l);  // the piece's first chunk index
 #pragma unroll
-      for (int e = 0; e < Q::EP; ++e) {
-        if (mc & (1u << (k * Q::EP + e))) *dst++ = x[k * Q::EP + e];
+        for (int e = 0; e < Q::EP; ++e) {
+          const uint32_t bit = 1u << (k * Q::EP + e);
+          if (mc & bit) cb[r++] = x[k * Q::EP + e];
+          else if (vc & bit) cb[tc + (i0 + e - r)] = x[k * Q::EP + e];
+        }
+      }
+      bcc += tc;
+    } else {
+#pragma unroll
+      for (int k = 0; k < Q::P; ++k) {
+        const int tb0 = pre + Q::field(ex[c], k);  // trues before the piece
+        T* dst = buf + tb0;
+        pre += Q::field(wt[c], k);
+#pragma unroll
+        for (int e = 0; e < Q::EP; ++e)
+          if (mc & (1u << (k * Q::EP + e))) *dst++ = x[k * Q::EP + e];
       }
     }
   }
@@ -816,7 +912,25 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   constexpr bool kBulk = (kSeg && IXG_BULK_ST) || (!kSeg && !kPeer && (IXG_BULK_ALL || sizeof(T) == 8));
   const bool bulk = kBulk && ((((uintptr_t)ys) | (kSeg ? (uintptr_t)zs : (uintptr_t)0)) & 15) == 0;  // 16-byte aligned outputs
   T* run = buf;
-  if constexpr (kPeer) {
+  if constexpr (kDual) {
+    const long long gt = peer_gbase(po, 0, base);                                      // the tile's first true
+    const long long gf = peer_gbase(po, 1, po.d_counts[po.rank] + (tile_base - base));  // and first false
+    int pt[B::CH + 1], pf[B::CH + 1], dt[B::CH], df[B::CH];
+    pt[0] = pf[0] = 0;
+#pragma unroll
+    for (int c = 0; c < B::CH; ++c) {
+      const long long left = n - tile_base - (long long)c * kBChunk;
+      const int nv = left <= 0 ? 0 : (left >= kBChunk ? kBChunk : (int)left);
+      const int tc = fieldc<B::CH>(tot, c);
+      dt[c] = B::PAD + c * kBChunk - pt[c];
+      df[c] = B::PAD + c * kBChunk + tc - pf[c];
+      pt[c + 1] = pt[c] + tc;
+      pf[c + 1] = pf[c] + nv - tc;
+    }
+    const bool wide = po.shard >= B::TILE;  // a class run is <= a tile
+    store_class_peer<T, B::CH, kBT>(po, buf, gt, pt[B::CH], pt, dt, wide ? gt / po.shard : -1);
+    store_class_peer<T, B::CH, kBT>(po, buf, gf, pf[B::CH], pf, df, wide ? gf / po.shard : -1);
+  } else if constexpr (kPeer) {
     store_run_peer<T, kBT>(po, peer_gbase(po, seg, base), cnt, buf);
   } else if (bulk) {
     const int sh0 = (int)(base & (B::EP - 1));

@@ -122,9 +122,10 @@ def test_sharded_scan_filter_partition3_kernels(cuda, G, n):
     assert np.array_equal(out, wys)
 
 
-@pytest.mark.parametrize("G,per", [(2, 100_000), (4, 300_000), (8, 40_000), (3, 4)])
+@pytest.mark.parametrize("G,per,thr", [(2, 100_000, 0), (4, 300_000, 0), (8, 40_000, 0), (3, 4, 0),
+                                        (5, 70_004, -(1 << 30)), (2, 1 << 20, (1 << 31) - 2), (3, 8_196, -(1 << 31))])
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
-def test_partition2_peer_kernel(cuda, G, per, dtype):
+def test_partition2_peer_kernel(cuda, G, per, thr, dtype):
     """ixg_partition2_peer for G simulated ranks in one process: every rank's
     kernel stores its runs straight into the G destination shards (the
     pointer table a rank gets from CUDA IPC); the shards concatenate to the
@@ -135,7 +136,7 @@ def test_partition2_peer_kernel(cuda, G, per, dtype):
 
     n = G * per
     xs = gen.uniform(G * 31 + per, n, -(1 << 31), (1 << 31) - 1, dtype)
-    p = Pred.lt(0)
+    p = Pred.lt(thr)  # 50 %, 25 %, ~all and no trues
     want_nt, want = O.partition2(p, xs)
     tdt = torch.int32 if dtype == np.int32 else torch.int64
     bufs = [torch.full((per,), -7, dtype=tdt, device=cuda) for _ in range(G)]
