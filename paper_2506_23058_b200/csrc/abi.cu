@@ -371,15 +371,72 @@ int launch_segsum_b(const T* vs, long long n, const long long* d_n, const uint32
                     LBChan ch, long long carry_v, int carry_f, longlong2* d_total, ixg_status* st, cudaStream_t s,
                     const long long* d_flag_base = nullptr, F fn = F{}) {
   auto kern = k_segsum_b<T, Z, M, F>;
-  using B = Big<T, kSegsumCH<T, Z>>;
+  using B = Big<T, F::kCH ? F::kCH : kSegsumCH<T, Z>>;
   static std::atomic<unsigned long long> attr{0};
   allow_smem(kern, B::SMEM, attr);
   TimedLaunch tl(IXG_K_SEGSUM, s);
-  kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, d_flag_base, zs, ch,
-                                                                  next_nonce(), carry_v, carry_f, d_total, st, fn);
-  LAUNCHED();
+  if constexpr (F::kTrigger) {  // a programmatic dependent of the previous kernel (the bitmap clear)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tiles_of(n, B::TILE));
+    cfg.blockDim = dim3(kBT + 32);
+    cfg.dynamicSmemBytes = B::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, vs, n, d_n, bits, flag_base, d_flag_base, zs, ch, next_nonce(),
+                                       carry_v, carry_f, d_total, st, fn);
+    LAUNCHED();
+    if (e != cudaSuccess) return cuda_rc(e);
+  } else {
+    kern<<<(unsigned)tiles_of(n, B::TILE), kBT + 32, B::SMEM, s>>>(vs, n, d_n, bits, flag_base, d_flag_base, zs, ch,
+                                                                    next_nonce(), carry_v, carry_f, d_total, st, fn);
+    LAUNCHED();
+  }
   CHECK_LAUNCH();
   return IXG_OK;
+}
+
+// mkFlags into a cleared bitmap: the big-tile scan (TMA tiles, dedicated
+// look-back warp, 8 K shape values per tile) setting the start bits; with
+// IXG_MKF_BIG=0 the generic k_scan (A/B)
+inline bool mkf_big_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_MKF_BIG");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+int launch_mkflags(const long long* shape, long long m, uint32_t* bits, long long nbits, const long long* d_nbits,
+                   LBChan c, cudaStream_t s) {
+  const bool big = mkf_big_enabled() && aligned16(shape) && aligned16(bits) && m > 0;
+  if (big) {  // the clear heads a programmatic-launch chain (see k_bitmap_zero)
+    k_bitmap_zero<<<grid_for((nbits + 127) / 128), kGThreads, 0, s>>>(
+        bits, (long long)(bitmap_bytes(nbits) / 4), d_nbits);
+    LAUNCHED();
+    CHECK_LAUNCH();
+  } else if (d_nbits) {
+    k_bitmap_clear<<<grid_for((nbits + 31) / 32 + 514), kGThreads, 0, s>>>(bits, d_nbits);
+    LAUNCHED();
+    CHECK_LAUNCH();
+  } else {
+    cudaMemsetAsync(bits, 0, bitmap_bytes(nbits), s);
+    LAUNCHED();
+  }
+  if (m <= 0) return IXG_OK;
+  if (big) {
+    ScanSegStartBits fn{};
+    fn.bits = bits;
+    fn.nb = nbits;
+    fn.d_nb = d_nbits;
+    return launch_segsum_b<long long, long long, SumOp>(shape, m, nullptr, nullptr, 0, nullptr, c, 0, 0, nullptr,
+                                                        nullptr, s, nullptr, fn);
+  }
+  return launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, nbits, d_nbits, nullptr},
+                            c, s);
 }
 
 // filter / filter_by on element type T.  Sites: 0 = offs[n-1], 1 = scatter.
@@ -505,10 +562,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     // load, count and compact while the scan runs and wait only before they
     // read the bitmap (a kernel clearing the bitmap instead of the memset, to
     // chain all three launches, measured no faster)
-    cudaMemsetAsync(bits, 0, bitmap_bytes(n), s);
-    LAUNCHED();
-    int rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, n, nullptr, nullptr},
-                                cs, s);
+    int rc = launch_mkflags(shape, m, bits, n, nullptr, cs, s);  // clear + scan
     if (rc) return rc;
     if constexpr (sizeof(Z) == sizeof(T)) {
       if (!seg_split_mode()) {
@@ -1211,18 +1265,8 @@ int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbi
   cudaStream_t s = S(stream);
   WS w(ws);
   LBChan c = w.chan(0, tiles_of(m, kGTile));
-  if (d_nbits) {  // nbits on the device (<= the capacity nbits): clear just those words
-    k_bitmap_clear<<<grid_for((nbits + 31) / 32 + 514), kGThreads, 0, s>>>(bits, (const long long*)d_nbits);
-    LAUNCHED();
-    CHECK_LAUNCH();
-  } else {
-    cudaMemsetAsync(bits, 0, bitmap_bytes(nbits), s);
-    LAUNCHED();
-  }
-  return launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
-                            EpiSegStarts{m, (const long long*)shape, nullptr, bits, nbits,
-                                         (const long long*)d_nbits, nullptr},
-                            c, s);
+  // (d_nbits: nbits on the device, <= the capacity nbits -- only those words are cleared)
+  return launch_mkflags((const long long*)shape, m, bits, nbits, (const long long*)d_nbits, c, s);
 }
 
 int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,

@@ -84,6 +84,9 @@ constexpr int kSegsumCH = (sizeof(T) == 4 && sizeof(Z) == 8) ? IXG_SCAN32_CH : 0
 #ifndef IXG_LB_DEFER
 #define IXG_LB_DEFER 1  // look-back polling deferred until it can succeed: C2 0.463 -> 0.458 ms, filter -0.7 %
 #endif
+#ifndef IXG_MKF_CH
+#define IXG_MKF_CH 1  // mkFlags scan: chunks (4 K int64 shape values) per tile
+#endif
 #ifndef IXG_SEGSUM_MINB
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
 #endif
@@ -1101,6 +1104,10 @@ IXG_DEV int seg_f(const typename M::T& a) {
 struct ScanId {
   static constexpr bool kOvf = true;
   static constexpr bool kFlagArr = false;
+  static constexpr bool kStore = true;     // out() is stored to zs (else called for its effect only)
+  static constexpr bool kTrigger = false;  // PDL chain member: release the dependent at the top, wait for
+                                           // the predecessor only before the outputs
+  static constexpr int kCH = 0;            // chunks per tile if not the default
   IXG_DEV uint32_t flags16(long long, long long) const { return 0u; }
   IXG_DEV void init() {}
   template <typename T>
@@ -1142,10 +1149,36 @@ struct SegFlagArr : ScanId {
   }
 };
 
+// mkFlags as a bitmap (the ELIDED C2, ixg_flag_bitmap): the exclusive scan
+// of the segment shape; a nonempty segment sets the bit of its start
+// (mkSgmDescr's `if shape[i] <= 0 then -1 else scn[i]`, PAPER.md:399-402,
+// scattered under Ss2 with starts outside [0, nbits) skipped).  The C2 fused
+// kernel is its programmatic dependent.
+struct ScanSegStartBits : ScanId {
+  static constexpr bool kOvf = false;
+  static constexpr bool kStore = false;
+  static constexpr bool kTrigger = true;
+  static constexpr int kCH = IXG_MKF_CH;  // 4 K-value tiles: 256 CTAs for C2's 2^20 segments
+  uint32_t* bits;
+  long long nb;
+  const long long* d_nb;  // nullable: nbits on the device
+  IXG_DEV void init() {
+    if (d_nb) nb = *d_nb;
+  }
+  IXG_DEV long long out(long long run, long long xv, long long) const {
+    const long long start = run - xv;
+    if (xv > 0 && start >= 0 && start < nb) atomicOr(&bits[start >> 5], 1u << (start & 31));
+    return 0;
+  }
+};
+
 template <typename T>
 struct ScanFilterInds {  // inds[i] = if p xs[i] then offs[i] - 1 else -1; *d_count = offs[n-1]
   static constexpr bool kOvf = false;
   static constexpr bool kFlagArr = false;
+  static constexpr bool kStore = true;
+  static constexpr bool kTrigger = false;
+  static constexpr int kCH = 0;
   IXG_DEV uint32_t flags16(long long, long long) const { return 0u; }
   PredBit<T> pb;
   long long* d_count;
@@ -1158,6 +1191,9 @@ template <typename T>
 struct ScanPart2Inds {  // indices[i] = if p x then indicesT[i] - 1 else i + 1 - indicesT[i] + num_true - 1
   static constexpr bool kOvf = false;
   static constexpr bool kFlagArr = false;
+  static constexpr bool kStore = true;
+  static constexpr bool kTrigger = false;
+  static constexpr int kCH = 0;
   IXG_DEV uint32_t flags16(long long, long long) const { return 0u; }
   PredBit<T> pb;
   const long long* d_nt;
@@ -1179,7 +1215,9 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
                                                           Z* __restrict__ zs, LBChan ch, uint32_t nonce,
                                                           long long carry_v, int carry_f, longlong2* d_total,
                                                           ixg_status* st, F fn = F{}) {
-  using B = Big<T, kSegsumCH<T, Z>>;
+  constexpr int CHO = F::kCH ? F::kCH : kSegsumCH<T, Z>;
+  using B = Big<T, CHO>;
+  if constexpr (F::kTrigger) pdl_trigger();
   fn.init();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf = reinterpret_cast<T*>(smem_raw);
@@ -1223,7 +1261,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     }
     bar_sync(1, kBT);  // the mbarriers are initialised
   } else {
-    big_issue<T, kSegsumCH<T, Z>>(buf, vs, n, tile_base, t);
+    big_issue<T, CHO>(buf, vs, n, tile_base, t);
   }
   // the thread's 16 flag bits per chunk (positions are known up front)
   uint32_t fl[B::CH];
@@ -1294,6 +1332,7 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     else lb_publish<M>(ch, nonce, tile, tagg, false);
   }
   bar_sync(2, kBT + 32);
+  if constexpr (F::kTrigger) pdl_wait();  // (mkFlags) the bitmap's clear has finished
   const typename M::T carry = s_carry;
   bool narrow = false;
   long long ovf_at = LLONG_MAX;  // first element whose int64 sum overflowed (Z = int64)
@@ -1320,9 +1359,11 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
       if (F::kOvf && sizeof(Z) == 8 && (((prev ^ run) & (xv ^ run)) < 0) && g + j < n && ovf_at == LLONG_MAX)
         ovf_at = g + j;
       if (g + j == n - 1) fn.last(run);
-      z[j] = (Z)fn.out(run, xv, g + j);
+      if constexpr (F::kStore) z[j] = (Z)fn.out(run, xv, g + j);
+      else if (g + j < n) fn.out(run, xv, g + j);
     }
-    if (g + kSItems <= n) {
+    if constexpr (!F::kStore) {
+    } else if (g + kSItems <= n) {
       constexpr int ZV = 32 / (int)sizeof(Z);  // elements per 256-bit store
 #pragma unroll
       for (int v = 0; v < kSItems / ZV; ++v) {

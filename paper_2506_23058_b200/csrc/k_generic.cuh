@@ -652,6 +652,21 @@ __global__ void __launch_bounds__(kGThreads) k_bitmap_clear(uint32_t* __restrict
   for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) bits[w] = 0u;
 }
 
+// the mkFlags bitmap's clear as the head of C2's programmatic-launch chain
+// (clear -> mkFlags scan -> fused filter + sgmSum): words [0, words) (or the
+// words of *d_nbits + the look-back slack) in 16-byte stores; the mkFlags
+// scan starts at once and waits for this grid only before it sets bits
+__global__ void __launch_bounds__(kGThreads) k_bitmap_zero(uint32_t* __restrict__ bits, long long words,
+                                                            const long long* __restrict__ d_nbits) {
+  pdl_trigger();
+  if (d_nbits) words = (*d_nbits + 31) / 32 + 2 + 512;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nv = words / 4;  // bits is 16-byte aligned
+  for (long long k = tid; k < nv; k += stride) reinterpret_cast<int4*>(bits)[k] = make_int4(0, 0, 0, 0);
+  for (long long w = nv * 4 + tid; w < words; w += stride) bits[w] = 0u;
+}
+
 // ---------------------------------------------------------------- fill / iota
 template <typename E>
 __global__ void __launch_bounds__(kGThreads) k_fill(E* __restrict__ out, long long n,
