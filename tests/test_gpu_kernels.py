@@ -181,6 +181,47 @@ def test_c2_sum_below_k(cuda):
             assert np.array_equal(_np(zs)[:kk].astype(np.int64), want_zs)
 
 
+def _flag_bits_ref(shape, nbits):
+    """mkFlags as a bitmap: bit scn[i] for every shape[i] > 0 whose start
+    scn[i] (exclusive prefix of shape) lies in [0, nbits)."""
+    scn = np.concatenate([[0], np.cumsum(shape)[:-1]]).astype(np.int64) if len(shape) else np.zeros(0, np.int64)
+    words = np.zeros((nbits + 31) // 32 + 1, np.uint32)
+    for s_, st_ in zip(shape, scn):
+        if s_ > 0 and 0 <= st_ < nbits:
+            words[st_ >> 5] |= np.uint32(1 << (int(st_) & 31))
+    return words[: (nbits + 31) // 32]
+
+
+@pytest.mark.parametrize("m", [0, 1, 7, 4095, 4096, 4097, 12_345, 300_001])
+@pytest.mark.parametrize("kind", ["segments", "unit", "negatives", "past_nbits"])
+@pytest.mark.parametrize("on_device", [False, True])
+def test_flag_bitmap(cuda, m, kind, on_device):
+    """ixg_flag_bitmap (the C2 mkFlags: bitmap clear + big-tile scan) against
+    the definition, with empty and negative segments (starts that move
+    backwards), starts at or past nbits, and nbits read from the device."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    rng = np.random.default_rng(m + len(kind))
+    if kind == "unit":
+        shape = np.ones(m, np.int64)
+    elif kind == "negatives":
+        shape = rng.integers(-3, 9, m).astype(np.int64)
+    else:
+        shape = rng.integers(0, 6, m).astype(np.int64)
+    total = int(shape[shape > 0].sum()) if m else 0
+    nbits = max(1, total // 2) if kind == "past_nbits" else total + 70
+    cap = nbits + 4096 if on_device else nbits
+    d_nbits = torch.tensor([nbits], dtype=torch.int64, device=cuda) if on_device else None
+    bits = torch.full((int(ops._lib().ixg_bitmap_words(cap)),), -1, dtype=torch.int32, device=cuda)  # stale words
+    ops.flag_bitmap(_t(shape, cuda), cap, d_nbits=d_nbits, bits=bits)
+    got = _np(bits).view(np.uint32)[: (nbits + 31) // 32].copy()
+    if nbits % 32:
+        got[-1] &= np.uint32((1 << (nbits % 32)) - 1)
+    assert np.array_equal(got, _flag_bits_ref(shape, nbits))
+
+
 @pytest.mark.parametrize("n", SIZES)
 def test_scan_add(cuda, n):
     from paper_2506_23058_b200 import ops
