@@ -251,7 +251,7 @@ class C2:
         return [(L.K_SEGSUM, 12 * n + 16 * k, "k_segsum_b x2 (pred -> offs -> inds i64; sgmSum over the i64 "
                                               "flag array + ys -> zs), big-tile scans"),
                 (L.K_SCAN, 16 * m, "k_scan (mkFlags segment starts)"),
-                (L.K_SCATTER, 12 * n + 4 * k + 24 * m, "k_scatter_pc x2 (ys, flags; privatised claims)")]
+                (L.K_SCATTER, 12 * n + 4 * k + 24 * m, "k_scatter_sa x2 (ys, flags; claims in set-associative shared windows)")]
 
     def checked_launches(self, kid):
         from paper_2506_23058_b200 import _lib as L
@@ -442,7 +442,7 @@ class C1:
         n = self.N
         return [(L.K_CLASS_COUNT, 4 * n, "k_class_count (num_true)"),
                 (L.K_SEGSUM, 12 * n, "k_segsum_b<ScanPart2Inds> (pred -> indices i64, big-tile scan)"),
-                (L.K_SCATTER, 16 * n, "k_scatter_pc (indices + xs -> ys; privatised claims)")]
+                (L.K_SCATTER, 16 * n, "k_scatter_sa (indices + xs -> ys; claims in set-associative shared windows)")]
 
     def e2e_bufs(self, variant):
         import torch
@@ -620,7 +620,7 @@ class C3:
     def checked_families(self):
         from paper_2506_23058_b200 import _lib as L
 
-        fams = [(L.K_SCATTER, 16 * self.N, "k_scatter_pc (claims privatised in shared-memory windows)"
+        fams = [(L.K_SCATTER, 16 * self.N, "k_scatter_sa (claims in 2-way set-associative shared-memory windows)"
                  if self.perm != "random" else "k_scatter_pc<u32> over the binned pairs (8 + 4 + 4 B)")]
         if self.perm == "random":
             fams.append((L.K_BIN, 20 * self.N, "k_bin_partition (12 B in, 8 B binned pairs out)"))

@@ -182,6 +182,18 @@ inline void bin_geometry(long long ndst, int* shift, int* nb) {
 // checked/elided scatter of m pairs into out[0..ndst) (ndst from d_ndst when
 // given).  layout: IXG_SCATTER_DIRECT, or IXG_SCATTER_BINNED (pairs first
 // partitioned by destination window; ndst <= 2^32 and a host-known ndst).
+// IXG_SCATTER_SA=0: the CHECKED direct scatter with searched claim windows
+// and per-thread window caches (k_scatter_pc) instead of the set-associative
+// windows (k_scatter_sa), for A/B
+inline bool scatter_sa_enabled() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("IXG_SCATTER_SA");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
 template <typename E>
 int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long ndst_cap, const long long* is,
                    const E* vs, long long m, uint32_t bits, int stmt, int site, ixg_status* st, WS& ws,
@@ -273,7 +285,11 @@ int launch_scatter(E* out, long long ndst, const long long* d_ndst, long long nd
     // sources); CHECKED claims through the shared-memory windows
     // (k_scatter_pc); IXG_SCATTER=1: the register-blocked kernels for A/B
     if (mode == 0 && aligned16(is) && aligned16(vs)) {
-      if (check) {
+      if (check && scatter_sa_enabled()) {
+        static std::atomic<unsigned long long> attr{0};
+        allow_smem(k_scatter_sa<E>, PcSmem<long long, E>::BYTES, attr);
+        k_scatter_sa<E><<<tiles, 256, PcSmem<long long, E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m, claim, hdr);
+      } else if (check) {
         static std::atomic<unsigned long long> attr{0};
         allow_smem(k_scatter_pc<long long, E>, PcSmem<long long, E>::BYTES, attr);
         k_scatter_pc<long long, E><<<tiles, 256, PcSmem<long long, E>::BYTES, s>>>(out, ndst, d_ndst, is, vs, m,

@@ -262,6 +262,101 @@ __global__ void __launch_bounds__(256) k_scatter_pc(E* __restrict__ out, long lo
   if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
 }
 
+// CHECKED scatter, claims in 2-way set-associative shared-memory windows:
+// window w (4096 destinations) lives in set w & 3, one of its two ways, so a
+// claim finds its slot with ONE 16-byte tag load and two compares -- no
+// window search, no per-thread window cache, no divergent lookup loop.  Two
+// interleaved monotone streams (C3: each touches <= 2 consecutive windows
+// per tile, i.e. two consecutive sets) always fit; a window that finds its
+// set full claims straight in the global bitmap.  Each thread claims 16
+// consecutive sources (rotated reads, conflict-free), one shared atomic per
+// in-range pair whose old value flags a duplicate inside the tile; the
+// windows are then merged with one coalesced global atomicOr per non-zero
+// word (the old value flags one across tiles).  Stores are striped.
+template <typename E>
+__global__ void __launch_bounds__(256) k_scatter_sa(E* __restrict__ out, long long ndst,
+                                                    const long long* __restrict__ d_ndst,
+                                                    const long long* __restrict__ is, const E* __restrict__ vs,
+                                                    long long m, uint32_t* __restrict__ claim, LBHeader* hdr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  long long* s_is = reinterpret_cast<long long*>(smem_raw);
+  E* s_vs = reinterpret_cast<E*>(smem_raw + kScTile * sizeof(long long));
+  __shared__ uint32_t s_bits[kWinSlots * kWinWords];
+  __shared__ __align__(16) unsigned long long s_win[kWinSlots];  // set q: ways 2q, 2q + 1
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (d_ndst) ndst = *d_ndst;
+  const long long base = (long long)blockIdx.x * kScTile;
+  if (base >= m) return;
+  const int t = threadIdx.x;
+  const bool full = base + kScTile <= m;
+  for (int q = t; q < kWinSlots * kWinWords; q += 256) s_bits[q] = 0u;
+  if (t < kWinSlots) s_win[t] = ~0ull;
+  if (full && t == 0) {
+    mbar_init(&s_mbar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&s_mbar, (uint32_t)PcSmem<long long, E>::BYTES);
+    bulk_g2s(s_is, is + base, kScTile * (uint32_t)sizeof(long long), &s_mbar);
+    bulk_g2s(s_vs, vs + base, kScTile * (uint32_t)sizeof(E), &s_mbar);
+  }
+  __syncthreads();
+  bool dup = false;
+  const uint32_t win_sa = smem_u32(s_win);  // (the shared address once, not per claim)
+  auto claim_one = [&](long long d) {
+    if ((unsigned long long)d >= (unsigned long long)ndst) return;  // oracle.py:300
+    const unsigned long long w = (unsigned long long)d >> kWinBits;
+    const int q = 2 * (int)(w & (kWinSlots / 2 - 1));
+    unsigned long long t0, t1;  // both ways' tags, one 16-byte shared load
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(t0), "=l"(t1) : "r"(win_sa + 8u * q));
+    int sl = t0 == w ? q : (t1 == w ? q + 1 : -1);
+    if (sl < 0) {  // first touch of w in this tile, or its set is full
+#pragma unroll 1
+      for (int j = q; j < q + 2; ++j) {
+        unsigned long long cur = reinterpret_cast<volatile unsigned long long*>(s_win)[j];
+        if (cur == ~0ull) {
+          cur = atom_cas_shared(&s_win[j], ~0ull, w);
+          if (cur == ~0ull) cur = w;
+        }
+        if (cur == w) {
+          sl = j;
+          break;
+        }
+      }
+    }
+    const uint32_t bit = 1u << (d & 31);
+    if (sl >= 0) {
+      if (atom_or_shared(&s_bits[sl * kWinWords + (int)((d >> 5) & (kWinWords - 1))], bit) & bit) dup = true;
+    } else if (atomicOr(&claim[d >> 5], bit) & bit) {
+      dup = true;
+    }
+  };
+  if (full) {
+    mbar_wait(&s_mbar, 0);
+#pragma unroll 4
+    for (int jj = 0; jj < kScTile / 256; ++jj)
+      claim_one(s_is[t * (kScTile / 256) + ((jj + t) & (kScTile / 256 - 1))]);
+    __syncwarp();  // reconverged: the striped stores leave as whole-warp stores
+    for (int k = t; k < kScTile; k += 256) {
+      const long long d = s_is[k];
+      if ((unsigned long long)d < (unsigned long long)ndst) out[d] = s_vs[k];
+    }
+  } else {
+    for (long long i = base + t; i < m; i += 256) {
+      const long long d = is[i];
+      claim_one(d);
+      if ((unsigned long long)d < (unsigned long long)ndst) out[d] = vs[i];
+    }
+  }
+  __syncthreads();
+  // merge the touched windows: ONE coalesced atomicOr per non-zero word
+  for (int gq = t; gq < kWinSlots * kWinWords; gq += 256) {
+    const unsigned long long w = s_win[gq / kWinWords];
+    if (w == ~0ull) continue;
+    const uint32_t word = s_bits[gq];
+    if (word && (atomicOr(&claim[w * kWinWords + gq % kWinWords], word) & word)) dup = true;
+  }
+  if (__any_sync(0xffffffffu, dup) && lane_id() == 0) atomicExch(&hdr->dup, 1u);
+}
+
 // ELIDED scatter of TMA-staged tiles (k_scatter_t) for any index type, with
 // the pair count optionally on the device (binned pairs)
 template <typename I, typename E>
