@@ -1014,8 +1014,12 @@ def run_ours(args):
     sampler.start()
     # soak so the clock sampler sees the loaded state
     t_end = time.time() + (0.3 if args.quick else 1.5)
-    while time.time() < t_end:
+    while True:
         wl.step(selected)
+        # every rank must run the same number of steps (each step holds
+        # collectives): stop when any rank is past its deadline
+        if (time.time() >= t_end) if ws == 1 else max_over_ranks(float(time.time() >= t_end), ws) > 0:
+            break
     torch.cuda.synchronize()
     kid, kbytes, kname = wl.kernel()
     # the step on its own (nothing but the pipeline's launches in the stream),
@@ -1285,6 +1289,10 @@ def _free_port() -> int:
 
 
 def main():
+    if os.environ.get("IXG_HANG_DUMP"):  # diagnostics: every thread's stack to stderr after N s
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["IXG_HANG_DUMP"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)

@@ -57,7 +57,8 @@ def main():
     while time.time() < t_end:
         it += 1
         op = rng.choice(["filter", "partition2", "partition3", "c2", "scan", "segscan", "scatter", "csr", "hist",
-                         "filter_chk", "partition2_chk", "partition3_chk", "c2_chk", "scatter_binned"])
+                         "filter_chk", "partition2_chk", "partition3_chk", "c2_chk", "scatter_binned",
+                         "scatter_streams", "scatter_conflict", "flags", "peer"])
         dt = rng.choice([np.int32, np.int64])
         lg = rng.randint(0, a.max_log2)
         n = max(0, (1 << lg) + rng.randint(-7, 7) * rng.choice([1, 17, 4099]))
@@ -124,6 +125,66 @@ def main():
             ops.scatter(out, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev), bits, st,
                         layout=L.SCATTER_BINNED)
             ok = np.array_equal(out.cpu().numpy(), O.scatter(dst_h, is_h, vs_h))
+        elif op == "scatter_streams":
+            # CHECKED over C3's index pattern (two interleaved monotone streams: the set-associative
+            # claim windows' fast path), a few indices moved out of range
+            c_h = gen.uniform(it, n, 0, 1, np.int64) == 0
+            t = np.cumsum(c_h)
+            is_h = np.where(c_h, t - 1, (t[-1] if n else 0) + (np.arange(1, n + 1) - t) - 1).astype(np.int64)
+            if n:
+                is_h[gen.uniform(it + 1, max(1, n // 97), 0, n - 1, np.int64)] = -1
+            vs_h = gen.uniform(it + 2, n, -(1 << 30), 1 << 30, np.int64)
+            dst_h = gen.uniform(it + 3, n, -9, 9, np.int64)
+            out = torch.from_numpy(dst_h.copy()).to(dev)
+            ops.scatter(out, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev),
+                        L.V_BOUNDS | L.V_CONFLICT | L.V_INIT, st)
+            ok = np.array_equal(out.cpu().numpy(), O.scatter(dst_h, is_h, vs_h))
+        elif op == "scatter_conflict":
+            # CHECKED with ONE conflicting duplicate among equal-valued ones: NonIdempotentScatter
+            if n < 2:
+                continue
+            is_h = gen.uniform(it + 2, n, 0, max(0, n - 1), np.int64)
+            vs_h = is_h * 3 + 1
+            j = rng.randrange(n)
+            k2 = rng.randrange(n)
+            is_h[k2] = is_h[j]
+            if j != k2:
+                vs_h[k2] = vs_h[j] + 1
+            out = torch.from_numpy(np.zeros(n, np.int64)).to(dev)
+            ops.scatter(out, torch.from_numpy(is_h).to(dev), torch.from_numpy(vs_h).to(dev),
+                        L.V_BOUNDS | L.V_CONFLICT | L.V_INIT, st)
+            s2 = st.read()
+            ok = (not s2.ok and bool(s2.codes & (1 << L.CONFLICT))) if j != k2 else s2.ok
+            st = ops.Status(dev)  # the expected failure is checked; the common check below sees a clean status
+        elif op == "flags":
+            # mkFlags as a bitmap (the C2 chain's clear + big-tile scan), empty / negative segments
+            m = max(0, n // rng.choice([1, 3, 64]))
+            shape_h = gen.uniform(it, m, rng.choice([0, -3]), rng.choice([1, 8, 300]), np.int64)
+            scn = np.concatenate([[0], np.cumsum(shape_h)[:-1]]) if m else np.zeros(0, np.int64)
+            nbits = int(shape_h[shape_h > 0].sum()) + rng.choice([0, 1, 77]) if m else rng.choice([1, 33])
+            bits = ops.flag_bitmap(torch.from_numpy(shape_h).to(dev), nbits)
+            got = bits.cpu().numpy().view(np.uint32)[: (nbits + 31) // 32].copy()
+            if nbits % 32:
+                got[-1] &= np.uint32((1 << (nbits % 32)) - 1)
+            want = np.zeros((nbits + 31) // 32, np.uint32)
+            sel = (shape_h > 0) & (scn >= 0) & (scn < nbits)
+            np.bitwise_or.at(want, (scn[sel] >> 5).astype(np.int64), (np.uint32(1) << (scn[sel] & 31).astype(np.uint32)))
+            ok = np.array_equal(got, want)
+        elif op == "peer":
+            # the sharded partition2 (one read, both classes placed) for G simulated ranks
+            G = rng.choice([1, 2, 3, 5, 8])
+            ep = 4 if dt == np.int32 else 2
+            per = max(ep, (n // G) // ep * ep)
+            xs_h = gen.uniform(it, G * per, span[0], span[1], dt)
+            wnt, wys = O.partition2(p, xs_h)
+            tdt = xs.dtype
+            bufs = [torch.empty(per, dtype=tdt, device=dev) for _ in range(G)]
+            shards = [torch.from_numpy(xs_h[r * per:(r + 1) * per].copy()).to(dev) for r in range(G)]
+            d_counts = torch.cat([ops.partition_counts(x, p) for x in shards])
+            for r in range(G):
+                ops.partition2_peer(shards[r], p, [b.data_ptr() for b in bufs], per, d_counts, r)
+            ok = int(d_counts.sum().item()) == wnt and np.array_equal(
+                torch.cat(bufs).cpu().numpy().astype(np.int64), wys)
         elif op == "csr":
             ncols = rng.choice([1, 97, 1 << 16])
             x_h = gen.uniform(it, ncols, -(1 << 15), (1 << 15) - 1, np.int64)
