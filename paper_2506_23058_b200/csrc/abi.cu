@@ -427,7 +427,7 @@ inline bool mkf_big_enabled() {
   return mode == 1;
 }
 int launch_mkflags(const long long* shape, long long m, uint32_t* bits, long long nbits, const long long* d_nbits,
-                   LBChan c, cudaStream_t s) {
+                   LBChan c, cudaStream_t s, ixg_status* st = nullptr) {
   const bool big = mkf_big_enabled() && aligned16(shape) && aligned16(bits) && m > 0;
   if (big) {  // the clear heads a programmatic-launch chain (see k_bitmap_zero)
     k_bitmap_zero<<<grid_for((nbits + 127) / 128), kGThreads, 0, s>>>(
@@ -449,7 +449,7 @@ int launch_mkflags(const long long* shape, long long m, uint32_t* bits, long lon
     fn.nb = nbits;
     fn.d_nb = d_nbits;
     return launch_segsum_b<long long, long long, SumOp>(shape, m, nullptr, nullptr, 0, nullptr, c, 0, 0, nullptr,
-                                                        nullptr, s, nullptr, fn);
+                                                        st, s, nullptr, fn);
   }
   return launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, nbits, d_nbits, nullptr},
                             c, s);
@@ -578,7 +578,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
     // load, count and compact while the scan runs and wait only before they
     // read the bitmap (a kernel clearing the bitmap instead of the memset, to
     // chain all three launches, measured no faster)
-    int rc = launch_mkflags(shape, m, bits, n, nullptr, cs, s);  // clear + scan
+    int rc = launch_mkflags(shape, m, bits, n, nullptr, cs, s, st);  // clear + scan
     if (rc) return rc;
     if constexpr (sizeof(Z) == sizeof(T)) {
       if (!seg_split_mode()) {

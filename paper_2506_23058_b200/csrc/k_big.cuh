@@ -1155,7 +1155,7 @@ struct SegFlagArr : ScanId {
 // scattered under Ss2 with starts outside [0, nbits) skipped).  The C2 fused
 // kernel is its programmatic dependent.
 struct ScanSegStartBits : ScanId {
-  static constexpr bool kOvf = false;
+  static constexpr bool kOvf = true;  // a start past int64 is IXG_OVERFLOW, never a wrapped bit (§2.2)
   static constexpr bool kStore = false;
   static constexpr bool kTrigger = true;
   static constexpr int kCH = IXG_MKF_CH;  // 4 K-value tiles: 256 CTAs for C2's 2^20 segments
