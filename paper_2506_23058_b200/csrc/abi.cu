@@ -451,7 +451,7 @@ int launch_mkflags(const long long* shape, long long m, uint32_t* bits, long lon
     return launch_segsum_b<long long, long long, SumOp>(shape, m, nullptr, nullptr, 0, nullptr, c, 0, 0, nullptr,
                                                         st, s, nullptr, fn);
   }
-  return launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, nbits, d_nbits, nullptr},
+  return launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, nbits, d_nbits, nullptr, st},
                             c, s);
 }
 
@@ -603,7 +603,7 @@ int do_c2(const T* xs, long long n, const ixg_pred* p, const long long* shape, l
   long long* flags = (long long*)ws.take((size_t)(n > 0 ? n : 1) * 8);
   if (ws.dry) return launch_scatter<long long>(flags, 0, d_k, n, ind, ones, m, sb3, 3, 3, st, ws, 4, s);
   if (n <= 0) return IXG_OK;
-  if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr, nullptr}, cs, s)))
+  if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, ind, nullptr, 0, nullptr, nullptr, st}, cs, s)))
     return rc;
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
   if ((rc = launch_fill<long long>(flags, 0, d_k, 0LL, s))) return rc;
@@ -1112,7 +1112,8 @@ int ixg_mksgmdescr(const int64_t* shape, const int64_t* xs, int64_t m, int64_t n
   if (m == 0) return cuda_rc(cudaMemsetAsync(d_len, 0, 8, s));
   // scn / ind / len (mksgmdescr.ixl:6-9); len = scn[m-1] + shape[m-1] = sum shape
   int rc = launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
-                              EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr, (long long*)d_len}, c, s);
+                              EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr, (long long*)d_len, st}, c,
+                              s);
   if (rc || cap == 0) return rc;
   // the scatter is never proved for mkSgmDescr: the host
   // passes cap >= len (read back from d_len), res[0..len) = 0, checked scatter.
@@ -1257,7 +1258,7 @@ int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint
   if (k > 0 && (rc = launch_fill<long long>((long long*)flags, k, nullptr, 0LL, s))) return rc;
   if (m == 0) return IXG_OK;
   if ((rc = launch_scan<SumOp>(m, SrcArrT<long long>{(const long long*)shape},
-                               EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr, nullptr}, c, s)))
+                               EpiSegStarts{m, (const long long*)shape, ind, nullptr, 0, nullptr, nullptr, st}, c, s)))
     return rc;
   if ((rc = launch_fill<long long>(ones, m, nullptr, 1LL, s))) return rc;
   return launch_scatter<long long>((long long*)flags, k, nullptr, k, ind, ones, m,

@@ -184,16 +184,18 @@ def test_c2_sum_below_k(cuda):
 def test_c2_shape_prefix_past_int64(cuda):
     """A segment shape whose running sum leaves int64 (the reference's ints
     are unbounded, its starts past n are simply dropped): the ELIDED mkFlags
-    scan records IXG_OVERFLOW instead of setting a bit at a wrapped start."""
+    scan (and the CHECKED pipeline's materialised starts) record IXG_OVERFLOW
+    instead of setting a flag at a wrapped start."""
     from paper_2506_23058_b200 import ops
 
     n = 10_000
     xs = gen.uniform(17, n, -128, 127, np.int32)
     shape = np.array([5, 1 << 62, 1 << 62, 3, 7], np.int64)
-    st = ops.Status(cuda)
-    ops.c2(_t(xs, cuda), Pred.ge(0), _t(shape, cuda), L.VARIANT_ELIDED, st)
-    s = st.read()
-    assert not s.ok and s.codes & (1 << L.OVERFLOW)
+    for variant in VARIANTS:
+        st = ops.Status(cuda)
+        ops.c2(_t(xs, cuda), Pred.ge(0), _t(shape, cuda), variant, st)
+        s = st.read()
+        assert not s.ok and s.codes & (1 << L.OVERFLOW), variant
 
 
 def _flag_bits_ref(shape, nbits):
