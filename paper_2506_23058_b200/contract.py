@@ -44,7 +44,10 @@ def conjuncts(e):
         yield e
 
 
-def has_preconditions(fdef) -> bool:
+def has_preconditions(fdef, required=None) -> bool:
+    """any annotation to check (required: see check)?"""
+    if required is not None:
+        return bool(required)
     return any(p.pre is not None for p in fdef.params)
 
 
@@ -170,14 +173,21 @@ def _atom(atom, env) -> bool:
     return bool(scalar(atom, env))
 
 
-def check(fdef, values: dict):
+def check(fdef, values: dict, required=None):
     """Do `fdef`'s parameter annotations hold for `values` (param name ->
-    device tensor / host scalar)?  Returns (ok, reason)."""
+    device tensor / host scalar)?  Returns (ok, reason).  `required`: the
+    "param|atom" keys the verdicts depend on (select.required_atoms); the
+    other conjuncts back no elided check and are not evaluated.  None: all."""
+    from .select import atom_key
+
+    need = None if required is None else set(required)
     env = bind_sizes(fdef, values)
     for p in fdef.params:
         if p.pre is None:
             continue
         for atom in conjuncts(p.pre):
+            if need is not None and atom_key(p.name, atom) not in need:
+                continue
             try:
                 ok = _atom(atom, env)
             except Unknown as ex:

@@ -193,9 +193,10 @@ class Interp:
     def _contract_ok(self, fdef, values: dict) -> bool:
         """Do fdef's annotations hold for these arguments?  Checked on the
         device (contract.py) unless the caller vouches for them."""
-        if self.preconditions == "trust" or not contract.has_preconditions(fdef):
+        required = sel.selection_for(self.program, fdef).required
+        if self.preconditions == "trust" or not contract.has_preconditions(fdef, required):
             return True
-        ok, why = contract.check(fdef, values)
+        ok, why = contract.check(fdef, values, required)
         self.trace.append(("pre", fdef.name, ok, why))
         return ok
 

@@ -72,6 +72,9 @@ class FunSelection:
     sites: list = field(default_factory=list)
     closure: str = ""  # ir.closure_fingerprint: the key the verdicts are valid for
     source: str = ""   # "live" | "frozen" | "checked" (where these verdicts came from)
+    # the parameter annotations the elided sites' proofs need ("param|atom",
+    # see required_atoms); None = all of them (no ablation ran)
+    required: Optional[list] = None
 
     @property
     def elides(self) -> bool:
@@ -97,7 +100,7 @@ class FunSelection:
     @classmethod
     def from_json(cls, d):
         sites = [SiteVerdict(**{**s, "pos": tuple(s["pos"])}) for s in d["sites"]]
-        return cls(d["name"], d["fingerprint"], d["status"], sites, d.get("closure", ""))
+        return cls(d["name"], d["fingerprint"], d["status"], sites, d.get("closure", ""), "", d.get("required"))
 
 
 @dataclass
@@ -144,36 +147,99 @@ def _scatter_result_names(fundef):
     return out
 
 
-def select(program, max_rewrites: int = 1000) -> Selection:
+def _analyze(a, infer, props, f):
+    """(status, site verdicts, FunInfo or None) of one definition."""
+    status, info = "verified", None
+    try:
+        info = a.analyze_fun(f)
+    except infer.InferError as exc:  # keep the partial obligation list
+        status = f"failed: {type(exc).__name__}: {exc}"
+    obls = list(getattr(a, "obligations", []))
+    names = _scatter_result_names(f)
+    sites = []
+    for kind, pos, node in ir.sites(f):
+        rec = [o for o in obls if tuple(o.pos) == pos and o.kind == kind]
+        v = SiteVerdict(kind, pos, ir.expr_str(node), recorded=bool(rec), proved=bool(rec) and all(o.proved for o in rec))
+        if kind == "scatter-safety" and rec:
+            v.rule = rec[0].text.replace("scatter via ", "").replace("scatter", "").strip()
+            nm = names.get(pos)
+            if v.proved and info is not None and nm in info.gamma:
+                try:
+                    v.sc1 = props._inv_pattern(info.gamma[nm]) is not None
+                except Exception:
+                    v.sc1 = False
+        sites.append(v)
+    return status, sites, info
+
+
+def atom_key(param_name: str, atom) -> str:
+    """The identity of one annotation conjunct (same text for the reference's
+    AST and this package's IR mirror)."""
+    return f"{param_name}|{ir.expr_str(atom)}"
+
+
+def _conjuncts(e):
+    if ir.kind(e) == "BinOp" and e.op == "&&":
+        yield from _conjuncts(e.lhs)
+        yield from _conjuncts(e.rhs)
+    else:
+        yield e
+
+
+def required_atoms(a, infer, props, f, base_bits) -> Optional[list]:
+    """Which parameter annotations do the verdicts depend on?  Ablation with
+    the verifier itself: drop one conjunct at a time and re-analyze; a
+    conjunct whose removal leaves every site's bits unchanged is not needed
+    by any elision.  The conjuncts found free one by one are then dropped
+    TOGETHER and re-checked (two may each be redundant only given the
+    other); if that changes any bits, every conjunct stays required.  Only
+    the required ones are checked on the device before ELIDED variants run
+    (contract.py) -- an annotation no proof used cannot make an elided
+    check unsafe."""
+    import dataclasses
+
+    atoms = [(pi, k, atom) for pi, q in enumerate(f.params) if q.pre is not None
+             for k, atom in enumerate(_conjuncts(q.pre))]
+    if not atoms:
+        return []
+    mod = sys.modules[type(atoms[0][2]).__module__]
+
+    def bits_without(drop):
+        params = list(f.params)
+        for pi, q in enumerate(f.params):
+            if q.pre is None:
+                continue
+            keep = [atom for k, atom in enumerate(_conjuncts(q.pre)) if (pi, k) not in drop]
+            pre = None
+            for atom in keep:
+                pre = atom if pre is None else mod.BinOp("&&", pre, atom, atom.pos)
+            params[pi] = dataclasses.replace(q, pre=pre)
+        try:
+            _, sites, _ = _analyze(a, infer, props, dataclasses.replace(f, params=tuple(params)))
+        except Exception:
+            return None
+        return [s.bits for s in sites]
+
+    free = {(pi, k) for pi, k, _ in atoms if bits_without({(pi, k)}) == base_bits}
+    if free and len(free) > 1 and bits_without(free) != base_bits:
+        free = set()
+    return [atom_key(f.params[pi].name, atom) for pi, k, atom in atoms if (pi, k) not in free]
+
+
+def select(program, max_rewrites: int = 1000, ablate: bool = True) -> Selection:
     """Run the reference verifier per definition and derive site verdicts.
     `program` must be the reference's normalized Program."""
     infer, props = _import_reference()
     a = infer.Analyzer(program, max_rewrites=max_rewrites)
     funcs = {}
     for f in program.defs:
-        status = "verified"
-        try:
-            a.infos[f.name] = a.analyze_fun(f)
-        except infer.InferError as exc:  # keep the partial obligation list
-            status = f"failed: {type(exc).__name__}: {exc}"
-        obls = list(getattr(a, "obligations", []))
-        info = a.infos.get(f.name)
-        names = _scatter_result_names(f)
-        sites = []
-        for kind, pos, node in ir.sites(f):
-            rec = [o for o in obls if tuple(o.pos) == pos and o.kind == kind]
-            v = SiteVerdict(kind, pos, ir.expr_str(node), recorded=bool(rec), proved=bool(rec) and all(o.proved for o in rec))
-            if kind == "scatter-safety" and rec:
-                v.rule = rec[0].text.replace("scatter via ", "").replace("scatter", "").strip()
-                nm = names.get(pos)
-                if v.proved and info is not None and nm in info.gamma:
-                    try:
-                        v.sc1 = props._inv_pattern(info.gamma[nm]) is not None
-                    except Exception:
-                        v.sc1 = False
-            sites.append(v)
-        funcs[f.name] = FunSelection(f.name, ir.fingerprint(f), status, sites, ir.closure_fingerprint(program, f),
-                                     "live")
+        status, sites, info = _analyze(a, infer, props, f)
+        if info is not None:
+            a.infos[f.name] = info
+        fs = FunSelection(f.name, ir.fingerprint(f), status, sites, ir.closure_fingerprint(program, f), "live")
+        if ablate and fs.elides:
+            fs.required = required_atoms(a, infer, props, f, [s.bits for s in sites])
+        funcs[f.name] = fs
     return Selection(funcs)
 
 
@@ -273,5 +339,5 @@ def _selection_for(program, fundef, live: bool) -> FunSelection:
             cur = ir.sites(fundef)
             if len(cur) == len(fz.sites) and all(a.kind == k for a, (k, _, _) in zip(fz.sites, cur)):
                 sites = [SiteVerdict(**{**asdict(s), "pos": pos}) for s, (_, pos, _) in zip(fz.sites, cur)]
-                return FunSelection(fundef.name, fz.fingerprint, fz.status, sites, key, "frozen")
+                return FunSelection(fundef.name, fz.fingerprint, fz.status, sites, key, "frozen", fz.required)
     return checked_selection(fundef)

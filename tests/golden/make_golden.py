@@ -96,7 +96,7 @@ def run(program, fun, args, budget=BUDGET):
 PROPERTY_HEADS = {"Range", "Equiv", "Mono", "Inj", "Bij", "FiltPart", "InvFiltPart", "OrthogPreds"}
 
 
-def ref_pre_holds(program, fun, args):
+def ref_pre_holds(program, fun, args, required=None):
     """Do the entry function's annotations hold for these arguments, by the
     reference's own concrete predicates?  Range / Mono through
     oracle.py:712-734 _check_pre_atom, Inj / Bij over their codomain interval
@@ -109,10 +109,13 @@ def ref_pre_holds(program, fun, args):
         return None
     env = {p.name: a for p, a in zip(f.params, args)}
     interp._bind_sizes(f, args, env)
+    need = None if required is None else set(required)
     for p in f.params:
         if p.pre is None:
             continue
         for atom in _conjuncts(p.pre):
+            if need is not None and sel.atom_key(p.name, atom) not in need:
+                continue  # no elided check depends on it (select.required_atoms)
             head = atom.fun.name if type(atom).__name__ == "App" and type(atom.fun).__name__ == "VarE" else None
             try:
                 if head in ("Inj", "Bij"):
@@ -384,7 +387,7 @@ def main():
                 # a never-ending loop is cut by the default budget (oracle.py:118)
                 bud = 10**6 if (f.name, origin_kind) == ("countdown", "error") else BUDGET
                 rec.update(run(prog, f.name, a, bud))
-                rec["pre"] = ref_pre_holds(prog, f.name, a)
+                rec["pre"] = ref_pre_holds(prog, f.name, a, s.funcs[f.name].required)
                 rec["budget"] = bud  # the step budget the reference ran with
                 cases.append(rec)
     data = os.path.join(ROOT, "paper_2506_23058_b200", "data")

@@ -494,3 +494,37 @@ def test_contract_host_side():
     assert lo == float("-inf") and hi == float("inf")
     assert contract._clamp_int(lo, hi, -5, 9) == (-5, 9)
     assert contract._clamp_int(0, 3, -5, 9) == (0, 3)
+
+
+def test_required_annotations_by_ablation():
+    """Only the annotations some elision depends on are checked at run time
+    (select.required_atoms: the verifier re-run with each conjunct dropped).
+    get_smallest_pairs' `Inj is (-inf, inf)` backs no elided check (the
+    H[i] gather needs `Range es` only), so an input violating it still runs
+    ELIDED; kmeans_ker needs all three of its Range annotations."""
+    from paper_2506_23058_b200 import contract
+
+    gsp = SELECTION["ref:maxmatching.ixl:get_smallest_pairs"]
+    assert gsp["required"] == ["es|Range es ((0, n_verts - 1))"]
+    km = SELECTION["ref:kmeans_ker.ixl:kmeans_ker"]
+    assert len(km["required"]) == 3 and all(r.split("|")[1].startswith("Range") for r in km["required"])
+    assert SELECTION["own:c3_scatter.ixl:sc_inj"]["required"] == ["is|Inj is ((0, n - 1))"]
+    # the frozen verdict carries the list; nothing left to check -> no device work at all
+    prog = _prog("ref:maxmatching.ixl")
+    f = ir.find_def(prog, "get_smallest_pairs")
+    fs = sel.selection_for(prog, f, live=False)
+    assert fs.source == "frozen" and fs.required == gsp["required"]
+    assert contract.check(f, {}, required=[]) == (True, "")
+    assert not contract.has_preconditions(f, required=[]) and contract.has_preconditions(f)
+
+
+@pytest.mark.reference
+def test_required_annotations_live(reference):
+    """The live selector computes the same required set as the frozen table."""
+    from ixverify.normalize import normalize
+    from ixverify.parser import parse_program
+
+    src = PROGRAMS["ref:maxmatching.ixl"]["source"]
+    prog = normalize(parse_program(src, "maxmatching.ixl"))
+    fs = sel.selection_for(prog, ir.find_def(prog, "get_smallest_pairs"))
+    assert fs.source == "live" and fs.required == ["es|Range es ((0, n_verts - 1))"]
