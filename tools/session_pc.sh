@@ -22,7 +22,7 @@ for kind in sys.argv[1:]:
     del is_, vs, out
 PY
 export PYTHONPATH=$PWD
-ncu --set full --import-source on --clock-control none -k regex:"${1:-k_scatter_sa}" -c 1 -o gpurun_out/ncu_pc python /tmp/c3prof.py streams_chk > gpurun_out/ncu_pc.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"${1:-k_scatter_sa}" -c 1 -o gpurun_out/ncu_pc python /tmp/c3prof.py ${2:-streams_chk} > gpurun_out/ncu_pc.log 2>&1
 ncu -i gpurun_out/ncu_pc.ncu-rep --page details --csv > gpurun_out/ncu_pc_details.csv 2>/dev/null
 ncu -i gpurun_out/ncu_pc.ncu-rep --page source --csv > gpurun_out/ncu_pc_source.csv 2>/dev/null
 tail -2 gpurun_out/ncu_pc.log
