@@ -1,7 +1,7 @@
-export PYTHONPATH=$PWD
-python -m pytest tests/test_gpu_kernels.py -q -p no:cacheprovider -x -k "scatter or stream" > gpurun_out/pytest_sc.txt 2>&1; tail -5 gpurun_out/pytest_sc.txt
-for p in streams random; do timeout 600 python bench.py --config c3 --perm $p --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_c3_$p.json 2> gpurun_out/bench_c3_$p.err; echo "c3 $p rc=$?"; done
-cat > /tmp/c3prof.py <<'PY'
+"""C3 scatter inputs for ncu captures (development tool): python tools/c3prof.py KIND...
+
+KIND: streams | random (the C3 / C3-secondary index patterns at 2^29), with the
+suffix _chk for the CHECKED scatter; two scatters each."""
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2506_23058_b200 import ops, _lib as L
@@ -23,5 +23,3 @@ for kind in sys.argv[1:]:
         ops.scatter(out, is_, vs, bits, st)
     torch.cuda.synchronize()
     del is_, vs, out
-PY
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_write.sum,lts__t_sectors_op_atom.sum --clock-control none -k regex:"k_scatter|k_bin" --csv python /tmp/c3prof.py streams streams_chk random random_chk > gpurun_out/ncu_c3.csv 2> gpurun_out/ncu_c3.err

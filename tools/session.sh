@@ -1,26 +1,3 @@
-cat > /tmp/c3prof.py <<'PY'
-import sys, torch
-sys.path.insert(0, '.')
-from paper_2506_23058_b200 import ops, _lib as L
-n = 1 << 29
-dev = torch.device('cuda')
-g = torch.Generator(device=dev); g.manual_seed(11)
-for kind in sys.argv[1:]:
-    if kind.startswith('random'):
-        is_ = torch.randperm(n, generator=g, device=dev, dtype=torch.int64)
-    else:
-        xs = ops.gen_uniform(n, -(1 << 31), (1 << 31) - 1, 11, torch.int32)
-        c = xs < 0; t = torch.cumsum(c, 0, dtype=torch.int64); i1 = torch.arange(1, n + 1, device=dev, dtype=torch.int64)
-        is_ = torch.where(c, t - 1, t[-1] + (i1 - t) - 1); del xs, c, t, i1
-    vs = ops.gen_uniform(n, -(1 << 31), (1 << 31) - 1, 12, torch.int32)
-    out = torch.zeros(n, dtype=torch.int32, device=dev)
-    st = ops.Status(dev)
-    bits = L.V_CONFLICT | L.V_INIT if kind.endswith('chk') else 0
-    for _ in range(2):
-        ops.scatter(out, is_, vs, bits, st)
-    torch.cuda.synchronize()
-    del is_, vs, out
-PY
 # One GPU session: the GPU test suite, smoke, every bench config (ours + the
 # reference arm), ncu launch lists of each config's step and --set full
 # captures of the dominant kernels.  Outputs under gpurun_out/ (copy the
@@ -55,4 +32,4 @@ cap() {  # name, kernel regex, launch-skip, command...
 cap c2_fused "k_filter_b" 2 python tools/prof_run.py c2 28 4
 cap c5_place "k_filter_b" 2 python tools/prof_run.py partition2 28 4
 cap c4_gather "k_csr_gather" 2 python tools/prof_run.py csr 28 4
-cap c3_scatter "k_scatter_t" 1 python /tmp/c3prof.py streams
+cap c3_scatter "k_scatter_t" 1 python tools/c3prof.py streams
