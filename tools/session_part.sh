@@ -42,7 +42,7 @@ case "${1:-}" in
     CHECKED=1 cap chk_p2_scan "k_segsum_b" 0 python tools/prof_run.py partition2 28 2
     CHECKED=1 cap chk_p2_scatter "k_scatter_sa" 1 python tools/prof_run.py partition2 28 2
     cap peer "k_filter_b" 2 python tools/prof_run.py peer 28 2
-    cap map_jit "ixg_map" 1 python tools/prof_run.py map_jit 26 2
+    cap map_jit "ixg_jit_map" 1 python tools/prof_run.py map_jit 26 2
     cap scan_jit "ixg_scan_down" 1 python tools/prof_run.py scan_jit 26 2
     ;;
   scatter)
