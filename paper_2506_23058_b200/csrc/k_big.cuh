@@ -424,24 +424,33 @@ IXG_DEV void store_run_peer(const PeerOut<E>& po, long long gbase, int cnt, cons
   }
 }
 
-// kDual store of ONE class of a tile: its elements, in class order, are the
-// CH per-chunk sub-runs of the in-place partitioned tile buffer (class rank
-// r in chunk c, pre[c] <= r < pre[c + 1], sits at slot r + D[c] of `buf`,
-// a 16-byte aligned base), and they go to the global positions
-// [g0, g0 + len) of the sharded output.  One loop over the 16-byte output
-// pieces: a piece inside one sub-run is funnel-shifted from the two aligned
-// 16-byte words it straddles, the few pieces at run or chunk edges go
-// element by element.  r0 = g0 / shard when len <= shard (the run then
-// crosses at most one shard edge: each piece picks one of two precomputed
-// bases), else -1 (a division per piece -- shards smaller than a tile).
-template <typename E, int CH, int NT>
-IXG_DEV void store_class_peer(const PeerOut<E>& po, const E* buf, long long g0, int len, const int (&pre)[CH + 1],
-                              const int (&D)[CH], long long r0) {
+// One WARP stores one contiguous run of shared memory (starting at any
+// element) to the global positions [gbase, gbase + cnt) of the sharded
+// output: 16-byte pieces funnel-shifted from the two aligned 16-byte words
+// each straddles (the shift is uniform over the run).  r0 = gbase / shard
+// when the run is no longer than a shard (one shard edge at most: two
+// precomputed bases), else -1 (a division per piece).
+// One WARP stores one contiguous run of shared memory (starting at any
+// element) to the global positions [gbase, gbase + cnt) of the sharded
+// output: 16-byte pieces funnel-shifted from the two aligned 16-byte words
+// each straddles (the shift is uniform over the run).  r0 = gbase / shard
+// when the run is no longer than a shard (one shard edge at most: two
+// precomputed bases), else -1 (a division per piece).  (Specialising the
+// interior pieces of a single-shard run -- no per-piece shard or bounds
+// logic -- cut the kernel's instructions by a quarter but not its time:
+// past this point it waits on memory latency, and the extra registers
+// spilled.)
+template <typename E>
+IXG_DEV void store_run_peer_w(const PeerOut<E>& po, long long gbase, int cnt, const E* run, long long r0) {
   constexpr int EP = 16 / (int)sizeof(E);
-  if (len <= 0) return;
-  const long long c0 = g0 / EP;
-  const int s = (int)(g0 - c0 * EP);
-  const int nch = (int)((g0 + len - 1) / EP - c0) + 1;
+  if (cnt <= 0) return;
+  const int lane = lane_id();
+  const long long c0 = gbase / EP;
+  const int s = (int)(gbase - c0 * EP);
+  const int nch = (int)((gbase + cnt - 1) / EP - c0) + 1;
+  const int o = (int)((smem_u32(run) & 15u) / sizeof(E));  // run's element offset in its 16-byte word
+  const E* al = run - o;
+  const int sw = ((o - s + EP) % EP) * (int)sizeof(E) / 4;
   E* p0 = nullptr;
   E* p1 = nullptr;
   long long edge = 0;
@@ -450,20 +459,8 @@ IXG_DEV void store_class_peer(const PeerOut<E>& po, const E* buf, long long g0, 
     p0 = po.dst[r0] - r0 * po.shard;
     p1 = r0 + 1 < po.ranks ? po.dst[r0 + 1] - edge : p0;
   }
-  auto chunk_of = [&](int r) {
-    int c = 0;
-#pragma unroll
-    for (int q = 1; q < CH; ++q) c += r >= pre[q] ? 1 : 0;
-    return c;
-  };
-  auto slot_of = [&](int r) {
-    int d = D[0];
-#pragma unroll
-    for (int q = 1; q < CH; ++q) d = r >= pre[q] ? D[q] : d;
-    return r + d;
-  };
-  for (int j = threadIdx.x; j < nch; j += NT) {
-    const int l = j * EP - s;  // class rank of the piece's first element
+  for (int j = lane; j < nch; j += 32) {
+    const int l = j * EP - s;
     const long long g = (c0 + j) * EP;
     E* dst;
     if (r0 >= 0) {
@@ -472,17 +469,15 @@ IXG_DEV void store_class_peer(const PeerOut<E>& po, const E* buf, long long g0, 
       const long long r = g / po.shard;
       dst = po.dst[r] + (g - r * po.shard);
     }
-    if (l >= 0 && l + EP <= len && chunk_of(l) == chunk_of(l + EP - 1)) {
-      const int a = slot_of(l);
-      const int a0 = a & ~(EP - 1);
-      const int sw = (a - a0) * (int)sizeof(E) / 4;
-      const uint4 x = *reinterpret_cast<const uint4*>(buf + a0);
-      uint4 v = x;
+    if (l >= 0 && l + EP <= cnt) {
+      const int a0 = (o + l) & ~(EP - 1);
+      const uint4 a = *reinterpret_cast<const uint4*>(al + a0);
+      uint4 v = a;
       if (sw) {
-        const uint4 y = *reinterpret_cast<const uint4*>(buf + a0 + EP);
-        if (sw == 1) v = make_uint4(x.y, x.z, x.w, y.x);
-        else if (sw == 2) v = make_uint4(x.z, x.w, y.x, y.y);
-        else v = make_uint4(x.w, y.x, y.y, y.z);
+        const uint4 b = *reinterpret_cast<const uint4*>(al + a0 + EP);
+        if (sw == 1) v = make_uint4(a.y, a.z, a.w, b.x);
+        else if (sw == 2) v = make_uint4(a.z, a.w, b.x, b.y);
+        else v = make_uint4(a.w, b.x, b.y, b.z);
       }
       asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(v.x), "r"(v.y),
                    "r"(v.z), "r"(v.w)
@@ -490,7 +485,7 @@ IXG_DEV void store_class_peer(const PeerOut<E>& po, const E* buf, long long g0, 
     } else {
 #pragma unroll
       for (int e = 0; e < EP; ++e)
-        if (l + e >= 0 && l + e < len) dst[e] = buf[slot_of(l + e)];
+        if (l + e >= 0 && l + e < cnt) dst[e] = run[l + e];
     }
   }
 }
@@ -916,23 +911,32 @@ __global__ void __launch_bounds__(kBT + 32, big_min_blocks<T>()) k_filter_b(cons
   const bool bulk = kBulk && ((((uintptr_t)ys) | (kSeg ? (uintptr_t)zs : (uintptr_t)0)) & 15) == 0;  // 16-byte aligned outputs
   T* run = buf;
   if constexpr (kDual) {
-    const long long gt = peer_gbase(po, 0, base);                                      // the tile's first true
-    const long long gf = peer_gbase(po, 1, po.d_counts[po.rank] + (tile_base - base));  // and first false
-    int pt[B::CH + 1], pf[B::CH + 1], dt[B::CH], df[B::CH];
-    pt[0] = pf[0] = 0;
+    // 2 x CH sub-runs (chunk c's trues, then its falses), one worker warp
+    // each: a warp's loop runs ~16 pieces per lane with its setup done once
+    static_assert(2 * B::CH <= kBW, "one worker warp per sub-run");
+    const int w = warp_id();
+    if (w < 2 * B::CH) {
+      const int c = w >> 1, cls = w & 1;
+      int pre = 0, tc_c = 0, nv_c = 0;
 #pragma unroll
-    for (int c = 0; c < B::CH; ++c) {
-      const long long left = n - tile_base - (long long)c * kBChunk;
-      const int nv = left <= 0 ? 0 : (left >= kBChunk ? kBChunk : (int)left);
-      const int tc = fieldc<B::CH>(tot, c);
-      dt[c] = B::PAD + c * kBChunk - pt[c];
-      df[c] = B::PAD + c * kBChunk + tc - pf[c];
-      pt[c + 1] = pt[c] + tc;
-      pf[c + 1] = pf[c] + nv - tc;
+      for (int q = 0; q < B::CH; ++q) {
+        const long long left = n - tile_base - (long long)q * kBChunk;
+        const int nv = left <= 0 ? 0 : (left >= kBChunk ? kBChunk : (int)left);
+        const int tc = fieldc<B::CH>(tot, q);
+        if (q < c) pre += cls ? nv - tc : tc;
+        if (q == c) {
+          tc_c = tc;
+          nv_c = nv;
+        }
+      }
+      const long long g0 =
+          cls ? peer_gbase(po, 1, po.d_counts[po.rank] + (tile_base - base)) + pre  // the tile's falses
+              : peer_gbase(po, 0, base) + pre;                                       // its trues
+      const int len = cls ? nv_c - tc_c : tc_c;
+      // a sub-run is <= a chunk: with shards of >= a chunk, one division per warp
+      store_run_peer_w<T>(po, g0, len, buf + B::PAD + c * kBChunk + (cls ? tc_c : 0),
+                          po.shard >= kBChunk ? g0 / po.shard : -1);
     }
-    const bool wide = po.shard >= B::TILE;  // a class run is <= a tile
-    store_class_peer<T, B::CH, kBT>(po, buf, gt, pt[B::CH], pt, dt, wide ? gt / po.shard : -1);
-    store_class_peer<T, B::CH, kBT>(po, buf, gf, pf[B::CH], pf, df, wide ? gf / po.shard : -1);
   } else if constexpr (kPeer) {
     store_run_peer<T, kBT>(po, peer_gbase(po, seg, base), cnt, buf);
   } else if (bulk) {
