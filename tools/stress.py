@@ -9,7 +9,7 @@ bit against oracle/ixoracle.  Runs
 for --seconds (default 300) and prints a JSON summary; exits 1 on the first
 mismatch.
 
-python tools/stress.py [--seconds S] [--max-log2 L]
+python tools/stress.py [--seconds S] [--max-log2 L] [--seed N]
 """
 
 import argparse
@@ -48,9 +48,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--max-log2", type=int, default=25)
+    ap.add_argument("--seed", type=int, default=1234)
     a = ap.parse_args()
     dev = torch.device("cuda")
-    rng = random.Random(1234)
+    rng = random.Random(a.seed)
     t_end = time.time() + a.seconds
     counts = {}
     it = 0
@@ -225,7 +226,7 @@ def main():
         if not ok:
             print(json.dumps({"mismatch": op, "n": n, "dtype": np.dtype(dt).name, "pred": repr(p), "iter": it}))
             sys.exit(1)
-    print(json.dumps({"iterations": it, "per_op": counts, "ok": True}))
+    print(json.dumps({"seed": a.seed, "iterations": it, "per_op": counts, "ok": True}))
 
 
 if __name__ == "__main__":
