@@ -227,9 +227,10 @@ class C2:
         from paper_2506_23058_b200 import _lib as L
 
         if self.ws == 1:
-            # one pass: xs read once, ys and zs written once, the flag bits
-            # of the k outputs read from the mkFlags bitmap
-            return (L.K_FILTER_FUSED, 4 * self.N + 8 * self.k + self.k // 8,
+            # one pass: xs read once, ys and zs written once; the mkFlags
+            # bitmap it also reads (k/8 B) is an intermediate, which
+            # SURVEY.md §8(d) counts as zero
+            return (L.K_FILTER_FUSED, 4 * self.N + 8 * self.k,
                     "k_filter_b<int32,kSeg> (filter + sgmSum in one pass: 48 KB TMA tiles, runs leave as phase-shifted bulk stores, two look-back chains)")
         # sharded: the filter pass; the sgmSum pass is reported alongside
         return L.K_FILTER_FUSED, 4 * self.N + 4 * self.k, "k_filter_b<int32> (single-pass filter, 48 KB TMA tiles)"
