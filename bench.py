@@ -451,6 +451,11 @@ class C1:
         xs_h = self.xs_h if self.xs_h is not None else self.xs.cpu().numpy()
         return (torch.from_numpy(xs_h).pin_memory(), torch.empty(self.N, dtype=torch.int32).pin_memory(), variant)
 
+    @property
+    def e2e_steps(self):
+        """C1's pipelined e2e step is ~0.1 ms: time 100 of them (C5: the default)"""
+        return 0 if (self.big or self.ws > 1) else 100
+
     def e2e_pipeline(self, variant, steps):
         """pipelined e2e for C1 (see pipeline_e2e); C5 at 2^32 keeps the
         sequential e2e (two pinned 16 GiB output sets would be needed)"""
@@ -478,7 +483,8 @@ class C1:
             b["nt_p"].copy_(b["dnt"], non_blocking=True)
             return 4 * self.N + 8
 
-        ms, d2h_bytes = pipeline_e2e(make_set, h2d, compute, d2h, steps)
+        # partition2's result has a fixed size (n): no host wait per step
+        ms, d2h_bytes = pipeline_e2e(make_set, h2d, compute, d2h, steps, host_sync=False)
         return ms, 4 * self.N, d2h_bytes
 
     def e2e_step(self, bufs):
@@ -882,13 +888,62 @@ class C4:
 
 
 # ----------------------------------------------------------------- timing
-def pipeline_e2e(make_set, h2d, compute, d2h, steps, warm=2):
+def link_probe(h2d_bytes, d2h_bytes, reps=3):
+    """The box's pinned-copy ceiling for an e2e step: the step's H2D bytes
+    alone, its D2H bytes alone, and both at once on two streams (PCIe is
+    full duplex on most boxes, not all).  e2e.link_frac = duplex_ms / the
+    e2e step: 1.0 means the step runs at the link."""
+    import torch
+
+    h2d_bytes, d2h_bytes = max(int(h2d_bytes), 1), max(int(d2h_bytes), 1)
+    # at most 1 GiB each way (C5 moves 16 GiB): times scale with the bytes
+    scale = max(h2d_bytes, d2h_bytes) / min(max(h2d_bytes, d2h_bytes), 1 << 30)
+    nb_in, nb_out = max(1, int(h2d_bytes / scale)), max(1, int(d2h_bytes / scale))
+    h_in = torch.empty(nb_in, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nb_out, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(nb_in, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty(nb_out, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        for _ in range(reps):
+            fn()
+        b.record(cur)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def duplex():
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    t_in = timed(lambda: d_in.copy_(h_in, non_blocking=True)) * scale
+    t_out = timed(lambda: h_out.copy_(d_out, non_blocking=True)) * scale
+    t_dup = timed(duplex) * scale
+    del h_in, h_out, d_in, d_out
+    return {"h2d_GBs": round(h2d_bytes / (t_in * 1e-3) / 1e9, 2), "d2h_GBs": round(d2h_bytes / (t_out * 1e-3) / 1e9, 2),
+            "serial_ms": round(t_in + t_out, 3), "duplex_ms": round(t_dup, 3)}
+
+
+def pipeline_e2e(make_set, h2d, compute, d2h, steps, warm=2, host_sync=True):
     """The e2e step as a server runs it: two device/host buffer sets and three
     streams, so step i's host->device copy overlaps step i-1's device->host
     read-back (PCIe is full duplex) and the kernels run between them.  Every
     step still copies its whole input in and its whole result out.  d2h(b) is
     called on the host once step b's compute has finished (so it may read a
-    result size from a pinned scalar).  Returns (ms per step, d2h bytes)."""
+    result size from a pinned scalar); host_sync=False when the result's size
+    is fixed (the read-back then follows the compute on the device only, and
+    the host never waits inside the loop).  Returns (ms per step, d2h bytes)."""
     import torch
 
     sets = [make_set() for _ in range(2)]
@@ -915,7 +970,8 @@ def pipeline_e2e(make_set, h2d, compute, d2h, steps, warm=2):
 
     def read_back(i):
         b = sets[i % 2]
-        b["e_cmp"].synchronize()
+        if host_sync:
+            b["e_cmp"].synchronize()
         s_d2h.wait_event(b["e_cmp"])
         with torch.cuda.stream(s_d2h):
             out_bytes.append(d2h(b))
@@ -1057,6 +1113,8 @@ def run_ours(args):
 
     # e2e: pinned host buffers, copies inside the timed region
     e2e_steps = max(3, min(args.steps, 10))
+    if getattr(wl, "e2e_steps", None):  # sub-millisecond steps: more of them
+        e2e_steps = max(e2e_steps, wl.e2e_steps)
     pipelined = getattr(wl, "e2e_pipeline", None)
     res = pipelined(selected, e2e_steps) if pipelined is not None else None
     e2e_mode = "sequential: H2D, pipeline, D2H per step"
@@ -1079,6 +1137,11 @@ def run_ours(args):
         t1.record()
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(t0.elapsed_time(t1) / e2e_steps, ws)
+    try:  # this box's PCIe ceiling for the same bytes (box-dependent: e2e is copy-bound)
+        link = link_probe(h2d, d2h)
+    except Exception as ex:  # e.g. host memory: report, do not fail the line
+        link = None
+        print(f"bench.py: link probe skipped ({ex})", file=sys.stderr)
     units_total = wl.units() * ws
     value = units_total / (ms * 1e-3) / 1e9
     achieved = (kbytes / (kms * 1e-3) / 1e9) if kms else None
@@ -1134,6 +1197,8 @@ def run_ours(args):
             "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(e2e_ms, 3),
             "mode": e2e_mode,
+            "link": link,
+            "link_frac": round(link["duplex_ms"] / e2e_ms, 4) if link else None,
         },
         "cpu_baseline": cpu,
         "clocks": clocks,

@@ -1,7 +1,7 @@
 """Per-CTA timeline of the big-tile compaction kernel (development tool).
 
 Needs a library built with -DIXG_TRACE (IXGPU_LIB=...):
-    IXG_TILE=12288 python tools/trace_filter.py <filter|c2> [log2n]
+    IXG_TILE=12288 python tools/trace_filter.py <filter|c2> [log2n] [i32|i64]   (i64: IXG_TILE=8192)
 Prints per-phase durations (ns) over CTAs and the number of CTAs in flight.
 k_filter_b trace slots: 0 start, 1 counted, 2 CTA scan, 3 compacted, 4 base
 known (bar 2), 5 look-back warp done, 6 stores done (filter), 7 look-back
@@ -35,9 +35,10 @@ def main():
     n = 1 << (int(sys.argv[2]) if len(sys.argv) > 2 else 28)
     dev = torch.device("cuda")
     st = ops.Status(dev)
-    xs = ops.gen_uniform(n, -128, 127, 0, torch.int32, device=dev)
-    ys = torch.empty(n, dtype=torch.int32, device=dev)
-    zs = torch.empty(n, dtype=torch.int32, device=dev)
+    dt = torch.int64 if (len(sys.argv) > 3 and sys.argv[3] == "i64") else torch.int32
+    xs = ops.gen_uniform(n, -128, 127, 0, dt, device=dev)
+    ys = torch.empty(n, dtype=dt, device=dev)
+    zs = torch.empty(n, dtype=dt, device=dev)
     dk = torch.empty(1, dtype=torch.int64, device=dev)
     k = int((xs >= 0).sum().item())
     shape = torch.from_numpy(gen.segment_shape(1, max(1, n >> 8), k)).to(dev)
