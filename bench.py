@@ -995,9 +995,14 @@ def pipeline_e2e(make_set, h2d, compute, d2h, steps, warm=2, host_sync=True):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(cur)
     s_h2d.wait_stream(cur)
+    w0 = time.perf_counter()
     run(steps)
+    w1 = time.perf_counter()
     t1.record(cur)
     torch.cuda.synchronize()
+    if os.environ.get("IXG_E2E_HOSTTIME"):  # diagnostics: host enqueue time per step
+        print(f"pipeline_e2e: host {1e3 * (w1 - w0) / steps:.4f} ms/step, device {t0.elapsed_time(t1) / steps:.4f}",
+              file=sys.stderr)
     return t0.elapsed_time(t1) / steps, max(out_bytes)
 
 
