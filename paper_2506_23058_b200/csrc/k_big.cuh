@@ -87,6 +87,9 @@ constexpr int kSegsumCH = (sizeof(T) == 4 && sizeof(Z) == 8) ? IXG_SCAN32_CH : 0
 #ifndef IXG_MKF_CH
 #define IXG_MKF_CH 1  // mkFlags scan: chunks (4 K int64 shape values) per tile
 #endif
+#ifndef IXG_SEGSUM_WSCAN
+#define IXG_SEGSUM_WSCAN 1  // k_segsum_b: the (chunk, warp) prefixes by one warp scan instead of a loop per thread
+#endif
 #ifndef IXG_SEGSUM_MINB
 #define IXG_SEGSUM_MINB 3  // k_segsum_b: 72 registers; measured 0.313 ms vs 0.321 (4) / 0.351 (2) at k = 2^27
 #endif
@@ -1319,16 +1322,30 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   // tile aggregate (chunk-major order) and each (chunk, warp) prefix
   typename M::T tagg = M::identity();
   typename M::T chunk_pre[B::CH];
+  if constexpr (IXG_SEGSUM_WSCAN && B::CH * kBW <= 32) {
+    // one warp-wide scan over the CH x kBW (chunk, warp) aggregates, in every
+    // warp: lane l holds aggregate l (chunk l / kBW, warp l % kBW)
+    const int l = lane_id();
+    typename M::T ag = M::identity();
+    if (l < B::CH * kBW) ag = s_w[l / kBW][l % kBW];
+    const typename M::T inc = warp_inclusive<M>(ag);
+    typename M::T exc = M::shfl_up(inc, 1);
+    if (l == 0) exc = M::identity();
+    tagg = M::shfl(inc, B::CH * kBW - 1);
 #pragma unroll
-  for (int c = 0; c < B::CH; ++c) {
-    chunk_pre[c] = tagg;
-    typename M::T wp = M::identity();
+    for (int c = 0; c < B::CH; ++c) chunk_pre[c] = M::op(M::shfl(exc, c * kBW + warp_id()), a[c]);
+  } else {
 #pragma unroll
-    for (int w = 0; w < kBW; ++w) {
-      if (w < warp_id()) wp = M::op(wp, s_w[c][w]);
-      tagg = M::op(tagg, s_w[c][w]);
+    for (int c = 0; c < B::CH; ++c) {
+      chunk_pre[c] = tagg;
+      typename M::T wp = M::identity();
+#pragma unroll
+      for (int w = 0; w < kBW; ++w) {
+        if (w < warp_id()) wp = M::op(wp, s_w[c][w]);
+        tagg = M::op(tagg, s_w[c][w]);
+      }
+      chunk_pre[c] = M::op(M::op(chunk_pre[c], wp), a[c]);
     }
-    chunk_pre[c] = M::op(M::op(chunk_pre[c], wp), a[c]);
   }
   if (t == 0) {
     s_agg = tagg;
