@@ -87,6 +87,9 @@ constexpr int kSegsumCH = (sizeof(T) == 4 && sizeof(Z) == 8) ? IXG_SCAN32_CH : 0
 #ifndef IXG_MKF_CH
 #define IXG_MKF_CH 1  // mkFlags scan: chunks (4 K int64 shape values) per tile
 #endif
+#ifndef IXG_SEGSUM_RUN32
+#define IXG_SEGSUM_RUN32 1  // k_segsum_b<int32, int32, SegOp>: the pass-2 run in 32 bits with an exact overflow test
+#endif
 #ifndef IXG_SEGSUM_WSCAN
 #define IXG_SEGSUM_WSCAN 1  // k_segsum_b: the (chunk, warp) prefixes by one warp scan instead of a loop per thread
 #endif
@@ -1370,6 +1373,27 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     const long long g = tile_base + (long long)c * kBChunk + (long long)kSItems * t;
     long long run = M::op(carry, chunk_pre[c]).v;
     Z z[kSItems];
+    // int32 sgmSum into int32 (C2's zs): from an exact start inside int32
+    // the run is carried modulo 2^32 -- a result leaves int32 iff its signed
+    // add overflows (before the first such add every start is exact), so
+    // NARROW is the same as the 64-bit run's; a start outside int32 (only
+    // a carry from earlier shards can be one) takes the 64-bit loop
+    constexpr bool k32 = IXG_SEGSUM_RUN32 && sizeof(T) == 4 && sizeof(Z) == 4 && std::is_same<M, SegOp>::value &&
+                         (std::is_same<F, ScanId>::value || std::is_same<F, SegFlagArr>::value);
+    if (k32 && run == (long long)(int)run) {
+      int32_t r = (int32_t)run;
+      uint32_t ov = 0;
+#pragma unroll
+      for (int j = 0; j < kSItems; ++j) {
+        const int32_t xv = (int32_t)x[j];
+        const int32_t pr = ((fl[c] >> j) & 1u) ? 0 : r;
+        const int32_t nr = (int32_t)((uint32_t)pr + (uint32_t)xv);
+        ov |= (uint32_t)((pr ^ nr) & (xv ^ nr));
+        z[j] = (Z)nr;
+        r = nr;
+      }
+      if ((int32_t)ov < 0) narrow = true;
+    } else
 #pragma unroll
     for (int j = 0; j < kSItems; ++j) {
       const long long prev = ((fl[c] >> j) & 1u) ? 0LL : run;

@@ -263,6 +263,66 @@ def test_segscan(cuda, n):
     assert np.array_equal(_np(ops.segscan_add(_t(flags, cuda), _t(xs, cuda))), want)
 
 
+@pytest.mark.parametrize("case", ["local_overflow_carried_back", "overflow", "wide_carry_flag_first",
+                                  "wide_carry_no_flag", "random"])
+def test_segsum_int32_narrow_exact(cuda, case):
+    """ixg_segsum int32 -> int32 (the sharded C2 sgmSum): values exact, and
+    NARROW iff an exact value (the carry of earlier shards included) leaves
+    int32 -- the kernel carries the run in 32 bits from an in-range start
+    and in 64 bits from a start outside int32."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    tile = 12288
+    n = 3 * tile + 100
+    xs = np.zeros(n, np.int32)
+    starts = [0, 30_000]
+    carry_v, carry_f = 0, False
+    if case == "local_overflow_carried_back":  # a tile-local prefix past int32, the exact value back in range
+        xs[:2047] = -(1 << 20)
+        xs[tile:tile + 2100] = 1 << 20
+    elif case == "overflow":
+        xs[tile:tile + 2100] = 1 << 20
+    elif case == "wide_carry_flag_first":  # an earlier shard's carry outside int32, a flag at 0 resets it
+        carry_v, carry_f = 1 << 33, True
+        xs[:] = gen.uniform(3, n, -1000, 1000, np.int32)
+    elif case == "wide_carry_no_flag":  # the same carry reaches the first elements: NARROW
+        carry_v, carry_f = 1 << 33, True
+        starts = [30_000]
+        xs[:] = gen.uniform(4, n, -1000, 1000, np.int32)
+    else:
+        xs[:] = gen.uniform(5, n, -(1 << 31), (1 << 31) - 1, np.int32)
+        carry_v, carry_f = -(1 << 31), True
+        starts = sorted(set([0] + list(gen.uniform(6, 400, 1, n - 1, np.int64))))
+    # this array's flags start `base` bits into the mkFlags bitmap (a shard
+    # that begins inside a segment: no flag at its position 0)
+    base = 5 if case == "wide_carry_no_flag" else 0
+    gstarts = [0] + [q + base for q in starts if q + base > 0]
+    shape = np.diff(np.array(gstarts + [n + base], np.int64))
+    flags = np.zeros(n, bool)
+    flags[np.array([q - base for q in gstarts if q >= base])] = True
+    want = np.zeros(n, np.int64)
+    run = carry_v
+    for i in range(n):  # segmented inclusive sum after the carry, in Python ints
+        run = int(xs[i]) if flags[i] else run + int(xs[i])
+        want[i] = run
+    overflow = bool(np.any((want < -(1 << 31)) | (want > (1 << 31) - 1)))
+    bits = ops.flag_bitmap(_t(shape, cuda), n + base)
+    zs = torch.empty(n, dtype=torch.int32, device=cuda)
+    tot = torch.empty(2, dtype=torch.int64, device=cuda)
+    st = ops.Status(cuda)
+    ops.segsum(_t(xs, cuda), n, bits, base, zs, carry_v, carry_f, tot, st)
+    s = st.read()
+    assert s.narrow == overflow, case
+    if case in ("local_overflow_carried_back", "wide_carry_flag_first"):
+        assert not overflow
+    if case in ("overflow", "wide_carry_no_flag"):
+        assert overflow
+    if not overflow:
+        assert np.array_equal(_np(zs).astype(np.int64), want), case
+
+
 @pytest.mark.parametrize("n", [0, 1, 1000, 1 << 20])
 def test_scatter_perm(cuda, n):
     """Injective scatter (a partition2 permutation): all variants agree."""
