@@ -323,6 +323,15 @@ int ixg_mkflags(int64_t k, const int64_t* shape, int64_t m, int64_t* flags, uint
 int64_t ixg_bitmap_words(int64_t nbits);
 int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, const int64_t* d_nbits, void* ws,
                     size_t ws_bytes, void* stream);
+/* The same bitmap restricted to one shard's outputs: bit j = flag of global
+ * output position *d_lo + j, j < nbits (or *d_nbits) -- a rank's window
+ * [K, K + k) of the mkFlags array, so a rank clears and sets k bits instead
+ * of all shards' K_total.  Replaces, for the sharded sgmSum, the reference's
+ * mkFlags (scatter of `replicate m 1` at the exclusive scan of shape,
+ * corpus/c2_filter_sgmsum.ixl; oracle.py:294-305) restricted to the
+ * positions this shard's outputs occupy. */
+int ixg_flag_bitmap_window(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, const int64_t* d_nbits,
+                           const int64_t* d_lo, void* ws, size_t ws_bytes, void* stream);
 int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,
                const int64_t* d_flag_base, int dt_z, void* zs, int64_t carry_v, int carry_f, int64_t* d_total,
                ixg_status* st, void* ws, size_t ws_bytes, void* stream);

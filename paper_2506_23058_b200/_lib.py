@@ -103,6 +103,7 @@ SIGNATURES = {
     "ixg_map": (_I, [_P, _I, _P, _I, _P, _I, _P, _I, _I64, _I, _P, _P]),
     "ixg_bitmap_words": (_I64, [_I64]),
     "ixg_flag_bitmap": (_I, [_P, _I64, _P, _I64, _P, _P, _SZ, _P]),
+    "ixg_flag_bitmap_window": (_I, [_P, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
     "ixg_segsum": (_I, [_I, _P, _I64, _P, _P, _I64, _P, _I, _P, _I64, _I, _P, _P, _P, _SZ, _P]),
     "ixg_seg_carry": (_I, [_P, _I64, _P, _I, _P, _I64, _P, _I64, _P, _I, _P, _P, _P]),
     "ixg_timer_start": (_I, [_I]),

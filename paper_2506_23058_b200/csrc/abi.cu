@@ -427,7 +427,7 @@ inline bool mkf_big_enabled() {
   return mode == 1;
 }
 int launch_mkflags(const long long* shape, long long m, uint32_t* bits, long long nbits, const long long* d_nbits,
-                   LBChan c, cudaStream_t s, ixg_status* st = nullptr) {
+                   LBChan c, cudaStream_t s, ixg_status* st = nullptr, const long long* d_lo = nullptr) {
   const bool big = mkf_big_enabled() && aligned16(shape) && aligned16(bits) && m > 0;
   if (big) {  // the clear heads a programmatic-launch chain (see k_bitmap_zero)
     k_bitmap_zero<<<grid_for((nbits + 127) / 128), kGThreads, 0, s>>>(
@@ -448,11 +448,12 @@ int launch_mkflags(const long long* shape, long long m, uint32_t* bits, long lon
     fn.bits = bits;
     fn.nb = nbits;
     fn.d_nb = d_nbits;
+    fn.d_lo = d_lo;
     return launch_segsum_b<long long, long long, SumOp>(shape, m, nullptr, nullptr, 0, nullptr, c, 0, 0, nullptr,
                                                         st, s, nullptr, fn);
   }
-  return launch_scan<SumOp>(m, SrcArrT<long long>{shape}, EpiSegStarts{m, shape, nullptr, bits, nbits, d_nbits, nullptr, st},
-                            c, s);
+  return launch_scan<SumOp>(m, SrcArrT<long long>{shape},
+                            EpiSegStarts{m, shape, nullptr, bits, nbits, d_nbits, nullptr, st, d_lo}, c, s);
 }
 
 // filter / filter_by on element type T.  Sites: 0 = offs[n-1], 1 = scatter.
@@ -1284,6 +1285,17 @@ int ixg_flag_bitmap(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbi
   LBChan c = w.chan(0, tiles_of(m, kGTile));
   // (d_nbits: nbits on the device, <= the capacity nbits -- only those words are cleared)
   return launch_mkflags((const long long*)shape, m, bits, nbits, (const long long*)d_nbits, c, s);
+}
+
+int ixg_flag_bitmap_window(const int64_t* shape, int64_t m, uint32_t* bits, int64_t nbits, const int64_t* d_nbits,
+                           const int64_t* d_lo, void* ws, size_t ws_bytes, void* stream) {
+  if (m < 0 || nbits < 0 || (m > 0 && !shape) || !bits || !d_lo) return IXG_BADARG;
+  if (ws_bytes < ixg_ws_bytes(IXG_OP_SCAN, m, 0)) return IXG_BADARG;
+  cudaStream_t s = S(stream);
+  WS w(ws);
+  LBChan c = w.chan(0, tiles_of(m, kGTile));
+  return launch_mkflags((const long long*)shape, m, bits, nbits, (const long long*)d_nbits, c, s, nullptr,
+                        (const long long*)d_lo);
 }
 
 int ixg_segsum(int dt, const void* vs, int64_t n, const int64_t* d_n, const uint32_t* bits, int64_t flag_base,

@@ -1172,12 +1172,15 @@ struct ScanSegStartBits : ScanId {
   uint32_t* bits;
   long long nb;
   const long long* d_nb;  // nullable: nbits on the device
+  const long long* d_lo = nullptr;  // nullable: bitmap window [*d_lo, *d_lo + nb) (a shard's outputs)
+  long long lo = 0;
   IXG_DEV void init() {
     if (d_nb) nb = *d_nb;
+    if (d_lo) lo = *d_lo;
   }
   IXG_DEV long long out(long long run, long long xv, long long) const {
     const long long start = run - xv;
-    if (xv > 0 && start >= 0 && start < nb) atomicOr(&bits[start >> 5], 1u << (start & 31));
+    if (xv > 0 && start >= lo && start - lo < nb) atomicOr(&bits[(start - lo) >> 5], 1u << ((start - lo) & 31));
     return 0;
   }
 };

@@ -286,8 +286,10 @@ struct EpiSegStarts {  // mkSgmDescr / mkFlags: ind[i] = if shape[i] <= 0 then -
   const long long* d_nbits;  // nullable: nbits on the device
   long long* d_total;    // nullable: scn[m-1] + shape[m-1]
   ixg_status* st = nullptr;  // nullable: IXG_OVERFLOW at the first prefix leaving int64 (§2.2)
+  const long long* d_lo = nullptr;  // nullable: bitmap window [*d_lo, *d_lo + nb) (a shard's outputs)
   IXG_DEV void operator()(long long i0, long long n, const Run16<SumOp::T>& r) const {
     const long long nb = d_nbits ? *d_nbits : nbits;
+    const long long lo = d_lo ? *d_lo : 0;
     long long o[kGItems];
     long long ovf = -1;
 #pragma unroll
@@ -295,8 +297,8 @@ struct EpiSegStarts {  // mkSgmDescr / mkFlags: ind[i] = if shape[i] <= 0 then -
       const long long s = r.x(q).v, start = r.incl[q].v - s;
       if (ovf < 0 && i0 + q < n && step_ovf(r.incl[q].v, s)) ovf = i0 + q;
       o[q] = s <= 0 ? -1 : start;
-      if (bits && i0 + q < n && s > 0 && start >= 0 && start < nb)
-        atomicOr(&bits[start >> 5], 1u << (start & 31));
+      if (bits && i0 + q < n && s > 0 && start >= lo && start - lo < nb)
+        atomicOr(&bits[(start - lo) >> 5], 1u << ((start - lo) & 31));
     }
     if (ovf >= 0) status_overflow(st, 0, ovf);
     if (ind) store16_i64(ind, i0, n, o);

@@ -428,10 +428,10 @@ class GpuC2Local:
     def step_device(self, group=None):
         """The whole sharded C2 step with every count, offset and carry kept
         on the device (no host round trip): filter -> all-gather of the
-        counts -> [K_r, K_total] -> mkFlags bitmap over the K_total global
-        outputs -> sgmSum of this rank's outputs from flag K_r -> all-gather
-        of the segmented aggregates -> the carry of the ranks before, added
-        before the first flag.  Outputs: ys / zs [0, *dk), global offset
+        counts -> [K_r, K_total] -> the mkFlags bits of this rank's window
+        [K_r, K_r + k_r) of the global outputs -> sgmSum of this rank's
+        outputs -> all-gather of the segmented aggregates -> the carry of the
+        ranks before, added before the first flag.  Outputs: ys / zs [0, *dk), global offset
         d_off[0]."""
         import torch
         import torch.distributed as dist
@@ -444,16 +444,16 @@ class GpuC2Local:
             self.d_ks = torch.empty(world, dtype=torch.int64, device=self.dev)
             self.d_off = torch.empty(2, dtype=torch.int64, device=self.dev)
             self.d_aggs = torch.empty(2 * world, dtype=torch.int64, device=self.dev)
-            self.cap = n * world  # every global output position (K_total <= cap)
         self.ops.filter(self.xs, self.pred, L.VARIANT_ELIDED, self.st, ys=self.ys, d_count=self.dk)
         all_gather_dev(self.dk, self.d_ks, group)
         self.ops.rank_offsets(self.d_ks, world, rank, out=self.d_off)
-        self.bits = self.ops.flag_bitmap(self.shape, self.cap, d_nbits=self.d_off[1:], bits=self.bits)
-        self.ops.segsum(self.ys, n, self.bits, 0, self.zs, 0, False, self.tot, self.st, d_n=self.dk,
-                        d_flag_base=self.d_off)
+        # the mkFlags bits of this rank's own outputs only: global positions
+        # [K_r, K_r + k_r) (d_off[0], dk), k_r bits instead of all K_total
+        self.bits = self.ops.flag_bitmap(self.shape, n, d_nbits=self.dk, bits=self.bits, d_lo=self.d_off)
+        self.ops.segsum(self.ys, n, self.bits, 0, self.zs, 0, False, self.tot, self.st, d_n=self.dk)
         all_gather_dev(self.tot, self.d_aggs, group)
-        self.ops.seg_carry(self.bits, 0, self.zs, n, 0, self.scratch, self.st, d_n=self.dk, d_flag_base=self.d_off,
-                           d_aggs=self.d_aggs, rank=rank)
+        self.ops.seg_carry(self.bits, 0, self.zs, n, 0, self.scratch, self.st, d_n=self.dk, d_aggs=self.d_aggs,
+                           rank=rank)
 
     def filter(self) -> int:
         from . import _lib as L

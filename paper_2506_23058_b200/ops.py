@@ -484,16 +484,21 @@ def mkflags(k: int, shape: torch.Tensor, variant: int, status: Status) -> torch.
     return out
 
 
-def flag_bitmap(shape: torch.Tensor, nbits: int, d_nbits=None, bits=None) -> torch.Tensor:
+def flag_bitmap(shape: torch.Tensor, nbits: int, d_nbits=None, bits=None, d_lo=None) -> torch.Tensor:
     """mkFlags over nbits output positions as a bitmap (int32 words); with
-    d_nbits, over the device count (nbits is then the capacity)."""
+    d_nbits, over the device count (nbits is then the capacity); with d_lo
+    (a device int64), over the window of positions [*d_lo, *d_lo + nbits)."""
     shape = _contig(shape.to(torch.int64))
     words = int(_lib().ixg_bitmap_words(nbits))
     if bits is None or bits.numel() < words:
         bits = torch.empty(words, dtype=torch.int32, device=shape.device)
     ws, wsb = _ws(L.OP_SCAN, shape.numel(), 0, shape.device)
-    L.check(_lib().ixg_flag_bitmap(_ptr(shape), shape.numel(), _ptr(bits), nbits, _ptr(d_nbits), ws, wsb, _stream()),
-            "flag_bitmap")
+    if d_lo is None:
+        rc = _lib().ixg_flag_bitmap(_ptr(shape), shape.numel(), _ptr(bits), nbits, _ptr(d_nbits), ws, wsb, _stream())
+    else:
+        rc = _lib().ixg_flag_bitmap_window(_ptr(shape), shape.numel(), _ptr(bits), nbits, _ptr(d_nbits), _ptr(d_lo),
+                                           ws, wsb, _stream())
+    L.check(rc, "flag_bitmap")
     return bits
 
 

@@ -239,6 +239,36 @@ def test_flag_bitmap(cuda, m, kind, on_device):
     assert np.array_equal(got, _flag_bits_ref(shape, nbits))
 
 
+@pytest.mark.parametrize("m", [1, 7, 4097, 300_001])
+@pytest.mark.parametrize("kind", ["segments", "unit", "negatives"])
+@pytest.mark.parametrize("win", [(0, 1000), (37, 5000), (100_003, 77_777), (10 ** 9, 64)])
+def test_flag_bitmap_window(cuda, m, kind, win):
+    """ixg_flag_bitmap_window (a shard's window of mkFlags: the sharded C2
+    step): bit j = the flag of global position lo + j, j < nb (nb on the
+    device), the rest of the buffer's words cleared."""
+    import torch
+
+    from paper_2506_23058_b200 import ops
+
+    rng = np.random.default_rng(m + 3 * len(kind))
+    if kind == "unit":
+        shape = np.ones(m, np.int64)
+    elif kind == "negatives":
+        shape = rng.integers(-3, 9, m).astype(np.int64)
+    else:
+        shape = rng.integers(0, 6, m).astype(np.int64)
+    lo, nb = win
+    full = _flag_bits_ref(shape, lo + nb)
+    want = np.array([(full[(lo + j) >> 5] >> np.uint32((lo + j) & 31)) & 1 for j in range(nb)], np.uint32)
+    cap = nb + 4096
+    bits = torch.full((int(ops._lib().ixg_bitmap_words(cap)),), -1, dtype=torch.int32, device=cuda)  # stale words
+    ops.flag_bitmap(_t(shape, cuda), cap, d_nbits=torch.tensor([nb], dtype=torch.int64, device=cuda), bits=bits,
+                    d_lo=torch.tensor([lo], dtype=torch.int64, device=cuda))
+    got_w = _np(bits).view(np.uint32)
+    got = np.array([(got_w[j >> 5] >> np.uint32(j & 31)) & 1 for j in range(nb)], np.uint32)
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("n", SIZES)
 def test_scan_add(cuda, n):
     from paper_2506_23058_b200 import ops
