@@ -1396,19 +1396,36 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
         r = nr;
       }
       if ((int32_t)ov < 0) narrow = true;
-    } else
+    } else {
+      // exact: the sequential step prev + x in the reference's unbounded
+      // ints -- the steps' signed-overflow bits are OR-ed, and the first
+      // overflowing element is looked for only when one did (elements past
+      // n are zero-filled: prev + 0 never overflows)
+      const long long run0 = run;
+      long long ovm = 0;
 #pragma unroll
-    for (int j = 0; j < kSItems; ++j) {
-      const long long prev = ((fl[c] >> j) & 1u) ? 0LL : run;
-      const long long xv = fn.elem(x[j]);
-      run = (long long)((unsigned long long)prev + (unsigned long long)xv);
-      if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
-      // exact: the sequential step prev + x in the reference's unbounded ints
-      if (F::kOvf && sizeof(Z) == 8 && (((prev ^ run) & (xv ^ run)) < 0) && g + j < n && ovf_at == LLONG_MAX)
-        ovf_at = g + j;
-      if (g + j == n - 1) fn.last(run);
-      if constexpr (F::kStore) z[j] = (Z)fn.out(run, xv, g + j);
-      else if (g + j < n) fn.out(run, xv, g + j);
+      for (int j = 0; j < kSItems; ++j) {
+        const long long prev = ((fl[c] >> j) & 1u) ? 0LL : run;
+        const long long xv = fn.elem(x[j]);
+        run = (long long)((unsigned long long)prev + (unsigned long long)xv);
+        if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
+        if constexpr (F::kOvf && sizeof(Z) == 8) ovm |= (prev ^ run) & (xv ^ run);
+        if (g + j == n - 1) fn.last(run);
+        if constexpr (F::kStore) z[j] = (Z)fn.out(run, xv, g + j);
+        else if (g + j < n) fn.out(run, xv, g + j);
+      }
+      if (F::kOvf && sizeof(Z) == 8 && ovm < 0 && ovf_at == LLONG_MAX) {
+        long long r2 = run0;
+        for (int j = 0; j < kSItems; ++j) {
+          const long long prev = ((fl[c] >> j) & 1u) ? 0LL : r2;
+          const long long xv = fn.elem(x[j]);
+          r2 = (long long)((unsigned long long)prev + (unsigned long long)xv);
+          if ((((prev ^ r2) & (xv ^ r2)) < 0) && g + j < n) {
+            ovf_at = g + j;
+            break;
+          }
+        }
+      }
     }
     if constexpr (!F::kStore) {
     } else if (g + kSItems <= n) {
