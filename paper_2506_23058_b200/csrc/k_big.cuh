@@ -90,6 +90,9 @@ constexpr int kSegsumCH = (sizeof(T) == 4 && sizeof(Z) == 8) ? IXG_SCAN32_CH : 0
 #ifndef IXG_SEGSUM_RUN32
 #define IXG_SEGSUM_RUN32 1  // k_segsum_b<int32, int32, SegOp>: the pass-2 run in 32 bits with an exact overflow test
 #endif
+#ifndef IXG_SEGSUM_BITS
+#define IXG_SEGSUM_BITS 1  // k_segsum_b with a predicate-bit element (CHECKED index scans): popcount sums
+#endif
 #ifndef IXG_SEGSUM_WSCAN
 #define IXG_SEGSUM_WSCAN 1  // k_segsum_b: the (chunk, warp) prefixes by one warp scan instead of a loop per thread
 #endif
@@ -1115,6 +1118,7 @@ struct ScanId {
   static constexpr bool kOvf = true;
   static constexpr bool kFlagArr = false;
   static constexpr bool kStore = true;     // out() is stored to zs (else called for its effect only)
+  static constexpr bool kBits = false;     // elem() is a 0 / 1 predicate bit (mask16 gives 16 of them)
   static constexpr bool kTrigger = false;  // PDL chain member: release the dependent at the top, wait for
                                            // the predecessor only before the outputs
   static constexpr int kCH = 0;            // chunks per tile if not the default
@@ -1196,6 +1200,13 @@ struct ScanFilterInds {  // inds[i] = if p xs[i] then offs[i] - 1 else -1; *d_co
   PredBit<T> pb;
   long long* d_count;
   IXG_DEV void init() { pb.init(); }
+  static constexpr bool kBits = true;
+  IXG_DEV uint32_t mask16(const T (&x)[kSItems]) const {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) m |= (uint32_t)pb.bit(x[j]) << j;
+    return m;
+  }
   IXG_DEV long long elem(T x) const { return pb.bit(x); }
   IXG_DEV long long out(long long run, long long xv, long long) const { return xv ? run - 1 : -1; }
   IXG_DEV void last(long long run) const { *d_count = run; }
@@ -1214,6 +1225,13 @@ struct ScanPart2Inds {  // indices[i] = if p x then indicesT[i] - 1 else i + 1 -
   IXG_DEV void init() {
     pb.init();
     nt = *d_nt;
+  }
+  static constexpr bool kBits = true;
+  IXG_DEV uint32_t mask16(const T (&x)[kSItems]) const {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < kSItems; ++j) m |= (uint32_t)pb.bit(x[j]) << j;
+    return m;
   }
   IXG_DEV long long elem(T x) const { return pb.bit(x); }
   IXG_DEV long long out(long long run, long long xv, long long g) const { return xv ? run - 1 : (g + 1 - run) + nt - 1; }
@@ -1293,6 +1311,8 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
   }
   if (!tma) cp_async_wait_all();
   typename M::T a[B::CH];
+  uint32_t pm[B::CH];  // F::kBits: the chunk's 16 element bits
+  (void)pm;
 #pragma unroll
   for (int c = 0; c < B::CH; ++c) {
     T x[kSItems];
@@ -1315,8 +1335,13 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
     const uint32_t vm = valid_mask(g, n);
     const uint32_t tail = fl[c] ? (vm & ~((1u << (31 - __clz(fl[c]))) - 1u)) : vm;
     long long s = 0;
+    if constexpr (F::kBits && IXG_SEGSUM_BITS) {  // 0 / 1 elements: their sum is a popcount, the bits kept for pass 2
+      pm[c] = fn.mask16(x);
+      s = __popc(pm[c] & tail);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kSItems; ++j) s += ((tail >> j) & 1u) ? fn.elem(x[j]) : 0LL;
+      for (int j = 0; j < kSItems; ++j) s += ((tail >> j) & 1u) ? fn.elem(x[j]) : 0LL;
+    }
     a[c] = seg_mk<M>(s, fl[c] != 0);
     typename M::T inc = warp_inclusive<M>(a[c]);
     if (lane_id() == 31) s_w[c][warp_id()] = inc;
@@ -1406,7 +1431,9 @@ __global__ void __launch_bounds__(kBT + 32, IXG_SEGSUM_MINB) k_segsum_b(const T*
 #pragma unroll
       for (int j = 0; j < kSItems; ++j) {
         const long long prev = ((fl[c] >> j) & 1u) ? 0LL : run;
-        const long long xv = fn.elem(x[j]);
+        long long xv;
+        if constexpr (F::kBits && IXG_SEGSUM_BITS) xv = (long long)((pm[c] >> j) & 1u);
+        else xv = fn.elem(x[j]);
         run = (long long)((unsigned long long)prev + (unsigned long long)xv);
         if (sizeof(Z) == 4 && run != (long long)(int)run) narrow = true;
         if constexpr (F::kOvf && sizeof(Z) == 8) ovm |= (prev ^ run) & (xv ^ run);
